@@ -1,0 +1,100 @@
+// C-ABI plumbing: error strings, version, device check, Philox known-answer
+// and ALU-roofline probe kernels.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace fgl {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return FGL_E_CUDA;
+}
+
+__global__ void philox_words_kernel(uint64_t k0, uint64_t k1, int64_t start, int64_t count,
+                                    uint64_t* out) {
+  const int64_t first_blk = start >> 2;
+  const int64_t last_blk = (start + count - 1) >> 2;
+  for (int64_t b = first_blk + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= last_blk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    philox4x64_10((uint64_t)b + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t p = 4 * b + q;
+      if (p >= start && p < start + count) out[p - start] = w[q];
+    }
+  }
+}
+
+// ALU roofline probe: each thread draws a strided run of Philox blocks and
+// folds them with xor so nothing is dead code; one word per thread is stored.
+__global__ void philox_bench_kernel(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint64_t acc = 0;
+  for (int64_t b = tid; b < blocks; b += stride) {
+    uint64_t w0, w1, w2, w3;
+    philox4x64_10((uint64_t)b + 1, k0, k1, w0, w1, w2, w3);
+    acc ^= (w0 >> 11) + (w1 >> 11) + (w2 >> 11) + (w3 >> 11);
+  }
+  out[tid] = acc;
+}
+
+}  // namespace fgl
+
+extern "C" {
+
+const char* fgl_last_error(void) { return fgl::g_last_error.c_str(); }
+
+int fgl_version(void) { return 100; }
+
+int fgl_device_check(int device) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return fgl::cuda_status(e, "cudaGetDeviceProperties");
+  if (p.major != 10) {
+    fgl::set_error("libfastgl_b200 is built for sm_100a; device %d is sm_%d%d", device, p.major,
+                   p.minor);
+    return FGL_E_UNSUPPORTED;
+  }
+  return FGL_OK;
+}
+
+int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uint64_t* out,
+                     void* stream) {
+  if (start < 0 || count < 0 || (count > 0 && out == nullptr)) {
+    fgl::set_error("fgl_philox_words: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (count == 0) return FGL_OK;
+  const int64_t blocks = ((start + count - 1) >> 2) - (start >> 2) + 1;
+  const int threads = 256;
+  const int grid = (int)std::min<int64_t>(fgl::ceil_div(blocks, threads), 148 * 32);
+  fgl::philox_words_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(k0, k1, start, count, out);
+  FGL_LAUNCH_CHECK("philox_words_kernel");
+  return FGL_OK;
+}
+
+int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream) {
+  // `out` must hold 148*8*256 words (one per thread of the fixed grid).
+  fgl::philox_bench_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(k0, k1, blocks, out);
+  FGL_LAUNCH_CHECK("philox_bench_kernel");
+  return FGL_OK;
+}
+
+}  // extern "C"

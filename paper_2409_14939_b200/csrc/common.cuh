@@ -1,0 +1,130 @@
+// Shared device utilities for the FastGL B200 hot path (sm_100a).
+//
+// Everything here is plain CUDA C++ compiled with
+//   nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false
+// --fmad=false is load-bearing: the reference aggregation accumulates
+// `acc = acc + w*x` with a rounded multiply and a rounded add
+// (compute.py:115-148); contracting that into an FMA would change bits.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fastgl_b200.h"
+
+namespace fgl {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------------------ errors --
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+#define FGL_CUDA(call)                                              \
+  do {                                                              \
+    cudaError_t _e = (call);                                        \
+    if (_e != cudaSuccess) return ::fgl::cuda_status(_e, #call);    \
+  } while (0)
+
+#define FGL_LAUNCH_CHECK(what)                                      \
+  do {                                                              \
+    cudaError_t _e = cudaGetLastError();                            \
+    if (_e != cudaSuccess) return ::fgl::cuda_status(_e, what);     \
+  } while (0)
+
+// ------------------------------------------------------------------ philox --
+// Random123 Philox4x64-10 as used by numpy's np.random.Philox.  Draw j of a
+// generator with key (k0,k1) is word (j & 3) of philox(counter=(j>>2)+1, 0, 0, 0);
+// Generator.random() keeps the top 53 bits (word >> 11).  See oracle/philox.py.
+constexpr uint64_t kPhiloxM0 = 0xD2E7470EE14C6C93ull;
+constexpr uint64_t kPhiloxM1 = 0xCA5A826395121157ull;
+constexpr uint64_t kPhiloxW0 = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kPhiloxW1 = 0xBB67AE8584CAA73Bull;
+
+__device__ __forceinline__ void philox4x64_10(uint64_t ctr, uint64_t k0, uint64_t k1,
+                                              uint64_t& o0, uint64_t& o1, uint64_t& o2,
+                                              uint64_t& o3) {
+  uint64_t c0 = ctr, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi0 = __umul64hi(kPhiloxM0, c0);
+    const uint64_t lo0 = kPhiloxM0 * c0;
+    const uint64_t hi1 = __umul64hi(kPhiloxM1, c2);
+    const uint64_t lo1 = kPhiloxM1 * c2;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
+// --------------------------------------------------------------- warp/block --
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan; returns the exclusive prefix for this thread and
+// the block total in *total.  `smem` needs blockDim.x/32 + 1 entries.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
+  const int lane = lane_id(), wid = warp_id(), nw = blockDim.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) smem[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T s = lane < nw ? smem[lane] : T(0);
+    T si = warp_incl_scan(s);
+    if (lane < nw) smem[lane] = si - s;
+    if (lane == nw - 1) smem[32] = si;
+  }
+  __syncthreads();
+  T res = inc - v + smem[wid];
+  *total = smem[32];
+  __syncthreads();
+  return res;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  const int lane = lane_id(), wid = warp_id(), nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (wid == 0) {
+    r = lane < nw ? smem[lane] : T(0);
+    r = warp_sum(r);
+    if (lane == 0) smem[32] = r;
+  }
+  __syncthreads();
+  r = smem[32];
+  __syncthreads();
+  return r;
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Fixed grid for device-count-driven ("persistent") kernels: 2 CTAs per SM.
+constexpr int kPersistentCTAs = 2 * kNumSMs;
+
+}  // namespace fgl

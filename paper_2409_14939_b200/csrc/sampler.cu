@@ -1,0 +1,634 @@
+// Fused-Map k-hop window sampler (sm_100a).
+//
+// Replaces, per batch, sampler.sample_khop (sampler.py:120-139) and -- on the
+// trainer path -- idmap.build + translate_batch (idmap.py:198-233, :294-303).
+// A whole window of nb batches is sampled by one launch sequence with no host
+// synchronisation: sizes live on the device, kernels are launched on fixed
+// persistent grids and read their trip counts from device memory.
+//
+// Data layout in HBM:
+//  * per batch two node bitmaps of W = ceil(N/32) words: `front` (sources of
+//    the hop being sampled -> next frontier) and `all` (seeds + every sampled
+//    source = unique_nodes).  A bitmap is a direct-addressed hash set with an
+//    identity hash: insertion is one atomicOr, dedup is free, and compaction
+//    in word order yields the SORTED unique list the reference's np.unique
+//    produces (sampler.py:129,135,138) -- so the frontier order (which fixes
+//    the Philox stream positions) and the local IDs (rank in unique_nodes,
+//    trainer.py:167) come out without any sort.
+//  * rank(g) = prefix[word(g)] + popc(word & below(g)): O(1) global->local.
+//
+// Per hop: (1) degree scan over the concatenated frontier (exclusive scans of
+// deg and min(deg,f)) -> candidate stream positions and output offsets;
+// (2) select: one warp per frontier node draws one Philox4x64-10 block per
+// lane per iteration (4 candidates), keeps a warp-distributed sorted list of
+// the f smallest (key53, slot) pairs, emits them in key order and marks the
+// sources in `front`; (3) compaction of `front` -> next frontier (cleared as
+// it is read, OR-ed into `all`).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fgl {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kMaxFanout = 256;
+
+struct SampleWs {
+  uint32_t* bm_front;  // [nb*W]
+  uint32_t* bm_all;    // [nb*W]
+  int32_t* wprefix;    // [nb*W] exclusive popcount prefix of bm_all (global)
+  int32_t* front;      // [fcap]
+  int32_t* fb;         // [fcap] batch of each frontier entry
+  int64_t* scan_deg;   // [fcap]
+  int64_t* scan_sel;   // [fcap]
+  int64_t* part;       // [2*kPersistentCTAs + 2]
+  int64_t* fr_off;     // [nb+1]
+  int64_t* pos;        // [nb]   running Philox position per batch
+  int64_t* hop_pos;    // [nb]   position at the start of the current hop
+  int64_t* scal;       // [8]
+};
+
+enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5 };
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct WsLayout {
+  int64_t words, fcap, bytes;
+  int64_t off_front_bm, off_all_bm, off_wprefix, off_front, off_fb, off_sdeg, off_ssel, off_part,
+      off_froff, off_pos, off_hoppos, off_scal;
+};
+
+WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap) {
+  WsLayout L;
+  L.words = align_up(ceil_div(num_nodes, 32), 4);
+  L.fcap = std::max<int64_t>(fcap, 1);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 256); return r; };
+  L.off_front_bm = take(4 * L.words * nb);
+  L.off_all_bm = take(4 * L.words * nb);
+  L.off_wprefix = take(4 * L.words * nb);
+  L.off_front = take(4 * L.fcap);
+  L.off_fb = take(4 * L.fcap);
+  L.off_sdeg = take(8 * L.fcap);
+  L.off_ssel = take(8 * L.fcap);
+  L.off_part = take(8 * (2 * kPersistentCTAs + 2));
+  L.off_froff = take(8 * (nb + 1));
+  L.off_pos = take(8 * nb);
+  L.off_hoppos = take(8 * nb);
+  L.off_scal = take(8 * 8);
+  L.bytes = o;
+  return L;
+}
+
+SampleWs carve(void* base, const WsLayout& L) {
+  char* p = static_cast<char*>(base);
+  SampleWs w;
+  w.bm_front = reinterpret_cast<uint32_t*>(p + L.off_front_bm);
+  w.bm_all = reinterpret_cast<uint32_t*>(p + L.off_all_bm);
+  w.wprefix = reinterpret_cast<int32_t*>(p + L.off_wprefix);
+  w.front = reinterpret_cast<int32_t*>(p + L.off_front);
+  w.fb = reinterpret_cast<int32_t*>(p + L.off_fb);
+  w.scan_deg = reinterpret_cast<int64_t*>(p + L.off_sdeg);
+  w.scan_sel = reinterpret_cast<int64_t*>(p + L.off_ssel);
+  w.part = reinterpret_cast<int64_t*>(p + L.off_part);
+  w.fr_off = reinterpret_cast<int64_t*>(p + L.off_froff);
+  w.pos = reinterpret_cast<int64_t*>(p + L.off_pos);
+  w.hop_pos = reinterpret_cast<int64_t*>(p + L.off_hoppos);
+  w.scal = reinterpret_cast<int64_t*>(p + L.off_scal);
+  return w;
+}
+
+__device__ __forceinline__ int find_segment(const int64_t* off, int n, int64_t i) {
+  // largest s with off[s] <= i (off non-decreasing, n+1 entries); n <= 64 so
+  // a branch-light binary search over cached loads is enough
+  int lo = 0, hi = n;  // invariant off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void set_status(int64_t* status, int64_t code) {
+  atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull, (unsigned long long)code);
+}
+
+// ---------------------------------------------------------------- seeds ----
+__global__ void mark_seeds_kernel(const int32_t* __restrict__ seeds, const int64_t* __restrict__ seed_off,
+                                  int32_t nb, int64_t total, int64_t num_nodes, int64_t words,
+                                  uint32_t* __restrict__ bm, int64_t* status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = seeds[i];
+    if (s < 0 || s >= num_nodes) { set_status(status, FGL_E_INVALID); continue; }
+    const int b = find_segment(seed_off, nb, i);
+    atomicOr(bm + b * words + (s >> 5), 1u << (s & 31));
+  }
+}
+
+// ------------------------------------------------------------ bitmap scan --
+// chunked over nwords words by kPersistentCTAs CTAs
+__global__ void bm_count_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t* part) {
+  __shared__ int64_t sm[33];
+  const int64_t chunk = ceil_div(nwords, gridDim.x);
+  const int64_t w0 = blockIdx.x * chunk, w1 = min(nwords, w0 + chunk);
+  int64_t c = 0;
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) c += __popc(bm[w]);
+  c = block_sum(c, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = c;
+}
+
+// exclusive scan of n partials in place (one CTA); total -> *total (and
+// optionally also to *total2)
+__global__ void scan_partials_kernel(int64_t* part, int n, int64_t* total, int64_t* total2) {
+  __shared__ int64_t sm[33];
+  int64_t carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int64_t v = i < n ? part[i] : 0, tot;
+    int64_t ex = block_excl_scan(v, sm, &tot);
+    if (i < n) part[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    *total = carry;
+    if (total2) *total2 = carry;
+  }
+}
+
+// Emit set bits of a batch-major bitmap in word order.  Optionally writes the
+// node IDs + batch of each bit, the per-batch start offsets, the per-word
+// global exclusive prefix, ORs the words into `or_into`, and clears them.
+__global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int64_t words,
+                                  const int64_t* __restrict__ part, int32_t* __restrict__ ids,
+                                  int32_t* __restrict__ batch_of, int64_t* __restrict__ batch_off,
+                                  int32_t* __restrict__ wprefix, uint32_t* __restrict__ or_into,
+                                  int clear, int64_t cap, int64_t* status) {
+  __shared__ int64_t sm[33];
+  const int64_t chunk = ceil_div(nwords, gridDim.x);
+  const int64_t w0 = blockIdx.x * chunk, w1 = min(nwords, w0 + chunk);
+  int64_t base = part[blockIdx.x];
+  for (int64_t t0 = w0; t0 < w1; t0 += blockDim.x) {
+    const int64_t w = t0 + threadIdx.x;
+    const uint32_t v = w < w1 ? bm[w] : 0u;
+    int64_t tot;
+    const int64_t ex = base + block_excl_scan<int64_t>(__popc(v), sm, &tot);
+    if (w < w1) {
+      const int64_t b = w / words;
+      if (batch_off && w == b * words) batch_off[b] = ex;
+      if (wprefix) wprefix[w] = (int32_t)ex;
+      if (v) {
+        if (or_into) or_into[w] |= v;
+        if (clear) bm[w] = 0u;
+        if (ids) {
+          if (ex + __popc(v) > cap) {
+            set_status(status, FGL_E_CAPACITY);
+          } else {
+            const int32_t node0 = (int32_t)((w - b * words) << 5);
+            uint32_t m = v;
+            int64_t o = ex;
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1;
+              ids[o] = node0 + bit;
+              if (batch_of) batch_of[o] = (int32_t)b;
+              ++o;
+            }
+          }
+        }
+      }
+    }
+    base += tot;
+  }
+}
+
+// ------------------------------------------------------------ degree scan --
+__device__ __forceinline__ void node_deg_sel(const int64_t* __restrict__ off, int32_t u, int fan,
+                                             int64_t& d, int64_t& s) {
+  d = __ldg(off + u + 1) - __ldg(off + u);
+  s = d < fan ? d : fan;
+}
+
+__global__ void deg_up_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ front,
+                              const int64_t* __restrict__ scal, int fan, int64_t* part) {
+  __shared__ int64_t sm[33];
+  const int64_t F = scal[kF];
+  const int64_t chunk = ceil_div(F, gridDim.x);
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(F, i0 + chunk);
+  int64_t cd = 0, cs = 0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    int64_t d, s;
+    node_deg_sel(off, front[i], fan, d, s);
+    cd += d;
+    cs += s;
+  }
+  cd = block_sum(cd, sm);
+  cs = block_sum(cs, sm);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = cd;
+    part[gridDim.x + 1 + blockIdx.x] = cs;
+  }
+}
+
+__global__ void deg_down_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ front,
+                                const int64_t* __restrict__ scal, int fan,
+                                const int64_t* __restrict__ part, int64_t* __restrict__ scan_deg,
+                                int64_t* __restrict__ scan_sel) {
+  __shared__ int64_t sm[33];
+  const int64_t F = scal[kF];
+  const int64_t chunk = ceil_div(F, gridDim.x);
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(F, i0 + chunk);
+  int64_t bd = part[blockIdx.x], bs = part[gridDim.x + 1 + blockIdx.x];
+  for (int64_t t0 = i0; t0 < i1; t0 += blockDim.x) {
+    const int64_t i = t0 + threadIdx.x;
+    int64_t d = 0, s = 0;
+    if (i < i1) node_deg_sel(off, front[i], fan, d, s);
+    int64_t td, ts;
+    const int64_t ed = block_excl_scan(d, sm, &td);
+    const int64_t es = block_excl_scan(s, sm, &ts);
+    if (i < i1) {
+      scan_deg[i] = bd + ed;
+      scan_sel[i] = bs + es;
+    }
+    bd += td;
+    bs += ts;
+  }
+}
+
+// per-batch bookkeeping of one hop (one thread per batch)
+__global__ void hop_book_kernel(SampleWs w, int32_t nb, int hop, int64_t* __restrict__ counts,
+                                int H, int64_t edge_cap) {
+  const int64_t F = w.scal[kF];
+  if (threadIdx.x == 0) {
+    w.scal[kHopEdgeBase] = w.scal[kEdgeBase];
+  }
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int64_t f0 = w.fr_off[b], f1 = w.fr_off[b + 1];
+    const int64_t c0 = f0 < F ? w.scan_deg[f0] : w.scal[kCandTot];
+    const int64_t c1 = f1 < F ? w.scan_deg[f1] : w.scal[kCandTot];
+    const int64_t s0 = f0 < F ? w.scan_sel[f0] : w.scal[kSelTot];
+    w.hop_pos[b] = w.pos[b] - c0;  // so that pos = hop_pos[b] + scan_deg[i]
+    w.pos[b] += c1 - c0;
+    counts[FGL_CNT_DRAWS(H, nb) + b] += c1 - c0;
+    counts[FGL_CNT_FRONT(H, nb) + hop * nb + b] = f1 - f0;
+    counts[hop * nb + b] = w.scal[kEdgeBase] + s0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    w.scal[kEdgeBase] += w.scal[kSelTot];
+    counts[(hop + 1) * nb] = w.scal[kEdgeBase];
+    if (w.scal[kEdgeBase] > edge_cap) {  // caller's edge buffer too small: emit nothing
+      set_status(counts + FGL_CNT_STATUS(H, nb), FGL_E_CAPACITY);
+      w.scal[kF] = 0;
+    }
+  }
+}
+
+// --------------------------------------------------------------- select ----
+__device__ __forceinline__ bool key_less(uint64_t ak, uint32_t aj, uint64_t bk, uint32_t bj) {
+  return ak < bk || (ak == bk && aj < bj);
+}
+
+// Warp-distributed sorted list of up to 32*K (key, slot) pairs; entry
+// r = k*32 + lane lives in lane `lane`, register k.
+template <int K>
+struct TopList {
+  uint64_t key[K];
+  uint32_t slot[K];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < K; ++k) { key[k] = ~0ull; slot[k] = 0xffffffffu; }
+  }
+  __device__ __forceinline__ void entry(int r, uint64_t& k_out, uint32_t& s_out) const {
+    const int kk = r >> 5, ln = r & 31;
+    uint64_t kv = 0; uint32_t sv = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t a = __shfl_sync(0xffffffffu, key[k], ln);
+      const uint32_t b = __shfl_sync(0xffffffffu, slot[k], ln);
+      if (k == kk) { kv = a; sv = b; }
+    }
+    k_out = kv; s_out = sv;
+  }
+  // insert (ck, cs) keeping the first `f` entries sorted; warp-uniform call
+  __device__ __forceinline__ void insert(uint64_t ck, uint32_t cs, int f) {
+    int pos = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      pos += __popc(__ballot_sync(0xffffffffu, key_less(key[k], slot[k], ck, cs)));
+    if (pos >= f) return;
+    const int lane = lane_id();
+    uint64_t up_k[K]; uint32_t up_s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      up_k[k] = __shfl_up_sync(0xffffffffu, key[k], 1);
+      up_s[k] = __shfl_up_sync(0xffffffffu, slot[k], 1);
+    }
+    uint64_t carry_k[K]; uint32_t carry_s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      carry_k[k] = __shfl_sync(0xffffffffu, key[k], 31);
+      carry_s[k] = __shfl_sync(0xffffffffu, slot[k], 31);
+    }
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      const int r = k * 32 + lane;
+      uint64_t pk = up_k[k]; uint32_t ps = up_s[k];
+      if (lane == 0) {
+        if (k > 0) { pk = carry_k[k - 1]; ps = carry_s[k - 1]; }
+      }
+      if (r == pos) { key[k] = ck; slot[k] = cs; }
+      else if (r > pos) { key[k] = pk; slot[k] = ps; }
+    }
+  }
+};
+
+struct SelectArgs {
+  const int64_t* off;
+  const int32_t* col;
+  const float* ew;
+  const int32_t* front;
+  const int32_t* fb;
+  const int64_t* scan_deg;
+  const int64_t* scan_sel;
+  const int64_t* fr_off;
+  const int64_t* hop_pos;
+  const uint64_t* keys;
+  const int64_t* scal;
+  uint32_t* bm_front;
+  int64_t words;
+  int32_t* tgt;
+  int32_t* src;
+  float* wgt;
+  int fan;
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
+  const int lane = lane_id();
+  const int64_t F = a.scal[kF];
+  const int64_t ebase = a.scal[kHopEdgeBase];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int fan = a.fan;
+  for (int64_t i = gw; i < F; i += nwarps) {
+    const int32_t u = a.front[i];
+    const int64_t e0 = __ldg(a.off + u);
+    const int64_t d = __ldg(a.off + u + 1) - e0;
+    if (d == 0) continue;
+    const int b = a.fb[i];
+    const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+    const int64_t p0 = a.hop_pos[b] + a.scan_deg[i];
+    const int64_t p1 = p0 + d;  // exclusive
+    const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
+    TopList<K> list;
+    list.init();
+    uint64_t thr_k = ~0ull; uint32_t thr_s = 0xffffffffu;  // entry f-1 (inf until full)
+    for (int64_t bb = blk0; bb <= blk_last; bb += 32) {
+      const int64_t blk = bb + lane;
+      uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+      const bool valid = blk <= blk_last;
+      if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t p = 4 * blk + q;
+        const bool in = valid && p >= p0 && p < p1;
+        const uint64_t key = w[q] >> 11;
+        const uint32_t slot = (uint32_t)(p - p0);
+        unsigned m = __ballot_sync(0xffffffffu, in && key_less(key, slot, thr_k, thr_s));
+        while (m) {
+          const int srcl = __ffs(m) - 1;
+          m &= m - 1;
+          const uint64_t ck = __shfl_sync(0xffffffffu, key, srcl);
+          const uint32_t cs = __shfl_sync(0xffffffffu, slot, srcl);
+          if (key_less(ck, cs, thr_k, thr_s)) {
+            list.insert(ck, cs, fan);
+            list.entry(fan - 1, thr_k, thr_s);
+          }
+        }
+      }
+    }
+    // emit min(d, fan) entries in ascending key order
+    const int64_t nsel = d < fan ? d : fan;
+    const int64_t obase = ebase + a.scan_sel[i];
+    uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int r = k * 32 + lane;
+      if (r < nsel) {
+        const int64_t e = e0 + list.slot[k];
+        const int32_t s = __ldg(a.col + e);
+        a.tgt[obase + r] = u;
+        a.src[obase + r] = s;
+        a.wgt[obase + r] = a.ew ? __ldg(a.ew + e) : 1.0f;
+        atomicOr(bm + (s >> 5), 1u << (s & 31));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ translate ----
+__device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
+                                           const int32_t* __restrict__ wprefix, int64_t base_word,
+                                           int64_t uniq_base, int32_t g) {
+  const int64_t w = base_word + (g >> 5);
+  const uint32_t below = (1u << (g & 31)) - 1u;
+  return (int32_t)(wprefix[w] + __popc(bm[w] & below) - uniq_base);
+}
+
+__global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
+                                 const int64_t* __restrict__ counts, int hn, int32_t nb,
+                                 const uint32_t* __restrict__ bm_all,
+                                 const int32_t* __restrict__ wprefix, int64_t words,
+                                 const int64_t* __restrict__ uniq_off, int32_t* __restrict__ lt,
+                                 int32_t* __restrict__ ls) {
+  const int64_t total = counts[hn];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int seg = find_segment(counts, hn, e);
+    const int b = seg % nb;
+    const int64_t bw = (int64_t)b * words, ub = uniq_off[b];
+    lt[e] = bm_rank(bm_all, wprefix, bw, ub, tgt[e]);
+    ls[e] = bm_rank(bm_all, wprefix, bw, ub, src[e]);
+  }
+}
+
+__global__ void translate_seeds_kernel(const int32_t* __restrict__ seeds,
+                                       const int64_t* __restrict__ seed_off, int32_t nb,
+                                       int64_t total, const uint32_t* __restrict__ bm_all,
+                                       const int32_t* __restrict__ wprefix, int64_t words,
+                                       const int64_t* __restrict__ uniq_off,
+                                       int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = find_segment(seed_off, nb, i);
+    const int32_t s = seeds[i];
+    out[i] = bm_rank(bm_all, wprefix, (int64_t)b * words, uniq_off[b], s);
+  }
+}
+
+int select_grid(int K) {
+  static int cache[9] = {0};
+  if (cache[K]) return cache[K];
+  int per_sm = 0;
+  cudaError_t e = cudaSuccess;
+  switch (K) {
+    case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<1>, 256, 0); break;
+    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<2>, 256, 0); break;
+    case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<4>, 256, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<8>, 256, 0); break;
+  }
+  if (e != cudaSuccess || per_sm < 1) per_sm = 2;
+  cache[K] = per_sm * kNumSMs;
+  return cache[K];
+}
+
+}  // namespace
+}  // namespace fgl
+
+using namespace fgl;
+
+extern "C" {
+
+int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t nb,
+                      const int32_t* fanouts, int32_t H, int64_t* out) {
+  if (num_nodes < 1 || nb < 1 || H < 1 || H > FGL_MAX_HOPS || !batch_sizes || !fanouts || !out) {
+    set_error("fgl_sample_bounds: bad arguments");
+    return FGL_E_INVALID;
+  }
+  int64_t edges = 0, uniq = 0;
+  std::vector<int64_t> hop_front(H + 1, 0);
+  for (int b = 0; b < nb; ++b) {
+    int64_t f = std::min<int64_t>(batch_sizes[b], num_nodes);
+    int64_t u = batch_sizes[b];
+    hop_front[0] += f;
+    for (int h = 0; h < H; ++h) {
+      const int64_t e = f * (int64_t)fanouts[h];
+      edges += e;
+      u += e;
+      f = std::min<int64_t>(num_nodes, e);
+      hop_front[h + 1] += f;
+    }
+    uniq += std::min<int64_t>(num_nodes, u);
+  }
+  int64_t fcap = *std::max_element(hop_front.begin(), hop_front.end());
+  out[0] = std::max<int64_t>(edges, 1);
+  out[1] = std::max<int64_t>(fcap, 1);
+  out[2] = std::max<int64_t>(uniq, 1);
+  out[3] = ws_layout(num_nodes, nb, out[1]).bytes;
+  out[4] = FGL_CNT_LEN(H, nb);
+  return FGL_OK;
+}
+
+int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* seed_off,
+                      int64_t total_seeds, int32_t nb, const uint64_t* keys,
+                      const int32_t* fanouts, int32_t H, int32_t* tgt, int32_t* src, float* wgt,
+                      int64_t edge_cap, int32_t* local_tgt, int32_t* local_src,
+                      int32_t* unique_nodes, int64_t unique_cap, int32_t* seed_locals,
+                      int64_t* counts, void* ws, int64_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!g || !seeds || !seed_off || !keys || !fanouts || !tgt || !src || !wgt || !unique_nodes ||
+      !counts || !ws || nb < 1 || H < 1 || H > FGL_MAX_HOPS || total_seeds < 1) {
+    set_error("fgl_sample_window: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (g->num_nodes < 1 || g->num_nodes >= (1ll << 31) || (int64_t)nb * g->num_nodes >= (1ll << 31)) {
+    set_error("fgl_sample_window: num_nodes * num_batches must stay below 2^31");
+    return FGL_E_UNSUPPORTED;
+  }
+  for (int h = 0; h < H; ++h) {
+    if (fanouts[h] < 1) { set_error("every fanout must be >= 1"); return FGL_E_INVALID; }
+    if (fanouts[h] > kMaxFanout) {
+      set_error("fanout %d exceeds the supported maximum %d", fanouts[h], kMaxFanout);
+      return FGL_E_UNSUPPORTED;
+    }
+  }
+  // capacities: the caller sizes buffers with fgl_sample_bounds from the host batch sizes;
+  // the frontier capacity is the largest one whose workspace layout fits ws_bytes
+  int64_t lo = 1, hi = std::max<int64_t>(1, (int64_t)nb * g->num_nodes);
+  if (ws_layout(g->num_nodes, nb, 1).bytes > ws_bytes) {
+    set_error("sample workspace too small (%lld bytes)", (long long)ws_bytes);
+    return FGL_E_CAPACITY;
+  }
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo + 1) / 2;
+    if (ws_layout(g->num_nodes, nb, mid).bytes <= ws_bytes) lo = mid; else hi = mid - 1;
+  }
+  const WsLayout Lw = ws_layout(g->num_nodes, nb, lo);
+  SampleWs w = carve(ws, Lw);
+  const int64_t words = Lw.words;
+  const int64_t nwords = words * nb;
+  const int G = kPersistentCTAs;
+  const int hn = H * nb;
+  int64_t* status = counts + FGL_CNT_STATUS(H, nb);
+  int64_t* uniq_off = counts + FGL_CNT_UNIQ(H, nb);
+
+  FGL_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * FGL_CNT_LEN(H, nb), stream));
+  FGL_CUDA(cudaMemsetAsync(w.bm_front, 0, 4 * nwords, stream));
+  FGL_CUDA(cudaMemsetAsync(w.bm_all, 0, 4 * nwords, stream));
+  FGL_CUDA(cudaMemsetAsync(w.pos, 0, 8 * nb, stream));
+  FGL_CUDA(cudaMemsetAsync(w.scal, 0, 8 * 8, stream));
+
+  // frontier 0 = sorted unique seeds per batch
+  mark_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0, stream>>>(
+      seeds, seed_off, nb, total_seeds, g->num_nodes, words, w.bm_front, status);
+  FGL_LAUNCH_CHECK("mark_seeds_kernel");
+  auto compact_front = [&](bool write_ids) -> int {
+    bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
+    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, w.fr_off + nb);
+    bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(
+        w.bm_front, nwords, words, w.part, write_ids ? w.front : nullptr,
+        write_ids ? w.fb : nullptr, w.fr_off, nullptr, w.bm_all, 1, Lw.fcap, status);
+    FGL_LAUNCH_CHECK("frontier compaction");
+    return FGL_OK;
+  };
+  int rc = compact_front(true);
+  if (rc) return rc;
+
+  const int sel_grid_k1 = select_grid(1);
+  for (int h = 0; h < H; ++h) {
+    const int fan = fanouts[h];
+    deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, w.front, w.scal, fan, w.part);
+    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kCandTot, nullptr);
+    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part + G + 1, G, w.scal + kSelTot, nullptr);
+    deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, w.front, w.scal, fan, w.part,
+                                                    w.scan_deg, w.scan_sel);
+    hop_book_kernel<<<1, 64, 0, stream>>>(w, nb, h, counts, H, edge_cap);
+    FGL_LAUNCH_CHECK("degree scan");
+    SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, w.front, w.fb,
+                 w.scan_deg, w.scan_sel, w.fr_off, w.hop_pos, keys, w.scal,
+                 w.bm_front, words, tgt, src, wgt, fan};
+    if (fan <= 32) select_kernel<1><<<sel_grid_k1, 256, 0, stream>>>(a);
+    else if (fan <= 64) select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
+    else if (fan <= 128) select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
+    else select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
+    FGL_LAUNCH_CHECK("select_kernel");
+    rc = compact_front(h + 1 < H);
+    if (rc) return rc;
+  }
+
+  // unique nodes = compaction of the `all` bitmaps; keeps per-word prefixes for ranks
+  bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
+  scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kUniqTot, uniq_off + nb);
+  bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part, unique_nodes,
+                                                    nullptr, uniq_off, w.wprefix, nullptr, 0,
+                                                    unique_cap, status);
+  FGL_LAUNCH_CHECK("unique compaction");
+  if (local_tgt && local_src) {
+    translate_kernel<<<4 * G, 256, 0, stream>>>(tgt, src, counts, hn, nb, w.bm_all, w.wprefix,
+                                                words, uniq_off, local_tgt, local_src);
+    FGL_LAUNCH_CHECK("translate_kernel");
+  }
+  if (seed_locals) {
+    translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0,
+                             stream>>>(seeds, seed_off, nb, total_seeds, w.bm_all, w.wprefix, words,
+                                       uniq_off, seed_locals);
+    FGL_LAUNCH_CHECK("translate_seeds_kernel");
+  }
+  return FGL_OK;
+}
+
+}  // extern "C"

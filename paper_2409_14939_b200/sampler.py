@@ -1,0 +1,273 @@
+"""k-hop sampler: drop-in for ``minigl.sampler`` backed by the Fused-Map CUDA
+window sampler (csrc/sampler.cu via fgl_sample_window).
+
+``sample_khop(g, seeds, fanouts, seed)`` keeps the reference signature and
+returns the reference's ``SubgraphBatch`` layout (uint64 global IDs, f32
+weights), bit-exact with sampler.py:120-139.  :class:`WindowSampler` is the
+device-level API the trainer uses: a whole window of batches per call, all
+results left in HBM (int32 IDs) with per-batch offsets.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+from .graph import device_graph
+
+__all__ = ["Fanouts", "SubgraphBatch", "sample_khop", "make_epoch_batches", "philox_key",
+           "derive_seed", "WindowSampler", "DeviceWindow"]
+
+
+def derive_seed(base: int, *parts: int) -> int:
+    """Child seed (trainer.py:40-42): first word of SeedSequence((base, *parts))."""
+    return int(np.random.SeedSequence((base, *parts)).generate_state(1)[0])
+
+
+def philox_key(seed: int) -> tuple[int, int]:
+    """Key of np.random.Philox(seed) = SeedSequence(seed).generate_state(2)."""
+    k = np.random.SeedSequence(int(seed)).generate_state(2, np.uint64)
+    return int(k[0]), int(k[1])
+
+
+@dataclass
+class Fanouts:
+    """Per-hop neighbor sample counts; ``counts[0]`` expands the seeds (sampler.py:27-44)."""
+
+    counts: tuple[int, ...]
+
+    def __init__(self, counts):
+        object.__setattr__(self, "counts", tuple(int(c) for c in counts))
+        if not self.counts:
+            raise ValidationError("fanouts must not be empty")
+        if any(c < 1 for c in self.counts):
+            raise ValidationError("every fanout must be >= 1")
+
+    def __len__(self):
+        return len(self.counts)
+
+    def __iter__(self):
+        return iter(self.counts)
+
+
+@dataclass
+class SubgraphBatch:
+    """Sampled mini-batch, field-compatible with sampler.py:47-68."""
+
+    seeds: np.ndarray
+    layers: list
+    unique_nodes: np.ndarray
+    local_layers: list = field(default_factory=list)
+    num_local: int = 0
+
+    @property
+    def num_unique(self) -> int:
+        return len(self.unique_nodes)
+
+    def num_sampled_edges(self) -> int:
+        return sum(len(t) for t, _, _ in self.layers)
+
+
+def _validate_seeds(num_nodes: int, seeds) -> np.ndarray:
+    seeds = np.asarray(seeds, dtype=np.uint64)
+    if seeds.size == 0:
+        raise ValidationError("seeds must not be empty")
+    if seeds.max() >= np.uint64(num_nodes):
+        raise ValidationError("seed id out of range")
+    return seeds
+
+
+@dataclass
+class DeviceWindow:
+    """Results of one window in HBM.  ``counts`` is the FGL_CNT_* vector."""
+
+    num_batches: int
+    num_hops: int
+    tgt: object
+    src: object
+    wgt: object
+    local_tgt: object
+    local_src: object
+    unique: object
+    seed_locals: object
+    seeds: object
+    seed_off_host: np.ndarray
+    counts: object
+    sampler: "WindowSampler"
+    _host_counts: np.ndarray | None = None
+
+    def host_counts(self) -> np.ndarray:
+        """One device->host read of the counts vector (the batch's only sync)."""
+        if self._host_counts is None:
+            self._host_counts = self.counts.cpu().numpy()
+            H, nb = self.num_hops, self.num_batches
+            _lib.status_error(int(self._host_counts[H * nb + 1 + nb + 1 + nb + H * nb]),
+                              "fgl_sample_window")
+        return self._host_counts
+
+    def edge_range(self, hop: int, b: int):
+        c = self.host_counts()
+        k = hop * self.num_batches + b
+        return int(c[k]), int(c[k + 1])
+
+    def unique_range(self, b: int):
+        c = self.host_counts()
+        u0 = self.num_hops * self.num_batches + 1
+        return int(c[u0 + b]), int(c[u0 + b + 1])
+
+    def draws(self, b: int) -> int:
+        c = self.host_counts()
+        d0 = self.num_hops * self.num_batches + 1 + self.num_batches + 1
+        return int(c[d0 + b])
+
+    def total_edges(self) -> int:
+        return int(self.host_counts()[self.num_hops * self.num_batches])
+
+    def to_batch(self, b: int) -> SubgraphBatch:
+        """Host SubgraphBatch of batch b in the reference's dtypes."""
+        layers, local = [], []
+        for h in range(self.num_hops):
+            e0, e1 = self.edge_range(h, b)
+            t = self.tgt[e0:e1].cpu().numpy().astype(np.uint64)
+            s = self.src[e0:e1].cpu().numpy().astype(np.uint64)
+            w = self.wgt[e0:e1].cpu().numpy()
+            layers.append((t, s, w))
+            if self.local_tgt is not None:
+                local.append((self.local_tgt[e0:e1].cpu().numpy().astype(np.int64),
+                              self.local_src[e0:e1].cpu().numpy().astype(np.int64), w))
+        u0, u1 = self.unique_range(b)
+        s0, s1 = int(self.seed_off_host[b]), int(self.seed_off_host[b + 1])
+        uniq = self.unique[u0:u1].cpu().numpy().astype(np.uint64)
+        seeds = self.seeds[s0:s1].cpu().numpy().astype(np.uint64)
+        return SubgraphBatch(seeds=seeds, layers=layers, unique_nodes=uniq, local_layers=local,
+                             num_local=len(uniq) if local else 0)
+
+
+class WindowSampler:
+    """Device sampler for windows of up to ``max_batches`` batches of up to
+    ``max_batch_size`` seeds.  Buffers are allocated once (worst-case bounds
+    from fgl_sample_bounds) and reused; results of a call stay valid until the
+    next call."""
+
+    def __init__(self, dgraph, fanouts, max_batch_size: int, max_batches: int = 1,
+                 local_ids: bool = True, device="cuda"):
+        import torch
+        self.torch = torch
+        self.g = dgraph
+        self.fanouts = Fanouts(fanouts)
+        self.H = len(self.fanouts)
+        self.max_nb = int(max_batches)
+        self.max_bs = int(max_batch_size)
+        self.device = device
+        out = (ctypes.c_int64 * 5)()
+        sizes = _lib.i64_array([self.max_bs] * self.max_nb)
+        _lib.call("fgl_sample_bounds", self.g.num_nodes, sizes, self.max_nb,
+                  _lib.i32_array(self.fanouts.counts), self.H, out)
+        self.edge_cap, self.fcap, self.uniq_cap, self.ws_bytes, self.counts_len = (int(x) for x in out)
+        e = self.edge_cap
+        i32 = dict(dtype=torch.int32, device=device)
+        self.tgt = torch.empty(e, **i32)
+        self.src = torch.empty(e, **i32)
+        self.wgt = torch.empty(e, dtype=torch.float32, device=device)
+        self.local_tgt = torch.empty(e, **i32) if local_ids else None
+        self.local_src = torch.empty(e, **i32) if local_ids else None
+        self.unique = torch.empty(self.uniq_cap, **i32)
+        self.seed_locals = torch.empty(self.max_nb * self.max_bs, **i32)
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.seeds_dev = torch.empty(self.max_nb * self.max_bs, **i32)
+        self.seed_off = torch.empty(self.max_nb + 1, dtype=torch.int64, device=device)
+        self.keys = torch.empty(2 * self.max_nb, dtype=torch.int64, device=device)
+        self.counts = torch.empty(self.counts_len, dtype=torch.int64, device=device)
+        self._fan = _lib.i32_array(self.fanouts.counts)
+
+    def counts_len_for(self, nb):
+        return (self.H * nb + 1) + (nb + 1) + nb + self.H * nb + 1
+
+    def stage(self, seed_lists, seeds_for_rng, pinned=None):
+        """Host->device copy of a window's seeds, offsets and Philox keys
+        (non-blocking from pinned memory when ``pinned`` buffers are given)."""
+        torch = self.torch
+        nb = len(seed_lists)
+        if nb < 1 or nb > self.max_nb:
+            raise ValidationError(f"window of {nb} batches exceeds max_batches={self.max_nb}")
+        sizes = [len(s) for s in seed_lists]
+        if max(sizes) > self.max_bs:
+            raise ValidationError("batch exceeds max_batch_size")
+        off = np.zeros(nb + 1, dtype=np.int64)
+        np.cumsum(sizes, out=off[1:])
+        flat = np.concatenate([np.asarray(s) for s in seed_lists]).astype(np.int64)
+        if flat.size == 0 or min(sizes) == 0:
+            raise ValidationError("seeds must not be empty")
+        if flat.max() >= self.g.num_nodes or flat.min() < 0:
+            raise ValidationError("seed id out of range")
+        keys = np.array([philox_key(s) for s in seeds_for_rng], dtype=np.uint64).reshape(-1)
+        n = int(off[-1])
+        self.seeds_dev[:n].copy_(torch.from_numpy(flat.astype(np.int32)), non_blocking=True)
+        self.seed_off[: nb + 1].copy_(torch.from_numpy(off), non_blocking=True)
+        self.keys[: 2 * nb].copy_(torch.from_numpy(keys.view(np.int64)), non_blocking=True)
+        return nb, off
+
+    def run(self, nb: int, seed_off_host: np.ndarray, stream=None) -> DeviceWindow:
+        """Launch the window sampler on staged inputs (asynchronous)."""
+        torch = self.torch
+        st = stream if stream is not None else torch.cuda.current_stream()
+        total = int(seed_off_host[-1])
+        lt = self.local_tgt.data_ptr() if self.local_tgt is not None else None
+        ls = self.local_src.data_ptr() if self.local_src is not None else None
+        _lib.call("fgl_sample_window", self.g.struct, self.seeds_dev.data_ptr(),
+                  self.seed_off.data_ptr(), total, nb, self.keys.data_ptr(), self._fan, self.H,
+                  self.tgt.data_ptr(), self.src.data_ptr(), self.wgt.data_ptr(), self.edge_cap,
+                  lt, ls, self.unique.data_ptr(), self.uniq_cap, self.seed_locals.data_ptr(),
+                  self.counts.data_ptr(), self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+        return DeviceWindow(nb, self.H, self.tgt, self.src, self.wgt, self.local_tgt,
+                            self.local_src, self.unique, self.seed_locals, self.seeds_dev,
+                            seed_off_host, self.counts, self)
+
+    def sample(self, seed_lists, seeds_for_rng) -> DeviceWindow:
+        nb, off = self.stage(seed_lists, seeds_for_rng)
+        return self.run(nb, off)
+
+
+_samplers: dict = {}
+
+
+def _sampler_for(dg, fanouts, bs):
+    key = (id(dg), tuple(fanouts))
+    s = _samplers.get(key)
+    if s is None or s.max_bs < bs or s.g is not dg:
+        s = WindowSampler(dg, fanouts, max(bs, 1), 1)
+        _samplers[key] = s
+    return s
+
+
+def sample_khop(g, seeds, fanouts, seed: int) -> SubgraphBatch:
+    """K-hop uniform neighbor sampling; hop ``l`` uses ``fanouts.counts[l]``.
+
+    Drop-in for sampler.py:120-139 (bit-exact, Philox(seed) stream)."""
+    seeds = _validate_seeds(g.num_nodes, seeds)
+    if not isinstance(fanouts, Fanouts):
+        fanouts = Fanouts(fanouts)
+    dg = device_graph(g)
+    smp = _sampler_for(dg, fanouts.counts, len(seeds))
+    win = smp.sample([seeds.astype(np.int64)], [seed])
+    b = win.to_batch(0)
+    b.seeds = seeds
+    b.local_layers = []
+    b.num_local = 0
+    return b
+
+
+def make_epoch_batches(g, train_ids, batch_size: int, shuffle_seed: int):
+    """Seeded shuffle of the training IDs split into batches (sampler.py:189-198).
+    Host-side (numpy Philox permutation); produces the seeds fed to the GPU."""
+    if batch_size < 1:
+        raise ValidationError("batch_size must be >= 1")
+    train_ids = np.asarray(train_ids, dtype=np.uint64)
+    if train_ids.size and train_ids.max() >= np.uint64(g.num_nodes):
+        raise ValidationError("train id out of range")
+    perm = np.random.Generator(np.random.Philox(shuffle_seed)).permutation(train_ids)
+    return [perm[i : i + batch_size] for i in range(0, len(perm), batch_size)]
