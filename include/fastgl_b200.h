@@ -55,10 +55,35 @@ typedef struct fgl_graph {
 /* ------------------------------------------------------------- sampler ---- */
 /* Worst-case sizes for a window of `num_batches` batches with the given seed
  * counts (host) and fanouts (host): out[0] = edge capacity (all hops, all
- * batches), out[1] = concatenated frontier capacity of one hop, out[2] =
- * unique-node capacity, out[3] = workspace bytes, out[4] = counts length. */
+ * batches), out[1] = frontier stride (capacity of one hop's concatenated
+ * frontier), out[2] = unique-node capacity, out[3] = workspace bytes,
+ * out[4] = counts length. */
 int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t num_batches,
                       const int32_t* fanouts, int32_t num_hops, int64_t* out);
+
+/* Output buffers of fgl_sample_window (all DEVICE, caller-owned).  Edge arrays
+ * are hop-major, batch-minor.  Optional pointers may be NULL. */
+typedef struct fgl_sample_out {
+  int32_t* tgt;          /* global target IDs (= the frontier node expanded) */
+  int32_t* src;          /* global source IDs (the sampled neighbour) */
+  float* wgt;            /* graph edge weight, or 1.0 */
+  int64_t edge_cap;
+  int32_t* tgt_row;      /* optional: window row of tgt = uniq_off[b] + rank in
+                            batch b's sorted unique_nodes (trainer local ID) */
+  int32_t* src_row;      /* optional: window row of src */
+  int32_t* tgt_front;    /* optional: index of tgt in hop h's frontier list */
+  int32_t* src_front;    /* optional: index of src in hop h+1's frontier list;
+                            for the last hop: window row of src */
+  int32_t* unique_nodes; /* batch-major, each batch sorted ascending */
+  int64_t unique_cap;
+  int32_t* frontier;     /* frontier lists: hop h at frontier + h*frontier_stride,
+                            batch-major, each sorted (required if tgt_front or
+                            src_front is requested) */
+  int64_t frontier_stride;
+  int32_t* seed_rows;    /* optional: window rows of the seeds */
+  int32_t* seed_front;   /* optional: index of each seed in hop 0's frontier */
+  int64_t* counts;       /* int64[counts_len], layout FGL_CNT_* below */
+} fgl_sample_out;
 
 /*
  * Fused-Map k-hop sampling of a window of batches + global->local remap.
@@ -72,34 +97,26 @@ int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t num
  *  seed_off    device int64[num_batches+1]
  *  keys        device uint64[2*num_batches]
  *  fanouts     host int32[num_hops]; fanouts[0] expands the seeds; 1..256
- *  tgt/src/wgt device outputs, capacity edge_cap: hop-major, batch-minor
- *  local_tgt/local_src  optional (NULL) device int32 local IDs of tgt/src
- *  unique_nodes device int32, capacity unique_cap, batch-major, each sorted
- *  seed_locals optional (NULL) device int32 local IDs of the seeds
- *  counts      device int64[counts_len] (see FGL_CNT_* below)
  *  ws          device workspace of fgl_sample_bounds()[3] bytes
  * Per-batch node bitmaps stay valid in `ws` after the call (used by
- * fgl_match_counts / fgl_gather_delta) until the next call on the same ws.
+ * fgl_match_counts) until the next call on the same ws.
  */
 int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* seed_off,
                       int64_t total_seeds, int32_t num_batches, const uint64_t* keys,
-                      const int32_t* fanouts, int32_t num_hops,
-                      int32_t* tgt, int32_t* src, float* wgt, int64_t edge_cap,
-                      int32_t* local_tgt, int32_t* local_src,
-                      int32_t* unique_nodes, int64_t unique_cap, int32_t* seed_locals,
-                      int64_t* counts, void* ws, int64_t ws_bytes, void* stream);
+                      const int32_t* fanouts, int32_t num_hops, const fgl_sample_out* out,
+                      void* ws, int64_t ws_bytes, void* stream);
 
 /* counts layout for H hops, nb batches:
- *   [0, H*nb]              edge offsets: hop h batch b spans
- *                          [counts[h*nb+b], counts[h*nb+b+1])
- *   [U0, U0+nb]            unique offsets, U0 = H*nb+1
- *   [D0, D0+nb)            Philox draws (candidates) per batch, D0 = U0+nb+1
- *   [F0, F0+H*nb)          frontier size per (hop, batch), F0 = D0+nb
- *   [S0]                   status (0 ok), S0 = F0+H*nb                        */
-#define FGL_CNT_UNIQ(H, nb) ((H) * (nb) + 1)
+ *   [0, H*nb]            edge offsets: hop h batch b spans [c[h*nb+b], c[h*nb+b+1])
+ *   [FO, FO+H*(nb+1))    frontier offsets, relative to hop h's list:
+ *                        hop h batch b spans [c[FO+h*(nb+1)+b], c[FO+h*(nb+1)+b+1])
+ *   [U0, U0+nb]          unique offsets (window rows)
+ *   [D0, D0+nb)          Philox draws (candidates) per batch
+ *   [S0]                 status (0 ok)                                          */
+#define FGL_CNT_FRONT(H, nb) ((H) * (nb) + 1)
+#define FGL_CNT_UNIQ(H, nb) (FGL_CNT_FRONT(H, nb) + (H) * ((nb) + 1))
 #define FGL_CNT_DRAWS(H, nb) (FGL_CNT_UNIQ(H, nb) + (nb) + 1)
-#define FGL_CNT_FRONT(H, nb) (FGL_CNT_DRAWS(H, nb) + (nb))
-#define FGL_CNT_STATUS(H, nb) (FGL_CNT_FRONT(H, nb) + (H) * (nb))
+#define FGL_CNT_STATUS(H, nb) (FGL_CNT_DRAWS(H, nb) + (nb))
 #define FGL_CNT_LEN(H, nb) (FGL_CNT_STATUS(H, nb) + 1)
 
 /* Philox4x64-10 stream words at absolute positions [start, start+count) for
@@ -109,6 +126,100 @@ int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uin
                      void* stream);
 /* Draws `count` Philox blocks and reduces them to one word (ALU roofline probe). */
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream);
+
+/* ------------------------------------------------------------- prepare ---- */
+/* indptr[r] = base + (first e with rows[e] >= r), r in [0, num_rows]; `rows`
+ * non-decreasing.  The forward CSR of a sampled hop (targets arrive grouped in
+ * ascending order, so compute.edges_to_csr's stable argsort is the identity,
+ * compute.py:219-230). */
+int fgl_csr_offsets_sorted(const int32_t* rows, int64_t nnz, int64_t num_rows, int64_t base,
+                           int64_t* indptr, void* stream);
+
+/* Stable counting sort of `keys` (values in [0, num_keys)): indptr[num_keys+1]
+ * and perm[nnz] = element indices grouped by key, ascending index within a
+ * key (np.argsort(kind="stable"), compute.py:224).  counts_out optional
+ * (int32[num_keys] histogram).  ws: fgl_stable_group_ws_bytes(num_keys). */
+int64_t fgl_stable_group_ws_bytes(int64_t num_keys);
+int fgl_stable_group(const int32_t* keys, int64_t nnz, int64_t num_keys, int64_t* indptr,
+                     int32_t* perm, int32_t* counts_out, void* ws, int64_t ws_bytes, void* stream);
+/* a_out[p] = a[perm[p]], b_out[p] = b[perm[p]] (either pair may be NULL). */
+int fgl_gather_i32_f32(const int32_t* perm, int64_t n, const int32_t* a, const float* b,
+                       int32_t* a_out, float* b_out, void* stream);
+
+/* One model layer's block CSR (trainer._prepare_batch, trainer.py:165-179):
+ * lt (non-decreasing, in [0,num_rows)) / ls (in [0,num_cols)) are the hop's
+ * edge endpoints in the layer's row / column index spaces.  Outputs:
+ * indptr[num_rows+1], w[nnz] (GCN 1/sqrt(indeg*outdeg) in fp64 -> f32,
+ * trainer.py:156-162, or 1.0 when arch_gcn == 0), and the stable transpose
+ * t_indptr[num_cols+1], t_col[nnz] (= lt), t_w[nnz] (compute.py:233-239). */
+int64_t fgl_prepare_layer_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_cols);
+int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
+                      int64_t num_cols, int32_t arch_gcn, int64_t* indptr, float* w,
+                      int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
+                      void* stream);
+
+/* ------------------------------------------------------------- compute ---- */
+/* Memory-Aware CSR aggregation (compute.py:115-195):
+ * Y[r] = sum_{e in [indptr[r], indptr[r+1])} w[e] * X[col[e] - col_base]
+ * (+ self_x[r] when self_x != NULL, the GIN self term), fp32, CSR order, no
+ * FMA -- bit-identical to the reference.  Leading dims multiples of 4,
+ * feature pointers 16-byte aligned, d <= 1024. */
+int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
+             int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
+             float* Y, int64_t ldy, int32_t d, void* stream);
+
+/* Z = act(H @ W + b), W row-major [din, dout] (compute.py:198-216). */
+int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
+                  const float* b, int32_t dout, float* Z, int64_t ldz, int32_t relu, void* stream);
+
+/* dZ = dX * (Xout > 0) (Xout NULL: no mask), dW = H^T dZ, db = colsum(dZ),
+ * dH = dZ W^T (dH may be NULL) -- trainer.py:212-228.  Deterministic. */
+int64_t fgl_dense_bwd_ws_bytes(int32_t din, int32_t dout);
+int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
+                  int32_t dout, const float* dX, int64_t lddx, const float* Xout, int64_t ldxo,
+                  float* dW, float* db, float* dH, int64_t lddh, void* ws, int64_t ws_bytes,
+                  void* stream);
+
+/* fp64 softmax cross entropy over the B seed rows of logits (trainer.py:198-209):
+ * row r_i = rows[i] - row_base, label y_i = labels[seed_ids[i]] (or labels[i]
+ * when seed_ids is NULL); dlogits[r_i] = (softmax - onehot(y_i)) / B as f32;
+ * *loss_sum = sum_i -log(p_i + 1e-30) (device double; mean = loss_sum / B). */
+int64_t fgl_softmax_xent_ws_bytes(void);
+int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,
+                     const int32_t* seed_ids, const int64_t* labels, int64_t B, int32_t C,
+                     float* dlogits, int64_t ldd, double* loss_sum, void* ws, int64_t ws_bytes,
+                     void* stream);
+
+/* params -= f32(lr) * grads, separately rounded (trainer.py:321-323). */
+int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream);
+
+/* Y[r, :d] = act(rowval) (rowval NULL: zeros) for r < nrows. */
+int fgl_fill_rows(float* Y, int64_t ldy, int64_t nrows, int32_t d, const float* rowval,
+                  int32_t relu, void* stream);
+
+/* -------------------------------------------------------------- loader ---- */
+/* Where fgl_sample_window leaves the per-batch unique-node bitmaps in its
+ * workspace: out[0] = byte offset of the bitmaps (batch b at word b*words),
+ * out[1] = byte offset of the int32 per-word exclusive popcount prefixes
+ * (window rows), out[2] = words per batch. */
+int fgl_sample_ws_bitmaps(int64_t num_nodes, int32_t num_batches, int64_t frontier_stride,
+                          int64_t unique_cap, int64_t* out);
+
+/* |U_i ∩ U_j| for all pairs of a window's batches (2 <= nb <= 16) from their
+ * bitmaps: out_pairs uint64[120], pair (i<j) at i*16 - i*(i+1)/2 + (j-i-1).
+ * The match degree of schedule.py:68-89 is count / min(|U_i|, |U_j|). */
+int fgl_match_counts(const uint32_t* bitmaps, int64_t words, int32_t num_batches,
+                     uint64_t* out_pairs, void* stream);
+
+/* x0 rows of one batch (trainer.py:315): out[r] = feats[ids[r]] (feats may be
+ * device memory or mapped pinned host memory), except that rows whose ID is
+ * set in prev_bitmap (the previously executed batch, Match reuse) are copied
+ * from prev_x[rank] where rank = prev_prefix[word] + popc(...) - prev_base.
+ * *loaded (device uint64, accumulated) counts rows read from feats. */
+int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
+                    const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
+                    const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
+                    void* stream);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,16 @@ class FglGraph(C.Structure):
     ]
 
 
+class FglSampleOut(C.Structure):
+    _fields_ = [
+        ("tgt", vp), ("src", vp), ("wgt", vp), ("edge_cap", C.c_int64),
+        ("tgt_row", vp), ("src_row", vp), ("tgt_front", vp), ("src_front", vp),
+        ("unique_nodes", vp), ("unique_cap", C.c_int64),
+        ("frontier", vp), ("frontier_stride", C.c_int64),
+        ("seed_rows", vp), ("seed_front", vp), ("counts", vp),
+    ]
+
+
 # name -> (restype, argtypes); every entry is declared in include/fastgl_b200.h
 SIGNATURES = {
     "fgl_last_error": (C.c_char_p, []),
@@ -47,9 +57,33 @@ SIGNATURES = {
     "fgl_sample_bounds": (C.c_int, [C.c_int64, c_i64p, C.c_int32, c_i32p, C.c_int32, c_i64p]),
     "fgl_sample_window": (C.c_int, [
         C.POINTER(FglGraph), vp, vp, C.c_int64, C.c_int32, vp, c_i32p, C.c_int32,
-        vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp]),
+        C.POINTER(FglSampleOut), vp, C.c_int64, vp]),
     "fgl_philox_words": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
+    "fgl_csr_offsets_sorted": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, vp]),
+    "fgl_stable_group_ws_bytes": (C.c_int64, [C.c_int64]),
+    "fgl_stable_group": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]),
+    "fgl_gather_i32_f32": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp]),
+    "fgl_prepare_layer_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64]),
+    "fgl_prepare_layer": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp, vp,
+                                    vp, vp, vp, vp, C.c_int64, vp]),
+    "fgl_spmm": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64,
+                           vp, C.c_int64, C.c_int32, vp]),
+    "fgl_dense_fwd": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, vp, C.c_int32, vp,
+                                C.c_int64, C.c_int32, vp]),
+    "fgl_dense_bwd_ws_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
+    "fgl_dense_bwd": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, C.c_int32, vp,
+                                C.c_int64, vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64,
+                                vp]),
+    "fgl_softmax_xent_ws_bytes": (C.c_int64, []),
+    "fgl_softmax_xent": (C.c_int, [vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, C.c_int32,
+                                   vp, C.c_int64, vp, vp, C.c_int64, vp]),
+    "fgl_sgd": (C.c_int, [vp, vp, C.c_int64, C.c_float, vp]),
+    "fgl_fill_rows": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, C.c_int32, vp]),
+    "fgl_sample_ws_bitmaps": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int64, c_i64p]),
+    "fgl_match_counts": (C.c_int, [vp, C.c_int64, C.c_int32, vp, vp]),
+    "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
+                                  vp, C.c_int64, vp, C.c_int64, vp, vp]),
 }
 
 _lib = None

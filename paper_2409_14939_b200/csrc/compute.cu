@@ -1,0 +1,471 @@
+// Model compute of one mini-batch on the sampled block graph (sm_100a).
+//
+//  * fgl_spmm      -- Memory-Aware CSR aggregation, compute.py:115-195: one
+//                     row per lane group, neighbour (col, w) lists staged in
+//                     registers and broadcast with warp shuffles, 16-byte
+//                     feature loads, fp32 accumulation in CSR order with a
+//                     rounded multiply then a rounded add (no FMA) -- bit-
+//                     identical to the reference; backward = the same kernel
+//                     on the stable transpose (compute.py:188-195).
+//  * fgl_dense_fwd -- act(h @ W + b) (compute.py:198-216), fused bias + ReLU.
+//  * fgl_dense_bwd -- dz = dx * (x_out > 0), dW = h^T dz (deterministic
+//                     split-K), db = sum dz, dh = dz W^T (trainer.py:212-228).
+//  * fgl_softmax_xent -- fp64 softmax cross entropy over the seed rows
+//                     (trainer.py:198-209) writing dlogits/B as f32.
+//  * fgl_sgd       -- w -= f32(lr) * g (trainer.py:321-323).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace fgl {
+namespace {
+
+// --------------------------------------------------------------- spmm -----
+__device__ __forceinline__ float4 fmadd4(float4 acc, float w, float4 x) {
+  acc.x = __fadd_rn(acc.x, __fmul_rn(w, x.x));
+  acc.y = __fadd_rn(acc.y, __fmul_rn(w, x.y));
+  acc.z = __fadd_rn(acc.z, __fmul_rn(w, x.z));
+  acc.w = __fadd_rn(acc.w, __fmul_rn(w, x.w));
+  return acc;
+}
+
+template <int L, int CPL>
+__global__ void __launch_bounds__(256) spmm_kernel(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+    const float* __restrict__ w, int64_t nrows, int64_t col_base, const float* __restrict__ X,
+    int64_t ldx, const float* __restrict__ self_x, int64_t ld_self, float* __restrict__ Y,
+    int64_t ldy, int d4) {
+  constexpr int G = 32 / L;  // rows per warp
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / L, g = lane % L;
+  const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (grp * L));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t rbase = warp * G; rbase < nrows; rbase += nwarps * G) {
+    const int64_t r = rbase + grp;
+    const bool live = r < nrows;
+    const int64_t e0 = live ? indptr[r] : 0, e1 = live ? indptr[r + 1] : 0;
+    float4 acc[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t e = e0; e < e1; e += L) {
+      const int64_t me = e + g;
+      const int32_t cl = me < e1 ? (int32_t)(col[me] - col_base) : 0;
+      const float wl = me < e1 ? w[me] : 0.f;
+      const int n = (int)(e1 - e < L ? e1 - e : L);
+      int k = 0;
+      for (; k + 4 <= n; k += 4) {
+        int32_t c[4];
+        float wk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          c[u] = __shfl_sync(gmask, cl, k + u, L);
+          wk[u] = __shfl_sync(gmask, wl, k + u, L);
+        }
+        float4 x[4][CPL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4* xr = reinterpret_cast<const float4*>(X + (int64_t)c[u] * ldx);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int ch = g + q * L;
+            x[u][q] = ch < d4 ? __ldg(xr + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) acc[q] = fmadd4(acc[q], wk[u], x[u][q]);
+      }
+      for (; k < n; ++k) {
+        const int32_t c = __shfl_sync(gmask, cl, k, L);
+        const float wk = __shfl_sync(gmask, wl, k, L);
+        const float4* xr = reinterpret_cast<const float4*>(X + (int64_t)c * ldx);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int ch = g + q * L;
+          if (ch < d4) acc[q] = fmadd4(acc[q], wk, __ldg(xr + ch));
+        }
+      }
+    }
+    if (live) {
+      float4* yr = reinterpret_cast<float4*>(Y + r * ldy);
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int ch = g + q * L;
+        if (ch < d4) {
+          float4 v = acc[q];
+          if (self_x) {  // GIN: h = aggregate + x, one rounded add (trainer.py:189-190)
+            const float4 s = reinterpret_cast<const float4*>(self_x + r * ld_self)[ch];
+            v.x = __fadd_rn(v.x, s.x); v.y = __fadd_rn(v.y, s.y);
+            v.z = __fadd_rn(v.z, s.z); v.w = __fadd_rn(v.w, s.w);
+          }
+          yr[ch] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int L, int CPL>
+void launch_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows,
+                 int64_t col_base, const float* X, int64_t ldx, const float* self_x,
+                 int64_t ld_self, float* Y, int64_t ldy, int d4, cudaStream_t st) {
+  constexpr int G = 32 / L;
+  const int64_t warps = ceil_div(nrows, G);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), 148 * 16));
+  spmm_kernel<L, CPL><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
+                                            ld_self, Y, ldy, d4);
+}
+
+// --------------------------------------------------------------- dense ----
+// C[M, N] = A[M, K] @ B + bias  (B is [K, N] row-major, or B^T stored as [N, K]
+// when b_trans); optional ReLU.  64x64 output tile per CTA, 256 threads with
+// 4x4 register micro-tiles, K staged through shared memory in chunks of 32.
+constexpr int BM = 64, BN = 64, BK = 32;
+
+__global__ void __launch_bounds__(256) gemm_kernel(
+    const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int b_trans,
+    const float* __restrict__ bias, float* __restrict__ C, int64_t ldc, int64_t M, int N, int K,
+    int relu, const float* __restrict__ amask, int64_t ldm) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = blockIdx.x * (int64_t)BM;
+  const int n0 = blockIdx.y * BN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    // A tile: 64 rows x 32 k, stored k-major in smem
+    for (int i = tid; i < BM * BK; i += 256) {
+      const int r = i / BK, k = i % BK;
+      const int64_t gr = m0 + r;
+      float v = 0.f;
+      if (gr < M && k0 + k < K) {
+        v = A[gr * lda + k0 + k];
+        if (amask && !(amask[gr * ldm + k0 + k] > 0.f)) v = 0.f;  // relu mask of dz
+      }
+      As[k][r] = v;
+    }
+    for (int i = tid; i < BK * BN; i += 256) {
+      const int k = i / BN, n = i % BN;
+      float v = 0.f;
+      if (k0 + k < K && n0 + n < N) v = b_trans ? B[(int64_t)(n0 + n) * ldb + k0 + k] : B[(int64_t)(k0 + k) * ldb + n0 + n];
+      Bs[k][n] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < BK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = m0 + ty * 4 + i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = n0 + tx * 4 + j;
+      if (c >= N) continue;
+      float v = acc[i][j];
+      if (bias) v = __fadd_rn(v, bias[c]);
+      if (relu) v = v > 0.f ? v : 0.f;
+      C[r * ldc + c] = v;
+    }
+  }
+}
+
+// Partial dW = A^T dZ and db = colsum(dZ) over a fixed row chunk per CTA.
+// Thread layout: 256 threads own a 32(k) x 64(n) tile of the output through a
+// 2x4 micro tile; rows are streamed through shared memory 32 at a time.
+constexpr int WK = 32, WN = 64, WR = 32;
+
+__global__ void __launch_bounds__(256) wgrad_partial_kernel(
+    const float* __restrict__ A, int64_t lda, const float* __restrict__ dZ, int64_t ldz,
+    const float* __restrict__ zmask, int64_t ldm, int64_t M, int K, int N, int64_t rows_per_cta,
+    float* __restrict__ part_w, float* __restrict__ part_b) {
+  __shared__ float As[WR][WK + 1];
+  __shared__ float Zs[WR][WN + 1];
+  const int tid = threadIdx.x;
+  const int tn = tid % 16, tk = tid / 16;  // 16 x 16 threads; each 2 (k) x 4 (n)
+  const int k0 = blockIdx.y * WK, n0 = blockIdx.z * WN;
+  const int64_t r_begin = blockIdx.x * rows_per_cta;
+  const int64_t r_end = min(M, r_begin + rows_per_cta);
+  float acc[2][4] = {};
+  float bacc[4] = {};
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += WR) {
+    for (int i = tid; i < WR * WK; i += 256) {
+      const int rr = i / WK, k = i % WK;
+      const int64_t r = r0 + rr;
+      As[rr][k] = (r < r_end && k0 + k < K) ? A[r * lda + k0 + k] : 0.f;
+    }
+    for (int i = tid; i < WR * WN; i += 256) {
+      const int rr = i / WN, n = i % WN;
+      const int64_t r = r0 + rr;
+      float v = 0.f;
+      if (r < r_end && n0 + n < N) {
+        v = dZ[r * ldz + n0 + n];
+        if (zmask && !(zmask[r * ldm + n0 + n] > 0.f)) v = 0.f;
+      }
+      Zs[rr][n] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < WR; ++rr) {
+      float a0 = As[rr][tk * 2], a1 = As[rr][tk * 2 + 1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float z = Zs[rr][tn * 4 + j];
+        acc[0][j] = __fmaf_rn(a0, z, acc[0][j]);
+        acc[1][j] = __fmaf_rn(a1, z, acc[1][j]);
+        if (tk == 0 && blockIdx.y == 0) bacc[j] = __fadd_rn(bacc[j], z);
+      }
+    }
+    __syncthreads();
+  }
+  float* pw = part_w + (int64_t)blockIdx.x * K * N;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int k = k0 + tk * 2 + i;
+    if (k >= K) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tn * 4 + j;
+      if (n < N) pw[(int64_t)k * N + n] = acc[i][j];
+    }
+  }
+  if (tk == 0 && blockIdx.y == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tn * 4 + j;
+      if (n < N) part_b[(int64_t)blockIdx.x * N + n] = bacc[j];
+    }
+  }
+}
+
+// sum partials over chunks in a fixed order (deterministic)
+__global__ void reduce_partials_kernel(const float* __restrict__ part, int chunks, int64_t n,
+                                       float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s = __fadd_rn(s, part[(int64_t)c * n + i]);
+    out[i] = s;
+  }
+}
+
+// --------------------------------------------------------------- loss -----
+__global__ void softmax_xent_kernel(const float* __restrict__ logits, int64_t ldl,
+                                    const int32_t* __restrict__ rows, int64_t row_base,
+                                    const int32_t* __restrict__ seed_ids,
+                                    const int64_t* __restrict__ labels, int64_t B, int C,
+                                    float* __restrict__ dlog, int64_t ldd,
+                                    double* __restrict__ loss_part) {
+  // one warp per seed row; fp64 throughout (trainer.py:198-209)
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double lsum = 0.0;
+  for (int64_t i = warp; i < B; i += nwarps) {
+    const int64_t r = rows[i] - row_base;
+    const float* z = logits + r * ldl;
+    double mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmax(mx, (double)z[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double se = 0.0;
+    for (int c = lane; c < C; c += 32) se += exp((double)z[c] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int64_t y = labels[seed_ids ? (int64_t)seed_ids[i] : i];
+    for (int c = lane; c < C; c += 32) {
+      const double p = exp((double)z[c] - mx) / se;
+      const double g = (c == y ? p - 1.0 : p) / (double)B;
+      dlog[r * ldd + c] = (float)g;
+      if (c == y) lsum += -log(p + 1e-30);
+    }
+  }
+  lsum = warp_sum(lsum);
+  if (lane == 0) loss_part[warp] = lsum;
+}
+
+__global__ void sum_doubles_kernel(const double* __restrict__ v, int n, double* out) {
+  __shared__ double sm[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+}
+
+__global__ void fill_rows_kernel(float* __restrict__ Y, int64_t ldy, int64_t nrows, int d,
+                                 const float* __restrict__ rowval, int relu) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows * d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d;
+    const int c = (int)(i % d);
+    float v = rowval ? rowval[c] : 0.f;
+    if (relu) v = v > 0.f ? v : 0.f;
+    Y[r * ldy + c] = v;
+  }
+}
+
+int blocks_for(int64_t n, int t = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, t), 148 * 16));
+}
+
+}  // namespace
+}  // namespace fgl
+
+using namespace fgl;
+
+extern "C" {
+
+int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
+             int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
+             float* Y, int64_t ldy, int32_t d, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (num_rows < 0 || d < 1 || !indptr || !Y || ldy < d || ldx < d || (ldx % 4) || (ldy % 4) ||
+      (self_x && (ld_self % 4))) {
+    set_error("fgl_spmm: bad arguments (d=%d ldx=%lld ldy=%lld; leading dims must be multiples of 4)",
+              d, (long long)ldx, (long long)ldy);
+    return FGL_E_INVALID;
+  }
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) |
+       reinterpret_cast<uintptr_t>(self_x)) & 15) {
+    set_error("fgl_spmm: feature pointers must be 16-byte aligned");
+    return FGL_E_INVALID;
+  }
+  if (num_rows == 0) return FGL_OK;
+  const int d4 = (d + 3) / 4;
+  if (d4 <= 1) launch_spmm<1, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 4) launch_spmm<4, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 8) launch_spmm<8, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 16) launch_spmm<16, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 32) launch_spmm<32, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 64) launch_spmm<32, 2>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 128) launch_spmm<32, 4>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 256) launch_spmm<32, 8>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else {
+    set_error("fgl_spmm: feature dim %d above 1024 is not supported", d);
+    return FGL_E_UNSUPPORTED;
+  }
+  FGL_LAUNCH_CHECK("spmm_kernel");
+  return FGL_OK;
+}
+
+int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
+                  const float* b, int32_t dout, float* Z, int64_t ldz, int32_t relu, void* stream) {
+  if (n < 0 || din < 1 || dout < 1 || !W || !Z || ldh < din || ldz < dout) {
+    set_error("fgl_dense_fwd: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (n == 0) return FGL_OK;
+  dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
+  gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
+                                                      relu, nullptr, 0);
+  FGL_LAUNCH_CHECK("gemm_kernel(fwd)");
+  return FGL_OK;
+}
+
+int64_t fgl_dense_bwd_ws_bytes(int32_t din, int32_t dout) {
+  return (int64_t)kPersistentCTAs * ((int64_t)din * dout + dout) * 4;
+}
+
+int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
+                  int32_t dout, const float* dX, int64_t lddx, const float* Xout, int64_t ldxo,
+                  float* dW, float* db, float* dH, int64_t lddh, void* ws, int64_t ws_bytes,
+                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || din < 1 || dout < 1 || !W || !dW || !db || lddx < dout || (Xout && ldxo < dout) ||
+      (dH && lddh < din)) {
+    set_error("fgl_dense_bwd: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (ws_bytes < fgl_dense_bwd_ws_bytes(din, dout)) {
+    set_error("fgl_dense_bwd: workspace too small");
+    return FGL_E_CAPACITY;
+  }
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kPersistentCTAs, ceil_div(n, 256)));
+  const int64_t rows_per = std::max<int64_t>(1, ceil_div(n, chunks));
+  float* pw = static_cast<float*>(ws);
+  float* pb = pw + (int64_t)chunks * din * dout;
+  if (n > 0) {
+    dim3 g(chunks, (unsigned)ceil_div(din, WK), (unsigned)ceil_div(dout, WN));
+    wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, rows_per,
+                                            pw, pb);
+    reduce_partials_kernel<<<blocks_for((int64_t)din * dout), 256, 0, st>>>(pw, chunks, (int64_t)din * dout, dW);
+    reduce_partials_kernel<<<blocks_for(dout), 256, 0, st>>>(pb, chunks, dout, db);
+    if (dH) {
+      dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
+      gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,
+                                        Xout, ldxo);
+    }
+  } else {
+    FGL_CUDA(cudaMemsetAsync(dW, 0, 4 * (int64_t)din * dout, st));
+    FGL_CUDA(cudaMemsetAsync(db, 0, 4 * (int64_t)dout, st));
+  }
+  FGL_LAUNCH_CHECK("dense_bwd");
+  return FGL_OK;
+}
+
+int64_t fgl_softmax_xent_ws_bytes(void) { return 8 * (148 * 8 * 8 + 1); }
+
+int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,
+                     const int32_t* seed_ids, const int64_t* labels, int64_t B, int32_t C,
+                     float* dlogits, int64_t ldd, double* loss_sum, void* ws, int64_t ws_bytes,
+                     void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (B < 1 || C < 1 || !logits || !rows || !labels || !dlogits || !loss_sum || ldl < C || ldd < C ||
+      ws_bytes < fgl_softmax_xent_ws_bytes()) {
+    set_error("fgl_softmax_xent: bad arguments");
+    return FGL_E_INVALID;
+  }
+  const int blocks = (int)std::min<int64_t>(148 * 8, ceil_div(B, 8));
+  double* part = static_cast<double*>(ws);
+  softmax_xent_kernel<<<blocks, 256, 0, st>>>(logits, ldl, rows, row_base, seed_ids, labels, B, C,
+                                              dlogits, ldd, part);
+  sum_doubles_kernel<<<1, 1024, 0, st>>>(part, blocks * 8, loss_sum);
+  FGL_LAUNCH_CHECK("softmax_xent");
+  return FGL_OK;
+}
+
+int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream) {
+  if (n < 0 || (n > 0 && (!params || !grads))) {
+    set_error("fgl_sgd: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (n == 0) return FGL_OK;
+  sgd_kernel<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
+  FGL_LAUNCH_CHECK("sgd_kernel");
+  return FGL_OK;
+}
+
+int fgl_fill_rows(float* Y, int64_t ldy, int64_t nrows, int32_t d, const float* rowval,
+                  int32_t relu, void* stream) {
+  if (nrows < 0 || d < 1 || ldy < d || (nrows > 0 && !Y)) {
+    set_error("fgl_fill_rows: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (nrows == 0) return FGL_OK;
+  fill_rows_kernel<<<blocks_for(nrows * d), 256, 0, (cudaStream_t)stream>>>(Y, ldy, nrows, d, rowval, relu);
+  FGL_LAUNCH_CHECK("fill_rows_kernel");
+  return FGL_OK;
+}
+
+}  // extern "C"

@@ -39,12 +39,11 @@ struct SampleWs {
   uint32_t* bm_front;  // [nb*W]
   uint32_t* bm_all;    // [nb*W]
   int32_t* wprefix;    // [nb*W] exclusive popcount prefix of bm_all (global)
-  int32_t* front;      // [fcap]
+  int32_t* posmap;     // [ucap] window row -> index in a hop's frontier list
   int32_t* fb;         // [fcap] batch of each frontier entry
   int64_t* scan_deg;   // [fcap]
   int64_t* scan_sel;   // [fcap]
   int64_t* part;       // [2*kPersistentCTAs + 2]
-  int64_t* fr_off;     // [nb+1]
   int64_t* pos;        // [nb]   running Philox position per batch
   int64_t* hop_pos;    // [nb]   position at the start of the current hop
   int64_t* scal;       // [8]
@@ -56,11 +55,11 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
   int64_t words, fcap, bytes;
-  int64_t off_front_bm, off_all_bm, off_wprefix, off_front, off_fb, off_sdeg, off_ssel, off_part,
-      off_froff, off_pos, off_hoppos, off_scal;
+  int64_t off_front_bm, off_all_bm, off_wprefix, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
+      off_pos, off_hoppos, off_scal;
 };
 
-WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap) {
+WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   WsLayout L;
   L.words = align_up(ceil_div(num_nodes, 32), 4);
   L.fcap = std::max<int64_t>(fcap, 1);
@@ -69,12 +68,11 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap) {
   L.off_front_bm = take(4 * L.words * nb);
   L.off_all_bm = take(4 * L.words * nb);
   L.off_wprefix = take(4 * L.words * nb);
-  L.off_front = take(4 * L.fcap);
+  L.off_posmap = take(4 * std::max<int64_t>(ucap, 1));
   L.off_fb = take(4 * L.fcap);
   L.off_sdeg = take(8 * L.fcap);
   L.off_ssel = take(8 * L.fcap);
   L.off_part = take(8 * (2 * kPersistentCTAs + 2));
-  L.off_froff = take(8 * (nb + 1));
   L.off_pos = take(8 * nb);
   L.off_hoppos = take(8 * nb);
   L.off_scal = take(8 * 8);
@@ -88,12 +86,11 @@ SampleWs carve(void* base, const WsLayout& L) {
   w.bm_front = reinterpret_cast<uint32_t*>(p + L.off_front_bm);
   w.bm_all = reinterpret_cast<uint32_t*>(p + L.off_all_bm);
   w.wprefix = reinterpret_cast<int32_t*>(p + L.off_wprefix);
-  w.front = reinterpret_cast<int32_t*>(p + L.off_front);
+  w.posmap = reinterpret_cast<int32_t*>(p + L.off_posmap);
   w.fb = reinterpret_cast<int32_t*>(p + L.off_fb);
   w.scan_deg = reinterpret_cast<int64_t*>(p + L.off_sdeg);
   w.scan_sel = reinterpret_cast<int64_t*>(p + L.off_ssel);
   w.part = reinterpret_cast<int64_t*>(p + L.off_part);
-  w.fr_off = reinterpret_cast<int64_t*>(p + L.off_froff);
   w.pos = reinterpret_cast<int64_t*>(p + L.off_pos);
   w.hop_pos = reinterpret_cast<int64_t*>(p + L.off_hoppos);
   w.scal = reinterpret_cast<int64_t*>(p + L.off_scal);
@@ -258,21 +255,20 @@ __global__ void deg_down_kernel(const int64_t* __restrict__ off, const int32_t* 
 }
 
 // per-batch bookkeeping of one hop (one thread per batch)
-__global__ void hop_book_kernel(SampleWs w, int32_t nb, int hop, int64_t* __restrict__ counts,
-                                int H, int64_t edge_cap) {
+__global__ void hop_book_kernel(SampleWs w, const int64_t* __restrict__ fr_off, int32_t nb,
+                                int hop, int64_t* __restrict__ counts, int H, int64_t edge_cap) {
   const int64_t F = w.scal[kF];
   if (threadIdx.x == 0) {
     w.scal[kHopEdgeBase] = w.scal[kEdgeBase];
   }
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    const int64_t f0 = w.fr_off[b], f1 = w.fr_off[b + 1];
+    const int64_t f0 = fr_off[b], f1 = fr_off[b + 1];
     const int64_t c0 = f0 < F ? w.scan_deg[f0] : w.scal[kCandTot];
     const int64_t c1 = f1 < F ? w.scan_deg[f1] : w.scal[kCandTot];
     const int64_t s0 = f0 < F ? w.scan_sel[f0] : w.scal[kSelTot];
     w.hop_pos[b] = w.pos[b] - c0;  // so that pos = hop_pos[b] + scan_deg[i]
     w.pos[b] += c1 - c0;
     counts[FGL_CNT_DRAWS(H, nb) + b] += c1 - c0;
-    counts[FGL_CNT_FRONT(H, nb) + hop * nb + b] = f1 - f0;
     counts[hop * nb + b] = w.scal[kEdgeBase] + s0;
   }
   __syncthreads();
@@ -363,6 +359,7 @@ struct SelectArgs {
   int32_t* tgt;
   int32_t* src;
   float* wgt;
+  int32_t* tgt_front;
   int fan;
 };
 
@@ -423,6 +420,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
         const int32_t s = __ldg(a.col + e);
         a.tgt[obase + r] = u;
         a.src[obase + r] = s;
+        if (a.tgt_front) a.tgt_front[obase + r] = (int32_t)i;
         a.wgt[obase + r] = a.ew ? __ldg(a.ew + e) : 1.0f;
         atomicOr(bm + (s >> 5), 1u << (s & 31));
       }
@@ -439,20 +437,36 @@ __device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
   return (int32_t)(wprefix[w] + __popc(bm[w] & below) - uniq_base);
 }
 
+// posmap[row(frontier[j])] = j for every entry j of one hop's frontier list
+__global__ void posmap_kernel(const int32_t* __restrict__ front, const int64_t* __restrict__ fo,
+                              int32_t nb, const uint32_t* __restrict__ bm_all,
+                              const int32_t* __restrict__ wprefix, int64_t words,
+                              int32_t* __restrict__ posmap) {
+  const int64_t F = fo[nb];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < F;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int b = find_segment(fo, nb, j);
+    posmap[bm_rank(bm_all, wprefix, (int64_t)b * words, 0, front[j])] = (int32_t)j;
+  }
+}
+
+// window rows of hop h's edges (+ frontier index of the source in hop h+1's
+// list through posmap, or the source row itself for the last hop)
 __global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
-                                 const int64_t* __restrict__ counts, int hn, int32_t nb,
+                                 const int64_t* __restrict__ eoff, int32_t nb,
                                  const uint32_t* __restrict__ bm_all,
                                  const int32_t* __restrict__ wprefix, int64_t words,
-                                 const int64_t* __restrict__ uniq_off, int32_t* __restrict__ lt,
-                                 int32_t* __restrict__ ls) {
-  const int64_t total = counts[hn];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+                                 const int32_t* __restrict__ posmap, int32_t* __restrict__ lt,
+                                 int32_t* __restrict__ ls, int32_t* __restrict__ sf) {
+  const int64_t e0 = eoff[0], e1 = eoff[nb];
+  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int seg = find_segment(counts, hn, e);
-    const int b = seg % nb;
-    const int64_t bw = (int64_t)b * words, ub = uniq_off[b];
-    lt[e] = bm_rank(bm_all, wprefix, bw, ub, tgt[e]);
-    ls[e] = bm_rank(bm_all, wprefix, bw, ub, src[e]);
+    const int b = find_segment(eoff, nb, e);
+    const int64_t bw = (int64_t)b * words;
+    const int32_t rs = bm_rank(bm_all, wprefix, bw, 0, src[e]);
+    if (lt) lt[e] = bm_rank(bm_all, wprefix, bw, 0, tgt[e]);
+    if (ls) ls[e] = rs;
+    if (sf) sf[e] = posmap ? posmap[rs] : rs;
   }
 }
 
@@ -460,13 +474,14 @@ __global__ void translate_seeds_kernel(const int32_t* __restrict__ seeds,
                                        const int64_t* __restrict__ seed_off, int32_t nb,
                                        int64_t total, const uint32_t* __restrict__ bm_all,
                                        const int32_t* __restrict__ wprefix, int64_t words,
-                                       const int64_t* __restrict__ uniq_off,
-                                       int32_t* __restrict__ out) {
+                                       const int32_t* __restrict__ posmap,
+                                       int32_t* __restrict__ rows, int32_t* __restrict__ fidx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int b = find_segment(seed_off, nb, i);
-    const int32_t s = seeds[i];
-    out[i] = bm_rank(bm_all, wprefix, (int64_t)b * words, uniq_off[b], s);
+    const int32_t r = bm_rank(bm_all, wprefix, (int64_t)b * words, 0, seeds[i]);
+    if (rows) rows[i] = r;
+    if (fidx) fidx[i] = posmap[r];
   }
 }
 
@@ -514,24 +529,36 @@ int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t nb,
     }
     uniq += std::min<int64_t>(num_nodes, u);
   }
-  int64_t fcap = *std::max_element(hop_front.begin(), hop_front.end());
+  const int64_t fcap = *std::max_element(hop_front.begin(), hop_front.end());
   out[0] = std::max<int64_t>(edges, 1);
   out[1] = std::max<int64_t>(fcap, 1);
   out[2] = std::max<int64_t>(uniq, 1);
-  out[3] = ws_layout(num_nodes, nb, out[1]).bytes;
+  out[3] = ws_layout(num_nodes, nb, out[1], out[2]).bytes;
   out[4] = FGL_CNT_LEN(H, nb);
+  return FGL_OK;
+}
+
+int fgl_sample_ws_bitmaps(int64_t num_nodes, int32_t nb, int64_t frontier_stride,
+                          int64_t unique_cap, int64_t* out) {
+  if (num_nodes < 1 || nb < 1 || !out) {
+    set_error("fgl_sample_ws_bitmaps: bad arguments");
+    return FGL_E_INVALID;
+  }
+  const WsLayout L = ws_layout(num_nodes, nb, frontier_stride, unique_cap);
+  out[0] = L.off_all_bm;
+  out[1] = L.off_wprefix;
+  out[2] = L.words;
   return FGL_OK;
 }
 
 int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* seed_off,
                       int64_t total_seeds, int32_t nb, const uint64_t* keys,
-                      const int32_t* fanouts, int32_t H, int32_t* tgt, int32_t* src, float* wgt,
-                      int64_t edge_cap, int32_t* local_tgt, int32_t* local_src,
-                      int32_t* unique_nodes, int64_t unique_cap, int32_t* seed_locals,
-                      int64_t* counts, void* ws, int64_t ws_bytes, void* stream_) {
+                      const int32_t* fanouts, int32_t H, const fgl_sample_out* o, void* ws,
+                      int64_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  if (!g || !seeds || !seed_off || !keys || !fanouts || !tgt || !src || !wgt || !unique_nodes ||
-      !counts || !ws || nb < 1 || H < 1 || H > FGL_MAX_HOPS || total_seeds < 1) {
+  if (!g || !seeds || !seed_off || !keys || !fanouts || !o || !o->tgt || !o->src || !o->wgt ||
+      !o->unique_nodes || !o->frontier || !o->counts || !ws || nb < 1 || H < 1 ||
+      H > FGL_MAX_HOPS || total_seeds < 1 || o->frontier_stride < 1) {
     set_error("fgl_sample_window: bad arguments");
     return FGL_E_INVALID;
   }
@@ -546,25 +573,21 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       return FGL_E_UNSUPPORTED;
     }
   }
-  // capacities: the caller sizes buffers with fgl_sample_bounds from the host batch sizes;
-  // the frontier capacity is the largest one whose workspace layout fits ws_bytes
-  int64_t lo = 1, hi = std::max<int64_t>(1, (int64_t)nb * g->num_nodes);
-  if (ws_layout(g->num_nodes, nb, 1).bytes > ws_bytes) {
-    set_error("sample workspace too small (%lld bytes)", (long long)ws_bytes);
+  const WsLayout Lw = ws_layout(g->num_nodes, nb, o->frontier_stride, o->unique_cap);
+  if (Lw.bytes > ws_bytes) {
+    set_error("sample workspace too small (%lld < %lld bytes)", (long long)ws_bytes,
+              (long long)Lw.bytes);
     return FGL_E_CAPACITY;
   }
-  while (lo < hi) {
-    int64_t mid = lo + (hi - lo + 1) / 2;
-    if (ws_layout(g->num_nodes, nb, mid).bytes <= ws_bytes) lo = mid; else hi = mid - 1;
-  }
-  const WsLayout Lw = ws_layout(g->num_nodes, nb, lo);
   SampleWs w = carve(ws, Lw);
   const int64_t words = Lw.words;
   const int64_t nwords = words * nb;
+  const int64_t fcap = o->frontier_stride;
   const int G = kPersistentCTAs;
-  const int hn = H * nb;
+  int64_t* counts = o->counts;
   int64_t* status = counts + FGL_CNT_STATUS(H, nb);
   int64_t* uniq_off = counts + FGL_CNT_UNIQ(H, nb);
+  auto fr_off = [&](int h) { return counts + FGL_CNT_FRONT(H, nb) + (int64_t)h * (nb + 1); };
 
   FGL_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * FGL_CNT_LEN(H, nb), stream));
   FGL_CUDA(cudaMemsetAsync(w.bm_front, 0, 4 * nwords, stream));
@@ -576,57 +599,70 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   mark_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0, stream>>>(
       seeds, seed_off, nb, total_seeds, g->num_nodes, words, w.bm_front, status);
   FGL_LAUNCH_CHECK("mark_seeds_kernel");
-  auto compact_front = [&](bool write_ids) -> int {
+  // compaction of `front` into hop h's frontier list (h == H: no list, only OR into `all`)
+  auto compact_front = [&](int h) -> int {
+    const bool write = h < H;
     bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
-    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, w.fr_off + nb);
+    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, write ? fr_off(h) + nb : nullptr);
     bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(
-        w.bm_front, nwords, words, w.part, write_ids ? w.front : nullptr,
-        write_ids ? w.fb : nullptr, w.fr_off, nullptr, w.bm_all, 1, Lw.fcap, status);
+        w.bm_front, nwords, words, w.part, write ? o->frontier + h * fcap : nullptr,
+        write ? w.fb : nullptr, write ? fr_off(h) : nullptr, nullptr, w.bm_all, 1, fcap, status);
     FGL_LAUNCH_CHECK("frontier compaction");
     return FGL_OK;
   };
-  int rc = compact_front(true);
+  int rc = compact_front(0);
   if (rc) return rc;
 
-  const int sel_grid_k1 = select_grid(1);
   for (int h = 0; h < H; ++h) {
     const int fan = fanouts[h];
-    deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, w.front, w.scal, fan, w.part);
+    const int32_t* front = o->frontier + h * fcap;
+    deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part);
     scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kCandTot, nullptr);
     scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part + G + 1, G, w.scal + kSelTot, nullptr);
-    deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, w.front, w.scal, fan, w.part,
+    deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part,
                                                     w.scan_deg, w.scan_sel);
-    hop_book_kernel<<<1, 64, 0, stream>>>(w, nb, h, counts, H, edge_cap);
+    hop_book_kernel<<<1, 64, 0, stream>>>(w, fr_off(h), nb, h, counts, H, o->edge_cap);
     FGL_LAUNCH_CHECK("degree scan");
-    SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, w.front, w.fb,
-                 w.scan_deg, w.scan_sel, w.fr_off, w.hop_pos, keys, w.scal,
-                 w.bm_front, words, tgt, src, wgt, fan};
-    if (fan <= 32) select_kernel<1><<<sel_grid_k1, 256, 0, stream>>>(a);
+    SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
+                 w.scan_deg, w.scan_sel, fr_off(h), w.hop_pos, keys, w.scal,
+                 w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan};
+    if (fan <= 32) select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
     else if (fan <= 64) select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
     else if (fan <= 128) select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
     else select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
     FGL_LAUNCH_CHECK("select_kernel");
-    rc = compact_front(h + 1 < H);
+    rc = compact_front(h + 1);
     if (rc) return rc;
   }
 
   // unique nodes = compaction of the `all` bitmaps; keeps per-word prefixes for ranks
   bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
   scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kUniqTot, uniq_off + nb);
-  bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part, unique_nodes,
-                                                    nullptr, uniq_off, w.wprefix, nullptr, 0,
-                                                    unique_cap, status);
+  bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part,
+                                                    o->unique_nodes, nullptr, uniq_off, w.wprefix,
+                                                    nullptr, 0, o->unique_cap, status);
   FGL_LAUNCH_CHECK("unique compaction");
-  if (local_tgt && local_src) {
-    translate_kernel<<<4 * G, 256, 0, stream>>>(tgt, src, counts, hn, nb, w.bm_all, w.wprefix,
-                                                words, uniq_off, local_tgt, local_src);
-    FGL_LAUNCH_CHECK("translate_kernel");
-  }
-  if (seed_locals) {
-    translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0,
-                             stream>>>(seeds, seed_off, nb, total_seeds, w.bm_all, w.wprefix, words,
-                                       uniq_off, seed_locals);
-    FGL_LAUNCH_CHECK("translate_seeds_kernel");
+
+  // translation: window rows, and frontier indices through per-hop position maps
+  const bool want_rows = o->tgt_row || o->src_row || o->src_front;
+  const int TG = 4 * G;
+  for (int h = 0; h <= H; ++h) {
+    const bool has_list = h < H && (o->src_front || (h == 0 && o->seed_front));
+    if (has_list) {
+      posmap_kernel<<<TG, 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb, w.bm_all,
+                                            w.wprefix, words, w.posmap);
+    }
+    if (h == 0 && (o->seed_rows || o->seed_front)) {
+      translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), TG), 256, 0,
+                               stream>>>(seeds, seed_off, nb, total_seeds, w.bm_all, w.wprefix,
+                                         words, w.posmap, o->seed_rows, o->seed_front);
+    }
+    if (h >= 1 && want_rows) {  // hop h-1 sources live in hop h's frontier
+      translate_kernel<<<TG, 256, 0, stream>>>(o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all,
+                                               w.wprefix, words, h < H ? w.posmap : nullptr,
+                                               o->tgt_row, o->src_row, o->src_front);
+    }
+    FGL_LAUNCH_CHECK("translate");
   }
   return FGL_OK;
 }

@@ -81,32 +81,36 @@ def _validate_seeds(num_nodes: int, seeds) -> np.ndarray:
     return seeds
 
 
+def counts_layout(H: int, nb: int) -> dict:
+    """Offsets of the FGL_CNT_* sections (include/fastgl_b200.h)."""
+    fo = H * nb + 1
+    uo = fo + H * (nb + 1)
+    do = uo + nb + 1
+    so = do + nb
+    return {"front": fo, "uniq": uo, "draws": do, "status": so, "len": so + 1}
+
+
 @dataclass
 class DeviceWindow:
-    """Results of one window in HBM.  ``counts`` is the FGL_CNT_* vector."""
+    """Results of one sampled window, resident in HBM.
+
+    Edge arrays are hop-major / batch-minor; ``tgt_row``/``src_row`` are window
+    rows (batch b's local ID + its unique offset), ``tgt_front``/``src_front``
+    index hop h's / hop h+1's frontier list (last hop: window row)."""
 
     num_batches: int
     num_hops: int
-    tgt: object
-    src: object
-    wgt: object
-    local_tgt: object
-    local_src: object
-    unique: object
-    seed_locals: object
-    seeds: object
+    s: "WindowSampler"
     seed_off_host: np.ndarray
-    counts: object
-    sampler: "WindowSampler"
     _host_counts: np.ndarray | None = None
 
     def host_counts(self) -> np.ndarray:
-        """One device->host read of the counts vector (the batch's only sync)."""
+        """One device->host read of the counts vector (the window's only sync)."""
         if self._host_counts is None:
-            self._host_counts = self.counts.cpu().numpy()
-            H, nb = self.num_hops, self.num_batches
-            _lib.status_error(int(self._host_counts[H * nb + 1 + nb + 1 + nb + H * nb]),
+            c = self.s.counts[: counts_layout(self.num_hops, self.num_batches)["len"]].cpu().numpy()
+            _lib.status_error(int(c[counts_layout(self.num_hops, self.num_batches)["status"]]),
                               "fgl_sample_window")
+            self._host_counts = c
         return self._host_counts
 
     def edge_range(self, hop: int, b: int):
@@ -114,35 +118,53 @@ class DeviceWindow:
         k = hop * self.num_batches + b
         return int(c[k]), int(c[k + 1])
 
+    def hop_edges(self, hop: int):
+        c = self.host_counts()
+        return int(c[hop * self.num_batches]), int(c[(hop + 1) * self.num_batches])
+
+    def front_range(self, hop: int, b: int):
+        c = self.host_counts()
+        k = counts_layout(self.num_hops, self.num_batches)["front"] + hop * (self.num_batches + 1) + b
+        return int(c[k]), int(c[k + 1])
+
+    def front_total(self, hop: int) -> int:
+        return self.front_range(hop, self.num_batches - 1)[1]
+
     def unique_range(self, b: int):
         c = self.host_counts()
-        u0 = self.num_hops * self.num_batches + 1
+        u0 = counts_layout(self.num_hops, self.num_batches)["uniq"]
         return int(c[u0 + b]), int(c[u0 + b + 1])
+
+    def unique_total(self) -> int:
+        return self.unique_range(self.num_batches - 1)[1]
 
     def draws(self, b: int) -> int:
         c = self.host_counts()
-        d0 = self.num_hops * self.num_batches + 1 + self.num_batches + 1
-        return int(c[d0 + b])
+        return int(c[counts_layout(self.num_hops, self.num_batches)["draws"] + b])
 
     def total_edges(self) -> int:
         return int(self.host_counts()[self.num_hops * self.num_batches])
 
+    def frontier(self, hop: int):
+        return self.s.frontier[hop * self.s.fcap : hop * self.s.fcap + self.front_total(hop)]
+
     def to_batch(self, b: int) -> SubgraphBatch:
         """Host SubgraphBatch of batch b in the reference's dtypes."""
+        s = self.s
         layers, local = [], []
+        u0, u1 = self.unique_range(b)
         for h in range(self.num_hops):
             e0, e1 = self.edge_range(h, b)
-            t = self.tgt[e0:e1].cpu().numpy().astype(np.uint64)
-            s = self.src[e0:e1].cpu().numpy().astype(np.uint64)
-            w = self.wgt[e0:e1].cpu().numpy()
-            layers.append((t, s, w))
-            if self.local_tgt is not None:
-                local.append((self.local_tgt[e0:e1].cpu().numpy().astype(np.int64),
-                              self.local_src[e0:e1].cpu().numpy().astype(np.int64), w))
-        u0, u1 = self.unique_range(b)
+            t = s.tgt[e0:e1].cpu().numpy().astype(np.uint64)
+            src = s.src[e0:e1].cpu().numpy().astype(np.uint64)
+            w = s.wgt[e0:e1].cpu().numpy()
+            layers.append((t, src, w))
+            if s.tgt_row is not None:
+                local.append((s.tgt_row[e0:e1].cpu().numpy().astype(np.int64) - u0,
+                              s.src_row[e0:e1].cpu().numpy().astype(np.int64) - u0, w))
         s0, s1 = int(self.seed_off_host[b]), int(self.seed_off_host[b + 1])
-        uniq = self.unique[u0:u1].cpu().numpy().astype(np.uint64)
-        seeds = self.seeds[s0:s1].cpu().numpy().astype(np.uint64)
+        uniq = s.unique[u0:u1].cpu().numpy().astype(np.uint64)
+        seeds = s.seeds_dev[s0:s1].cpu().numpy().astype(np.uint64)
         return SubgraphBatch(seeds=seeds, layers=layers, unique_nodes=uniq, local_layers=local,
                              num_local=len(uniq) if local else 0)
 
@@ -170,62 +192,59 @@ class WindowSampler:
         self.edge_cap, self.fcap, self.uniq_cap, self.ws_bytes, self.counts_len = (int(x) for x in out)
         e = self.edge_cap
         i32 = dict(dtype=torch.int32, device=device)
+        opt = (lambda n: torch.empty(n, **i32)) if local_ids else (lambda n: None)
         self.tgt = torch.empty(e, **i32)
         self.src = torch.empty(e, **i32)
         self.wgt = torch.empty(e, dtype=torch.float32, device=device)
-        self.local_tgt = torch.empty(e, **i32) if local_ids else None
-        self.local_src = torch.empty(e, **i32) if local_ids else None
+        self.tgt_row, self.src_row = opt(e), opt(e)
+        self.tgt_front, self.src_front = opt(e), opt(e)
         self.unique = torch.empty(self.uniq_cap, **i32)
-        self.seed_locals = torch.empty(self.max_nb * self.max_bs, **i32)
+        self.frontier = torch.empty(self.H * self.fcap, **i32)
+        nseed = self.max_nb * self.max_bs
+        self.seed_rows, self.seed_front = opt(nseed), opt(nseed)
         self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=device)
-        self.seeds_dev = torch.empty(self.max_nb * self.max_bs, **i32)
+        self.seeds_dev = torch.empty(nseed, **i32)
         self.seed_off = torch.empty(self.max_nb + 1, dtype=torch.int64, device=device)
         self.keys = torch.empty(2 * self.max_nb, dtype=torch.int64, device=device)
         self.counts = torch.empty(self.counts_len, dtype=torch.int64, device=device)
         self._fan = _lib.i32_array(self.fanouts.counts)
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        self._out = _lib.FglSampleOut(
+            ptr(self.tgt), ptr(self.src), ptr(self.wgt), e, ptr(self.tgt_row), ptr(self.src_row),
+            ptr(self.tgt_front), ptr(self.src_front), ptr(self.unique), self.uniq_cap,
+            ptr(self.frontier), self.fcap, ptr(self.seed_rows), ptr(self.seed_front),
+            ptr(self.counts))
 
-    def counts_len_for(self, nb):
-        return (self.H * nb + 1) + (nb + 1) + nb + self.H * nb + 1
-
-    def stage(self, seed_lists, seeds_for_rng, pinned=None):
-        """Host->device copy of a window's seeds, offsets and Philox keys
-        (non-blocking from pinned memory when ``pinned`` buffers are given)."""
+    def stage(self, seed_lists, seeds_for_rng):
+        """Host->device copy of a window's seeds, offsets and Philox keys."""
         torch = self.torch
         nb = len(seed_lists)
         if nb < 1 or nb > self.max_nb:
             raise ValidationError(f"window of {nb} batches exceeds max_batches={self.max_nb}")
         sizes = [len(s) for s in seed_lists]
+        if min(sizes) == 0:
+            raise ValidationError("seeds must not be empty")
         if max(sizes) > self.max_bs:
             raise ValidationError("batch exceeds max_batch_size")
         off = np.zeros(nb + 1, dtype=np.int64)
         np.cumsum(sizes, out=off[1:])
         flat = np.concatenate([np.asarray(s) for s in seed_lists]).astype(np.int64)
-        if flat.size == 0 or min(sizes) == 0:
-            raise ValidationError("seeds must not be empty")
         if flat.max() >= self.g.num_nodes or flat.min() < 0:
             raise ValidationError("seed id out of range")
         keys = np.array([philox_key(s) for s in seeds_for_rng], dtype=np.uint64).reshape(-1)
         n = int(off[-1])
-        self.seeds_dev[:n].copy_(torch.from_numpy(flat.astype(np.int32)), non_blocking=True)
-        self.seed_off[: nb + 1].copy_(torch.from_numpy(off), non_blocking=True)
-        self.keys[: 2 * nb].copy_(torch.from_numpy(keys.view(np.int64)), non_blocking=True)
+        self.seeds_dev[:n].copy_(torch.from_numpy(flat.astype(np.int32)))
+        self.seed_off[: nb + 1].copy_(torch.from_numpy(off))
+        self.keys[: 2 * nb].copy_(torch.from_numpy(keys.view(np.int64)))
         return nb, off
 
     def run(self, nb: int, seed_off_host: np.ndarray, stream=None) -> DeviceWindow:
         """Launch the window sampler on staged inputs (asynchronous)."""
-        torch = self.torch
-        st = stream if stream is not None else torch.cuda.current_stream()
-        total = int(seed_off_host[-1])
-        lt = self.local_tgt.data_ptr() if self.local_tgt is not None else None
-        ls = self.local_src.data_ptr() if self.local_src is not None else None
+        st = stream if stream is not None else self.torch.cuda.current_stream()
         _lib.call("fgl_sample_window", self.g.struct, self.seeds_dev.data_ptr(),
-                  self.seed_off.data_ptr(), total, nb, self.keys.data_ptr(), self._fan, self.H,
-                  self.tgt.data_ptr(), self.src.data_ptr(), self.wgt.data_ptr(), self.edge_cap,
-                  lt, ls, self.unique.data_ptr(), self.uniq_cap, self.seed_locals.data_ptr(),
-                  self.counts.data_ptr(), self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
-        return DeviceWindow(nb, self.H, self.tgt, self.src, self.wgt, self.local_tgt,
-                            self.local_src, self.unique, self.seed_locals, self.seeds_dev,
-                            seed_off_host, self.counts, self)
+                  self.seed_off.data_ptr(), int(seed_off_host[-1]), nb, self.keys.data_ptr(),
+                  self._fan, self.H, self._out, self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+        return DeviceWindow(nb, self.H, self, seed_off_host)
 
     def sample(self, seed_lists, seeds_for_rng) -> DeviceWindow:
         nb, off = self.stage(seed_lists, seeds_for_rng)

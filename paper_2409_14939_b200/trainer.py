@@ -1,0 +1,573 @@
+"""Mini-batch GNN training on B200: drop-in for ``minigl.trainer``.
+
+The epoch driver keeps the reference's structure (trainer.py:246-349): a
+fixed Philox partition of the training IDs into batches, windows of
+``window_n`` batches, per-batch sampling seed ``derive_seed(seed, 13, j)``,
+Match-Reorder of each window, then forward / fp64 loss / backward / SGD per
+batch in schedule order.  Everything per batch runs in HBM through
+``libfastgl_b200.so``:
+
+  sample  fgl_sample_window     whole window in one launch sequence
+  map     (fused into sampling) window rows + frontier indices
+  io      fgl_match_counts + greedy order, fgl_gather_rows (Match delta load)
+  prepare fgl_prepare_layer     block CSR + stable transpose + GCN weights
+  compute fgl_spmm / fgl_dense_fwd / fgl_softmax_xent / fgl_dense_bwd / fgl_sgd
+
+GCN runs on the sampled *block* graph: model layer i (hop h = H-1-i) computes
+only the rows of hop h's frontier -- every other row of the reference's
+all-rows layer (trainer.py:182-195) is a zero aggregation whose value no later
+layer or loss term reads.  GIN needs every row (its self term carries rows
+forward), so it runs the full unique-node layout like the reference.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+from .graph import device_graph
+from .sampler import Fanouts, WindowSampler, derive_seed, make_epoch_batches
+
+__all__ = ["ModelConfig", "PipelineFlags", "EpochStats", "TrainReport", "train", "derive_seed",
+           "init_params", "DeviceModel", "Pipeline", "phase_breakdown", "PHASES"]
+
+PHASES = ("sample", "map", "io_sim", "compute")
+
+
+def _ld(d: int) -> int:
+    return (int(d) + 3) // 4 * 4
+
+
+@dataclass
+class ModelConfig:
+    """Architecture and schedule knobs (trainer.py:45-79)."""
+
+    layer_dims: tuple
+    fanouts: Fanouts
+    arch: str = "gcn"
+    batch_size: int = 64
+    window_n: int = 8
+    epochs: int = 20
+    lr: float = 0.3
+    seed: int = 0
+    map_workers: int = 1
+    tiles: object = None
+
+    def __post_init__(self):
+        if not isinstance(self.fanouts, Fanouts):
+            self.fanouts = Fanouts(self.fanouts)
+        self.layer_dims = tuple(int(d) for d in self.layer_dims)
+        if self.arch not in ("gcn", "gin"):
+            raise ValidationError(f"unknown arch {self.arch!r}")
+        if len(self.layer_dims) < 2 or any(d < 1 for d in self.layer_dims):
+            raise ValidationError("layer_dims needs input dim, optional hiddens, and classes")
+        if len(self.fanouts) != len(self.layer_dims) - 1:
+            raise ValidationError(
+                f"{len(self.fanouts)} fanouts for {len(self.layer_dims) - 1} aggregation layers")
+        if self.batch_size < 1 or self.window_n < 1 or self.epochs < 1:
+            raise ValidationError("batch_size, window_n and epochs must be >= 1")
+        if self.lr < 0:
+            raise ValidationError("lr must be non-negative")
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.layer_dims) - 1
+
+
+@dataclass
+class PipelineFlags:
+    """IO-path switches (trainer.py:82-89); only ``reorder`` changes the trajectory."""
+
+    match: bool = True
+    reorder: bool = True
+    memory_aware: bool = True
+
+
+@dataclass
+class EpochStats:
+    loss: float
+    accuracy: float
+    traffic: dict
+    phase_seconds: dict
+    modeled_fetch_seconds: float = 0.0
+
+
+@dataclass
+class TrainReport:
+    config: ModelConfig
+    flags: PipelineFlags
+    epochs: list = field(default_factory=list)
+
+    @property
+    def losses(self) -> list:
+        return [e.loss for e in self.epochs]
+
+
+def init_params(layer_dims, seed: int):
+    """Glorot-normal weights, zero biases from Philox(derive_seed(seed, 101))
+    (trainer.py:145-153).  Host-side, once per run."""
+    rng = np.random.Generator(np.random.Philox(derive_seed(seed, 101)))
+    params = []
+    for d_in, d_out in zip(layer_dims, layer_dims[1:]):
+        scale = np.sqrt(2.0 / (d_in + d_out))
+        w = (rng.standard_normal((d_in, d_out)) * scale).astype(np.float32)
+        params.append([w, np.zeros(d_out, dtype=np.float32)])
+    return params
+
+
+class DeviceModel:
+    """All weights/biases in one flat f32 buffer (one allreduce bucket for DP),
+    with a matching flat gradient buffer."""
+
+    def __init__(self, layer_dims, params, device="cuda"):
+        import torch
+        self.dims = tuple(layer_dims)
+        sizes = []
+        for a, b in zip(self.dims, self.dims[1:]):
+            sizes += [a * b, b]
+        self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        flat = np.concatenate([np.concatenate([w.ravel(), b.ravel()]) for w, b in params])
+        self.flat = torch.from_numpy(flat.astype(np.float32)).to(device)
+        self.grad = torch.zeros_like(self.flat)
+
+    def _ptr(self, t, k):
+        return t.data_ptr() + 4 * int(self.offsets[k])
+
+    def W(self, i):
+        return self._ptr(self.flat, 2 * i)
+
+    def b(self, i):
+        return self._ptr(self.flat, 2 * i + 1)
+
+    def dW(self, i):
+        return self._ptr(self.grad, 2 * i)
+
+    def db(self, i):
+        return self._ptr(self.grad, 2 * i + 1)
+
+    def to_numpy(self):
+        f = self.flat.cpu().numpy()
+        out = []
+        for i, (a, b) in enumerate(zip(self.dims, self.dims[1:])):
+            o = self.offsets[2 * i]
+            out.append([f[o : o + a * b].reshape(a, b).copy(), f[o + a * b : o + a * b + b].copy()])
+        return out
+
+    def grads_numpy(self):
+        g = self.grad.cpu().numpy()
+        out = []
+        for i, (a, b) in enumerate(zip(self.dims, self.dims[1:])):
+            o = self.offsets[2 * i]
+            out.append([g[o : o + a * b].reshape(a, b).copy(), g[o + a * b : o + a * b + b].copy()])
+        return out
+
+
+def greedy_order(m: np.ndarray) -> list:
+    """Greedy chain of schedule.py:92-113 on a match-degree matrix: batch 0
+    first, then the unused batch with the highest degree to the last one;
+    ties and non-positive rows resolve to the lowest index."""
+    n = len(m)
+    order, used, cur = [0], np.zeros(n, dtype=bool), 0
+    used[0] = True
+    for _ in range(n - 1):
+        row = np.where(used, -1.0, m[cur])
+        h = int(np.argmax(row))
+        if row[h] <= 0.0:
+            h = int(np.flatnonzero(~used)[0])
+        order.append(h)
+        used[h] = True
+        cur = h
+    return order
+
+
+class Pipeline:
+    """Device-resident training pipeline for one graph / feature store / model.
+
+    ``feature_store``: "device" keeps the feature matrix in HBM; "host" keeps
+    it in pinned host memory and every x0 row not reused through Match crosses
+    the host link (zero-copy reads, config 4 of BASELINE.json).
+    """
+
+    def __init__(self, g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None,
+                 device="cuda", feature_store="device", params=None, dist=None):
+        import torch
+        self.torch = torch
+        self.cfg = cfg
+        self.flags = flags or PipelineFlags()
+        self.device = device
+        self.dist = dist
+        self.dg = device_graph(g, device)
+        data = feats.data if hasattr(feats, "data") else feats
+        if isinstance(data, torch.Tensor):
+            ft = data
+        else:
+            ft = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))
+        self.d0 = int(ft.shape[1])
+        if self.d0 != cfg.layer_dims[0]:
+            raise ValidationError(f"feature dim {self.d0} != model input dim {cfg.layer_dims[0]}")
+        self.ldf = _ld(self.d0)
+        self.feature_store = feature_store
+        if feature_store == "host":
+            host = torch.zeros((ft.shape[0], self.ldf), dtype=torch.float32).pin_memory()
+            host[:, : self.d0].copy_(ft.cpu() if ft.is_cuda else ft)
+            self.feats = host  # UVA: the pinned host pointer is device-addressable
+        else:
+            dev = torch.zeros((ft.shape[0], self.ldf), dtype=torch.float32, device=device)
+            dev[:, : self.d0].copy_(ft.to(device) if not ft.is_cuda else ft)
+            self.feats = dev
+        lab = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(np.asarray(labels, dtype=np.int64))
+        self.labels = lab.to(device=device, dtype=torch.int64)
+        self.sampler = WindowSampler(self.dg, cfg.fanouts, cfg.batch_size, cfg.window_n, device=device)
+        out = _lib.i64_array([0, 0, 0])
+        _lib.call("fgl_sample_ws_bitmaps", self.dg.num_nodes, cfg.window_n, self.sampler.fcap,
+                  self.sampler.uniq_cap, out)
+        self.bm_off, self.prefix_off, self.words = int(out[0]), int(out[1]), int(out[2])
+        self.model = DeviceModel(cfg.layer_dims, params if params is not None else init_params(cfg.layer_dims, cfg.seed), device)
+        self.L = cfg.num_layers
+        self.H = len(cfg.fanouts)
+        self.compact = cfg.arch == "gcn"
+        self.pairs = torch.zeros(120, dtype=torch.int64, device=device)
+        self.loaded = torch.zeros(1, dtype=torch.int64, device=device)
+        self.loss_dev = torch.zeros(max(cfg.window_n, 1), dtype=torch.float64, device=device)
+        dims = cfg.layer_dims
+        self.bwd_ws = torch.empty(max(_lib.lib().fgl_dense_bwd_ws_bytes(a, b) for a, b in zip(dims, dims[1:])),
+                                  dtype=torch.uint8, device=device)
+        self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
+        self._bufs = {}
+        self.gpu_launches = 0
+
+    # ------------------------------------------------------------ buffers --
+    def _buf(self, name, rows, cols, dtype=None):
+        torch = self.torch
+        dtype = dtype or torch.float32
+        need = max(int(rows), 1) * int(cols)
+        t = self._bufs.get(name)
+        if t is None or t.numel() < need or t.dtype != dtype:
+            t = torch.empty(int(need * 1.25) + 64, dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t
+
+    @property
+    def stream(self):
+        return self.torch.cuda.current_stream().cuda_stream
+
+    def _call(self, name, *args):
+        _lib.call(name, *args)
+        self.gpu_launches += 1
+
+    # ----------------------------------------------------------- schedule --
+    def schedule(self, win, nb: int) -> list:
+        """Match-degree matrix on the GPU from the batches' node bitmaps, greedy
+        chain on the host (schedule.py:68-113)."""
+        if not self.flags.reorder or nb < 2:
+            return list(range(nb))
+        ws = self.sampler.ws.data_ptr()
+        self._call("fgl_match_counts", ws + self.bm_off, self.words, nb, self.pairs.data_ptr(), self.stream)
+        pairs = self.pairs.cpu().numpy()
+        sizes = [win.unique_range(b)[1] - win.unique_range(b)[0] for b in range(nb)]
+        m = np.zeros((nb, nb), dtype=np.float64)
+        for i in range(nb):
+            for j in range(i + 1, nb):
+                k = i * 16 - i * (i + 1) // 2 + (j - i - 1)
+                m[i, j] = m[j, i] = int(pairs[k]) / min(sizes[i], sizes[j])
+        self.last_match = m
+        return greedy_order(m)
+
+    # ------------------------------------------------------------ prepare --
+    def prepare(self, win) -> list:
+        """Block CSR (+ stable transpose, GCN weights) of every model layer for
+        the whole window (trainer.py:165-179)."""
+        torch = self.torch
+        s = self.sampler
+        layers = [None] * self.L
+        for h in range(self.H):
+            e0, e1 = win.hop_edges(h)
+            nnz = e1 - e0
+            if self.compact:
+                lt, ls = s.tgt_front, s.src_front
+                rows = win.front_total(h)
+                cols = win.front_total(h + 1) if h + 1 < self.H else win.unique_total()
+            else:
+                lt, ls = s.tgt_row, s.src_row
+                rows = cols = win.unique_total()
+            rows, cols = max(rows, 1), max(cols, 1)
+            lay = {
+                "indptr": self._buf(f"ip{h}", rows + 1, 1, torch.int64),
+                "w": self._buf(f"w{h}", max(nnz, 1), 1),
+                "t_indptr": self._buf(f"tip{h}", cols + 1, 1, torch.int64),
+                "t_col": self._buf(f"tc{h}", max(nnz, 1), 1, torch.int32),
+                "t_w": self._buf(f"tw{h}", max(nnz, 1), 1),
+                "col": ls.data_ptr() + 4 * e0,
+                "nnz": nnz,
+            }
+            wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
+            pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
+            self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
+                       cols, 1 if self.cfg.arch == "gcn" else 0, lay["indptr"].data_ptr(),
+                       lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
+                       lay["t_w"].data_ptr(), pws.data_ptr(), wsb, self.stream)
+            layers[self.H - 1 - h] = lay
+        return layers
+
+    # ---------------------------------------------------------- row spaces --
+    def _rows(self, win, i, b):
+        """(first, last) row of batch b in model layer i's output row space."""
+        if self.compact:
+            return win.front_range(self.H - 1 - i, b)
+        return win.unique_range(b)
+
+    def _in_base(self, win, i, b):
+        """Row of batch b's first input row in layer i's input index space."""
+        if i == 0 or not self.compact:
+            return win.unique_range(b)[0]
+        return win.front_range(self.H - i, b)[0]
+
+    # -------------------------------------------------------------- batch --
+    def batch_step(self, win, b, prev, slot, layers, x0_slot):
+        """Load x0, forward, loss, backward, SGD for batch b of the window."""
+        torch = self.torch
+        s = self.sampler
+        m = self.model
+        dims = self.cfg.layer_dims
+        st = self.stream
+        u0, u1 = win.unique_range(b)
+        U = u1 - u0
+        x0 = self._buf(f"x0_{x0_slot}", U, self.ldf)
+        ws = s.ws.data_ptr()
+        if prev is not None:
+            p0 = win.unique_range(prev)[0]
+            prev_bm = ws + self.bm_off + 4 * prev * self.words
+            prev_pf = ws + self.prefix_off + 4 * prev * self.words
+            prev_x = self._bufs[f"x0_{1 - x0_slot}"].data_ptr()
+        else:
+            p0, prev_bm, prev_pf, prev_x = 0, None, None, None
+        self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0,
+                   s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
+                   x0.data_ptr(), self.ldf, self.loaded.data_ptr(), st)
+        # forward
+        X, ldx = x0, self.ldf
+        H_bufs, Y_bufs, ns = [], [], []
+        for i in range(self.L):
+            din, dout = dims[i], dims[i + 1]
+            r0, r1 = self._rows(win, i, b)
+            n = r1 - r0
+            lay = layers[i]
+            Hb = self._buf(f"h{i}", n, _ld(din))
+            self_x = X.data_ptr() if not self.compact else None
+            self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(), n,
+                       self._in_base(win, i, b), X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(),
+                       _ld(din), din, st)
+            Yb = self._buf(f"y{i}", n, _ld(dout))
+            self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout,
+                       Yb.data_ptr(), _ld(dout), 1 if i < self.L - 1 else 0, st)
+            H_bufs.append(Hb)
+            Y_bufs.append(Yb)
+            ns.append(n)
+            X, ldx = Yb, _ld(dout)
+        # loss over the seed rows of the last layer
+        s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
+        C = dims[-1]
+        r0, _ = self._rows(win, self.L - 1, b)
+        dY = self._buf("dy_last", ns[-1], _ld(C))
+        if not self.compact:
+            self._call("fgl_fill_rows", dY.data_ptr(), _ld(C), ns[-1], C, None, 0, st)
+        rows_ptr = (s.seed_front if self.compact else s.seed_rows).data_ptr() + 4 * s0
+        self._call("fgl_softmax_xent", Y_bufs[-1].data_ptr(), _ld(C), rows_ptr, r0,
+                   s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), s1 - s0, C,
+                   dY.data_ptr(), _ld(C), self.loss_dev.data_ptr() + 8 * slot,
+                   self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
+        # backward
+        dX, lddx = dY, _ld(C)
+        for i in range(self.L - 1, -1, -1):
+            din, dout = dims[i], dims[i + 1]
+            n = ns[i]
+            mask = Y_bufs[i].data_ptr() if i < self.L - 1 else None
+            dH = self._buf(f"dh{i}", n, _ld(din)) if i > 0 else None
+            self._call("fgl_dense_bwd", H_bufs[i].data_ptr(), _ld(din), n, din, m.W(i), dout,
+                       dX.data_ptr(), lddx, mask, _ld(dout), m.dW(i), m.db(i),
+                       dH.data_ptr() if dH is not None else None, _ld(din), self.bwd_ws.data_ptr(),
+                       self.bwd_ws.numel(), st)
+            if i > 0:
+                lay = layers[i]
+                q0, q1 = self._rows(win, i - 1, b)
+                nx = q1 - q0
+                dXn = self._buf(f"dx{i}", nx, _ld(din))
+                col_base = self._rows(win, i, b)[0]
+                self_x = dH.data_ptr() if not self.compact else None
+                self._call("fgl_spmm", lay["t_indptr"].data_ptr() + 8 * q0, lay["t_col"].data_ptr(),
+                           lay["t_w"].data_ptr(), nx, col_base, dH.data_ptr(), _ld(din), self_x,
+                           _ld(din), dXn.data_ptr(), _ld(din), din, st)
+                dX, lddx = dXn, _ld(din)
+        if self.dist is not None:
+            self.dist.allreduce_mean(self.model.grad)
+        self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+
+    # ------------------------------------------------------------- window --
+    def run_window(self, seed_lists, rng_seeds, phase=None):
+        """Sample, schedule, prepare and train one window; returns (order,
+        per-batch device losses tensor view)."""
+        torch = self.torch
+        tick = (lambda: (torch.cuda.synchronize(), time.perf_counter())[1]) if phase is not None else None
+        t0 = tick() if tick else 0.0
+        win = self.sampler.sample(seed_lists, rng_seeds)
+        self.gpu_launches += 1
+        win.host_counts()
+        nb = len(seed_lists)
+        t1 = tick() if tick else 0.0
+        order = self.schedule(win, nb)
+        t2 = tick() if tick else 0.0
+        layers = self.prepare(win)
+        t3 = tick() if tick else 0.0
+        for j, b in enumerate(order):
+            prev = order[j - 1] if (j > 0 and self.flags.match) else None
+            self.batch_step(win, b, prev, j, layers, j % 2)
+        if tick:
+            t4 = tick()
+            phase["sample"] += t1 - t0
+            phase["io_sim"] += t2 - t1
+            phase["map"] += t3 - t2
+            phase["compute"] += t4 - t3
+        self.last_window = win
+        return order, self.loss_dev[:nb]
+
+
+def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None, *,
+          train_ids=None, val_ids=None, cost_params=None, feature_store="device") -> TrainReport:
+    """Drop-in for trainer.train (trainer.py:246-349): same batch stream, same
+    schedule, per-batch SGD; loss/accuracy per epoch; IO accounting from the
+    loader's real row counts."""
+    import torch
+    flags = flags or PipelineFlags()
+    labels_np = np.asarray(labels, dtype=np.int64)
+    n = int(g.num_nodes)
+    if len(labels_np) != n:
+        raise ValidationError("labels length must equal num_nodes")
+    fdata = feats.data if hasattr(feats, "data") else feats
+    if fdata.shape[0] != n:
+        raise ValidationError("feature rows must equal num_nodes")
+    if fdata.shape[1] != cfg.layer_dims[0]:
+        raise ValidationError(f"feature dim {fdata.shape[1]} != model input dim {cfg.layer_dims[0]}")
+    if labels_np.max() >= cfg.layer_dims[-1]:
+        raise ValidationError("label exceeds the class count")
+    if train_ids is None or val_ids is None:
+        rng = np.random.Generator(np.random.Philox(derive_seed(cfg.seed, 7)))
+        perm = rng.permutation(n).astype(np.uint64)
+        cut = max(1, int(0.8 * n))
+        train_ids = perm[:cut] if train_ids is None else np.asarray(train_ids, np.uint64)
+        val_ids = perm[cut:] if val_ids is None else np.asarray(val_ids, np.uint64)
+    train_ids = np.asarray(train_ids, dtype=np.uint64)
+    val_ids = np.asarray(val_ids, dtype=np.uint64)
+    if train_ids.size == 0:
+        raise ValidationError("training split is empty")
+    pipe = Pipeline(g, feats, labels_np, cfg, flags, feature_store=feature_store)
+    seed_batches = make_epoch_batches(g, train_ids, cfg.batch_size, derive_seed(cfg.seed, 11))
+    windows = [seed_batches[i : i + cfg.window_n] for i in range(0, len(seed_batches), cfg.window_n)]
+    report = TrainReport(config=cfg, flags=flags)
+    d = pipe.d0
+    for _ in range(cfg.epochs):
+        phase = dict.fromkeys(PHASES, 0.0)
+        pipe.loaded.zero_()
+        loss_sum, seen, base, total_rows = 0.0, 0, 0, 0
+        for win_seeds in windows:
+            rs = [derive_seed(cfg.seed, 13, base + j) for j in range(len(win_seeds))]
+            base += len(win_seeds)
+            order, losses = pipe.run_window([w.astype(np.int64) for w in win_seeds], rs, phase)
+            lv = losses.cpu().numpy()
+            for j, bi in enumerate(order):
+                loss_sum += float(lv[j])  # sum of per-seed losses = mean * batch size
+                seen += len(win_seeds[bi])
+            win = pipe.last_window
+            total_rows += win.unique_total()
+        loaded = int(pipe.loaded.item())
+        if flags.match:
+            traffic = {"bytes_host_to_device": loaded * 4 * d,
+                       "bytes_served_by_match": (total_rows - loaded) * 4 * d,
+                       "bytes_served_by_cache": 0}
+        else:
+            traffic = {"bytes_host_to_device": total_rows * 4 * d, "bytes_served_by_match": 0,
+                       "bytes_served_by_cache": 0}
+        acc = evaluate(pipe, g, val_ids) if val_ids.size else float("nan")
+        report.epochs.append(EpochStats(loss=loss_sum / max(seen, 1), accuracy=acc, traffic=traffic,
+                                        phase_seconds=phase))
+    report.pipeline = pipe
+    return report
+
+
+def evaluate(pipe: Pipeline, g, eval_ids) -> float:
+    """Sampled-neighbourhood accuracy with fixed draws derive_seed(seed,17,i)
+    (trainer.py:352-365): forward only, argmax over the seed rows."""
+    import torch
+    cfg = pipe.cfg
+    correct = total = 0
+    eval_ids = np.asarray(eval_ids, dtype=np.uint64)
+    ev = getattr(pipe, "_eval_sampler", None)
+    if ev is None:
+        ev = WindowSampler(pipe.dg, cfg.fanouts, cfg.batch_size, 1, device=pipe.device)
+        pipe._eval_sampler = ev
+    saved = pipe.sampler
+    pipe.sampler = ev
+    try:
+        for i in range(0, len(eval_ids), cfg.batch_size):
+            seeds = eval_ids[i : i + cfg.batch_size]
+            win = ev.sample([seeds.astype(np.int64)], [derive_seed(cfg.seed, 17, i)])
+            win.host_counts()
+            layers = pipe.prepare(win)
+            logits, rows = pipe.forward_only(win, 0, layers)
+            pred = logits[rows].argmax(dim=1)
+            lab = pipe.labels[torch.from_numpy(seeds.astype(np.int64)).to(pipe.device)]
+            correct += int((pred == lab).sum().item())
+            total += len(seeds)
+    finally:
+        pipe.sampler = saved
+    return correct / max(total, 1)
+
+
+def _forward_only(self, win, b, layers):
+    """Forward pass of batch b; returns (logits tensor [n, C], seed row index tensor)."""
+    torch = self.torch
+    s = self.sampler
+    m = self.model
+    dims = self.cfg.layer_dims
+    st = self.stream
+    u0, u1 = win.unique_range(b)
+    x0 = self._buf("x0_eval", u1 - u0, self.ldf)
+    self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0, s.unique.data_ptr() + 4 * u0,
+               u1 - u0, None, None, 0, None, self.ldf, x0.data_ptr(), self.ldf, None, st)
+    X, ldx = x0, self.ldf
+    for i in range(self.L):
+        din, dout = dims[i], dims[i + 1]
+        r0, r1 = self._rows(win, i, b)
+        n = r1 - r0
+        Hb = self._buf(f"h{i}", n, _ld(din))
+        self._call("fgl_spmm", layers[i]["indptr"].data_ptr() + 8 * r0, layers[i]["col"],
+                   layers[i]["w"].data_ptr(), n, self._in_base(win, i, b), X.data_ptr(), ldx,
+                   X.data_ptr() if not self.compact else None, ldx, Hb.data_ptr(), _ld(din), din, st)
+        Yb = self._buf(f"ye{i}", n, _ld(dout))
+        self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout, Yb.data_ptr(),
+                   _ld(dout), 1 if i < self.L - 1 else 0, st)
+        X, ldx = Yb, _ld(dout)
+    C = dims[-1]
+    n_last = self._rows(win, self.L - 1, b)
+    n = n_last[1] - n_last[0]
+    logits = X[: n * _ld(C)].view(n, _ld(C))[:, :C]
+    s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
+    rows = (s.seed_front if self.compact else s.seed_rows)[s0:s1].long() - n_last[0]
+    return logits, rows
+
+
+Pipeline.forward_only = _forward_only
+
+
+def phase_breakdown(report: TrainReport) -> dict:
+    """Percentage of wall time per pipeline phase (trainer.py:368-376)."""
+    if not report.epochs:
+        raise ValidationError("cannot break down an empty report")
+    totals = {p: sum(e.phase_seconds[p] for e in report.epochs) for p in PHASES}
+    overall = sum(totals.values())
+    if overall <= 0:
+        raise ValidationError("report has no recorded time")
+    return {p: 100.0 * t / overall for p, t in totals.items()}

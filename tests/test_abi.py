@@ -50,7 +50,7 @@ def test_bounds_are_host_only(lib):
     edge_cap, fcap, uniq_cap, ws, clen = list(out)
     assert edge_cap == 64 * 5 + 64 * 5 * 3 + 32 * 5 + 32 * 5 * 3
     assert uniq_cap == min(1000, 64 + 320 + 960) + min(1000, 32 + 160 + 480)
-    assert clen == 2 * 2 + 1 + 3 + 2 + 2 * 2 + 1
+    assert clen == (2 * 2 + 1) + 2 * (2 + 1) + (2 + 1) + 2 + 1
     assert ws > 0
     with pytest.raises(Exception):
         _lib.call("fgl_sample_bounds", 0, _lib.i64_array([1]), 1, _lib.i32_array([1]), 1, out)

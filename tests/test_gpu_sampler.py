@@ -102,8 +102,28 @@ def test_window_local_ids(cfg1_graph):
             assert np.array_equal(lt, np.searchsorted(want.unique_nodes, t))
             assert np.array_equal(ls, np.searchsorted(want.unique_nodes, s))
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
-        sl = win.seed_locals[s0:s1].cpu().numpy()
-        assert np.array_equal(sl, np.searchsorted(want.unique_nodes, seed_lists[b].astype(np.uint64)))
+        u0 = win.unique_range(b)[0]
+        seeds_b = seed_lists[b].astype(np.uint64)
+        assert np.array_equal(ws.seed_rows[s0:s1].cpu().numpy() - u0,
+                              np.searchsorted(want.unique_nodes, seeds_b))
+        # block layout: frontier lists and frontier-indexed edges
+        fronts = [np.unique(seeds_b)] + [np.unique(s) for _, s, _ in want.layers]
+        for h in range(2):
+            f0, f1 = win.front_range(h, b)
+            fl = ws.frontier[h * ws.fcap + f0 : h * ws.fcap + f1].cpu().numpy().astype(np.uint64)
+            assert np.array_equal(fl, fronts[h])
+            e0, e1 = win.edge_range(h, b)
+            t, s, _ = want.layers[h]
+            assert np.array_equal(ws.tgt_front[e0:e1].cpu().numpy() - f0, np.searchsorted(fronts[h], t))
+            sf = ws.src_front[e0:e1].cpu().numpy()
+            if h == 0:
+                g0 = win.front_range(1, b)[0]
+                assert np.array_equal(sf - g0, np.searchsorted(fronts[1], s))
+            else:
+                assert np.array_equal(sf - u0, np.searchsorted(want.unique_nodes, s))
+        f0 = win.front_range(0, b)[0]
+        assert np.array_equal(ws.seed_front[s0:s1].cpu().numpy() - f0,
+                              np.searchsorted(fronts[0], seeds_b))
     # the same sampler object is reusable for a smaller window
     win2 = ws.sample(seed_lists[:2], rng_seeds[:2])
     assert_same_batch(win2.to_batch(1), oracle.sample_khop(cfg1_graph, seed_lists[1], [10, 5], rng_seeds[1]))
