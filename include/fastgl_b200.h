@@ -37,6 +37,8 @@ extern "C" {
 /* ------------------------------------------------------------------ misc -- */
 const char* fgl_last_error(void);
 int fgl_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+int64_t fgl_launch_count(void);
 /* Device properties the build was compiled for; returns FGL_E_CUDA without a GPU. */
 int fgl_device_check(int device);
 

@@ -53,6 +53,7 @@ class FglSampleOut(C.Structure):
 SIGNATURES = {
     "fgl_last_error": (C.c_char_p, []),
     "fgl_version": (C.c_int, []),
+    "fgl_launch_count": (C.c_int64, []),
     "fgl_device_check": (C.c_int, [C.c_int]),
     "fgl_sample_bounds": (C.c_int, [C.c_int64, c_i64p, C.c_int32, c_i32p, C.c_int32, c_i64p]),
     "fgl_sample_window": (C.c_int, [

@@ -1,6 +1,7 @@
 // C-ABI plumbing: error strings, version, device check, Philox known-answer
 // and ALU-roofline probe kernels.
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -10,6 +11,9 @@
 namespace fgl {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[512];
@@ -63,6 +67,8 @@ const char* fgl_last_error(void) { return fgl::g_last_error.c_str(); }
 
 int fgl_version(void) { return 100; }
 
+int64_t fgl_launch_count(void) { return fgl::g_launches.load(std::memory_order_relaxed); }
+
 int fgl_device_check(int device) {
   cudaDeviceProp p;
   cudaError_t e = cudaGetDeviceProperties(&p, device);
@@ -85,14 +91,14 @@ int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uin
   const int64_t blocks = ((start + count - 1) >> 2) - (start >> 2) + 1;
   const int threads = 256;
   const int grid = (int)std::min<int64_t>(fgl::ceil_div(blocks, threads), 148 * 32);
-  fgl::philox_words_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(k0, k1, start, count, out);
+  FGL_COUNT_LAUNCH(), fgl::philox_words_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(k0, k1, start, count, out);
   FGL_LAUNCH_CHECK("philox_words_kernel");
   return FGL_OK;
 }
 
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream) {
   // `out` must hold 148*8*256 words (one per thread of the fixed grid).
-  fgl::philox_bench_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(k0, k1, blocks, out);
+  FGL_COUNT_LAUNCH(), fgl::philox_bench_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(k0, k1, blocks, out);
   FGL_LAUNCH_CHECK("philox_bench_kernel");
   return FGL_OK;
 }

@@ -21,6 +21,11 @@ constexpr int kNumSMs = 148;
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 
+// Process-wide count of kernels this library has launched (bench.py reports
+// it as gpu_launches); every launch site is written FGL_COUNT_LAUNCH(), k<<<...>>>(...).
+void count_launch();
+#define FGL_COUNT_LAUNCH() ::fgl::count_launch()
+
 #define FGL_CUDA(call)                                              \
   do {                                                              \
     cudaError_t _e = (call);                                        \

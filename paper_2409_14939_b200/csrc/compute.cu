@@ -114,7 +114,7 @@ void launch_spmm(const int64_t* indptr, const int32_t* col, const float* w, int6
   constexpr int G = 32 / L;
   const int64_t warps = ceil_div(nrows, G);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), 148 * 16));
-  spmm_kernel<L, CPL><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
+  FGL_COUNT_LAUNCH(), spmm_kernel<L, CPL><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
                                             ld_self, Y, ldy, d4);
 }
 
@@ -377,7 +377,7 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   }
   if (n == 0) return FGL_OK;
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
-  gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
+  FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
                                                       relu, nullptr, 0);
   FGL_LAUNCH_CHECK("gemm_kernel(fwd)");
   return FGL_OK;
@@ -407,13 +407,13 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   float* pb = pw + (int64_t)chunks * din * dout;
   if (n > 0) {
     dim3 g(chunks, (unsigned)ceil_div(din, WK), (unsigned)ceil_div(dout, WN));
-    wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, rows_per,
+    FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, rows_per,
                                             pw, pb);
-    reduce_partials_kernel<<<blocks_for((int64_t)din * dout), 256, 0, st>>>(pw, chunks, (int64_t)din * dout, dW);
-    reduce_partials_kernel<<<blocks_for(dout), 256, 0, st>>>(pb, chunks, dout, db);
+    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<blocks_for((int64_t)din * dout), 256, 0, st>>>(pw, chunks, (int64_t)din * dout, dW);
+    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<blocks_for(dout), 256, 0, st>>>(pb, chunks, dout, db);
     if (dH) {
       dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
-      gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,
+      FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,
                                         Xout, ldxo);
     }
   } else {
@@ -438,9 +438,9 @@ int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int6
   }
   const int blocks = (int)std::min<int64_t>(148 * 8, ceil_div(B, 8));
   double* part = static_cast<double*>(ws);
-  softmax_xent_kernel<<<blocks, 256, 0, st>>>(logits, ldl, rows, row_base, seed_ids, labels, B, C,
+  FGL_COUNT_LAUNCH(), softmax_xent_kernel<<<blocks, 256, 0, st>>>(logits, ldl, rows, row_base, seed_ids, labels, B, C,
                                               dlogits, ldd, part);
-  sum_doubles_kernel<<<1, 1024, 0, st>>>(part, blocks * 8, loss_sum);
+  FGL_COUNT_LAUNCH(), sum_doubles_kernel<<<1, 1024, 0, st>>>(part, blocks * 8, loss_sum);
   FGL_LAUNCH_CHECK("softmax_xent");
   return FGL_OK;
 }
@@ -451,7 +451,7 @@ int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream
     return FGL_E_INVALID;
   }
   if (n == 0) return FGL_OK;
-  sgd_kernel<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
+  FGL_COUNT_LAUNCH(), sgd_kernel<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
   FGL_LAUNCH_CHECK("sgd_kernel");
   return FGL_OK;
 }
@@ -463,7 +463,7 @@ int fgl_fill_rows(float* Y, int64_t ldy, int64_t nrows, int32_t d, const float* 
     return FGL_E_INVALID;
   }
   if (nrows == 0) return FGL_OK;
-  fill_rows_kernel<<<blocks_for(nrows * d), 256, 0, (cudaStream_t)stream>>>(Y, ldy, nrows, d, rowval, relu);
+  FGL_COUNT_LAUNCH(), fill_rows_kernel<<<blocks_for(nrows * d), 256, 0, (cudaStream_t)stream>>>(Y, ldy, nrows, d, rowval, relu);
   FGL_LAUNCH_CHECK("fill_rows_kernel");
   return FGL_OK;
 }

@@ -113,7 +113,7 @@ int fgl_match_counts(const uint32_t* bitmaps, int64_t words, int32_t nb, uint64_
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(words, 256), 2 * kNumSMs));
   auto* o = reinterpret_cast<unsigned long long*>(out_pairs);
   // pair (i < j) lands at i*16 - i*(i+1)/2 + (j-i-1) of a 16 x 16 triangle
-  match_counts_kernel<kMaxMatchBatches><<<grid, 256, 0, st>>>(bitmaps, words, nb, o);
+  FGL_COUNT_LAUNCH(), match_counts_kernel<kMaxMatchBatches><<<grid, 256, 0, st>>>(bitmaps, words, nb, o);
   FGL_LAUNCH_CHECK("match_counts_kernel");
   return FGL_OK;
 }
@@ -134,10 +134,10 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), 148 * 16));
   auto* ld = reinterpret_cast<unsigned long long*>(loaded);
   if (vec)
-    gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
+    FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
         feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, out, ldo, ld);
   else
-    gather_rows_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(
+    FGL_COUNT_LAUNCH(), gather_rows_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(
         feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, out, ldo, ld);
   FGL_LAUNCH_CHECK("gather_rows_kernel");
   return FGL_OK;

@@ -282,16 +282,16 @@ int stable_group_impl(const int32_t* keys, int64_t nnz, int64_t num_keys, int64_
   FGL_CUDA(cudaMemsetAsync(counts, 0, 4 * num_keys, st));
   FGL_CUDA(cudaMemsetAsync(w.cursor, 0, 4 * num_keys, st));
   FGL_CUDA(cudaMemsetAsync(w.nlist, 0, 16, st));
-  if (nnz > 0) histogram_kernel<<<grid_for(nnz), kThreads, 0, st>>>(keys, nnz, counts);
+  if (nnz > 0) FGL_COUNT_LAUNCH(), histogram_kernel<<<grid_for(nnz), kThreads, 0, st>>>(keys, nnz, counts);
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kPersistentCTAs, ceil_div(num_keys, 1024)));
-  chunk_sum_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part);
-  part_scan_kernel<<<1, 1024, 0, st>>>(w.part, G);
-  chunk_scan_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part, base, indptr);
+  FGL_COUNT_LAUNCH(), chunk_sum_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part);
+  FGL_COUNT_LAUNCH(), part_scan_kernel<<<1, 1024, 0, st>>>(w.part, G);
+  FGL_COUNT_LAUNCH(), chunk_scan_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part, base, indptr);
   if (nnz > 0) {
-    scatter_kernel<<<grid_for(nnz), kThreads, 0, st>>>(keys, nnz, indptr, base, w.cursor, perm);
-    seg_sort_small_kernel<<<grid_for(num_keys), kThreads, 0, st>>>(indptr, num_keys, base, perm,
+    FGL_COUNT_LAUNCH(), scatter_kernel<<<grid_for(nnz), kThreads, 0, st>>>(keys, nnz, indptr, base, w.cursor, perm);
+    FGL_COUNT_LAUNCH(), seg_sort_small_kernel<<<grid_for(num_keys), kThreads, 0, st>>>(indptr, num_keys, base, perm,
                                                                     w.lists, w.nlist);
-    seg_sort_warp_kernel<<<4 * kNumSMs, 128, 4 * kWarpSortMax * 4, st>>>(indptr, base, perm,
+    FGL_COUNT_LAUNCH(), seg_sort_warp_kernel<<<4 * kNumSMs, 128, 4 * kWarpSortMax * 4, st>>>(indptr, base, perm,
                                                                          w.lists, w.nlist);
     static bool attr = false;
     if (!attr) {
@@ -299,9 +299,9 @@ int stable_group_impl(const int32_t* keys, int64_t nnz, int64_t num_keys, int64_
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBlockSortMax));
       attr = true;
     }
-    seg_sort_block_kernel<<<kNumSMs, 1024, 4 * kBlockSortMax, st>>>(
+    FGL_COUNT_LAUNCH(), seg_sort_block_kernel<<<kNumSMs, 1024, 4 * kBlockSortMax, st>>>(
         indptr, base, perm, w.lists + num_keys, w.nlist + 1, 0);
-    seg_sort_block_kernel<<<kNumSMs, 1024, 0, st>>>(indptr, base, perm, w.lists + 2 * num_keys,
+    FGL_COUNT_LAUNCH(), seg_sort_block_kernel<<<kNumSMs, 1024, 0, st>>>(indptr, base, perm, w.lists + 2 * num_keys,
                                                     w.nlist + 2, 1);
   }
   FGL_LAUNCH_CHECK("stable_group");
@@ -325,7 +325,7 @@ int fgl_csr_offsets_sorted(const int32_t* rows, int64_t nnz, int64_t num_rows, i
     set_error("fgl_csr_offsets_sorted: bad arguments");
     return FGL_E_INVALID;
   }
-  offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, (cudaStream_t)stream>>>(
+  FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, (cudaStream_t)stream>>>(
       rows, nnz, num_rows, base, indptr);
   FGL_LAUNCH_CHECK("offsets_from_sorted_kernel");
   return FGL_OK;
@@ -348,7 +348,7 @@ int fgl_gather_i32_f32(const int32_t* perm, int64_t n, const int32_t* a, const f
     return FGL_E_INVALID;
   }
   if (n == 0) return FGL_OK;
-  gather_i32_f32_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(perm, n, a, b, a_out, b_out);
+  FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(perm, n, a, b, a_out, b_out);
   FGL_LAUNCH_CHECK("gather_i32_f32_kernel");
   return FGL_OK;
 }
@@ -377,13 +377,13 @@ int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t
   int32_t* perm = reinterpret_cast<int32_t*>(p);
   int32_t* outdeg = reinterpret_cast<int32_t*>(p + al(4 * std::max<int64_t>(nnz, 1)));
   void* gws = p + al(4 * std::max<int64_t>(nnz, 1)) + al(4 * std::max<int64_t>(num_cols, 1));
-  offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
+  FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
   int rc = stable_group_impl(ls, nnz, num_cols, 0, t_indptr, perm, outdeg, gws,
                              fgl_stable_group_ws_bytes(num_cols), st);
   if (rc) return rc;
   if (nnz > 0) {
-    layer_weights_kernel<<<grid_for(nnz), kThreads, 0, st>>>(lt, ls, nnz, indptr, outdeg, arch_gcn, w);
-    gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, lt, w, t_col, t_w);
+    FGL_COUNT_LAUNCH(), layer_weights_kernel<<<grid_for(nnz), kThreads, 0, st>>>(lt, ls, nnz, indptr, outdeg, arch_gcn, w);
+    FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, lt, w, t_col, t_w);
   }
   FGL_LAUNCH_CHECK("prepare_layer");
   return FGL_OK;

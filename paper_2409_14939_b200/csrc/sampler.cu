@@ -596,15 +596,15 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   FGL_CUDA(cudaMemsetAsync(w.scal, 0, 8 * 8, stream));
 
   // frontier 0 = sorted unique seeds per batch
-  mark_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0, stream>>>(
+  FGL_COUNT_LAUNCH(), mark_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), 4 * G), 256, 0, stream>>>(
       seeds, seed_off, nb, total_seeds, g->num_nodes, words, w.bm_front, status);
   FGL_LAUNCH_CHECK("mark_seeds_kernel");
   // compaction of `front` into hop h's frontier list (h == H: no list, only OR into `all`)
   auto compact_front = [&](int h) -> int {
     const bool write = h < H;
-    bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
-    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, write ? fr_off(h) + nb : nullptr);
-    bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(
+    FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
+    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, write ? fr_off(h) + nb : nullptr);
+    FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(
         w.bm_front, nwords, words, w.part, write ? o->frontier + h * fcap : nullptr,
         write ? w.fb : nullptr, write ? fr_off(h) : nullptr, nullptr, w.bm_all, 1, fcap, status);
     FGL_LAUNCH_CHECK("frontier compaction");
@@ -616,29 +616,29 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   for (int h = 0; h < H; ++h) {
     const int fan = fanouts[h];
     const int32_t* front = o->frontier + h * fcap;
-    deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part);
-    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kCandTot, nullptr);
-    scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part + G + 1, G, w.scal + kSelTot, nullptr);
-    deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part,
+    FGL_COUNT_LAUNCH(), deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part);
+    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kCandTot, nullptr);
+    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part + G + 1, G, w.scal + kSelTot, nullptr);
+    FGL_COUNT_LAUNCH(), deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part,
                                                     w.scan_deg, w.scan_sel);
-    hop_book_kernel<<<1, 64, 0, stream>>>(w, fr_off(h), nb, h, counts, H, o->edge_cap);
+    FGL_COUNT_LAUNCH(), hop_book_kernel<<<1, 64, 0, stream>>>(w, fr_off(h), nb, h, counts, H, o->edge_cap);
     FGL_LAUNCH_CHECK("degree scan");
     SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
                  w.scan_deg, w.scan_sel, fr_off(h), w.hop_pos, keys, w.scal,
                  w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan};
-    if (fan <= 32) select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
-    else if (fan <= 64) select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
-    else if (fan <= 128) select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
-    else select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
+    if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
+    else if (fan <= 64) FGL_COUNT_LAUNCH(), select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
+    else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
+    else FGL_COUNT_LAUNCH(), select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
     FGL_LAUNCH_CHECK("select_kernel");
     rc = compact_front(h + 1);
     if (rc) return rc;
   }
 
   // unique nodes = compaction of the `all` bitmaps; keeps per-word prefixes for ranks
-  bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
-  scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kUniqTot, uniq_off + nb);
-  bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part,
+  FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
+  FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kUniqTot, uniq_off + nb);
+  FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part,
                                                     o->unique_nodes, nullptr, uniq_off, w.wprefix,
                                                     nullptr, 0, o->unique_cap, status);
   FGL_LAUNCH_CHECK("unique compaction");
@@ -649,16 +649,16 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   for (int h = 0; h <= H; ++h) {
     const bool has_list = h < H && (o->src_front || (h == 0 && o->seed_front));
     if (has_list) {
-      posmap_kernel<<<TG, 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb, w.bm_all,
+      FGL_COUNT_LAUNCH(), posmap_kernel<<<TG, 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb, w.bm_all,
                                             w.wprefix, words, w.posmap);
     }
     if (h == 0 && (o->seed_rows || o->seed_front)) {
-      translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), TG), 256, 0,
+      FGL_COUNT_LAUNCH(), translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), TG), 256, 0,
                                stream>>>(seeds, seed_off, nb, total_seeds, w.bm_all, w.wprefix,
                                          words, w.posmap, o->seed_rows, o->seed_front);
     }
     if (h >= 1 && want_rows) {  // hop h-1 sources live in hop h's frontier
-      translate_kernel<<<TG, 256, 0, stream>>>(o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all,
+      FGL_COUNT_LAUNCH(), translate_kernel<<<TG, 256, 0, stream>>>(o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all,
                                                w.wprefix, words, h < H ? w.posmap : nullptr,
                                                o->tgt_row, o->src_row, o->src_front);
     }

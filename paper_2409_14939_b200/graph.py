@@ -126,32 +126,33 @@ def chung_lu_graph(num_nodes: int, num_edges: int, exponent: float = 2.3, seed: 
     w = torch.arange(1, n + 1, device=device, dtype=torch.float64).pow_(-a)
     cdf = torch.cumsum(w, 0)
     cdf /= cdf[-1].clone()
-    half = int(num_edges * 0.5 * 1.03) + 16  # oversample for self loops / duplicates
-    parts = []
-    chunk = 1 << 26
-    for i in range(0, half, chunk):
-        m = min(chunk, half - i)
-        u = torch.rand(m, 2, device=device, dtype=torch.float64, generator=g)
-        parts.append(torch.searchsorted(cdf, u).clamp_(max=n - 1))
-    ends = torch.cat(parts)
-    if permute:
-        perm = torch.randperm(n, device=device, generator=g)
-        ends = perm[ends]
-    s, d = ends[:, 0], ends[:, 1]
-    keep = s != d
-    s, d = s[keep], d[keep]
-    key = torch.cat([s * n + d, d * n + s])
-    key = torch.unique(key)  # sorted, deduplicated
-    target = int(num_edges)
-    if key.numel() > target:  # trim deterministically to the requested edge count
-        # drop whole undirected pairs: keep pairs whose smaller-first key ranks low
-        lo = torch.minimum(key // n, key % n) * n + torch.maximum(key // n, key % n)
-        pairs = torch.unique(lo)
-        gen_perm = torch.randperm(pairs.numel(), device=device, generator=g)
-        kept = pairs[gen_perm[: target // 2]]
-        kept = torch.sort(kept).values
-        lo_keep = torch.isin(lo, kept)
-        key = key[lo_keep]
+    perm = torch.randperm(n, device=device, generator=g) if permute else None
+    want_pairs = int(num_edges) // 2
+    pairs = torch.empty(0, dtype=torch.int64, device=device)
+    draw = int(want_pairs * 1.1) + 16
+    for _ in range(64):  # top up until enough distinct undirected pairs exist
+        parts = []
+        chunk = 1 << 25
+        for i in range(0, draw, chunk):
+            m = min(chunk, draw - i)
+            u = torch.rand(m, 2, device=device, dtype=torch.float64, generator=g)
+            parts.append(torch.searchsorted(cdf, u).clamp_(max=n - 1))
+        ends = torch.cat(parts)
+        if perm is not None:
+            ends = perm[ends]
+        s, d = ends[:, 0], ends[:, 1]
+        keep = s != d
+        s, d = s[keep], d[keep]
+        lo = torch.minimum(s, d) * n + torch.maximum(s, d)
+        pairs = torch.unique(torch.cat([pairs, lo]))
+        if pairs.numel() >= want_pairs:
+            break
+        draw = int((want_pairs - pairs.numel()) * 1.5) + 1024
+    if pairs.numel() > want_pairs:  # keep a seeded random subset of exactly want_pairs
+        pick = torch.randperm(pairs.numel(), device=device, generator=g)[:want_pairs]
+        pairs = pairs[pick]
+    u, v = pairs // n, pairs % n
+    key = torch.sort(torch.cat([u * n + v, v * n + u])).values  # both directions, (src, dst) order
     src = key // n
     col = (key % n).to(torch.int32)
     counts = torch.bincount(src, minlength=n)

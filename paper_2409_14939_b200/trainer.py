@@ -166,6 +166,13 @@ class DeviceModel:
         return out
 
 
+def _feature_array(feats):
+    """The [N, d] array of a FeatureMatrix (graph.py:90-114), ndarray or tensor."""
+    if hasattr(feats, "dim") and hasattr(feats, "num_nodes") and not callable(feats.dim):
+        return feats.data
+    return feats
+
+
 def greedy_order(m: np.ndarray) -> list:
     """Greedy chain of schedule.py:92-113 on a match-degree matrix: batch 0
     first, then the unused batch with the highest degree to the last one;
@@ -201,7 +208,7 @@ class Pipeline:
         self.device = device
         self.dist = dist
         self.dg = device_graph(g, device)
-        data = feats.data if hasattr(feats, "data") else feats
+        data = _feature_array(feats)
         if isinstance(data, torch.Tensor):
             ft = data
         else:
@@ -446,7 +453,7 @@ def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None
     n = int(g.num_nodes)
     if len(labels_np) != n:
         raise ValidationError("labels length must equal num_nodes")
-    fdata = feats.data if hasattr(feats, "data") else feats
+    fdata = _feature_array(feats)
     if fdata.shape[0] != n:
         raise ValidationError("feature rows must equal num_nodes")
     if fdata.shape[1] != cfg.layer_dims[0]:
