@@ -199,6 +199,24 @@ int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream
 int fgl_fill_rows(float* Y, int64_t ldy, int64_t nrows, int32_t d, const float* rowval,
                   int32_t relu, void* stream);
 
+/* --------------------------------------------------------------- idmap ---- */
+/* Fused-Map ID table (idmap.py:88-117, :175-233) for arbitrary uint64 IDs:
+ * keys/values uint64[capacity] receive the reference's single-worker state --
+ * SENTINEL (all ones) in empty slots, local IDs in first-seen order, the slot
+ * layout of sequential linear probing from hash(gid) = gid % capacity
+ * (mod_hash) or (gid * 0x9E3779B97F4A7C15) >> shift.  Deterministic.
+ * status2 (device int64[2]): [0] = status (FGL_E_CAPACITY when the table is
+ * full), [1] = number of distinct IDs.  ws: fgl_idmap_ws_bytes(n, capacity). */
+int64_t fgl_idmap_ws_bytes(int64_t n, int64_t capacity);
+int fgl_idmap_build(const uint64_t* ids, int64_t n, int32_t mod_hash, int64_t capacity,
+                    int32_t shift, uint64_t* keys, uint64_t* values, int64_t* status2,
+                    void* ws, int64_t ws_bytes, void* stream);
+/* out[i] = local ID of ids[i], or SENTINEL on a miss (idmap.py:154-172);
+ * *first_miss (device, optional) = smallest missing index, or 0x7f7f7f7f7f7f7f7f. */
+int fgl_idmap_lookup(const uint64_t* keys, const uint64_t* values, int64_t capacity,
+                     int32_t mod_hash, int32_t shift, const uint64_t* ids, int64_t n,
+                     uint64_t* out, int64_t* first_miss, void* stream);
+
 /* -------------------------------------------------------------- loader ---- */
 /* Where fgl_sample_window leaves the per-batch unique-node bitmaps in its
  * workspace: out[0] = byte offset of the bitmaps (batch b at word b*words),

@@ -81,6 +81,11 @@ SIGNATURES = {
                                    vp, C.c_int64, vp, vp, C.c_int64, vp]),
     "fgl_sgd": (C.c_int, [vp, vp, C.c_int64, C.c_float, vp]),
     "fgl_fill_rows": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, C.c_int32, vp]),
+    "fgl_idmap_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
+    "fgl_idmap_build": (C.c_int, [vp, C.c_int64, C.c_int32, C.c_int64, C.c_int32, vp, vp, vp, vp,
+                                  C.c_int64, vp]),
+    "fgl_idmap_lookup": (C.c_int, [vp, vp, C.c_int64, C.c_int32, C.c_int32, vp, C.c_int64, vp, vp,
+                                   vp]),
     "fgl_sample_ws_bitmaps": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int64, c_i64p]),
     "fgl_match_counts": (C.c_int, [vp, C.c_int64, C.c_int32, vp, vp]),
     "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,

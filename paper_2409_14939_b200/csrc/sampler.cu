@@ -25,6 +25,7 @@
 // sources in `front`; (3) compaction of `front` -> next frontier (cleared as
 // it is read, OR-ed into `all`).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -428,6 +429,152 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
   }
 }
 
+// Threshold-collect select (fanouts <= kTauMaxFan).  The f smallest of d
+// uniform keys lie below ~(f + 4 sqrt f + 4)/d with overwhelming probability,
+// so one pass draws every candidate's key, keeps only those below that
+// threshold in a per-warp shared-memory buffer (warp-aggregated appends), and
+// ranks the few survivors by counting: rank = #{collected (key,slot) < own}.
+// Exact for any threshold that keeps at least min(d,f) candidates; if too few
+// survive the threshold is raised 4x and the node is redrawn, and a buffer
+// overflow falls back to the streaming top-list path.  No serial insertion
+// chain, so the kernel is Philox-throughput bound rather than latency bound.
+constexpr int kTauCap = 256;
+constexpr int kTauMaxFan = 128;
+constexpr uint64_t kKeyOne = 1ull << 53;
+
+template <int K>
+__device__ __noinline__ void stream_select_node(const SelectArgs& a, int64_t i, int32_t u,
+                                                   int64_t e0, int64_t d, int b, int64_t p0,
+                                                   int64_t obase) {
+  const int lane = lane_id();
+  const int fan = a.fan;
+  const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+  const int64_t p1 = p0 + d;
+  const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
+  TopList<K> list;
+  list.init();
+  uint64_t thr_k = ~0ull;
+  uint32_t thr_s = 0xffffffffu;
+  for (int64_t bb = blk0; bb <= blk_last; bb += 32) {
+    const int64_t blk = bb + lane;
+    uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+    const bool valid = blk <= blk_last;
+    if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t p = 4 * blk + q;
+      const bool in = valid && p >= p0 && p < p1;
+      const uint64_t key = w[q] >> 11;
+      const uint32_t slot = (uint32_t)(p - p0);
+      unsigned m = __ballot_sync(0xffffffffu, in && key_less(key, slot, thr_k, thr_s));
+      while (m) {
+        const int srcl = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t ck = __shfl_sync(0xffffffffu, key, srcl);
+        const uint32_t cs = __shfl_sync(0xffffffffu, slot, srcl);
+        if (key_less(ck, cs, thr_k, thr_s)) {
+          list.insert(ck, cs, fan);
+          list.entry(fan - 1, thr_k, thr_s);
+        }
+      }
+    }
+  }
+  const int64_t nsel = d < fan ? d : fan;
+  uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int r = k * 32 + lane;
+    if (r < nsel) {
+      const int64_t e = e0 + list.slot[k];
+      const int32_t s = __ldg(a.col + e);
+      a.tgt[obase + r] = u;
+      a.src[obase + r] = s;
+      a.wgt[obase + r] = a.ew ? __ldg(a.ew + e) : 1.0f;
+      if (a.tgt_front) a.tgt_front[obase + r] = (int32_t)i;
+      atomicOr(bm + (s >> 5), 1u << (s & 31));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) select_tau_kernel(SelectArgs a) {
+  __shared__ uint64_t skey[8][kTauCap];
+  __shared__ uint32_t sslot[8][kTauCap];
+  const int lane = lane_id(), wib = warp_id();
+  uint64_t* wk = skey[wib];
+  uint32_t* wsl = sslot[wib];
+  const int64_t F = a.scal[kF];
+  const int64_t ebase = a.scal[kHopEdgeBase];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int fan = a.fan;
+  const double expect = fan + 4.0 * sqrt((double)fan) + 4.0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t i = gw; i < F; i += nwarps) {
+    const int32_t u = a.front[i];
+    const int64_t e0 = __ldg(a.off + u);
+    const int64_t d = __ldg(a.off + u + 1) - e0;
+    if (d == 0) continue;
+    const int b = a.fb[i];
+    const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+    const int64_t p0 = a.hop_pos[b] + a.scan_deg[i];
+    const int64_t p1 = p0 + d;
+    const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
+    const int64_t want = d < fan ? d : fan;
+    const int64_t obase = ebase + a.scan_sel[i];
+    uint64_t tau = (double)d <= expect ? kKeyOne : (uint64_t)(expect / (double)d * (double)kKeyOne);
+    int m = 0;
+    for (;;) {
+      m = 0;
+      for (int64_t bb = blk0; bb <= blk_last; bb += 32) {
+        const int64_t blk = bb + lane;
+        const bool valid = blk <= blk_last;
+        uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+        if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t p = 4 * blk + q;
+          const uint64_t key = w[q] >> 11;
+          const bool take = valid && p >= p0 && p < p1 && key < tau;
+          const unsigned bal = __ballot_sync(0xffffffffu, take);
+          if (take) {
+            const int pos = m + __popc(bal & lt_mask);
+            if (pos < kTauCap) { wk[pos] = key; wsl[pos] = (uint32_t)(p - p0); }
+          }
+          m += __popc(bal);
+        }
+      }
+      if (m >= want || tau >= kKeyOne) break;
+      tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;  // too few survivors: widen and redraw
+    }
+    if (m > kTauCap) {  // pathological overflow: exact streaming fallback
+      __syncwarp();
+      if (fan <= 32) stream_select_node<1>(a, i, u, e0, d, b, p0, obase);
+      else if (fan <= 64) stream_select_node<2>(a, i, u, e0, d, b, p0, obase);
+      else stream_select_node<4>(a, i, u, e0, d, b, p0, obase);
+      continue;
+    }
+    __syncwarp();
+    uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+    for (int c = lane; c < m; c += 32) {
+      const uint64_t ck = wk[c];
+      const uint32_t cs = wsl[c];
+      int rank = 0;
+      for (int j = 0; j < m; ++j) rank += key_less(wk[j], wsl[j], ck, cs) ? 1 : 0;
+      if (rank < want) {
+        const int64_t e = e0 + cs;
+        const int32_t s = __ldg(a.col + e);
+        const int64_t o = obase + rank;
+        a.tgt[o] = u;
+        a.src[o] = s;
+        a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+        if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+        atomicOr(bm + (s >> 5), 1u << (s & 31));
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------ translate ----
 __device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
                                            const int32_t* __restrict__ wprefix, int64_t base_word,
@@ -494,6 +641,7 @@ int select_grid(int K) {
     case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<1>, 256, 0); break;
     case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<2>, 256, 0); break;
     case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<4>, 256, 0); break;
+    case 0: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_tau_kernel, 256, 0); break;
     default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<8>, 256, 0); break;
   }
   if (e != cudaSuccess || per_sm < 1) per_sm = 2;
@@ -626,7 +774,14 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
                  w.scan_deg, w.scan_sel, fr_off(h), w.hop_pos, keys, w.scal,
                  w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan};
-    if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
+    // FGL_SELECT=stream forces the streaming top-list kernel (A/B parity tests)
+    static const bool force_stream = [] {
+      const char* v = getenv("FGL_SELECT");
+      return v && v[0] == 's';
+    }();
+    if (fan <= kTauMaxFan && !force_stream)
+      FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, 0, stream>>>(a);
+    else if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
     else if (fan <= 64) FGL_COUNT_LAUNCH(), select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
     else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
     else FGL_COUNT_LAUNCH(), select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
