@@ -231,6 +231,13 @@ int fgl_sample_ws_bitmaps(int64_t num_nodes, int32_t num_batches, int64_t fronti
 int fgl_match_counts(const uint32_t* bitmaps, int64_t words, int32_t num_batches,
                      uint64_t* out_pairs, void* stream);
 
+/* Node bitmaps of nsets ID sets (set s = ids[offsets[s]..offsets[s+1]), IDs in
+ * [0, 32*words)): bitmaps uint32[nsets*words], cleared then marked. */
+int fgl_mark_bitmaps(const int32_t* ids, const int64_t* offsets, int32_t nsets, int64_t total,
+                     int64_t words, uint32_t* bitmaps, void* stream);
+/* hit[i] = 1 if ids[i] is set in bitmap (schedule.compute_transition overlap test). */
+int fgl_bitmap_test(const int32_t* ids, int64_t n, const uint32_t* bitmap, int8_t* hit, void* stream);
+
 /* x0 rows of one batch (trainer.py:315): out[r] = feats[ids[r]] (feats may be
  * device memory or mapped pinned host memory), except that rows whose ID is
  * set in prev_bitmap (the previously executed batch, Match reuse) are copied

@@ -88,6 +88,8 @@ SIGNATURES = {
                                    vp]),
     "fgl_sample_ws_bitmaps": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int64, c_i64p]),
     "fgl_match_counts": (C.c_int, [vp, C.c_int64, C.c_int32, vp, vp]),
+    "fgl_mark_bitmaps": (C.c_int, [vp, vp, C.c_int32, C.c_int64, C.c_int64, vp, vp]),
+    "fgl_bitmap_test": (C.c_int, [vp, C.c_int64, vp, vp, vp]),
     "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
                                   vp, C.c_int64, vp, C.c_int64, vp, vp]),
 }

@@ -184,82 +184,111 @@ __global__ void __launch_bounds__(256) gemm_kernel(
   }
 }
 
-// Partial dW = A^T dZ and db = colsum(dZ) over a fixed row chunk per CTA.
-// Thread layout: 256 threads own a 32(k) x 64(n) tile of the output through a
-// 2x4 micro tile; rows are streamed through shared memory 32 at a time.
-constexpr int WK = 32, WN = 64, WR = 32;
+// Partial [dW; db] = [H | 1]^T dZ over a fixed row chunk per CTA (the bias
+// gradient is the extra "ones" column of H, k == K).  Output tile 128 (k) x
+// 64 (n) per CTA; 256 threads each own an 8 x 4 register micro tile; rows are
+// streamed through shared memory 32 at a time with 16-byte loads.
+constexpr int WK = 128, WN = 64, WR = 32;
 
 __global__ void __launch_bounds__(256) wgrad_partial_kernel(
     const float* __restrict__ A, int64_t lda, const float* __restrict__ dZ, int64_t ldz,
     const float* __restrict__ zmask, int64_t ldm, int64_t M, int K, int N, int64_t rows_per_cta,
-    float* __restrict__ part_w, float* __restrict__ part_b) {
-  __shared__ float As[WR][WK + 1];
-  __shared__ float Zs[WR][WN + 1];
+    float* __restrict__ part, int vec) {
+  __shared__ __align__(16) float As[WR][WK];
+  __shared__ __align__(16) float Zs[WR][WN];
   const int tid = threadIdx.x;
-  const int tn = tid % 16, tk = tid / 16;  // 16 x 16 threads; each 2 (k) x 4 (n)
+  const int tn = tid % 16, tk = tid / 16;  // n = tn*4..+3, k = tk*8..+7
   const int k0 = blockIdx.y * WK, n0 = blockIdx.z * WN;
+  const int KE = K + 1;  // + ones column -> db
   const int64_t r_begin = blockIdx.x * rows_per_cta;
   const int64_t r_end = min(M, r_begin + rows_per_cta);
-  float acc[2][4] = {};
-  float bacc[4] = {};
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int64_t r0 = r_begin; r0 < r_end; r0 += WR) {
-    for (int i = tid; i < WR * WK; i += 256) {
-      const int rr = i / WK, k = i % WK;
+    // A tile: 32 rows x 128 k (4 float4 per thread)
+    for (int i = tid; i < WR * (WK / 4); i += 256) {
+      const int rr = i / (WK / 4), kq = (i % (WK / 4)) * 4;
       const int64_t r = r0 + rr;
-      As[rr][k] = (r < r_end && k0 + k < K) ? A[r * lda + k0 + k] : 0.f;
-    }
-    for (int i = tid; i < WR * WN; i += 256) {
-      const int rr = i / WN, n = i % WN;
-      const int64_t r = r0 + rr;
-      float v = 0.f;
-      if (r < r_end && n0 + n < N) {
-        v = dZ[r * ldz + n0 + n];
-        if (zmask && !(zmask[r * ldm + n0 + n] > 0.f)) v = 0.f;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < r_end) {
+        const int k = k0 + kq;
+        if (vec && k + 3 < K) {
+          v = *reinterpret_cast<const float4*>(A + r * lda + k);
+        } else {
+          float t[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] = (k + q < K) ? A[r * lda + k + q] : (k + q == K ? 1.f : 0.f);
+          v = make_float4(t[0], t[1], t[2], t[3]);
+        }
       }
-      Zs[rr][n] = v;
+      *reinterpret_cast<float4*>(&As[rr][kq]) = v;
+    }
+    // dZ tile: 32 rows x 64 n, ReLU-masked by the layer output
+    for (int i = tid; i < WR * (WN / 4); i += 256) {
+      const int rr = i / (WN / 4), nq = (i % (WN / 4)) * 4;
+      const int64_t r = r0 + rr;
+      float t[4] = {0.f, 0.f, 0.f, 0.f};
+      if (r < r_end) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int n = n0 + nq + q;
+          if (n < N) {
+            float v = dZ[r * ldz + n];
+            if (zmask && !(zmask[r * ldm + n] > 0.f)) v = 0.f;
+            t[q] = v;
+          }
+        }
+      }
+      *reinterpret_cast<float4*>(&Zs[rr][nq]) = make_float4(t[0], t[1], t[2], t[3]);
     }
     __syncthreads();
 #pragma unroll 4
     for (int rr = 0; rr < WR; ++rr) {
-      float a0 = As[rr][tk * 2], a1 = As[rr][tk * 2 + 1];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[rr][tk * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[rr][tk * 8 + 4]);
+      const float4 z = *reinterpret_cast<const float4*>(&Zs[rr][tn * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float zz[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float z = Zs[rr][tn * 4 + j];
-        acc[0][j] = __fmaf_rn(a0, z, acc[0][j]);
-        acc[1][j] = __fmaf_rn(a1, z, acc[1][j]);
-        if (tk == 0 && blockIdx.y == 0) bacc[j] = __fadd_rn(bacc[j], z);
-      }
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(a[i], zz[j], acc[i][j]);
     }
     __syncthreads();
   }
-  float* pw = part_w + (int64_t)blockIdx.x * K * N;
+  float* pw = part + (int64_t)blockIdx.x * KE * N;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int k = k0 + tk * 2 + i;
-    if (k >= K) continue;
+  for (int i = 0; i < 8; ++i) {
+    const int k = k0 + tk * 8 + i;
+    if (k >= KE) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tn * 4 + j;
       if (n < N) pw[(int64_t)k * N + n] = acc[i][j];
     }
   }
-  if (tk == 0 && blockIdx.y == 0) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tn * 4 + j;
-      if (n < N) part_b[(int64_t)blockIdx.x * N + n] = bacc[j];
-    }
-  }
 }
 
-// sum partials over chunks in a fixed order (deterministic)
+// Sum partials over chunks in a fixed order (deterministic): each CTA owns 32
+// outputs; 8 thread groups sum interleaved chunks, then a fixed-order combine.
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int chunks, int64_t n,
-                                       float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s = __fadd_rn(s, part[(int64_t)c * n + i]);
-    out[i] = s;
+                                       float* __restrict__ out, int64_t split, float* __restrict__ out2) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (i < n)
+    for (int c = grp; c < chunks; c += 8) s = __fadd_rn(s, part[(int64_t)c * n + i]);
+  sm[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && i < n) {
+    float t = sm[0][lane];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t = __fadd_rn(t, sm[g][lane]);
+    if (i < split) out[i] = t; else out2[i - split] = t;
   }
 }
 
@@ -384,7 +413,7 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
 }
 
 int64_t fgl_dense_bwd_ws_bytes(int32_t din, int32_t dout) {
-  return (int64_t)kPersistentCTAs * ((int64_t)din * dout + dout) * 4;
+  return (int64_t)2 * kPersistentCTAs * ((int64_t)din + 1) * dout * 4;
 }
 
 int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
@@ -401,16 +430,19 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     set_error("fgl_dense_bwd: workspace too small");
     return FGL_E_CAPACITY;
   }
-  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kPersistentCTAs, ceil_div(n, 256)));
+  const int ky = (int)ceil_div(din + 1, WK), nz = (int)ceil_div(dout, WN);
+  const int chunks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(n, 64), std::max(1, 4 * kNumSMs / (ky * nz))));
   const int64_t rows_per = std::max<int64_t>(1, ceil_div(n, chunks));
   float* pw = static_cast<float*>(ws);
-  float* pb = pw + (int64_t)chunks * din * dout;
+  const int64_t outs = (int64_t)(din + 1) * dout;
   if (n > 0) {
-    dim3 g(chunks, (unsigned)ceil_div(din, WK), (unsigned)ceil_div(dout, WN));
-    FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, rows_per,
-                                            pw, pb);
-    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<blocks_for((int64_t)din * dout), 256, 0, st>>>(pw, chunks, (int64_t)din * dout, dW);
-    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<blocks_for(dout), 256, 0, st>>>(pb, chunks, dout, db);
+    const int vec = (ldh % 4 == 0) && !(reinterpret_cast<uintptr_t>(H) & 15);
+    dim3 g(chunks, ky, nz);
+    FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
+                                                                rows_per, pw, vec);
+    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
+        pw, chunks, outs, dW, (int64_t)din * dout, db);
     if (dH) {
       dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
       FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,

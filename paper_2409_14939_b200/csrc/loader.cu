@@ -57,41 +57,105 @@ __device__ __forceinline__ bool bm_test(const uint32_t* bm, int32_t g) {
   return (__ldg(bm + (g >> 5)) >> (g & 31)) & 1u;
 }
 
-// one warp per output row; 16-byte vectors when every row is 16-byte aligned
+// Flattened (row, 16-byte chunk) copy: thread t moves chunks t, t+T, ... of
+// the n x d4 output, 4 independent loads in flight per thread.  The source of
+// a row is the previous batch's block when its bitmap holds the ID (Match),
+// else the feature store.  Rows whose first chunk a thread copies from the
+// store are counted as loaded.
 template <bool VEC>
-__global__ void gather_rows_kernel(const float* __restrict__ feats, int64_t ldf, int d,
-                                   const int32_t* __restrict__ ids, int64_t n,
-                                   const uint32_t* __restrict__ prev_bm,
-                                   const int32_t* __restrict__ prev_prefix, int64_t prev_base,
-                                   const float* __restrict__ prev_x, int64_t ldp,
-                                   float* __restrict__ out, int64_t ldo,
-                                   unsigned long long* __restrict__ loaded) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+__global__ void __launch_bounds__(256) gather_rows_kernel(
+    const float* __restrict__ feats, int64_t ldf, int d, const int32_t* __restrict__ ids, int64_t n,
+    const uint32_t* __restrict__ prev_bm, const int32_t* __restrict__ prev_prefix, int64_t prev_base,
+    const float* __restrict__ prev_x, int64_t ldp, float* __restrict__ out, int64_t ldo,
+    unsigned long long* __restrict__ loaded) {
+  const int w = VEC ? (d + 3) >> 2 : d;  // elements (float4 or float) per row
+  const int64_t total = n * w;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
   uint32_t my_loaded = 0;
-  for (int64_t r = warp; r < n; r += nwarps) {
-    const int32_t g = ids[r];
-    const float* src;
-    if (prev_bm && bm_test(prev_bm, g)) {
-      const int64_t wi = g >> 5;
-      const int64_t pr = prev_prefix[wi] + __popc(prev_bm[wi] & ((1u << (g & 31)) - 1u)) - prev_base;
-      src = prev_x + pr * ldp;
-    } else {
-      src = feats + (int64_t)g * ldf;
-      ++my_loaded;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += 4 * T) {
+    const float* src[4];
+    int64_t dst[4];
+    int cc[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t idx = base + u * T;
+      ok[u] = idx < total;
+      const int64_t r = ok[u] ? idx / w : 0;
+      cc[u] = ok[u] ? (int)(idx - r * w) : 0;
+      const int32_t g = ok[u] ? ids[r] : 0;
+      const float* sp = feats + (int64_t)g * ldf;
+      bool from_store = true;
+      if (prev_bm && ok[u]) {
+        const uint32_t word = __ldg(prev_bm + (g >> 5));
+        if ((word >> (g & 31)) & 1u) {
+          const int64_t pr = __ldg(prev_prefix + (g >> 5)) + __popc(word & ((1u << (g & 31)) - 1u)) - prev_base;
+          sp = prev_x + pr * ldp;
+          from_store = false;
+        }
+      }
+      if (ok[u] && from_store && cc[u] == 0) ++my_loaded;
+      src[u] = sp;
+      dst[u] = r * ldo;
     }
-    float* dst = out + r * ldo;
     if (VEC) {
-      const float4* s4 = reinterpret_cast<const float4*>(src);
-      float4* d4 = reinterpret_cast<float4*>(dst);
-      for (int c = lane; c < (d >> 2); c += 32) d4[c] = s4[c];
-      for (int c = (d & ~3) + lane; c < d; c += 32) dst[c] = src[c];
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) v[u] = reinterpret_cast<const float4*>(src[u])[cc[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!ok[u]) continue;
+        const int c0 = cc[u] * 4;
+        if (c0 + 3 < d) {
+          *reinterpret_cast<float4*>(out + dst[u] + c0) = v[u];
+        } else {  // ragged tail of a row whose width is not a multiple of 4
+          const float t[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          for (int q = 0; c0 + q < d; ++q) out[dst[u] + c0 + q] = t[q];
+        }
+      }
     } else {
-      for (int c = lane; c < d; c += 32) dst[c] = src[c];
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) v[u] = src[u][cc[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) out[dst[u] + cc[u]] = v[u];
     }
   }
-  if (loaded && lane == 0 && my_loaded) atomicAdd(loaded, (unsigned long long)my_loaded);
+  if (loaded) {
+    my_loaded = warp_sum(my_loaded);
+    if ((threadIdx.x & 31) == 0 && my_loaded) atomicAdd(loaded, (unsigned long long)my_loaded);
+  }
+}
+
+__device__ __forceinline__ int find_set(const int64_t* off, int n, int64_t i) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void mark_bitmaps_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ off,
+                                    int nsets, int64_t total, int64_t words, uint32_t* __restrict__ bm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = ids[i];
+    const int s = find_set(off, nsets, i);
+    atomicOr(bm + s * words + (g >> 5), 1u << (g & 31));
+  }
+}
+
+__global__ void bitmap_test_kernel(const int32_t* __restrict__ ids, int64_t n,
+                                   const uint32_t* __restrict__ bm, int8_t* __restrict__ hit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = ids[i];
+    hit[i] = (int8_t)((bm[g >> 5] >> (g & 31)) & 1u);
+  }
 }
 
 }  // namespace
@@ -118,6 +182,33 @@ int fgl_match_counts(const uint32_t* bitmaps, int64_t words, int32_t nb, uint64_
   return FGL_OK;
 }
 
+int fgl_mark_bitmaps(const int32_t* ids, const int64_t* offsets, int32_t nsets, int64_t total,
+                     int64_t words, uint32_t* bitmaps, void* stream) {
+  if (nsets < 1 || total < 0 || words < 1 || !bitmaps || (total > 0 && (!ids || !offsets))) {
+    set_error("fgl_mark_bitmaps: bad arguments");
+    return FGL_E_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  FGL_CUDA(cudaMemsetAsync(bitmaps, 0, 4 * words * (size_t)nsets, st));
+  if (total == 0) return FGL_OK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 16));
+  FGL_COUNT_LAUNCH(), mark_bitmaps_kernel<<<grid, 256, 0, st>>>(ids, offsets, nsets, total, words, bitmaps);
+  FGL_LAUNCH_CHECK("mark_bitmaps_kernel");
+  return FGL_OK;
+}
+
+int fgl_bitmap_test(const int32_t* ids, int64_t n, const uint32_t* bitmap, int8_t* hit, void* stream) {
+  if (n < 0 || (n > 0 && (!ids || !bitmap || !hit))) {
+    set_error("fgl_bitmap_test: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (n == 0) return FGL_OK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 16));
+  FGL_COUNT_LAUNCH(), bitmap_test_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ids, n, bitmap, hit);
+  FGL_LAUNCH_CHECK("bitmap_test_kernel");
+  return FGL_OK;
+}
+
 int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
                     const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
                     const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
@@ -131,7 +222,8 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
   const bool vec = ((ldf | ldo | (prev_bitmap ? ldp : 0)) % 4 == 0) &&
                    !((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(out) |
                       reinterpret_cast<uintptr_t>(prev_x)) & 15);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), 148 * 16));
+  const int64_t work = n * (vec ? (d + 3) / 4 : d);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256 * 4), 148 * 16));
   auto* ld = reinterpret_cast<unsigned long long*>(loaded);
   if (vec)
     FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
