@@ -57,76 +57,75 @@ __device__ __forceinline__ bool bm_test(const uint32_t* bm, int32_t g) {
   return (__ldg(bm + (g >> 5)) >> (g & 31)) & 1u;
 }
 
-// Flattened (row, 16-byte chunk) copy: thread t moves chunks t, t+T, ... of
-// the n x d4 output, 4 independent loads in flight per thread.  The source of
-// a row is the previous batch's block when its bitmap holds the ID (Match),
-// else the feature store.  Rows whose first chunk a thread copies from the
-// store are counted as loaded.
+// Row gather: each warp copies R = 4 rows per iteration (lane = 16-byte
+// chunk), so every lane keeps 4 independent loads in flight.  The source of a
+// row is the previous batch's block when its bitmap holds the ID (Match), else
+// the feature store (HBM or mapped pinned host memory).
 template <bool VEC>
 __global__ void __launch_bounds__(256) gather_rows_kernel(
     const float* __restrict__ feats, int64_t ldf, int d, const int32_t* __restrict__ ids, int64_t n,
     const uint32_t* __restrict__ prev_bm, const int32_t* __restrict__ prev_prefix, int64_t prev_base,
     const float* __restrict__ prev_x, int64_t ldp, float* __restrict__ out, int64_t ldo,
     unsigned long long* __restrict__ loaded) {
-  const int w = VEC ? (d + 3) >> 2 : d;  // elements (float4 or float) per row
-  const int64_t total = n * w;
-  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  constexpr int R = 4;
+  const int lane = threadIdx.x & 31;
+  const int w = VEC ? (d + 3) >> 2 : d;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_loaded = 0;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += 4 * T) {
-    const float* src[4];
-    int64_t dst[4];
-    int cc[4];
-    bool ok[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t idx = base + u * T;
-      ok[u] = idx < total;
-      const int64_t r = ok[u] ? idx / w : 0;
-      cc[u] = ok[u] ? (int)(idx - r * w) : 0;
-      const int32_t g = ok[u] ? ids[r] : 0;
-      const float* sp = feats + (int64_t)g * ldf;
-      bool from_store = true;
-      if (prev_bm && ok[u]) {
+  for (int64_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
+    // lanes 0..R-1 resolve the R rows' sources, then broadcast
+    const float* mine = nullptr;
+    if (lane < R && r0 + lane < n) {
+      const int32_t g = ids[r0 + lane];
+      mine = feats + (int64_t)g * ldf;
+      bool store = true;
+      if (prev_bm) {
         const uint32_t word = __ldg(prev_bm + (g >> 5));
         if ((word >> (g & 31)) & 1u) {
           const int64_t pr = __ldg(prev_prefix + (g >> 5)) + __popc(word & ((1u << (g & 31)) - 1u)) - prev_base;
-          sp = prev_x + pr * ldp;
-          from_store = false;
+          mine = prev_x + pr * ldp;
+          store = false;
         }
       }
-      if (ok[u] && from_store && cc[u] == 0) ++my_loaded;
-      src[u] = sp;
-      dst[u] = r * ldo;
+      my_loaded += store ? 1u : 0u;
     }
-    if (VEC) {
-      float4 v[4];
+    const float* src[R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (ok[u]) v[u] = reinterpret_cast<const float4*>(src[u])[cc[u]];
+    for (int q = 0; q < R; ++q)
+      src[q] = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q));
+    for (int c = lane; c < w; c += 32) {
+      if (VEC) {
+        float4 v[R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (!ok[u]) continue;
-        const int c0 = cc[u] * 4;
-        if (c0 + 3 < d) {
-          *reinterpret_cast<float4*>(out + dst[u] + c0) = v[u];
-        } else {  // ragged tail of a row whose width is not a multiple of 4
-          const float t[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-          for (int q = 0; c0 + q < d; ++q) out[dst[u] + c0 + q] = t[q];
+        for (int q = 0; q < R; ++q)
+          if (r0 + q < n) v[q] = reinterpret_cast<const float4*>(src[q])[c];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (r0 + q >= n) continue;
+          float* drow = out + (r0 + q) * ldo;
+          const int c0 = 4 * c;
+          if (c0 + 3 < d) {
+            *reinterpret_cast<float4*>(drow + c0) = v[q];
+          } else {  // ragged tail when d is not a multiple of 4
+            const float t[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            for (int k = 0; c0 + k < d; ++k) drow[c0 + k] = t[k];
+          }
         }
+      } else {
+        float v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (r0 + q < n) v[q] = src[q][c];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (r0 + q < n) out[(r0 + q) * ldo + c] = v[q];
       }
-    } else {
-      float v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (ok[u]) v[u] = src[u][cc[u]];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (ok[u]) out[dst[u] + cc[u]] = v[u];
     }
   }
   if (loaded) {
     my_loaded = warp_sum(my_loaded);
-    if ((threadIdx.x & 31) == 0 && my_loaded) atomicAdd(loaded, (unsigned long long)my_loaded);
+    if (lane == 0 && my_loaded) atomicAdd(loaded, (unsigned long long)my_loaded);
   }
 }
 
@@ -222,8 +221,7 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
   const bool vec = ((ldf | ldo | (prev_bitmap ? ldp : 0)) % 4 == 0) &&
                    !((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(out) |
                       reinterpret_cast<uintptr_t>(prev_x)) & 15);
-  const int64_t work = n * (vec ? (d + 3) / 4 : d);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256 * 4), 148 * 16));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8 * 4), 148 * 16));
   auto* ld = reinterpret_cast<unsigned long long*>(loaded);
   if (vec)
     FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(

@@ -496,7 +496,124 @@ __device__ __noinline__ void stream_select_node(const SelectArgs& a, int64_t i, 
   }
 }
 
-__global__ void __launch_bounds__(256) select_tau_kernel(SelectArgs a) {
+// Warp path of the threshold-collect select for one node (all 32 lanes).
+__device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, uint32_t* wsl,
+                                                int64_t i, int32_t u, int64_t e0, int64_t d, int b,
+                                                int64_t p0, int64_t obase, double expect) {
+  const int lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int fan = a.fan;
+  const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+  const int64_t p1 = p0 + d;
+  const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
+  const int64_t want = d < fan ? d : fan;
+  uint64_t tau = (double)d <= expect ? kKeyOne : (uint64_t)(expect / (double)d * (double)kKeyOne);
+  int m = 0;
+  for (;;) {
+    m = 0;
+    for (int64_t bb = blk0; bb <= blk_last; bb += 32) {
+      const int64_t blk = bb + lane;
+      const bool valid = blk <= blk_last;
+      uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+      if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t p = 4 * blk + q;
+        const uint64_t key = w[q] >> 11;
+        const bool take = valid && p >= p0 && p < p1 && key < tau;
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const int pos = m + __popc(bal & lt_mask);
+          if (pos < kTauCap) { wk[pos] = key; wsl[pos] = (uint32_t)(p - p0); }
+        }
+        m += __popc(bal);
+      }
+    }
+    if (m >= want || tau >= kKeyOne) break;
+    tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;  // too few survivors: widen and redraw
+  }
+  __syncwarp();
+  if (m > kTauCap) {  // pathological overflow: exact streaming fallback
+    if (fan <= 32) stream_select_node<1>(a, i, u, e0, d, b, p0, obase);
+    else if (fan <= 64) stream_select_node<2>(a, i, u, e0, d, b, p0, obase);
+    else stream_select_node<4>(a, i, u, e0, d, b, p0, obase);
+    return;
+  }
+  uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+  for (int c = lane; c < m; c += 32) {
+    const uint64_t ck = wk[c];
+    const uint32_t cs = wsl[c];
+    int rank = 0;
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) rank += key_less(wk[j], wsl[j], ck, cs) ? 1 : 0;
+    if (rank < want) {
+      const int64_t e = e0 + cs;
+      const int32_t s = __ldg(a.col + e);
+      const int64_t o = obase + rank;
+      a.tgt[o] = u;
+      a.src[o] = s;
+      a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+      if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+      atomicOr(bm + (s >> 5), 1u << (s & 31));
+    }
+  }
+  __syncwarp();
+}
+
+// Nodes of degree <= kTinyDeg are sampled by a single lane: at most three
+// Philox blocks cover them, the (key, slot) pairs stay in registers and are
+// ranked by counting.
+constexpr int kTinyDeg = 8;
+
+__device__ __forceinline__ void tiny_select_lane(const SelectArgs& a, int64_t i, int32_t u, int64_t e0,
+                                                 int d, int b, int64_t p0, int64_t obase) {
+  const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+  const int64_t blk0 = p0 >> 2;
+  const int off0 = (int)(p0 & 3);
+  const int nblk = (off0 + d + 3) >> 2;  // 1..3
+  uint64_t key[kTinyDeg];
+#pragma unroll
+  for (int j = 0; j < kTinyDeg; ++j) key[j] = ~0ull;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (t < nblk) {
+      uint64_t w0, w1, w2, w3;
+      philox4x64_10((uint64_t)(blk0 + t) + 1, k0, k1, w0, w1, w2, w3);
+#pragma unroll
+      for (int j = 0; j < kTinyDeg; ++j) {
+        const int pos = off0 + j - 4 * t;  // word of block t holding slot j, if any
+        if (j < d && pos >= 0 && pos < 4)
+          key[j] = (pos == 0 ? w0 : pos == 1 ? w1 : pos == 2 ? w2 : w3) >> 11;
+      }
+    }
+  }
+  const int want = d < a.fan ? d : a.fan;
+  uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+#pragma unroll
+  for (int j = 0; j < kTinyDeg; ++j) {
+    if (j >= d) break;
+    int rank = 0;
+#pragma unroll
+    for (int l = 0; l < kTinyDeg; ++l)
+      rank += (l < d && key_less(key[l], (uint32_t)l, key[j], (uint32_t)j)) ? 1 : 0;
+    if (rank < want) {
+      const int64_t e = e0 + j;
+      const int32_t s = __ldg(a.col + e);
+      const int64_t o = obase + rank;
+      a.tgt[o] = u;
+      a.src[o] = s;
+      a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+      if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+      atomicOr(bm + (s >> 5), 1u << (s & 31));
+    }
+  }
+}
+
+// Each warp takes 32 consecutive frontier entries: the lanes load the 32
+// nodes' parameters in parallel (one latency round for all of them), tiny
+// nodes are finished lane-locally, the rest go through the warp path one by
+// one with their parameters broadcast by shuffles.
+__global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
   __shared__ uint64_t skey[8][kTauCap];
   __shared__ uint32_t sslot[8][kTauCap];
   const int lane = lane_id(), wib = warp_id();
@@ -506,72 +623,35 @@ __global__ void __launch_bounds__(256) select_tau_kernel(SelectArgs a) {
   const int64_t ebase = a.scal[kHopEdgeBase];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int fan = a.fan;
-  const double expect = fan + 4.0 * sqrt((double)fan) + 4.0;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int64_t i = gw; i < F; i += nwarps) {
-    const int32_t u = a.front[i];
-    const int64_t e0 = __ldg(a.off + u);
-    const int64_t d = __ldg(a.off + u + 1) - e0;
-    if (d == 0) continue;
-    const int b = a.fb[i];
-    const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
-    const int64_t p0 = a.hop_pos[b] + a.scan_deg[i];
-    const int64_t p1 = p0 + d;
-    const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
-    const int64_t want = d < fan ? d : fan;
-    const int64_t obase = ebase + a.scan_sel[i];
-    uint64_t tau = (double)d <= expect ? kKeyOne : (uint64_t)(expect / (double)d * (double)kKeyOne);
-    int m = 0;
-    for (;;) {
-      m = 0;
-      for (int64_t bb = blk0; bb <= blk_last; bb += 32) {
-        const int64_t blk = bb + lane;
-        const bool valid = blk <= blk_last;
-        uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
-        if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t p = 4 * blk + q;
-          const uint64_t key = w[q] >> 11;
-          const bool take = valid && p >= p0 && p < p1 && key < tau;
-          const unsigned bal = __ballot_sync(0xffffffffu, take);
-          if (take) {
-            const int pos = m + __popc(bal & lt_mask);
-            if (pos < kTauCap) { wk[pos] = key; wsl[pos] = (uint32_t)(p - p0); }
-          }
-          m += __popc(bal);
-        }
-      }
-      if (m >= want || tau >= kKeyOne) break;
-      tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;  // too few survivors: widen and redraw
+  const double expect = a.fan + 4.0 * sqrt((double)a.fan) + 4.0;
+  for (int64_t t0 = gw * 32; t0 < F; t0 += nwarps * 32) {
+    const int64_t i = t0 + lane;
+    int32_t u = 0;
+    int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
+    int b = 0;
+    if (i < F) {
+      u = a.front[i];
+      b = a.fb[i];
+      const int64_t sd = a.scan_deg[i], ss = a.scan_sel[i];
+      e0 = __ldg(a.off + u);
+      d = __ldg(a.off + u + 1) - e0;
+      p0 = a.hop_pos[b] + sd;
+      obase = ebase + ss;
     }
-    if (m > kTauCap) {  // pathological overflow: exact streaming fallback
-      __syncwarp();
-      if (fan <= 32) stream_select_node<1>(a, i, u, e0, d, b, p0, obase);
-      else if (fan <= 64) stream_select_node<2>(a, i, u, e0, d, b, p0, obase);
-      else stream_select_node<4>(a, i, u, e0, d, b, p0, obase);
-      continue;
+    if (d > 0 && d <= kTinyDeg) tiny_select_lane(a, i, u, e0, (int)d, b, p0, obase);
+    unsigned big = __ballot_sync(0xffffffffu, d > kTinyDeg);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int64_t ii = t0 + src;
+      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+      const int64_t ee = __shfl_sync(0xffffffffu, e0, src);
+      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
+      const int bb = __shfl_sync(0xffffffffu, b, src);
+      const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
+      const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
+      tau_select_node(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
     }
-    __syncwarp();
-    uint32_t* bm = a.bm_front + (int64_t)b * a.words;
-    for (int c = lane; c < m; c += 32) {
-      const uint64_t ck = wk[c];
-      const uint32_t cs = wsl[c];
-      int rank = 0;
-      for (int j = 0; j < m; ++j) rank += key_less(wk[j], wsl[j], ck, cs) ? 1 : 0;
-      if (rank < want) {
-        const int64_t e = e0 + cs;
-        const int32_t s = __ldg(a.col + e);
-        const int64_t o = obase + rank;
-        a.tgt[o] = u;
-        a.src[o] = s;
-        a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
-        if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
-        atomicOr(bm + (s >> 5), 1u << (s & 31));
-      }
-    }
-    __syncwarp();
   }
 }
 
