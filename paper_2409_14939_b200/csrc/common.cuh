@@ -132,4 +132,11 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 // Fixed grid for device-count-driven ("persistent") kernels: 2 CTAs per SM.
 constexpr int kPersistentCTAs = 2 * kNumSMs;
 
+// tcgen05 3xTF32 GEMM (tc_gemm.cu).  mode 0: C = act(A W + bias), W [K, N];
+// mode 1: C = (A * (mask > 0)) W^T, W [N, K].  Returns false if the shape is
+// outside the kernel's envelope; *err receives an FGL status otherwise.
+bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
+             const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
+             cudaStream_t st, int* err);
+
 }  // namespace fgl

@@ -405,6 +405,9 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     return FGL_E_INVALID;
   }
   if (n == 0) return FGL_OK;
+  int err = 0;
+  if (tc_gemm(0, H, ldh, nullptr, 0, W, b, Z, ldz, n, dout, din, relu, (cudaStream_t)stream, &err))
+    return err;
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
   FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
                                                       relu, nullptr, 0);
@@ -443,7 +446,10 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
                                                                 rows_per, pw, vec);
     FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
         pw, chunks, outs, dW, (int64_t)din * dout, db);
-    if (dH) {
+    int err = 0;
+    if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
+      if (err) return err;
+    } else if (dH) {
       dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
       FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,
                                         Xout, ldxo);

@@ -497,6 +497,10 @@ __device__ __noinline__ void stream_select_node(const SelectArgs& a, int64_t i, 
 }
 
 // Warp path of the threshold-collect select for one node (all 32 lanes).
+// PACKED (d <= 2048): a candidate is the single 64-bit word key53 << 11 | slot,
+// whose unsigned order is exactly the (key, slot) order, so collecting and
+// ranking move and compare one word.  Otherwise keys and slots are kept apart.
+template <bool PACKED>
 __device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, uint32_t* wsl,
                                                 int64_t i, int32_t u, int64_t e0, int64_t d, int b,
                                                 int64_t p0, int64_t obase, double expect) {
@@ -507,7 +511,10 @@ __device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* w
   const int64_t p1 = p0 + d;
   const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
   const int64_t want = d < fan ? d : fan;
-  uint64_t tau = (double)d <= expect ? kKeyOne : (uint64_t)(expect / (double)d * (double)kKeyOne);
+  // threshold on key53: expect/d of the unit interval (any value keeping
+  // >= want survivors gives the exact answer; it only sets the work)
+  uint64_t tau = (double)d <= expect ? kKeyOne
+                                     : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
   int m = 0;
   for (;;) {
     m = 0;
@@ -524,7 +531,14 @@ __device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* w
         const unsigned bal = __ballot_sync(0xffffffffu, take);
         if (take) {
           const int pos = m + __popc(bal & lt_mask);
-          if (pos < kTauCap) { wk[pos] = key; wsl[pos] = (uint32_t)(p - p0); }
+          if (pos < kTauCap) {
+            if (PACKED) {
+              wk[pos] = (key << 11) | (uint64_t)(p - p0);
+            } else {
+              wk[pos] = key;
+              wsl[pos] = (uint32_t)(p - p0);
+            }
+          }
         }
         m += __popc(bal);
       }
@@ -542,10 +556,17 @@ __device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* w
   uint32_t* bm = a.bm_front + (int64_t)b * a.words;
   for (int c = lane; c < m; c += 32) {
     const uint64_t ck = wk[c];
-    const uint32_t cs = wsl[c];
+    uint32_t cs;
     int rank = 0;
+    if (PACKED) {
+      cs = (uint32_t)(ck & 0x7FFu);
+#pragma unroll 8
+      for (int j = 0; j < m; ++j) rank += wk[j] < ck ? 1 : 0;
+    } else {
+      cs = wsl[c];
 #pragma unroll 4
-    for (int j = 0; j < m; ++j) rank += key_less(wk[j], wsl[j], ck, cs) ? 1 : 0;
+      for (int j = 0; j < m; ++j) rank += key_less(wk[j], wsl[j], ck, cs) ? 1 : 0;
+    }
     if (rank < want) {
       const int64_t e = e0 + cs;
       const int32_t s = __ldg(a.col + e);
@@ -623,13 +644,16 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
   const int64_t ebase = a.scal[kHopEdgeBase];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const double expect = a.fan + 4.0 * sqrt((double)a.fan) + 4.0;
-  for (int64_t t0 = gw * 32; t0 < F; t0 += nwarps * 32) {
+  const double expect = a.fan + 3.0 * sqrt((double)a.fan) + 3.0;
+  // tile of T consecutive nodes per warp: 32 for large frontiers, fewer when
+  // the frontier is small so that every warp of the grid gets work
+  const int T = (int)min<int64_t>(32, max<int64_t>(1, ceil_div(F, nwarps)));
+  for (int64_t t0 = gw * T; t0 < F; t0 += nwarps * T) {
     const int64_t i = t0 + lane;
     int32_t u = 0;
     int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
     int b = 0;
-    if (i < F) {
+    if (lane < T && i < F) {
       u = a.front[i];
       b = a.fb[i];
       const int64_t sd = a.scan_deg[i], ss = a.scan_sel[i];
@@ -650,7 +674,8 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
       const int bb = __shfl_sync(0xffffffffu, b, src);
       const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
       const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
-      tau_select_node(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+      if (dd <= 2048) tau_select_node<true>(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+      else tau_select_node<false>(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
     }
   }
 }

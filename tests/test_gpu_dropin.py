@@ -21,7 +21,7 @@ def test_aggregation_golden(golden):
         assert np.array_equal(tw, st[f"agg{c}_tw"])
         assert np.array_equal(compute.aggregate_backward(tip, tix, tw, st[f"agg{c}_gy"], cfg), st[f"agg{c}_bwd"])
     got = compute.dense_update(st["dense_h"], st["dense_W"], st["dense_b"], "relu")
-    np.testing.assert_allclose(got, st["dense_relu"], rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(got, st["dense_relu"], rtol=1e-5, atol=1e-6)
 
 
 def test_prepare_layers_golden(golden, powerlaw_10k):
