@@ -440,12 +440,20 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   float* pw = static_cast<float*>(ws);
   const int64_t outs = (int64_t)(din + 1) * dout;
   if (n > 0) {
-    const int vec = (ldh % 4 == 0) && !(reinterpret_cast<uintptr_t>(H) & 15);
-    dim3 g(chunks, ky, nz);
-    FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
-                                                                rows_per, pw, vec);
+    int werr = 0;
+    const int tc_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 128)));
+    int used_chunks = chunks;
+    if (tc_wgrad(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc_chunks, st, &werr)) {
+      if (werr) return werr;
+      used_chunks = tc_chunks;
+    } else {
+      const int vec = (ldh % 4 == 0) && !(reinterpret_cast<uintptr_t>(H) & 15);
+      dim3 g(chunks, ky, nz);
+      FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
+                                                                  rows_per, pw, vec);
+    }
     FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
-        pw, chunks, outs, dW, (int64_t)din * dout, db);
+        pw, used_chunks, outs, dW, (int64_t)din * dout, db);
     int err = 0;
     if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
       if (err) return err;

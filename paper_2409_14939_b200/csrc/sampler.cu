@@ -647,7 +647,8 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
   const double expect = a.fan + 3.0 * sqrt((double)a.fan) + 3.0;
   // tile of T consecutive nodes per warp: 32 for large frontiers, fewer when
   // the frontier is small so that every warp of the grid gets work
-  const int T = (int)min<int64_t>(32, max<int64_t>(1, ceil_div(F, nwarps)));
+  const int64_t per_warp = ceil_div(F, nwarps);
+  const int T = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
   for (int64_t t0 = gw * T; t0 < F; t0 += nwarps * T) {
     const int64_t i = t0 + lane;
     int32_t u = 0;
