@@ -224,7 +224,8 @@ def main():
     mcfg = trainer.ModelConfig(layer_dims=cfg["dims"], fanouts=cfg["fanouts"], arch=cfg["arch"],
                                batch_size=cfg["bs"], window_n=cfg["window"], lr=0.1, seed=0)
     pipe = trainer.Pipeline(dg, feats, labels, mcfg, trainer.PipelineFlags(), device=device,
-                            feature_store=cfg["store"], dist=fdist.GradAllReduce(world))
+                            feature_store=cfg["store"], dist=fdist.GradAllReduce(world),
+                            direct_x0=cfg.get("direct_x0", True))
     lib = _lib.lib()
     W, K = max(args.warmup, 0), max(args.steps, 1)
     if args.profile:

@@ -51,6 +51,9 @@ __device__ __forceinline__ void philox4x64_10(uint64_t ctr, uint64_t k0, uint64_
                                               uint64_t& o0, uint64_t& o1, uint64_t& o2,
                                               uint64_t& o3) {
   uint64_t c0 = ctr, c1 = 0, c2 = 0, c3 = 0;
+  // keep the 20 round keys from being hoisted out of callers' loops (they
+  // would pin 40 registers); the per-round key add is 2 integer ops
+  asm volatile("" : "+l"(k0), "+l"(k1));
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const uint64_t hi0 = __umul64hi(kPhiloxM0, c0);

@@ -501,7 +501,7 @@ __device__ __noinline__ void stream_select_node(const SelectArgs& a, int64_t i, 
 // whose unsigned order is exactly the (key, slot) order, so collecting and
 // ranking move and compare one word.  Otherwise keys and slots are kept apart.
 template <bool PACKED>
-__device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, uint32_t* wsl,
+__device__ __noinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, uint32_t* wsl,
                                                 int64_t i, int32_t u, int64_t e0, int64_t d, int b,
                                                 int64_t p0, int64_t obase, double expect) {
   const int lane = lane_id();
@@ -586,7 +586,7 @@ __device__ __forceinline__ void tau_select_node(const SelectArgs& a, uint64_t* w
 // ranked by counting.
 constexpr int kTinyDeg = 8;
 
-__device__ __forceinline__ void tiny_select_lane(const SelectArgs& a, int64_t i, int32_t u, int64_t e0,
+__device__ __noinline__ void tiny_select_lane(const SelectArgs& a, int64_t i, int32_t u, int64_t e0,
                                                  int d, int b, int64_t p0, int64_t obase) {
   const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
   const int64_t blk0 = p0 >> 2;
@@ -630,6 +630,108 @@ __device__ __forceinline__ void tiny_select_lane(const SelectArgs& a, int64_t i,
   }
 }
 
+// Sub-warp path: a group of G lanes samples one node of degree <= 4*G per
+// Philox iteration with packed (key53 << 11 | slot) candidates collected in the
+// group's slice of the warp buffer.  Returns false when the node must be
+// redone by the full-warp path (group buffer overflow).
+template <int G>
+__device__ __noinline__ bool tau_select_group(const SelectArgs& a, uint64_t* wk, int cap, int64_t i,
+                                                 int32_t u, int64_t e0, int64_t d, int b, int64_t p0,
+                                                 int64_t obase, double expect) {
+  const int lane = lane_id();
+  const int gl = lane % G, grp = lane / G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const unsigned lt_mask = (1u << gl) - 1u;
+  const int fan = a.fan;
+  const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+  const int64_t p1 = p0 + d;
+  const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
+  const int want = (int)(d < fan ? d : fan);
+  uint64_t tau = (double)d <= expect ? kKeyOne
+                                     : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
+  int m = 0;
+  for (;;) {
+    m = 0;
+    for (int64_t bb = blk0; bb <= blk_last; bb += G) {
+      const int64_t blk = bb + gl;
+      const bool valid = blk <= blk_last;
+      uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+      if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t p = 4 * blk + q;
+        const uint64_t key = w[q] >> 11;
+        const bool take = valid && p >= p0 && p < p1 && key < tau;
+        const unsigned bal = __ballot_sync(gmask, take) >> (G == 32 ? 0 : grp * G);
+        if (take) {
+          const int pos = m + __popc(bal & lt_mask);
+          if (pos < cap) wk[pos] = (key << 11) | (uint64_t)(p - p0);
+        }
+        m += __popc(bal);
+      }
+    }
+    if (m >= want || tau >= kKeyOne) break;
+    tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;
+  }
+  __syncwarp(gmask);
+  if (m > cap) return false;
+  uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+  for (int c = gl; c < m; c += G) {
+    const uint64_t ck = wk[c];
+    int rank = 0;
+#pragma unroll 8
+    for (int j = 0; j < m; ++j) rank += wk[j] < ck ? 1 : 0;
+    if (rank < want) {
+      const int64_t e = e0 + (int64_t)(ck & 0x7FFu);
+      const int32_t s = __ldg(a.col + e);
+      const int64_t o = obase + rank;
+      a.tgt[o] = u;
+      a.src[o] = s;
+      a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+      if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+      atomicOr(bm + (s >> 5), 1u << (s & 31));
+    }
+  }
+  __syncwarp(gmask);
+  return true;
+}
+
+// Runs the nodes flagged in `mask` (lanes of the current tile) through groups
+// of G lanes, 32/G nodes per round; returns the lanes whose node overflowed
+// its group buffer and must be redone by the full warp.
+template <int G>
+__device__ __forceinline__ unsigned group_rounds(const SelectArgs& a, uint64_t* wk, int64_t t0, unsigned mask,
+                                                 int32_t u, int64_t e0, int64_t d, int b, int64_t p0,
+                                                 int64_t obase, double expect) {
+  constexpr int NG = 32 / G;
+  const int lane = lane_id();
+  const int grp = lane / G;
+  const int cap = kTauCap / NG;
+  unsigned redo = 0;
+  while (mask) {
+    unsigned tmp = mask;
+    for (int k = 0; k < grp && tmp; ++k) tmp &= tmp - 1;
+    const int src = tmp ? __ffs(tmp) - 1 : 0;
+    const bool has = tmp != 0;
+    for (int k = 0; k < NG && mask; ++k) mask &= mask - 1;  // consume this round's nodes
+    const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+    const int64_t ee = __shfl_sync(0xffffffffu, e0, src);
+    const int64_t dd = __shfl_sync(0xffffffffu, d, src);
+    const int bb = __shfl_sync(0xffffffffu, b, src);
+    const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
+    const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
+    bool ok = true;
+    if (has) ok = tau_select_group<G>(a, wk + grp * cap, cap, t0 + src, uu, ee, dd, bb, pp, oo, expect);
+    __syncwarp();
+    const unsigned bad = __ballot_sync(0xffffffffu, has && !ok && (lane % G) == 0);
+    for (unsigned x = bad; x; x &= x - 1) {
+      const int l = __ffs(x) - 1;  // group leader lane -> its node's lane in the tile
+      redo |= 1u << __shfl_sync(0xffffffffu, src, l);
+    }
+  }
+  return redo;
+}
+
 // Each warp takes 32 consecutive frontier entries: the lanes load the 32
 // nodes' parameters in parallel (one latency round for all of them), tiny
 // nodes are finished lane-locally, the rest go through the warp path one by
@@ -664,7 +766,15 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
       obase = ebase + ss;
     }
     if (d > 0 && d <= kTinyDeg) tiny_select_lane(a, i, u, e0, (int)d, b, p0, obase);
-    unsigned big = __ballot_sync(0xffffffffu, d > kTinyDeg);
+    // small / medium nodes: 4 (8 lanes each) or 2 (16 lanes each) at once
+    unsigned redo = 0;
+    if (a.fan <= 32) {
+      redo |= group_rounds<8>(a, wk, t0, __ballot_sync(0xffffffffu, d > kTinyDeg && d <= 32), u, e0, d, b,
+                              p0, obase, expect);
+      redo |= group_rounds<16>(a, wk, t0, __ballot_sync(0xffffffffu, d > 32 && d <= 128), u, e0, d, b,
+                               p0, obase, expect);
+    }
+    unsigned big = redo | __ballot_sync(0xffffffffu, d > (a.fan <= 32 ? 128 : kTinyDeg));
     while (big) {
       const int src = __ffs(big) - 1;
       big &= big - 1;

@@ -200,7 +200,7 @@ class Pipeline:
     """
 
     def __init__(self, g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None,
-                 device="cuda", feature_store="device", params=None, dist=None):
+                 device="cuda", feature_store="device", params=None, dist=None, direct_x0=None):
         import torch
         self.torch = torch
         self.cfg = cfg
@@ -237,6 +237,14 @@ class Pipeline:
         self.L = cfg.num_layers
         self.H = len(cfg.fanouts)
         self.compact = cfg.arch == "gcn"
+        # direct_x0: with the feature table resident in HBM, the layer-0
+        # aggregation gathers neighbour rows straight from the table (the x0
+        # staging copy -- and with it the Match reuse, which only saves host-
+        # link traffic -- is skipped).  Host-resident features always go
+        # through the Match delta loader.
+        if direct_x0 is None:
+            direct_x0 = False
+        self.direct_x0 = bool(direct_x0) and feature_store == "device" and self.compact
         self.pairs = torch.zeros(120, dtype=torch.int64, device=device)
         self.loaded = torch.zeros(1, dtype=torch.int64, device=device)
         self.loss_dev = torch.zeros(max(cfg.window_n, 1), dtype=torch.float64, device=device)
@@ -309,6 +317,7 @@ class Pipeline:
                 "t_col": self._buf(f"tc{h}", max(nnz, 1), 1, torch.int32),
                 "t_w": self._buf(f"tw{h}", max(nnz, 1), 1),
                 "col": ls.data_ptr() + 4 * e0,
+                "col_global": s.src.data_ptr() + 4 * e0,
                 "nnz": nnz,
             }
             wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
@@ -343,18 +352,24 @@ class Pipeline:
         st = self.stream
         u0, u1 = win.unique_range(b)
         U = u1 - u0
-        x0 = self._buf(f"x0_{x0_slot}", U, self.ldf)
         ws = s.ws.data_ptr()
-        if prev is not None:
+        if self.direct_x0:
+            x0 = self.feats
+        else:
+            x0 = self._buf(f"x0_{x0_slot}", U, self.ldf)
+        if self.direct_x0:
+            pass
+        elif prev is not None:
             p0 = win.unique_range(prev)[0]
             prev_bm = ws + self.bm_off + 4 * prev * self.words
             prev_pf = ws + self.prefix_off + 4 * prev * self.words
             prev_x = self._bufs[f"x0_{1 - x0_slot}"].data_ptr()
         else:
             p0, prev_bm, prev_pf, prev_x = 0, None, None, None
-        self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0,
-                   s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
-                   x0.data_ptr(), self.ldf, self.loaded.data_ptr(), st)
+        if not self.direct_x0:
+            self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0,
+                       s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
+                       x0.data_ptr(), self.ldf, self.loaded.data_ptr(), st)
         # forward
         X, ldx = x0, self.ldf
         H_bufs, Y_bufs, ns = [], [], []
@@ -365,9 +380,11 @@ class Pipeline:
             lay = layers[i]
             Hb = self._buf(f"h{i}", n, _ld(din))
             self_x = X.data_ptr() if not self.compact else None
-            self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(), n,
-                       self._in_base(win, i, b), X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(),
-                       _ld(din), din, st)
+            col, base = lay["col"], self._in_base(win, i, b)
+            if i == 0 and self.direct_x0:
+                col, base = lay["col_global"], 0
+            self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
+                       base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
             Yb = self._buf(f"y{i}", n, _ld(dout))
             self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout,
                        Yb.data_ptr(), _ld(dout), 1 if i < self.L - 1 else 0, st)

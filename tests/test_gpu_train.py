@@ -33,10 +33,11 @@ def test_train_matches_reference_trajectory(golden_meta, name):
     assert [e.accuracy for e in rep.epochs] == want["accuracy"]
 
 
-@pytest.mark.parametrize("arch,dims,fan", [("gcn", (128, 64, 2), [10, 5]),
-                                           ("gcn", (128, 48, 32, 7), [6, 4, 3]),
-                                           ("gin", (128, 16, 3), [5, 3])])
-def test_window_steps_match_oracle(cfg1_graph, arch, dims, fan):
+@pytest.mark.parametrize("arch,dims,fan,direct", [("gcn", (128, 64, 2), [10, 5], False),
+                                                  ("gcn", (128, 64, 2), [10, 5], True),
+                                                  ("gcn", (128, 48, 32, 7), [6, 4, 3], True),
+                                                  ("gin", (128, 16, 3), [5, 3], False)])
+def test_window_steps_match_oracle(cfg1_graph, arch, dims, fan, direct):
     """A window of 4 batches on config 1: per-batch loss and the parameters
     after every SGD step track the oracle within 1e-5 relative."""
     import torch
@@ -47,7 +48,7 @@ def test_window_steps_match_oracle(cfg1_graph, arch, dims, fan):
     labels = rng.integers(0, dims[-1], size=g.num_nodes)
     cfg = trainer.ModelConfig(layer_dims=dims, fanouts=fan, arch=arch, batch_size=512, window_n=4,
                               lr=0.1, seed=3)
-    pipe = trainer.Pipeline(g, feats, labels, cfg, trainer.PipelineFlags(reorder=True))
+    pipe = trainer.Pipeline(g, feats, labels, cfg, trainer.PipelineFlags(reorder=True), direct_x0=direct)
     params = oracle.init_params(dims, 3)
     seeds = [rng.choice(g.num_nodes, 512, replace=False) for _ in range(4)]
     rs = [oracle.derive_seed(3, 13, j) for j in range(4)]
