@@ -581,167 +581,74 @@ __device__ __noinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, 
   __syncwarp();
 }
 
-// Nodes of degree <= kTinyDeg are sampled by a single lane: at most three
-// Philox blocks cover them, the (key, slot) pairs stay in registers and are
-// ranked by counting.
-constexpr int kTinyDeg = 8;
+// Lane path: nodes of degree <= kLaneDeg are sampled by ONE lane each, 32
+// nodes per warp in lock step: the lane draws its node's <= 9 Philox blocks,
+// keeps the packed candidates (key53 << 11 | slot) below the node's threshold
+// in its own column of the warp's shared buffer, then picks the f smallest by
+// repeated minimum search.  Per node this costs a few hundred lane
+// instructions instead of a full warp iteration.
+constexpr int kLaneDeg = 32;
+constexpr int kLaneCap = 32;                       // survivors per lane (<= d)
+constexpr int kWarpBufWords = kLaneCap * 32;       // u64 words per warp (8 KB)
 
-__device__ __noinline__ void tiny_select_lane(const SelectArgs& a, int64_t i, int32_t u, int64_t e0,
-                                                 int d, int b, int64_t p0, int64_t obase) {
+__device__ __noinline__ void lane_select(const SelectArgs& a, uint64_t* colbuf, int64_t i, int32_t u,
+                                         int64_t e0, int d, int b, int64_t p0, int64_t obase,
+                                         double expect, int max_blocks) {
   const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
   const int64_t blk0 = p0 >> 2;
   const int off0 = (int)(p0 & 3);
-  const int nblk = (off0 + d + 3) >> 2;  // 1..3
-  uint64_t key[kTinyDeg];
-#pragma unroll
-  for (int j = 0; j < kTinyDeg; ++j) key[j] = ~0ull;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    if (t < nblk) {
-      uint64_t w0, w1, w2, w3;
-      philox4x64_10((uint64_t)(blk0 + t) + 1, k0, k1, w0, w1, w2, w3);
-#pragma unroll
-      for (int j = 0; j < kTinyDeg; ++j) {
-        const int pos = off0 + j - 4 * t;  // word of block t holding slot j, if any
-        if (j < d && pos >= 0 && pos < 4)
-          key[j] = (pos == 0 ? w0 : pos == 1 ? w1 : pos == 2 ? w2 : w3) >> 11;
-      }
-    }
-  }
+  const int nblk = (off0 + d + 3) >> 2;  // <= 9
   const int want = d < a.fan ? d : a.fan;
-  uint32_t* bm = a.bm_front + (int64_t)b * a.words;
-#pragma unroll
-  for (int j = 0; j < kTinyDeg; ++j) {
-    if (j >= d) break;
-    int rank = 0;
-#pragma unroll
-    for (int l = 0; l < kTinyDeg; ++l)
-      rank += (l < d && key_less(key[l], (uint32_t)l, key[j], (uint32_t)j)) ? 1 : 0;
-    if (rank < want) {
-      const int64_t e = e0 + j;
-      const int32_t s = __ldg(a.col + e);
-      const int64_t o = obase + rank;
-      a.tgt[o] = u;
-      a.src[o] = s;
-      a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
-      if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
-      atomicOr(bm + (s >> 5), 1u << (s & 31));
-    }
-  }
-}
-
-// Sub-warp path: a group of G lanes samples one node of degree <= 4*G per
-// Philox iteration with packed (key53 << 11 | slot) candidates collected in the
-// group's slice of the warp buffer.  Returns false when the node must be
-// redone by the full-warp path (group buffer overflow).
-template <int G>
-__device__ __noinline__ bool tau_select_group(const SelectArgs& a, uint64_t* wk, int cap, int64_t i,
-                                                 int32_t u, int64_t e0, int64_t d, int b, int64_t p0,
-                                                 int64_t obase, double expect) {
-  const int lane = lane_id();
-  const int gl = lane % G, grp = lane / G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const unsigned lt_mask = (1u << gl) - 1u;
-  const int fan = a.fan;
-  const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
-  const int64_t p1 = p0 + d;
-  const int64_t blk0 = p0 >> 2, blk_last = (p1 - 1) >> 2;
-  const int want = (int)(d < fan ? d : fan);
   uint64_t tau = (double)d <= expect ? kKeyOne
                                      : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
   int m = 0;
   for (;;) {
     m = 0;
-    for (int64_t bb = blk0; bb <= blk_last; bb += G) {
-      const int64_t blk = bb + gl;
-      const bool valid = blk <= blk_last;
-      uint64_t w[4] = {~0ull, ~0ull, ~0ull, ~0ull};
-      if (valid) philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+    for (int t = 0; t < max_blocks; ++t) {
+      if (t < nblk) {
+        uint64_t w[4];
+        philox4x64_10((uint64_t)(blk0 + t) + 1, k0, k1, w[0], w[1], w[2], w[3]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t p = 4 * blk + q;
-        const uint64_t key = w[q] >> 11;
-        const bool take = valid && p >= p0 && p < p1 && key < tau;
-        const unsigned bal = __ballot_sync(gmask, take) >> (G == 32 ? 0 : grp * G);
-        if (take) {
-          const int pos = m + __popc(bal & lt_mask);
-          if (pos < cap) wk[pos] = (key << 11) | (uint64_t)(p - p0);
+        for (int q = 0; q < 4; ++q) {
+          const int j = 4 * t + q - off0;  // slot
+          const uint64_t key = w[q] >> 11;
+          if (j >= 0 && j < d && key < tau) colbuf[32 * m++] = (key << 11) | (uint64_t)j;
         }
-        m += __popc(bal);
       }
     }
     if (m >= want || tau >= kKeyOne) break;
     tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;
   }
-  __syncwarp(gmask);
-  if (m > cap) return false;
   uint32_t* bm = a.bm_front + (int64_t)b * a.words;
-  for (int c = gl; c < m; c += G) {
-    const uint64_t ck = wk[c];
-    int rank = 0;
-#pragma unroll 8
-    for (int j = 0; j < m; ++j) rank += wk[j] < ck ? 1 : 0;
-    if (rank < want) {
-      const int64_t e = e0 + (int64_t)(ck & 0x7FFu);
-      const int32_t s = __ldg(a.col + e);
-      const int64_t o = obase + rank;
-      a.tgt[o] = u;
-      a.src[o] = s;
-      a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
-      if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
-      atomicOr(bm + (s >> 5), 1u << (s & 31));
+  uint64_t prev = 0;
+  for (int r = 0; r < want; ++r) {
+    uint64_t best = ~0ull;
+    for (int c = 0; c < m; ++c) {
+      const uint64_t x = colbuf[32 * c];
+      if ((r == 0 || x > prev) && x < best) best = x;
     }
+    prev = best;
+    const int64_t e = e0 + (int64_t)(best & 0x7FFu);
+    const int32_t s = __ldg(a.col + e);
+    const int64_t o = obase + r;
+    a.tgt[o] = u;
+    a.src[o] = s;
+    a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+    if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+    atomicOr(bm + (s >> 5), 1u << (s & 31));
   }
-  __syncwarp(gmask);
-  return true;
 }
 
-// Runs the nodes flagged in `mask` (lanes of the current tile) through groups
-// of G lanes, 32/G nodes per round; returns the lanes whose node overflowed
-// its group buffer and must be redone by the full warp.
-template <int G>
-__device__ __forceinline__ unsigned group_rounds(const SelectArgs& a, uint64_t* wk, int64_t t0, unsigned mask,
-                                                 int32_t u, int64_t e0, int64_t d, int b, int64_t p0,
-                                                 int64_t obase, double expect) {
-  constexpr int NG = 32 / G;
-  const int lane = lane_id();
-  const int grp = lane / G;
-  const int cap = kTauCap / NG;
-  unsigned redo = 0;
-  while (mask) {
-    unsigned tmp = mask;
-    for (int k = 0; k < grp && tmp; ++k) tmp &= tmp - 1;
-    const int src = tmp ? __ffs(tmp) - 1 : 0;
-    const bool has = tmp != 0;
-    for (int k = 0; k < NG && mask; ++k) mask &= mask - 1;  // consume this round's nodes
-    const int32_t uu = __shfl_sync(0xffffffffu, u, src);
-    const int64_t ee = __shfl_sync(0xffffffffu, e0, src);
-    const int64_t dd = __shfl_sync(0xffffffffu, d, src);
-    const int bb = __shfl_sync(0xffffffffu, b, src);
-    const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
-    const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
-    bool ok = true;
-    if (has) ok = tau_select_group<G>(a, wk + grp * cap, cap, t0 + src, uu, ee, dd, bb, pp, oo, expect);
-    __syncwarp();
-    const unsigned bad = __ballot_sync(0xffffffffu, has && !ok && (lane % G) == 0);
-    for (unsigned x = bad; x; x &= x - 1) {
-      const int l = __ffs(x) - 1;  // group leader lane -> its node's lane in the tile
-      redo |= 1u << __shfl_sync(0xffffffffu, src, l);
-    }
-  }
-  return redo;
-}
-
-// Each warp takes 32 consecutive frontier entries: the lanes load the 32
-// nodes' parameters in parallel (one latency round for all of them), tiny
-// nodes are finished lane-locally, the rest go through the warp path one by
-// one with their parameters broadcast by shuffles.
+// Each warp takes a tile of up to 32 consecutive frontier entries: the lanes
+// load the nodes' parameters in parallel (one latency round for all of them),
+// nodes of degree <= kLaneDeg are finished lane-parallel, the rest go through
+// the warp path one by one with their parameters broadcast by shuffles.
 __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
-  __shared__ uint64_t skey[8][kTauCap];
-  __shared__ uint32_t sslot[8][kTauCap];
+  extern __shared__ __align__(16) uint64_t sbuf[];
   const int lane = lane_id(), wib = warp_id();
-  uint64_t* wk = skey[wib];
-  uint32_t* wsl = sslot[wib];
+  uint64_t* wbuf = sbuf + (int64_t)wib * kWarpBufWords;  // lane path: [slot][lane]
+  uint64_t* wk = wbuf;                                      // warp path aliases it
+  uint32_t* wsl = reinterpret_cast<uint32_t*>(wbuf + kTauCap);
   const int64_t F = a.scal[kF];
   const int64_t ebase = a.scal[kHopEdgeBase];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -751,6 +658,7 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
   // the frontier is small so that every warp of the grid gets work
   const int64_t per_warp = ceil_div(F, nwarps);
   const int T = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
+  const bool lane_ok = a.fan <= kLaneCap;
   for (int64_t t0 = gw * T; t0 < F; t0 += nwarps * T) {
     const int64_t i = t0 + lane;
     int32_t u = 0;
@@ -765,16 +673,14 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
       p0 = a.hop_pos[b] + sd;
       obase = ebase + ss;
     }
-    if (d > 0 && d <= kTinyDeg) tiny_select_lane(a, i, u, e0, (int)d, b, p0, obase);
-    // small / medium nodes: 4 (8 lanes each) or 2 (16 lanes each) at once
-    unsigned redo = 0;
-    if (a.fan <= 32) {
-      redo |= group_rounds<8>(a, wk, t0, __ballot_sync(0xffffffffu, d > kTinyDeg && d <= 32), u, e0, d, b,
-                              p0, obase, expect);
-      redo |= group_rounds<16>(a, wk, t0, __ballot_sync(0xffffffffu, d > 32 && d <= 128), u, e0, d, b,
-                               p0, obase, expect);
+    const bool mine = lane_ok && d > 0 && d <= kLaneDeg;
+    const int nblk = mine ? (int)(((p0 & 3) + d + 3) >> 2) : 0;
+    const int max_blocks = __reduce_max_sync(0xffffffffu, (unsigned)nblk);
+    if (max_blocks > 0) {
+      if (mine) lane_select(a, wbuf + lane, i, u, e0, (int)d, b, p0, obase, expect, max_blocks);
+      __syncwarp();
     }
-    unsigned big = redo | __ballot_sync(0xffffffffu, d > (a.fan <= 32 ? 128 : kTinyDeg));
+    unsigned big = __ballot_sync(0xffffffffu, d > 0 && !mine);
     while (big) {
       const int src = __ffs(big) - 1;
       big &= big - 1;
@@ -790,6 +696,8 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
     }
   }
 }
+
+constexpr int kSelectSmem = 8 * kWarpBufWords * 8;  // 64 KB per 256-thread CTA
 
 // ------------------------------------------------------------ translate ----
 __device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
@@ -857,7 +765,11 @@ int select_grid(int K) {
     case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<1>, 256, 0); break;
     case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<2>, 256, 0); break;
     case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<4>, 256, 0); break;
-    case 0: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_tau_kernel, 256, 0); break;
+    case 0:
+      e = cudaFuncSetAttribute(select_tau_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelectSmem);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_tau_kernel, 256, kSelectSmem);
+      break;
     default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<8>, 256, 0); break;
   }
   if (e != cudaSuccess || per_sm < 1) per_sm = 2;
@@ -996,7 +908,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       return v && v[0] == 's';
     }();
     if (fan <= kTauMaxFan && !force_stream)
-      FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, 0, stream>>>(a);
+      FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, kSelectSmem, stream>>>(a);
     else if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
     else if (fan <= 64) FGL_COUNT_LAUNCH(), select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
     else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);

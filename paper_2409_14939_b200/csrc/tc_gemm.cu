@@ -1,23 +1,25 @@
 // Tensor-core (tcgen05, 5th-gen) dense layer GEMMs with 3xTF32 (sm_100a).
 //
 // The dense per-layer transform of the reference (compute.dense_update,
-// compute.py:198-216, and the dH = dZ W^T of trainer._backward,
-// trainer.py:219-221) in fp32 accuracy on the tensor cores: every fp32
-// operand x is split x = hi + lo with hi = tf32(x) (round to nearest) and
-// lo = x - hi, and  A B ~= A_lo B_hi + A_hi B_lo + A_hi B_hi  is accumulated
-// in fp32 in tensor memory (relative error ~1e-6, inside the 1e-5 bar).
+// compute.py:198-216) and the dH = dZ W^T / dW = h^T dZ of trainer._backward
+// (trainer.py:212-228) in fp32 accuracy on the tensor cores: every fp32
+// operand x is split x = hi + lo with hi = tf32(x) (round to nearest, low 13
+// bits zero) and lo = x - hi; A B ~= A_lo B_hi + A_hi B_lo + A_hi B_hi is
+// accumulated in fp32 in tensor memory (relative error ~1e-6, inside the
+// 1e-5 bar of the north star).
 //
-// Structure (one CTA of 4 warps per SM, persistent over 128-row tiles):
-//  * B (the layer weight, <= 256 x 128) is split and staged in shared memory
-//    once per CTA in the UMMA K-major canonical layout (no swizzle: 8x16-byte
-//    core matrices, LBO = 128 B between the two K halves of an MMA, SBO =
-//    KC*128 B between 8-row groups);
-//  * each tile's A rows are loaded with 16-byte loads, split hi/lo and stored
-//    in the same layout (plus the ReLU mask of dZ for the dgrad variant);
-//  * one elected thread issues 3*K/8 tcgen05.mma.kind::tf32 (M=128, N<=256)
-//    into a TMEM accumulator and commits to an mbarrier;
-//  * the 4 warps drain their 32 TMEM lanes with tcgen05.ld.32x32b.x16, add
-//    the bias, apply ReLU and store the rows.
+// Data movement (one CTA of 8 warps per SM, persistent over tiles):
+//  * operand tiles are copied global -> shared with 16-byte cp.async straight
+//    into the UMMA canonical no-swizzle layouts (K-major: 8 rows x 16 B core
+//    matrices; MN-major for the weight gradient, so the activations' rows copy
+//    in without a transpose); zero fill handles ragged rows / columns;
+//  * a split pass rewrites each raw chunk in place as its tf32 hi part and
+//    writes the lo part to a second buffer (conflict-free, chunk = thread);
+//  * one elected thread issues the 3*K/8 tcgen05.mma.kind::tf32 (M=128,
+//    N<=256) and commits to an mbarrier; the copies of the next tile are
+//    already in flight while the MMAs and the epilogue of this one run;
+//  * the epilogue drains TMEM with tcgen05.ld.32x32b.x16 (warp w reads lane
+//    quarter w%4, column half w/4), adds the bias, applies ReLU, stores rows.
 #include <algorithm>
 #include <cstdlib>
 
@@ -28,27 +30,13 @@ namespace {
 
 constexpr int TC_M = 128;
 constexpr int TC_THREADS = 256;
-constexpr int TC_LOADS = 8;  // 16-byte A loads in flight per thread
-constexpr int TC_MAX_SMEM = 200 * 1024;
-
-struct TcArgs {
-  const float* A;      // [M, K] row-major (lda)
-  int64_t lda;
-  const float* mask;   // dgrad: ReLU mask (layer output), same shape as A, or null
-  int64_t ldm;
-  const float* W;      // layer weight [din, dout] row-major
-  const float* bias;   // fwd: [N] or null
-  float* C;            // [M, N] row-major (ldc)
-  int64_t ldc;
-  int64_t M;
-  int N, K, N_pad, K_pad, relu, tmem_cols;
-};
+constexpr int TC_MAX_SMEM = 220 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// UMMA shared-memory matrix descriptor, K-major, SWIZZLE_NONE (sm100 version 1)
+// UMMA shared-memory matrix descriptor, SWIZZLE_NONE (sm100 descriptor version 1)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
@@ -57,32 +45,36 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// instruction descriptor: D f32, A/B tf32, both K-major, M x N
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// instruction descriptor: D f32, A/B tf32, M x N, operand majors (0 = K, 1 = MN)
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// byte offset of the 16-byte chunk holding (row r, k..k+3) in the canonical layout
+// K-major no-swizzle: 16-byte chunk (row r, k..k+3) of a tile with KC chunks per row
 __device__ __forceinline__ uint32_t kmaj_off(int r, int k, int KC) {
-  return (uint32_t)((r >> 3) * (KC * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+  return (uint32_t)((r >> 3) * (KC * 128) + (k >> 2) * 128 + (r & 7) * 16);
 }
 
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+// MN-major no-swizzle: 16-byte chunk (k-row kk, mn..mn+3) of a tile with MN4
+// 4-element groups per k-row: core matrix = 8 k-rows x 16 B, SBO = 128 B
+// between MN groups, LBO = MN4*128 B between 8-row K groups
+__device__ __forceinline__ uint32_t mnmaj_off(int kk, int mn, int MN4) {
+  return (uint32_t)((kk >> 3) * (MN4 * 128) + (mn >> 2) * 128 + (kk & 7) * 16);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
   uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  lo = __fsub_rn(x, hi);
+  return __uint_as_float(h);
 }
 
-__device__ __forceinline__ void store_split4(char* hi_base, char* lo_base, uint32_t off, float4 v) {
-  float4 h, l;
-  split_tf32(v.x, h.x, l.x);
-  split_tf32(v.y, h.y, l.y);
-  split_tf32(v.z, h.z, l.z);
-  split_tf32(v.w, h.w, l.w);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(lo_base + off) = l;
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
@@ -92,6 +84,15 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
       :
       : "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1));
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
@@ -107,25 +108,93 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   }
 }
 
-template <int MODE>  // 0: C = act(A W + b);  1: C = (A * (mask > 0)) W^T
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, int cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+__device__ __forceinline__ void tmem_free(uint32_t tmem, int cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
+// split the raw chunk at `off` in place into its tf32 hi part; lo -> lo_base
+__device__ __forceinline__ void split_chunk(char* raw, char* lo_base, uint32_t off, float4 x) {
+  float4 h, l;
+  h.x = tf32_hi(x.x); l.x = __fsub_rn(x.x, h.x);
+  h.y = tf32_hi(x.y); l.y = __fsub_rn(x.y, h.y);
+  h.z = tf32_hi(x.z); l.z = __fsub_rn(x.z, h.z);
+  h.w = tf32_hi(x.w); l.w = __fsub_rn(x.w, h.w);
+  *reinterpret_cast<float4*>(raw + off) = h;
+  *reinterpret_cast<float4*>(lo_base + off) = l;
+}
+
+// ------------------------------------------------------------- fwd / dgrad --
+struct TcArgs {
+  const float* A;      // [M, K] row-major (lda), 16-byte aligned rows
+  int64_t lda;
+  const float* mask;   // dgrad: ReLU mask (layer output) with A's shape, or null
+  int64_t ldm;
+  const float* W;      // layer weight [din, dout] row-major
+  const float* bias;   // fwd: [N] or null
+  float* C;            // [M, N] row-major (ldc)
+  int64_t ldc;
+  int64_t M;
+  int N, K, N_pad, K_pad, relu, tmem_cols, stages;
+};
+
+// issue the cp.async copies of one 128-row tile of A (and of the mask)
+template <int MODE>
+__device__ __forceinline__ void issue_tile(const TcArgs& p, int64_t m0, char* raw, char* mraw, int KC) {
+  for (int idx = threadIdx.x; idx < TC_M * KC; idx += TC_THREADS) {
+    // thread order = (row within 8-group, chunk, 8-group): 8 consecutive threads
+    // fill one 128-byte core matrix (conflict-free) from 8 rows
+    const int rl = idx & 7, rest = idx >> 3;
+    const int kc = rest % KC, rg = rest / KC;
+    const int r = rg * 8 + rl, k = 4 * kc;
+    const int64_t row = m0 + r;
+    const int valid = (row < p.M && k < p.K) ? (int)min(4, p.K - k) : 0;
+    const uint32_t off = (uint32_t)(rg * (KC * 128) + kc * 128 + rl * 16);
+    const float* src = valid ? p.A + row * p.lda + k : p.A;
+    cp_async16(smem_u32(raw + off), src, valid * 4);
+    if (MODE == 1 && p.mask) {
+      const float* msrc = valid ? p.mask + row * p.ldm + k : p.mask;
+      cp_async16(smem_u32(mraw + off), msrc, valid * 4);
+    }
+  }
+}
+
+template <int MODE>  // 0: C = act(A W + b), W [K, N];  1: C = (A * (mask > 0)) W^T, W [N, K]
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KC = p.K_pad / 4;
-  char* sA_hi = smem;
-  char* sA_lo = sA_hi + TC_M * p.K_pad * 4;
-  char* sB_hi = sA_lo + TC_M * p.K_pad * 4;
-  char* sB_lo = sB_hi + p.N_pad * p.K_pad * 4;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sB_lo + p.N_pad * p.K_pad * 4);
+  const int a_bytes = TC_M * p.K_pad * 4, b_bytes = p.N_pad * p.K_pad * 4;
+  char* sB_hi = smem;
+  char* sB_lo = sB_hi + b_bytes;
+  char* sA_lo = sB_lo + b_bytes;
+  char* sA_raw[2] = {sA_lo + a_bytes, sA_lo + 2 * a_bytes};
+  const bool use_mask = MODE == 1 && p.mask;
+  char* sM_raw[2] = {sA_lo + (1 + p.stages) * a_bytes, sA_lo + (2 + p.stages) * a_bytes};
+  char* tail = sA_lo + (1 + p.stages + (use_mask ? p.stages : 0)) * a_bytes;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tail);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
 
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(p.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
+  const int64_t tiles = ceil_div(p.M, TC_M);
+  int64_t t = blockIdx.x;
+  if (t < tiles) issue_tile<MODE>(p, t * TC_M, sA_raw[0], sM_raw[0], KC);
+  cp_async_commit();
+  if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(1));
+    mbar_init(smem_u32(mbar));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   // weight operand B[n][k], split once per CTA
@@ -133,91 +202,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
     const int n = idx / p.K_pad, k = idx % p.K_pad;
     float v = 0.f;
     if (n < p.N && k < p.K) v = MODE == 0 ? p.W[(int64_t)k * p.N + n] : p.W[(int64_t)n * p.K + k];
-    float h, l;
-    split_tf32(v, h, l);
-    const uint32_t off = kmaj_off(n, k, KC);
+    const float h = tf32_hi(v);
+    const uint32_t off = kmaj_off(n, k, KC) + (k & 3) * 4;
     *reinterpret_cast<float*>(sB_hi + off) = h;
-    *reinterpret_cast<float*>(sB_lo + off) = l;
+    *reinterpret_cast<float*>(sB_lo + off) = __fsub_rn(v, h);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const uint32_t bar = smem_u32(mbar);
-  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad);
-  const bool vec = (p.lda % 4 == 0) && !(reinterpret_cast<uintptr_t>(p.A) & 15) &&
-                   (MODE == 0 || ((p.ldm % 4 == 0) && !(reinterpret_cast<uintptr_t>(p.mask) & 15)));
+  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad, 0, 0);
+  const uint32_t sbo = KC * 128;
   uint32_t phase = 0;
-  const int64_t tiles = ceil_div(p.M, TC_M);
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  for (int j = 0; t < tiles; t += gridDim.x, ++j) {
+    const int buf = p.stages == 2 ? (j & 1) : 0;
     const int64_t m0 = t * TC_M;
-    // ---- A tile -> shared (hi / lo): TC_LOADS independent 16-byte loads per
-    // thread are issued before any of them is split and stored ----
-    for (int base = 0; base < TC_M * KC; base += TC_THREADS * TC_LOADS) {
-      float4 v[TC_LOADS], mk[TC_LOADS];
-#pragma unroll
-      for (int u = 0; u < TC_LOADS; ++u) {
-        const int idx = base + u * TC_THREADS + tid;
-        const int r = idx / KC, k = 4 * (idx % KC);
-        const int64_t row = m0 + r;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        mk[u] = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (idx < TC_M * KC && row < p.M && k < p.K) {
-          const float* src = p.A + row * p.lda + k;
-          if (vec && k + 3 < p.K) {
-            v[u] = __ldg(reinterpret_cast<const float4*>(src));
-            if (MODE == 1 && p.mask) mk[u] = __ldg(reinterpret_cast<const float4*>(p.mask + row * p.ldm + k));
-          } else {
-            float e[4], g[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              e[q] = (k + q < p.K) ? src[q] : 0.f;
-              g[q] = (MODE == 1 && p.mask && k + q < p.K) ? p.mask[row * p.ldm + k + q] : 1.f;
-            }
-            v[u] = make_float4(e[0], e[1], e[2], e[3]);
-            mk[u] = make_float4(g[0], g[1], g[2], g[3]);
-          }
-        }
+    const int64_t tn = t + gridDim.x;
+    if (p.stages == 2 && tn < tiles) {  // next tile's copies overlap this tile's work
+      issue_tile<MODE>(p, tn * TC_M, sA_raw[buf ^ 1], sM_raw[buf ^ 1], KC);
+      cp_async_commit();
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    // split pass (chunk = thread, smem order)
+    char* raw = sA_raw[buf];
+    for (int idx = tid; idx < TC_M * KC; idx += TC_THREADS) {
+      const uint32_t off = (uint32_t)idx * 16u;
+      float4 x = *reinterpret_cast<const float4*>(raw + off);
+      if (use_mask) {
+        const float4 m = *reinterpret_cast<const float4*>(sM_raw[buf] + off);
+        if (!(m.x > 0.f)) x.x = 0.f;
+        if (!(m.y > 0.f)) x.y = 0.f;
+        if (!(m.z > 0.f)) x.z = 0.f;
+        if (!(m.w > 0.f)) x.w = 0.f;
       }
-#pragma unroll
-      for (int u = 0; u < TC_LOADS; ++u) {
-        const int idx = base + u * TC_THREADS + tid;
-        if (idx >= TC_M * KC) continue;
-        float4 x = v[u];
-        if (MODE == 1) {
-          if (!(mk[u].x > 0.f)) x.x = 0.f;
-          if (!(mk[u].y > 0.f)) x.y = 0.f;
-          if (!(mk[u].z > 0.f)) x.z = 0.f;
-          if (!(mk[u].w > 0.f)) x.w = 0.f;
-        }
-        store_split4(sA_hi, sA_lo, kmaj_off(idx / KC, 4 * (idx % KC), KC), x);
-      }
+      split_chunk(raw, sA_lo, off, x);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // ---- MMA issue (one thread) ----
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a_hi = smem_u32(sA_hi), a_lo = smem_u32(sA_lo);
+      const uint32_t a_hi = smem_u32(raw), a_lo = smem_u32(sA_lo);
       const uint32_t b_hi = smem_u32(sB_hi), b_lo = smem_u32(sB_lo);
-      const uint32_t sbo = KC * 128;
       const int steps = p.K_pad / 8;
-      uint32_t acc = 0;
       for (int s = 0; s < steps; ++s) {  // small terms first
-        mma_tf32(tmem, umma_desc(a_lo + s * 256, 128, sbo), umma_desc(b_hi + s * 256, 128, sbo), idesc, acc);
-        acc = 1;
+        mma_tf32(tmem, umma_desc(a_lo + s * 256, 128, sbo), umma_desc(b_hi + s * 256, 128, sbo), idesc, s > 0);
         mma_tf32(tmem, umma_desc(a_hi + s * 256, 128, sbo), umma_desc(b_lo + s * 256, 128, sbo), idesc, 1);
       }
       for (int s = 0; s < steps; ++s)
         mma_tf32(tmem, umma_desc(a_hi + s * 256, 128, sbo), umma_desc(b_hi + s * 256, 128, sbo), idesc, 1);
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                   : "memory");
+      mma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
+    if (p.stages == 1 && tn < tiles) {  // single buffer: next copies start once the MMAs are done
+      issue_tile<MODE>(p, tn * TC_M, sA_raw[0], sM_raw[0], KC);
+      cp_async_commit();
+    }
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- epilogue: TMEM lanes 32w.. -> rows ----
-    // warp w drains TMEM lane quarter w%4 (rows) and column half w/4
+    // epilogue: warp w drains TMEM lane quarter w%4 (rows), column half w/4
     const int quarter = warp & 3, half = warp >> 2;
     const int64_t row = m0 + quarter * 32 + lane;
     const int chunks = p.N_pad / 16;
@@ -225,20 +271,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
     const int c_end = half == 0 ? ((chunks + 1) / 2) * 16 : p.N_pad;
     for (int c0 = c_begin; c0 < c_end; c0 += 16) {
       uint32_t v[16];
-      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
       if (row < p.M) {
         float* out = p.C + row * p.ldc;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
+        for (int q = 0; q < 16; ++q) {
+          const int col = c0 + q;
           if (col < p.N) {
-            float x = __uint_as_float(v[j]);
+            float x = __uint_as_float(v[q]);
             if (MODE == 0 && p.bias) x = __fadd_rn(x, p.bias[col]);
             if (p.relu) x = x > 0.f ? x : 0.f;
             out[col] = x;
@@ -247,23 +287,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM drained and shared A free before the next tile
+    __syncthreads();  // TMEM drained and sA_lo / the raw buffer free before reuse
   }
+  cp_async_wait_all();
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+    tmem_free(tmem, p.tmem_cols);
   }
+}
+
+int64_t tc_gemm_smem(int mode, bool has_mask, int N_pad, int K_pad, int stages) {
+  const int64_t a = (int64_t)TC_M * K_pad * 4, b = (int64_t)N_pad * K_pad * 4;
+  return 2 * b + a * (1 + stages + ((mode == 1 && has_mask) ? stages : 0)) + 64;
 }
 
 // ---------------------------------------------------------------- wgrad --
 // Partial [dW; db] of a row chunk: D[m][n] = sum_r A'[m][r] B'[n][r] with
-// A'[m][r] = H[r][m] (m < K), 1 (m == K: the bias row), B'[n][r] = dZ[r][n] *
-// (Xout[r][n] > 0).  The row dimension is the MMA K dimension, consumed in
-// stages of 32 rows through a 2-deep shared-memory ring (the loads of stage
-// s+1 overlap the MMAs of stage s); partials of all CTAs are summed by
-// reduce_partials_kernel in a fixed order (deterministic).
-constexpr int WG_KS = 32;  // rows per stage (MMA K)
+// A'[m][r] = H[r][m] (m < K), 1 (m == K: the bias row) and B'[n][r] =
+// dZ[r][n] * (Xout[r][n] > 0).  Rows r are the MMA K dimension; both operands
+// are MN-major, so every 16-byte chunk of an H / dZ row copies straight into
+// the canonical layout.  Stages of 32 rows, raw buffers double-buffered.
+constexpr int WG_KS = 32;
 
 struct WgArgs {
   const float* H; int64_t ldh;
@@ -275,95 +320,118 @@ struct WgArgs {
   int K, N, N_pad, tmem_cols;
 };
 
+__device__ __forceinline__ void wg_issue(const WgArgs& p, int64_t rs, int64_t r_end, char* a_raw, char* b_raw,
+                                         char* m_raw) {
+  constexpr int AM4 = TC_M / 4;
+  const int BN4 = p.N_pad / 4;
+  for (int idx = threadIdx.x; idx < WG_KS * AM4; idx += TC_THREADS) {
+    const int kk = idx / AM4, g = idx % AM4;  // row within the stage, 4-column group of H
+    const int64_t r = rs + kk;
+    const int m = 4 * g;
+    const int valid = (r < r_end && m < p.K) ? (int)min(4, p.K - m) : 0;
+    cp_async16(smem_u32(a_raw + mnmaj_off(kk, m, AM4)), valid ? p.H + r * p.ldh + m : p.H, valid * 4);
+  }
+  for (int idx = threadIdx.x; idx < WG_KS * BN4; idx += TC_THREADS) {
+    const int kk = idx / BN4, g = idx % BN4;
+    const int64_t r = rs + kk;
+    const int n = 4 * g;
+    const int valid = (r < r_end && n < p.N) ? (int)min(4, p.N - n) : 0;
+    const uint32_t off = mnmaj_off(kk, n, BN4);
+    cp_async16(smem_u32(b_raw + off), valid ? p.dZ + r * p.ldz + n : p.dZ, valid * 4);
+    if (p.mask) cp_async16(smem_u32(m_raw + off), valid ? p.mask + r * p.ldm + n : p.mask, valid * 4);
+  }
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int KC = WG_KS / 4;
+  constexpr int AM4 = TC_M / 4;
+  const int BN4 = p.N_pad / 4;
   const int a_bytes = TC_M * WG_KS * 4, b_bytes = p.N_pad * WG_KS * 4;
-  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(p.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
+  char* a_raw[2] = {smem, smem + a_bytes};
+  char* b_raw[2] = {smem + 2 * a_bytes, smem + 2 * a_bytes + b_bytes};
+  char* m_raw[2] = {smem + 2 * a_bytes + 2 * b_bytes, smem + 2 * a_bytes + 3 * b_bytes};
+  char* a_lo = smem + 2 * a_bytes + 4 * b_bytes;
+  char* b_lo = a_lo + a_bytes;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(b_lo + b_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+
+  const int64_t r_begin = blockIdx.x * p.rows_per_cta;
+  const int64_t r_end = min(p.M, r_begin + p.rows_per_cta);
+  const int stages = r_end > r_begin ? (int)ceil_div(r_end - r_begin, WG_KS) : 0;
+  if (stages > 0) wg_issue(p, r_begin, r_end, a_raw[0], b_raw[0], m_raw[0]);
+  cp_async_commit();
+  if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(1));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar + 1)), "r"(1));
+    mbar_init(smem_u32(mbar));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad);
-  const int64_t r_begin = blockIdx.x * p.rows_per_cta;
-  const int64_t r_end = min(p.M, r_begin + p.rows_per_cta);
-  const int stages = r_end > r_begin ? (int)ceil_div(r_end - r_begin, WG_KS) : 0;
-  uint32_t phase[2] = {0, 0};
+  const uint32_t bar = smem_u32(mbar);
+  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad, 1, 1);
+  uint32_t phase = 0;
   for (int s = 0; s < stages; ++s) {
     const int buf = s & 1;
-    char* a_hi = smem + buf * stage_bytes;
-    char* a_lo = a_hi + a_bytes;
-    char* b_hi = a_lo + a_bytes;
-    char* b_lo = b_hi + b_bytes;
-    if (s >= 2) {  // MMAs of stage s-2 must be done with this buffer
-      mbar_wait(smem_u32(mbar + buf), phase[buf]);
-      phase[buf] ^= 1;
-    }
     const int64_t rs = r_begin + (int64_t)s * WG_KS;
-    // A'[m][r]: item = (m, kq) gathers rows rs+4kq..+3 of column m
-    for (int it = tid; it < TC_M * KC; it += TC_THREADS) {
-      const int m = it % TC_M, kq = it / TC_M;
-      float e[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t r = rs + 4 * kq + q;
-        float x = 0.f;
-        if (r < r_end) x = m < p.K ? p.H[r * p.ldh + m] : (m == p.K ? 1.f : 0.f);
-        e[q] = x;
-      }
-      store_split4(a_hi, a_lo, kmaj_off(m, 4 * kq, KC), make_float4(e[0], e[1], e[2], e[3]));
+    if (s > 0) {  // MMAs of stage s-1 done: lo buffers and raw[buf^1] are free
+      mbar_wait(bar, phase);
+      phase ^= 1;
     }
-    for (int it = tid; it < p.N_pad * KC; it += TC_THREADS) {
-      const int n = it % p.N_pad, kq = it / p.N_pad;
-      float e[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t r = rs + 4 * kq + q;
-        float x = 0.f;
-        if (r < r_end && n < p.N) {
-          x = p.dZ[r * p.ldz + n];
-          if (p.mask && !(p.mask[r * p.ldm + n] > 0.f)) x = 0.f;
-        }
-        e[q] = x;
+    if (s + 1 < stages) {
+      wg_issue(p, rs + WG_KS, r_end, a_raw[buf ^ 1], b_raw[buf ^ 1], m_raw[buf ^ 1]);
+      cp_async_commit();
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    // split: A' chunks (plus the ones row m == K), B' chunks (ReLU-masked)
+    for (int idx = tid; idx < WG_KS * AM4; idx += TC_THREADS) {
+      const int kk = idx / AM4, g = idx % AM4;
+      const uint32_t off = mnmaj_off(kk, 4 * g, AM4);
+      float4 x = *reinterpret_cast<const float4*>(a_raw[buf] + off);
+      if ((p.K >> 2) == g && rs + kk < r_end) {  // bias row lives in this chunk
+        const int q = p.K & 3;
+        if (q == 0) x.x = 1.f; else if (q == 1) x.y = 1.f; else if (q == 2) x.z = 1.f; else x.w = 1.f;
       }
-      store_split4(b_hi, b_lo, kmaj_off(n, 4 * kq, KC), make_float4(e[0], e[1], e[2], e[3]));
+      split_chunk(a_raw[buf], a_lo, off, x);
+    }
+    for (int idx = tid; idx < WG_KS * BN4; idx += TC_THREADS) {
+      const int kk = idx / BN4, g = idx % BN4;
+      const uint32_t off = mnmaj_off(kk, 4 * g, BN4);
+      float4 x = *reinterpret_cast<const float4*>(b_raw[buf] + off);
+      if (p.mask) {
+        const float4 m = *reinterpret_cast<const float4*>(m_raw[buf] + off);
+        if (!(m.x > 0.f)) x.x = 0.f;
+        if (!(m.y > 0.f)) x.y = 0.f;
+        if (!(m.z > 0.f)) x.z = 0.f;
+        if (!(m.w > 0.f)) x.w = 0.f;
+      }
+      split_chunk(b_raw[buf], b_lo, off, x);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-      const uint32_t sbo = KC * 128;
+      const uint32_t ah = smem_u32(a_raw[buf]), al = smem_u32(a_lo);
+      const uint32_t bh = smem_u32(b_raw[buf]), bl = smem_u32(b_lo);
+      const uint32_t a_lbo = AM4 * 128, b_lbo = BN4 * 128;
 #pragma unroll
       for (int k = 0; k < WG_KS / 8; ++k) {
-        mma_tf32(tmem, umma_desc(al + k * 256, 128, sbo), umma_desc(bh + k * 256, 128, sbo), idesc,
-                 (s > 0 || k > 0) ? 1u : 0u);
-        mma_tf32(tmem, umma_desc(ah + k * 256, 128, sbo), umma_desc(bl + k * 256, 128, sbo), idesc, 1u);
-        mma_tf32(tmem, umma_desc(ah + k * 256, 128, sbo), umma_desc(bh + k * 256, 128, sbo), idesc, 1u);
+        const uint32_t ao = k * a_lbo, bo = k * b_lbo;
+        mma_tf32(tmem, umma_desc(al + ao, a_lbo, 128), umma_desc(bh + bo, b_lbo, 128), idesc, (s > 0 || k > 0));
+        mma_tf32(tmem, umma_desc(ah + ao, a_lbo, 128), umma_desc(bl + bo, b_lbo, 128), idesc, 1);
+        mma_tf32(tmem, umma_desc(ah + ao, a_lbo, 128), umma_desc(bh + bo, b_lbo, 128), idesc, 1);
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(mbar + buf))
-                   : "memory");
+      mma_commit(bar);
     }
   }
-  // drain: wait for the last (up to two) outstanding commits
-  for (int s = stages >= 2 ? stages - 2 : 0; s < stages; ++s) {
-    const int buf = s & 1;
-    mbar_wait(smem_u32(mbar + buf), phase[buf]);
-    phase[buf] ^= 1;
+  if (stages > 0) {
+    mbar_wait(bar, phase);
+    phase ^= 1;
   }
   asm volatile("tcgen05.fence::after_thread_sync;");
   const int quarter = warp & 3, half = warp >> 2;
@@ -374,18 +442,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
   float* out = p.part + (int64_t)blockIdx.x * (p.K + 1) * p.N;
   for (int c0 = c_begin; c0 < c_end; c0 += 16) {
     uint32_t v[16];
-    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
     if (m <= p.K) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = c0 + j;
-        if (n < p.N) out[(int64_t)m * p.N + n] = stages ? __uint_as_float(v[j]) : 0.f;
+      for (int q = 0; q < 16; ++q) {
+        const int n = c0 + q;
+        if (n < p.N) out[(int64_t)m * p.N + n] = stages ? __uint_as_float(v[q]) : 0.f;
       }
     }
   }
@@ -393,35 +455,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+    tmem_free(tmem, p.tmem_cols);
   }
 }
 
-inline int64_t tc_smem_bytes(int N_pad, int K_pad) {
-  return 4ll * K_pad * (2 * TC_M + 2 * N_pad) + 64;
+int64_t tc_wgrad_smem(int N_pad) {
+  const int64_t a = (int64_t)TC_M * WG_KS * 4, b = (int64_t)N_pad * WG_KS * 4;
+  return 3 * a + 5 * b + 64;
 }
 
-}  // namespace
-
-// Host-side dispatch; returns false when the shape is outside the kernel's
-// envelope (caller falls back to the SIMT kernels).
-bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
-             const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
-             cudaStream_t st, int* err) {
-  *err = 0;
+bool dense_tc_disabled() {
   static const int disabled = [] {
     const char* v = getenv("FGL_DENSE");
     return (v && v[0] == 's') ? 1 : 0;  // FGL_DENSE=simt forces the SIMT kernels
   }();
-  if (disabled || M < 1 || N < 1 || K < 1) return false;
+  return disabled != 0;
+}
+
+inline bool aligned16(const void* p) { return !(reinterpret_cast<uintptr_t>(p) & 15); }
+
+}  // namespace
+
+bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
+             const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
+             cudaStream_t st, int* err) {
+  *err = 0;
+  if (dense_tc_disabled() || M < 1 || N < 1 || K < 1) return false;
+  if ((lda % 4) || !aligned16(A) || (mask && ((ldm % 4) || !aligned16(mask)))) return false;
   const int N_pad = (N + 15) / 16 * 16;
   const int K_pad = (K + 7) / 8 * 8;
   if (N_pad > 256 || K_pad > 256) return false;
-  const int64_t smem = tc_smem_bytes(N_pad, K_pad);
+  const bool has_mask = mode == 1 && mask;
+  int stages = 2;
+  if (tc_gemm_smem(mode, has_mask, N_pad, K_pad, 2) > TC_MAX_SMEM) stages = 1;
+  const int64_t smem = tc_gemm_smem(mode, has_mask, N_pad, K_pad, stages);
   if (smem > TC_MAX_SMEM) return false;
   int cols = 32;
   while (cols < N_pad) cols <<= 1;
-  TcArgs p{A, lda, mask, ldm, W, bias, C, ldc, M, N, K, N_pad, K_pad, relu, cols};
+  TcArgs p{A, lda, mask, ldm, W, bias, C, ldc, M, N, K, N_pad, K_pad, relu, cols, stages};
   static bool attr_set[2] = {false, false};
   cudaError_t e;
   if (!attr_set[mode]) {
@@ -439,19 +510,15 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
   return true;
 }
 
-// [dW; db] partials over `chunks` row chunks into part[chunks][K+1][N];
-// false when the shape is outside the kernel's envelope.
 bool tc_wgrad(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
   *err = 0;
-  static const int disabled = [] {
-    const char* v = getenv("FGL_DENSE");
-    return (v && v[0] == 's') ? 1 : 0;
-  }();
-  if (disabled || M < 1 || K + 1 > TC_M || N < 1) return false;
+  if (dense_tc_disabled() || M < 1 || K + 1 > TC_M || N < 1) return false;
+  if ((ldh % 4) || (ldz % 4) || !aligned16(H) || !aligned16(dZ) || (mask && ((ldm % 4) || !aligned16(mask))))
+    return false;
   const int N_pad = (N + 15) / 16 * 16;
   if (N_pad > 256) return false;
-  const int64_t smem = 2ll * (2 * TC_M * WG_KS * 4 + 2 * N_pad * WG_KS * 4) + 64;
+  const int64_t smem = tc_wgrad_smem(N_pad);
   if (smem > TC_MAX_SMEM) return false;
   int cols = 32;
   while (cols < N_pad) cols <<= 1;
