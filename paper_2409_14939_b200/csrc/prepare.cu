@@ -96,12 +96,22 @@ __global__ void chunk_scan_kernel(const int32_t* __restrict__ v, int64_t n, cons
   const int64_t chunk = ceil_div(n, gridDim.x);
   const int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
   int64_t run = base + part[blockIdx.x];
-  for (int64_t t0 = i0; t0 < i1; t0 += blockDim.x) {
-    const int64_t i = t0 + threadIdx.x;
-    const int64_t x = i < i1 ? v[i] : 0;
+  constexpr int IT = 8;  // items per thread per tile (thread-blocked)
+  for (int64_t t0 = i0; t0 < i1; t0 += (int64_t)blockDim.x * IT) {
+    const int64_t first = t0 + (int64_t)threadIdx.x * IT;
+    int64_t x[IT], local = 0;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      x[q] = first + q < i1 ? v[first + q] : 0;
+      const int64_t t = x[q];
+      x[q] = local;  // exclusive within the thread
+      local += t;
+    }
     int64_t tot;
-    const int64_t ex = block_excl_scan(x, sm, &tot);
-    if (i < i1) out[i] = run + ex;
+    const int64_t ex = run + block_excl_scan(local, sm, &tot);
+#pragma unroll
+    for (int q = 0; q < IT; ++q)
+      if (first + q < i1) out[first + q] = ex + x[q];
     run += tot;
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = base + part[gridDim.x];

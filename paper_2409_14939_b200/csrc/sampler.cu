@@ -168,24 +168,34 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
   const int64_t chunk = ceil_div(nwords, gridDim.x);
   const int64_t w0 = blockIdx.x * chunk, w1 = min(nwords, w0 + chunk);
   int64_t base = part[blockIdx.x];
-  for (int64_t t0 = w0; t0 < w1; t0 += blockDim.x) {
-    const int64_t w = t0 + threadIdx.x;
-    const uint32_t v = w < w1 ? bm[w] : 0u;
+  constexpr int IT = 4;  // consecutive words per thread per tile
+  for (int64_t t0 = w0; t0 < w1; t0 += (int64_t)blockDim.x * IT) {
+    const int64_t wf = t0 + (int64_t)threadIdx.x * IT;
+    uint32_t v[IT];
+    int64_t local = 0;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      v[q] = wf + q < w1 ? bm[wf + q] : 0u;
+      local += __popc(v[q]);
+    }
     int64_t tot;
-    const int64_t ex = base + block_excl_scan<int64_t>(__popc(v), sm, &tot);
-    if (w < w1) {
+    int64_t ex = base + block_excl_scan<int64_t>(local, sm, &tot);
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      const int64_t w = wf + q;
+      if (w >= w1) break;
       const int64_t b = w / words;
       if (batch_off && w == b * words) batch_off[b] = ex;
       if (wprefix) wprefix[w] = (int32_t)ex;
-      if (v) {
-        if (or_into) or_into[w] |= v;
+      if (v[q]) {
+        if (or_into) or_into[w] |= v[q];
         if (clear) bm[w] = 0u;
         if (ids) {
-          if (ex + __popc(v) > cap) {
+          if (ex + __popc(v[q]) > cap) {
             set_status(status, FGL_E_CAPACITY);
           } else {
             const int32_t node0 = (int32_t)((w - b * words) << 5);
-            uint32_t m = v;
+            uint32_t m = v[q];
             int64_t o = ex;
             while (m) {
               const int bit = __ffs(m) - 1;
@@ -197,6 +207,7 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
           }
         }
       }
+      ex += __popc(v[q]);
     }
     base += tot;
   }
@@ -239,16 +250,31 @@ __global__ void deg_down_kernel(const int64_t* __restrict__ off, const int32_t* 
   const int64_t chunk = ceil_div(F, gridDim.x);
   const int64_t i0 = blockIdx.x * chunk, i1 = min(F, i0 + chunk);
   int64_t bd = part[blockIdx.x], bs = part[gridDim.x + 1 + blockIdx.x];
-  for (int64_t t0 = i0; t0 < i1; t0 += blockDim.x) {
-    const int64_t i = t0 + threadIdx.x;
-    int64_t d = 0, s = 0;
-    if (i < i1) node_deg_sel(off, front[i], fan, d, s);
+  constexpr int IT = 4;  // consecutive frontier entries per thread per tile
+  for (int64_t t0 = i0; t0 < i1; t0 += (int64_t)blockDim.x * IT) {
+    const int64_t first = t0 + (int64_t)threadIdx.x * IT;
+    int64_t d[IT], s[IT], ld = 0, ls = 0;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      d[q] = 0;
+      s[q] = 0;
+      if (first + q < i1) node_deg_sel(off, front[first + q], fan, d[q], s[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {  // exclusive within the thread
+      const int64_t a = d[q], c = s[q];
+      d[q] = ld; s[q] = ls;
+      ld += a; ls += c;
+    }
     int64_t td, ts;
-    const int64_t ed = block_excl_scan(d, sm, &td);
-    const int64_t es = block_excl_scan(s, sm, &ts);
-    if (i < i1) {
-      scan_deg[i] = bd + ed;
-      scan_sel[i] = bs + es;
+    const int64_t ed = bd + block_excl_scan(ld, sm, &td);
+    const int64_t es = bs + block_excl_scan(ls, sm, &ts);
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      if (first + q < i1) {
+        scan_deg[first + q] = ed + d[q];
+        scan_sel[first + q] = es + s[q];
+      }
     }
     bd += td;
     bs += ts;
@@ -673,7 +699,9 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
       p0 = a.hop_pos[b] + sd;
       obase = ebase + ss;
     }
-    const bool mine = lane_ok && d > 0 && d <= kLaneDeg;
+    // the lane path pays off only when enough lanes of the tile use it
+    const bool eligible = lane_ok && d > 0 && d <= kLaneDeg;
+    const bool mine = eligible && __popc(__ballot_sync(0xffffffffu, eligible)) >= 8;
     const int nblk = mine ? (int)(((p0 & 3) + d + 3) >> 2) : 0;
     const int max_blocks = __reduce_max_sync(0xffffffffu, (unsigned)nblk);
     if (max_blocks > 0) {
