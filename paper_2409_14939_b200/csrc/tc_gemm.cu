@@ -317,7 +317,7 @@ struct WgArgs {
   float* part;          // [chunks][K+1][N]
   int64_t M;            // rows
   int64_t rows_per_cta;
-  int K, N, N_pad, tmem_cols;
+  int K, N, N_pad, tmem_cols, swap;
 };
 
 __device__ __forceinline__ void wg_issue(const WgArgs& p, int64_t rs, int64_t r_end, char* a_raw, char* b_raw,
@@ -418,13 +418,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t ah = smem_u32(a_raw[buf]), al = smem_u32(a_lo);
       const uint32_t bh = smem_u32(b_raw[buf]), bl = smem_u32(b_lo);
-      const uint32_t a_lbo = AM4 * 128, b_lbo = BN4 * 128;
+      const uint32_t a_kst = AM4 * 128, b_kst = BN4 * 128;  // bytes between 8-row K groups
+      // MN-major no-swizzle: one offset is the MN-atom stride (128 B), the
+      // other the K-group stride; p.swap selects which field carries which
+      auto dsc = [&](uint32_t addr, uint32_t kst) {
+        return p.swap ? umma_desc(addr, 128, kst) : umma_desc(addr, kst, 128);
+      };
 #pragma unroll
       for (int k = 0; k < WG_KS / 8; ++k) {
-        const uint32_t ao = k * a_lbo, bo = k * b_lbo;
-        mma_tf32(tmem, umma_desc(al + ao, a_lbo, 128), umma_desc(bh + bo, b_lbo, 128), idesc, (s > 0 || k > 0));
-        mma_tf32(tmem, umma_desc(ah + ao, a_lbo, 128), umma_desc(bl + bo, b_lbo, 128), idesc, 1);
-        mma_tf32(tmem, umma_desc(ah + ao, a_lbo, 128), umma_desc(bh + bo, b_lbo, 128), idesc, 1);
+        const uint32_t ao = k * a_kst, bo = k * b_kst;
+        mma_tf32(tmem, dsc(al + ao, a_kst), dsc(bh + bo, b_kst), idesc, (s > 0 || k > 0));
+        mma_tf32(tmem, dsc(ah + ao, a_kst), dsc(bl + bo, b_kst), idesc, 1);
+        mma_tf32(tmem, dsc(ah + ao, a_kst), dsc(bh + bo, b_kst), idesc, 1);
       }
       mma_commit(bar);
     }
@@ -529,7 +534,11 @@ bool tc_wgrad(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const f
     if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad)"); return true; }
     attr = true;
   }
-  WgArgs p{H, ldh, dZ, ldz, mask, ldm, part, M, ceil_div(M, chunks), K, N, N_pad, cols};
+  static const int swap = [] {
+    const char* v = getenv("FGL_WG_SWAP");
+    return (v && v[0] == '1') ? 1 : 0;
+  }();
+  WgArgs p{H, ldh, dZ, ldz, mask, ldm, part, M, ceil_div(M, chunks), K, N, N_pad, cols, swap};
   FGL_COUNT_LAUNCH(), tc_wgrad_kernel<<<chunks, TC_THREADS, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad_kernel");
