@@ -10,9 +10,9 @@
 //
 // Data movement (one CTA of 8 warps per SM, persistent over tiles):
 //  * operand tiles are copied global -> shared with 16-byte cp.async straight
-//    into the UMMA canonical no-swizzle layouts (K-major: 8 rows x 16 B core
-//    matrices; MN-major for the weight gradient, so the activations' rows copy
-//    in without a transpose); zero fill handles ragged rows / columns;
+//    into the UMMA canonical K-major no-swizzle layout (8 rows x 16 B core
+//    matrices; the weight gradient stages rows and transposes in shared
+//    memory); zero fill handles ragged rows / columns;
 //  * a split pass rewrites each raw chunk in place as its tf32 hi part and
 //    writes the lo part to a second buffer (conflict-free, chunk = thread);
 //  * one elected thread issues the 3*K/8 tcgen05.mma.kind::tf32 (M=128,
@@ -137,6 +137,17 @@ __device__ __forceinline__ void split_chunk(char* raw, char* lo_base, uint32_t o
   *reinterpret_cast<float4*>(lo_base + off) = l;
 }
 
+// split x into hi -> hi_base + off and lo -> lo_base + off
+__device__ __forceinline__ void split_chunk_to(char* hi_base, char* lo_base, uint32_t off, float4 x) {
+  float4 h, l;
+  h.x = tf32_hi(x.x); l.x = __fsub_rn(x.x, h.x);
+  h.y = tf32_hi(x.y); l.y = __fsub_rn(x.y, h.y);
+  h.z = tf32_hi(x.z); l.z = __fsub_rn(x.z, h.z);
+  h.w = tf32_hi(x.w); l.w = __fsub_rn(x.w, h.w);
+  *reinterpret_cast<float4*>(hi_base + off) = h;
+  *reinterpret_cast<float4*>(lo_base + off) = l;
+}
+
 // ------------------------------------------------------------- fwd / dgrad --
 struct TcArgs {
   const float* A;      // [M, K] row-major (lda), 16-byte aligned rows
@@ -187,11 +198,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
   char* tail = sA_lo + (1 + p.stages + (use_mask ? p.stages : 0)) * a_bytes;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tail);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  float* sbias = reinterpret_cast<float*>(tail + 16);
+  const bool out_vec = (p.ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(p.C) & 15);
 
   const int64_t tiles = ceil_div(p.M, TC_M);
   int64_t t = blockIdx.x;
   if (t < tiles) issue_tile<MODE>(p, t * TC_M, sA_raw[0], sM_raw[0], KC);
   cp_async_commit();
+  for (int c = tid; c < p.N_pad; c += TC_THREADS) sbias[c] = (MODE == 0 && p.bias && c < p.N) ? p.bias[c] : 0.f;
   if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
   if (tid == 0) {
     mbar_init(smem_u32(mbar));
@@ -274,14 +288,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
       tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
       if (row < p.M) {
         float* out = p.C + row * p.ldc;
+        float x[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
+          float y = __uint_as_float(v[q]);
+          if (MODE == 0 && p.bias) y = __fadd_rn(y, sbias[c0 + q]);
+          if (p.relu) y = y > 0.f ? y : 0.f;
+          x[q] = y;
+        }
+        // 16-byte stores inside the row's leading dimension, scalar tail
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
           const int col = c0 + q;
-          if (col < p.N) {
-            float x = __uint_as_float(v[q]);
-            if (MODE == 0 && p.bias) x = __fadd_rn(x, p.bias[col]);
-            if (p.relu) x = x > 0.f ? x : 0.f;
-            out[col] = x;
+          if (col + 3 < p.ldc && col < p.N && out_vec) {
+            *reinterpret_cast<float4*>(out + col) = make_float4(x[q], x[q + 1], x[q + 2], x[q + 3]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (col + u < p.N) out[col + u] = x[q + u];
           }
         }
       }
@@ -299,16 +323,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcArgs p) {
 
 int64_t tc_gemm_smem(int mode, bool has_mask, int N_pad, int K_pad, int stages) {
   const int64_t a = (int64_t)TC_M * K_pad * 4, b = (int64_t)N_pad * K_pad * 4;
-  return 2 * b + a * (1 + stages + ((mode == 1 && has_mask) ? stages : 0)) + 64;
+  return 2 * b + a * (1 + stages + ((mode == 1 && has_mask) ? stages : 0)) + 64 + 4 * N_pad;
 }
 
 // ---------------------------------------------------------------- wgrad --
 // Partial [dW; db] of a row chunk: D[m][n] = sum_r A'[m][r] B'[n][r] with
 // A'[m][r] = H[r][m] (m < K), 1 (m == K: the bias row) and B'[n][r] =
-// dZ[r][n] * (Xout[r][n] > 0).  Rows r are the MMA K dimension; both operands
-// are MN-major, so every 16-byte chunk of an H / dZ row copies straight into
-// the canonical layout.  Stages of 32 rows, raw buffers double-buffered.
+// dZ[r][n] * (Xout[r][n] > 0).  Rows r are the MMA K dimension (K-major
+// operands).  Each stage of 32 rows is cp.async-copied row-major into a
+// double-buffered staging area; the split pass transposes 4 rows x 1 column
+// into each 16-byte K-major chunk (conflict-free shared loads), splits it
+// into tf32 hi/lo, and the MMAs of the stage run while the next stage lands.
 constexpr int WG_KS = 32;
+constexpr int WG_KC = WG_KS / 4;  // 16-byte chunks per operand row
 
 struct WgArgs {
   const float* H; int64_t ldh;
@@ -317,49 +344,50 @@ struct WgArgs {
   float* part;          // [chunks][K+1][N]
   int64_t M;            // rows
   int64_t rows_per_cta;
-  int K, N, N_pad, tmem_cols, swap;
+  int K, N, N_pad, tmem_cols;
 };
 
-__device__ __forceinline__ void wg_issue(const WgArgs& p, int64_t rs, int64_t r_end, char* a_raw, char* b_raw,
-                                         char* m_raw) {
-  constexpr int AM4 = TC_M / 4;
-  const int BN4 = p.N_pad / 4;
-  for (int idx = threadIdx.x; idx < WG_KS * AM4; idx += TC_THREADS) {
-    const int kk = idx / AM4, g = idx % AM4;  // row within the stage, 4-column group of H
+__device__ __forceinline__ void wg_issue(const WgArgs& p, int64_t rs, int64_t r_end, char* hs, char* zs,
+                                         char* ms) {
+  constexpr int H4 = TC_M / 4;  // staging row of H: 128 floats
+  const int Z4 = p.N_pad / 4;
+  for (int idx = threadIdx.x; idx < WG_KS * H4; idx += TC_THREADS) {
+    const int kk = idx / H4, c = idx % H4;
     const int64_t r = rs + kk;
-    const int m = 4 * g;
+    const int m = 4 * c;
     const int valid = (r < r_end && m < p.K) ? (int)min(4, p.K - m) : 0;
-    cp_async16(smem_u32(a_raw + mnmaj_off(kk, m, AM4)), valid ? p.H + r * p.ldh + m : p.H, valid * 4);
+    cp_async16(smem_u32(hs + (kk * H4 + c) * 16), valid ? p.H + r * p.ldh + m : p.H, valid * 4);
   }
-  for (int idx = threadIdx.x; idx < WG_KS * BN4; idx += TC_THREADS) {
-    const int kk = idx / BN4, g = idx % BN4;
+  for (int idx = threadIdx.x; idx < WG_KS * Z4; idx += TC_THREADS) {
+    const int kk = idx / Z4, c = idx % Z4;
     const int64_t r = rs + kk;
-    const int n = 4 * g;
+    const int n = 4 * c;
     const int valid = (r < r_end && n < p.N) ? (int)min(4, p.N - n) : 0;
-    const uint32_t off = mnmaj_off(kk, n, BN4);
-    cp_async16(smem_u32(b_raw + off), valid ? p.dZ + r * p.ldz + n : p.dZ, valid * 4);
-    if (p.mask) cp_async16(smem_u32(m_raw + off), valid ? p.mask + r * p.ldm + n : p.mask, valid * 4);
+    const int off = (kk * Z4 + c) * 16;
+    cp_async16(smem_u32(zs + off), valid ? p.dZ + r * p.ldz + n : p.dZ, valid * 4);
+    if (p.mask) cp_async16(smem_u32(ms + off), valid ? p.mask + r * p.ldm + n : p.mask, valid * 4);
   }
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
   extern __shared__ __align__(1024) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int AM4 = TC_M / 4;
-  const int BN4 = p.N_pad / 4;
+  const int hs_bytes = WG_KS * TC_M * 4, zs_bytes = WG_KS * p.N_pad * 4;
   const int a_bytes = TC_M * WG_KS * 4, b_bytes = p.N_pad * WG_KS * 4;
-  char* a_raw[2] = {smem, smem + a_bytes};
-  char* b_raw[2] = {smem + 2 * a_bytes, smem + 2 * a_bytes + b_bytes};
-  char* m_raw[2] = {smem + 2 * a_bytes + 2 * b_bytes, smem + 2 * a_bytes + 3 * b_bytes};
-  char* a_lo = smem + 2 * a_bytes + 4 * b_bytes;
-  char* b_lo = a_lo + a_bytes;
+  char* hs[2] = {smem, smem + hs_bytes};
+  char* zs[2] = {smem + 2 * hs_bytes, smem + 2 * hs_bytes + zs_bytes};
+  char* ms[2] = {smem + 2 * hs_bytes + 2 * zs_bytes, smem + 2 * hs_bytes + 3 * zs_bytes};
+  char* a_hi = smem + 2 * hs_bytes + 4 * zs_bytes;
+  char* a_lo = a_hi + a_bytes;
+  char* b_hi = a_lo + a_bytes;
+  char* b_lo = b_hi + b_bytes;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(b_lo + b_bytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
 
   const int64_t r_begin = blockIdx.x * p.rows_per_cta;
   const int64_t r_end = min(p.M, r_begin + p.rows_per_cta);
   const int stages = r_end > r_begin ? (int)ceil_div(r_end - r_begin, WG_KS) : 0;
-  if (stages > 0) wg_issue(p, r_begin, r_end, a_raw[0], b_raw[0], m_raw[0]);
+  if (stages > 0) wg_issue(p, r_begin, r_end, hs[0], zs[0], ms[0]);
   cp_async_commit();
   if (warp == 0) tmem_alloc(tmem_slot, p.tmem_cols);
   if (tid == 0) {
@@ -371,65 +399,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   const uint32_t bar = smem_u32(mbar);
-  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad, 1, 1);
+  const uint32_t idesc = idesc_tf32(TC_M, p.N_pad, 0, 0);
+  const int Z4 = p.N_pad / 4;
   uint32_t phase = 0;
   for (int s = 0; s < stages; ++s) {
     const int buf = s & 1;
     const int64_t rs = r_begin + (int64_t)s * WG_KS;
-    if (s > 0) {  // MMAs of stage s-1 done: lo buffers and raw[buf^1] are free
-      mbar_wait(bar, phase);
-      phase ^= 1;
-    }
     if (s + 1 < stages) {
-      wg_issue(p, rs + WG_KS, r_end, a_raw[buf ^ 1], b_raw[buf ^ 1], m_raw[buf ^ 1]);
+      wg_issue(p, rs + WG_KS, r_end, hs[buf ^ 1], zs[buf ^ 1], ms[buf ^ 1]);
       cp_async_commit();
       cp_async_wait_1();
     } else {
       cp_async_wait_all();
     }
     __syncthreads();
-    // split: A' chunks (plus the ones row m == K), B' chunks (ReLU-masked)
-    for (int idx = tid; idx < WG_KS * AM4; idx += TC_THREADS) {
-      const int kk = idx / AM4, g = idx % AM4;
-      const uint32_t off = mnmaj_off(kk, 4 * g, AM4);
-      float4 x = *reinterpret_cast<const float4*>(a_raw[buf] + off);
-      if ((p.K >> 2) == g && rs + kk < r_end) {  // bias row lives in this chunk
-        const int q = p.K & 3;
-        if (q == 0) x.x = 1.f; else if (q == 1) x.y = 1.f; else if (q == 2) x.z = 1.f; else x.w = 1.f;
-      }
-      split_chunk(a_raw[buf], a_lo, off, x);
+    if (s > 0) {  // the operand buffers are free once the previous stage's MMAs are done
+      mbar_wait(bar, phase);
+      phase ^= 1;
     }
-    for (int idx = tid; idx < WG_KS * BN4; idx += TC_THREADS) {
-      const int kk = idx / BN4, g = idx % BN4;
-      const uint32_t off = mnmaj_off(kk, 4 * g, BN4);
-      float4 x = *reinterpret_cast<const float4*>(b_raw[buf] + off);
-      if (p.mask) {
-        const float4 m = *reinterpret_cast<const float4*>(m_raw[buf] + off);
-        if (!(m.x > 0.f)) x.x = 0.f;
-        if (!(m.y > 0.f)) x.y = 0.f;
-        if (!(m.z > 0.f)) x.z = 0.f;
-        if (!(m.w > 0.f)) x.w = 0.f;
+    // A' chunk (m, 4 rows): column m of 4 staged H rows (+ the ones row m == K)
+    const float* H_s = reinterpret_cast<const float*>(hs[buf]);
+    for (int idx = tid; idx < TC_M * WG_KC; idx += TC_THREADS) {
+      const int m = idx % TC_M, kq = idx / TC_M;
+      float e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kk = 4 * kq + q;
+        e[q] = m == p.K ? (rs + kk < r_end ? 1.f : 0.f) : H_s[kk * TC_M + m];
       }
-      split_chunk(b_raw[buf], b_lo, off, x);
+      split_chunk_to(a_hi, a_lo, kmaj_off(m, 4 * kq, WG_KC), make_float4(e[0], e[1], e[2], e[3]));
+    }
+    const float* Z_s = reinterpret_cast<const float*>(zs[buf]);
+    const float* M_s = reinterpret_cast<const float*>(ms[buf]);
+    for (int idx = tid; idx < p.N_pad * WG_KC; idx += TC_THREADS) {
+      const int n = idx % p.N_pad, kq = idx / p.N_pad;
+      float e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kk = 4 * kq + q;
+        float x = Z_s[kk * 4 * Z4 + n];
+        if (p.mask && !(M_s[kk * 4 * Z4 + n] > 0.f)) x = 0.f;
+        e[q] = x;
+      }
+      split_chunk_to(b_hi, b_lo, kmaj_off(n, 4 * kq, WG_KC), make_float4(e[0], e[1], e[2], e[3]));
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = smem_u32(a_raw[buf]), al = smem_u32(a_lo);
-      const uint32_t bh = smem_u32(b_raw[buf]), bl = smem_u32(b_lo);
-      const uint32_t a_kst = AM4 * 128, b_kst = BN4 * 128;  // bytes between 8-row K groups
-      // MN-major no-swizzle: one offset is the MN-atom stride (128 B), the
-      // other the K-group stride; p.swap selects which field carries which
-      auto dsc = [&](uint32_t addr, uint32_t kst) {
-        return p.swap ? umma_desc(addr, 128, kst) : umma_desc(addr, kst, 128);
-      };
+      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+      const uint32_t sbo = WG_KC * 128;
 #pragma unroll
       for (int k = 0; k < WG_KS / 8; ++k) {
-        const uint32_t ao = k * a_kst, bo = k * b_kst;
-        mma_tf32(tmem, dsc(al + ao, a_kst), dsc(bh + bo, b_kst), idesc, (s > 0 || k > 0));
-        mma_tf32(tmem, dsc(ah + ao, a_kst), dsc(bl + bo, b_kst), idesc, 1);
-        mma_tf32(tmem, dsc(ah + ao, a_kst), dsc(bh + bo, b_kst), idesc, 1);
+        mma_tf32(tmem, umma_desc(al + k * 256, 128, sbo), umma_desc(bh + k * 256, 128, sbo), idesc, (s > 0 || k > 0));
+        mma_tf32(tmem, umma_desc(ah + k * 256, 128, sbo), umma_desc(bl + k * 256, 128, sbo), idesc, 1);
+        mma_tf32(tmem, umma_desc(ah + k * 256, 128, sbo), umma_desc(bh + k * 256, 128, sbo), idesc, 1);
       }
       mma_commit(bar);
     }
@@ -465,8 +489,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_wgrad_kernel(WgArgs p) {
 }
 
 int64_t tc_wgrad_smem(int N_pad) {
-  const int64_t a = (int64_t)TC_M * WG_KS * 4, b = (int64_t)N_pad * WG_KS * 4;
-  return 3 * a + 5 * b + 64;
+  const int64_t hs = (int64_t)WG_KS * TC_M * 4, zs = (int64_t)WG_KS * N_pad * 4;
+  return 2 * hs + 4 * zs + 2 * hs + 2 * zs + 64;
 }
 
 bool dense_tc_disabled() {
@@ -534,11 +558,7 @@ bool tc_wgrad(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const f
     if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad)"); return true; }
     attr = true;
   }
-  static const int swap = [] {
-    const char* v = getenv("FGL_WG_SWAP");
-    return (v && v[0] == '1') ? 1 : 0;
-  }();
-  WgArgs p{H, ldh, dZ, ldz, mask, ldm, part, M, ceil_div(M, chunks), K, N, N_pad, cols, swap};
+  WgArgs p{H, ldh, dZ, ldz, mask, ldm, part, M, ceil_div(M, chunks), K, N, N_pad, cols};
   FGL_COUNT_LAUNCH(), tc_wgrad_kernel<<<chunks, TC_THREADS, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad_kernel");
