@@ -613,17 +613,19 @@ __device__ __noinline__ void tau_select_node(const SelectArgs& a, uint64_t* wk, 
 // in its own column of the warp's shared buffer, then picks the f smallest by
 // repeated minimum search.  Per node this costs a few hundred lane
 // instructions instead of a full warp iteration.
-constexpr int kLaneDeg = 32;
-constexpr int kLaneCap = 32;                       // survivors per lane (<= d)
+constexpr int kLaneDeg = 64;
+constexpr int kLaneCap = 32;                       // survivors per lane
 constexpr int kWarpBufWords = kLaneCap * 32;       // u64 words per warp (8 KB)
 
-__device__ __noinline__ void lane_select(const SelectArgs& a, uint64_t* colbuf, int64_t i, int32_t u,
+// returns false (nothing emitted) if more than kLaneCap candidates survive;
+// the caller then redoes the node on the warp path
+__device__ __noinline__ bool lane_select(const SelectArgs& a, uint64_t* colbuf, int64_t i, int32_t u,
                                          int64_t e0, int d, int b, int64_t p0, int64_t obase,
                                          double expect, int max_blocks) {
   const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
   const int64_t blk0 = p0 >> 2;
   const int off0 = (int)(p0 & 3);
-  const int nblk = (off0 + d + 3) >> 2;  // <= 9
+  const int nblk = (off0 + d + 3) >> 2;  // <= 17
   const int want = d < a.fan ? d : a.fan;
   uint64_t tau = (double)d <= expect ? kKeyOne
                                      : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
@@ -638,10 +640,14 @@ __device__ __noinline__ void lane_select(const SelectArgs& a, uint64_t* colbuf, 
         for (int q = 0; q < 4; ++q) {
           const int j = 4 * t + q - off0;  // slot
           const uint64_t key = w[q] >> 11;
-          if (j >= 0 && j < d && key < tau) colbuf[32 * m++] = (key << 11) | (uint64_t)j;
+          if (j >= 0 && j < d && key < tau) {
+            if (m < kLaneCap) colbuf[32 * m] = (key << 11) | (uint64_t)j;
+            ++m;
+          }
         }
       }
     }
+    if (m > kLaneCap) return false;
     if (m >= want || tau >= kKeyOne) break;
     tau = tau > kKeyOne / 4 ? kKeyOne : tau * 4;
   }
@@ -663,6 +669,7 @@ __device__ __noinline__ void lane_select(const SelectArgs& a, uint64_t* colbuf, 
     if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
     atomicOr(bm + (s >> 5), 1u << (s & 31));
   }
+  return true;
 }
 
 // Each warp takes a tile of up to 32 consecutive frontier entries: the lanes
@@ -701,11 +708,11 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
     }
     // the lane path pays off only when enough lanes of the tile use it
     const bool eligible = lane_ok && d > 0 && d <= kLaneDeg;
-    const bool mine = eligible && __popc(__ballot_sync(0xffffffffu, eligible)) >= 8;
+    bool mine = eligible && __popc(__ballot_sync(0xffffffffu, eligible)) >= 8;
     const int nblk = mine ? (int)(((p0 & 3) + d + 3) >> 2) : 0;
     const int max_blocks = __reduce_max_sync(0xffffffffu, (unsigned)nblk);
     if (max_blocks > 0) {
-      if (mine) lane_select(a, wbuf + lane, i, u, e0, (int)d, b, p0, obase, expect, max_blocks);
+      if (mine) mine = lane_select(a, wbuf + lane, i, u, e0, (int)d, b, p0, obase, expect, max_blocks);
       __syncwarp();
     }
     unsigned big = __ballot_sync(0xffffffffu, d > 0 && !mine);
