@@ -708,7 +708,8 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
     }
     // the lane path pays off only when enough lanes of the tile use it
     const bool eligible = lane_ok && d > 0 && d <= kLaneDeg;
-    bool mine = eligible && __popc(__ballot_sync(0xffffffffu, eligible)) >= 8;
+    const unsigned elig_mask = __ballot_sync(0xffffffffu, eligible);  // every lane votes
+    bool mine = eligible && __popc(elig_mask) >= 8;
     const int nblk = mine ? (int)(((p0 & 3) + d + 3) >> 2) : 0;
     const int max_blocks = __reduce_max_sync(0xffffffffu, (unsigned)nblk);
     if (max_blocks > 0) {
