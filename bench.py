@@ -240,15 +240,15 @@ def main():
         W, K = max(W, 1), 2
     it = 0
 
-    def step():
+    def take(n):
         nonlocal it
-        seeds, rs = mine[it % len(mine)]
-        it += 1
-        order, losses = pipe.run_window(seeds, rs)
-        return pipe.last_window
+        out = [mine[(it + k) % len(mine)] for k in range(n)]
+        it += n
+        return out
 
-    for _ in range(W):
-        step()
+    # sampling of window w+1 overlaps the compute of window w (Pipeline.run_windows)
+    for _ in pipe.run_windows(take(W)):
+        pass
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -260,8 +260,8 @@ def main():
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record()
-        for _ in range(K):
-            win = step()
+        for _ in pipe.run_windows(take(K)):
+            win = pipe.last_window
             edges += win.total_edges()
             draws += sum(win.draws(b) for b in range(win.num_batches))
         ev1.record()
@@ -384,13 +384,15 @@ def e2e_measure(pipe, mine, it, K, torch, world, device):
     t0 = time.perf_counter()
     edges = 0
     h2d = d2h = 0
+    staged = []
     for k in range(K):
         seeds, rs = mine[(it + k) % len(mine)]
         pinned = [torch.from_numpy(s.astype(np.int64)).pin_memory() for s in seeds]
-        order, losses = pipe.run_window([p.numpy() for p in pinned], rs)
-        lv = losses.cpu().numpy()
-        edges += pipe.last_window.total_edges()
+        staged.append(([p.numpy() for p in pinned], rs))
         h2d += sum(len(s) for s in seeds) * 4 + (len(seeds) + 1) * 8 + 16 * len(seeds)
+    for order, losses in pipe.run_windows(staged):
+        lv = losses.cpu().numpy()  # per-batch losses back to the host every step
+        edges += pipe.last_window.total_edges()
         d2h += lv.nbytes
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0

@@ -280,7 +280,7 @@ class Pipeline:
         chain on the host (schedule.py:68-113)."""
         if not self.flags.reorder or nb < 2:
             return list(range(nb))
-        ws = self.sampler.ws.data_ptr()
+        ws = win.s.ws.data_ptr()
         self._call("fgl_match_counts", ws + self.bm_off, self.words, nb, self.pairs.data_ptr(), self.stream)
         pairs = self.pairs.cpu().numpy()
         sizes = [win.unique_range(b)[1] - win.unique_range(b)[0] for b in range(nb)]
@@ -457,6 +457,60 @@ class Pipeline:
             phase["compute"] += t4 - t3
         self.last_window = win
         return order, self.loss_dev[:nb]
+
+    # --------------------------------------------------------- pipelined --
+    def _sample_async(self, seed_lists, rng_seeds, slot):
+        """Stage + launch the window sampler of ping-pong slot `slot` on the
+        side stream (asynchronous)."""
+        torch = self.torch
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(device=self.device)
+            self._samplers = [self.sampler, WindowSampler(self.dg, self.cfg.fanouts, self.cfg.batch_size,
+                                                          self.cfg.window_n, device=self.device)]
+        smp = self._samplers[slot]
+        done = getattr(self, "_slot_done", {}).get(slot)
+        if done is not None:  # the compute of the window that last used this slot
+            self._side.wait_event(done)
+        with torch.cuda.stream(self._side):
+            nb, off = smp.stage(seed_lists, rng_seeds)
+            win = smp.run(nb, off, stream=self._side)
+        self.gpu_launches += 1
+        return win
+
+    def run_windows(self, windows):
+        """Train a sequence of windows [(seed_lists, rng_seeds), ...] with the
+        sampling of window w+1 (side stream, second sampler) overlapping the
+        schedule / prepare / compute of window w (current stream).  Yields
+        (order, device losses) per window; numerically identical to
+        run_window applied in sequence."""
+        torch = self.torch
+        windows = list(windows)
+        if not windows:
+            return
+        pending = self._sample_async(*windows[0], slot=0)
+        for w in range(len(windows)):
+            win = pending
+            nb = win.num_batches
+            with torch.cuda.stream(self._side):
+                win.host_counts()  # window w's sampling is complete
+                # match counts ride the side stream too, so their read-back does
+                # not wait for window w-1's compute on the main stream
+                order = self.schedule(win, nb)
+            if w + 1 < len(windows):
+                pending = self._sample_async(*windows[w + 1], slot=(w + 1) % 2)
+            self.sampler = win.s
+            layers = self.prepare(win)
+            for j, b in enumerate(order):
+                prev = order[j - 1] if (j > 0 and self.flags.match) else None
+                self.batch_step(win, b, prev, j, layers, j % 2)
+            ev = torch.cuda.Event()
+            ev.record()
+            if not hasattr(self, "_slot_done"):
+                self._slot_done = {}
+            self._slot_done[w % 2] = ev
+            self.last_window = win
+            yield order, self.loss_dev[:nb]
+        self.sampler = self._samplers[0]
 
 
 def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None, *,

@@ -102,3 +102,27 @@ def test_host_feature_store_bit_exact(cfg1_graph):
         pipe.run_window(seeds, rs)
         out.append(pipe.model.flat.cpu().numpy())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_pipelined_windows_bit_identical(cfg1_graph, direct):
+    """run_windows (window w+1 sampled on a side stream while window w trains)
+    gives exactly the parameters and losses of run_window in sequence."""
+    from paper_2409_14939_b200 import trainer
+    g = cfg1_graph
+    rng = np.random.default_rng(9)
+    feats = rng.standard_normal((g.num_nodes, 20)).astype(np.float32)
+    labels = rng.integers(0, 4, size=g.num_nodes)
+    cfg = trainer.ModelConfig(layer_dims=(20, 16, 16, 4), fanouts=[6, 4, 3], batch_size=200, window_n=4, lr=0.2)
+    wins = [([rng.choice(g.num_nodes, 200, replace=False) for _ in range(4)], [100 * w + j for j in range(4)])
+            for w in range(5)]
+    seq = trainer.Pipeline(g, feats, labels, cfg, direct_x0=direct)
+    seq_losses = []
+    for sl, rs in wins:
+        _, lo = seq.run_window(sl, rs)
+        seq_losses.append(lo.cpu().numpy().copy())
+    pip = trainer.Pipeline(g, feats, labels, cfg, direct_x0=direct)
+    pip_losses = [lo.cpu().numpy().copy() for _, lo in pip.run_windows(wins)]
+    assert np.array_equal(seq.model.flat.cpu().numpy(), pip.model.flat.cpu().numpy())
+    for a, b in zip(seq_losses, pip_losses):
+        assert np.array_equal(a, b)
