@@ -259,6 +259,8 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if args.profile:  # ncu --profile-from-start off: capture only the timed steps
+            torch.cuda.profiler.start()
         ev0.record()
         for _ in pipe.run_windows(take(K)):
             win = pipe.last_window
@@ -266,6 +268,8 @@ def main():
             draws += sum(win.draws(b) for b in range(win.num_batches))
         ev1.record()
         torch.cuda.synchronize()
+        if args.profile:
+            torch.cuda.profiler.stop()
     launches = lib.fgl_launch_count() - l0
     if world > 1:
         torch.distributed.barrier()

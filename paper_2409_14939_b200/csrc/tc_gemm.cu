@@ -24,129 +24,15 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace fgl {
 namespace {
+using namespace tc;
 
 constexpr int TC_M = 128;
 constexpr int TC_THREADS = 256;
 constexpr int TC_MAX_SMEM = 220 * 1024;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-// UMMA shared-memory matrix descriptor, SWIZZLE_NONE (sm100 descriptor version 1)
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-
-// instruction descriptor: D f32, A/B tf32, M x N, operand majors (0 = K, 1 = MN)
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// K-major no-swizzle: 16-byte chunk (row r, k..k+3) of a tile with KC chunks per row
-__device__ __forceinline__ uint32_t kmaj_off(int r, int k, int KC) {
-  return (uint32_t)((r >> 3) * (KC * 128) + (k >> 2) * 128 + (r & 7) * 16);
-}
-
-// MN-major no-swizzle: 16-byte chunk (k-row kk, mn..mn+3) of a tile with MN4
-// 4-element groups per k-row: core matrix = 8 k-rows x 16 B, SBO = 128 B
-// between MN groups, LBO = MN4*128 B between 8-row K groups
-__device__ __forceinline__ uint32_t mnmaj_off(int kk, int mn, int MN4) {
-  return (uint32_t)((kk >> 3) * (MN4 * 128) + (mn >> 2) * 128 + (kk & 7) * 16);
-}
-
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  return __uint_as_float(h);
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-      :
-      : "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1));
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(phase)
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot, int cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-
-__device__ __forceinline__ void tmem_free(uint32_t tmem, int cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
-}
-
-// split the raw chunk at `off` in place into its tf32 hi part; lo -> lo_base
-__device__ __forceinline__ void split_chunk(char* raw, char* lo_base, uint32_t off, float4 x) {
-  float4 h, l;
-  h.x = tf32_hi(x.x); l.x = __fsub_rn(x.x, h.x);
-  h.y = tf32_hi(x.y); l.y = __fsub_rn(x.y, h.y);
-  h.z = tf32_hi(x.z); l.z = __fsub_rn(x.z, h.z);
-  h.w = tf32_hi(x.w); l.w = __fsub_rn(x.w, h.w);
-  *reinterpret_cast<float4*>(raw + off) = h;
-  *reinterpret_cast<float4*>(lo_base + off) = l;
-}
-
-// split x into hi -> hi_base + off and lo -> lo_base + off
-__device__ __forceinline__ void split_chunk_to(char* hi_base, char* lo_base, uint32_t off, float4 x) {
-  float4 h, l;
-  h.x = tf32_hi(x.x); l.x = __fsub_rn(x.x, h.x);
-  h.y = tf32_hi(x.y); l.y = __fsub_rn(x.y, h.y);
-  h.z = tf32_hi(x.z); l.z = __fsub_rn(x.z, h.z);
-  h.w = tf32_hi(x.w); l.w = __fsub_rn(x.w, h.w);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(lo_base + off) = l;
-}
 
 // ------------------------------------------------------------- fwd / dgrad --
 struct TcArgs {
@@ -509,6 +395,7 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
              const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
              cudaStream_t st, int* err) {
   *err = 0;
+  if (tc_gemm3(mode, A, lda, mask, ldm, W, bias, C, ldc, M, N, K, relu, st, err)) return true;
   if (dense_tc_disabled() || M < 1 || N < 1 || K < 1) return false;
   if ((lda % 4) || !aligned16(A) || (mask && ((ldm % 4) || !aligned16(mask)))) return false;
   const int N_pad = (N + 15) / 16 * 16;

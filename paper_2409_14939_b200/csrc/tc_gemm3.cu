@@ -1,0 +1,476 @@
+// Warp-specialised bulk-copy + tcgen05 3xTF32 dense layer GEMM (sm_100a).
+//
+// Same contract as tc_gemm.cu's tc_gemm_kernel (compute.dense_update,
+// compute.py:198-216, and dH = (dZ * relu'(z)) W^T of trainer._backward,
+// trainer.py:212-228), organised so that the HBM stream of activation rows
+// never waits on the math and shared memory is not the bottleneck:
+//
+//   warp 0      producer: one 1-D bulk copy (TMA engine) per 128-row tile of
+//               A -- the rows are contiguous, so a tile is a single request --
+//               (and of the ReLU mask for dgrad) into a ring of R raw slots;
+//   warps 4-7   converters, thread = row = TMEM lane: read the row from shared
+//               memory (conflict-free 16-byte loads for ld = 4 mod 8 floats),
+//               mask, split x = hi + lo (hi = tf32(x)), and tcgen05.st both
+//               halves into a TMEM A buffer (double-buffered when it fits);
+//   warp 1      MMA issuer (one thread): per 8-wide K step three
+//               tcgen05.mma.kind::tf32 with A from TMEM and the split weight
+//               from shared memory (lo*hi, hi*lo, hi*hi) -> fp32 accumulator;
+//   warps 8-11  epilogue: tcgen05.ld the accumulator, bias, ReLU, stores.
+//
+// Because A never sits in shared memory in MMA layout, shared-memory traffic
+// per tile is just the raw rows in and out once plus the weight reads.
+// The weight (K <= 128 here, N <= 256) is split once per CTA into hi/lo
+// copies in the K-major no-swizzle canonical layout.  One persistent CTA/SM.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace fgl {
+namespace {
+using namespace tc;
+
+constexpr int G3_THREADS = 512;      // 16 warps, see the role map at the top
+constexpr int G3_M = 128;
+constexpr int G3_KCH = 32;           // K columns per TMEM A chunk (hi 32 + lo 32 TMEM columns)
+constexpr int G3_MAX_SMEM = 227 * 1024;
+constexpr int G3_MAX_SLOTS = 4;
+constexpr int G3_CONV_THREADS = 256; // warps 4-11
+constexpr int G3_EPI_THREADS = 128;  // warps 12-15
+
+struct G3Args {
+  const float* A;      // [M, K] row-major (lda)
+  const float* mask;   // dgrad: [M, K] (ldm) ReLU mask, or null
+  const float* W;      // mode 0: [K, N] row-major; mode 1: [N, K] row-major
+  const float* bias;   // mode 0 only, [N] or null
+  float* C;
+  int64_t lda, ldm, ldc;
+  int64_t M;
+  int N, K, N_pad, K_pad, R, NC, relu, has_mask, tmem_cols, a_slot_bytes, m_slot_bytes, dbg;
+  int stage_off, stage_pitch, w_vec;  // coalesced-epilogue staging tile (byte offset in smem, pitch in floats), or -1
+};
+
+// debug timeline (FGL_G3DBG & 8): per CTA, globaltimer stamps of each role's
+// progress; read back with fgl_debug_g3_trace
+constexpr int G3_TR = 72;
+__device__ int64_t g3_trace[148 * G3_TR];
+__device__ __forceinline__ int64_t gtime() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define G3T(slot) do { if ((p.dbg & 8) && blockIdx.x < 148 && (slot) < G3_TR) g3_trace[blockIdx.x * G3_TR + (slot)] = gtime(); } while (0)
+
+__device__ __forceinline__ uint32_t sw128_off(int row, int kk) {
+  // byte offset of element (row, kk) (kk < 32) inside a K-major SWIZZLE_128B box
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((kk >> 2) ^ (row & 7))) << 4) + (kk & 3) * 4);
+}
+
+__device__ __forceinline__ float tf32_rna_finite(float x) {
+  // round-to-nearest(-away) to tf32 for finite x: 2 integer ops (cvt.rna.tf32
+  // adds an inf/nan guard that activations never need)
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmC, G3Args p) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int R = p.R, NC = p.NC, N_pad = p.N_pad, K_pad = p.K_pad;
+  const int nch = (p.K + G3_KCH - 1) / G3_KCH;  // K chunks per tile
+  const int b_box = N_pad * 128, KB = (K_pad + 31) / 32;
+  const int b_bytes = KB * b_box;
+  char* sB_hi = smem;
+  char* sB_lo = sB_hi + b_bytes;
+  char* slots = sB_lo + b_bytes;
+  const int slot_bytes = p.a_slot_bytes + p.m_slot_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + R * slot_bytes);
+  // full[R] empty[R] cfull[8] cempty[8] tfull[2] tempty[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * R + 20);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  const int FULL = 0, EMPTY = R, CFULL = 2 * R, CEMPTY = 2 * R + 8, TFULL = 2 * R + 16, TEMPTY = 2 * R + 18;
+
+  if (tid == 0) {
+    G3T(0);
+    for (int s = 0; s < R; ++s) {
+      mbar_init_n(bar(FULL + s), 1);
+      mbar_init_n(bar(EMPTY + s), G3_CONV_THREADS);
+    }
+    for (int c = 0; c < 8; ++c) {
+      mbar_init_n(bar(CFULL + c), G3_CONV_THREADS);
+      mbar_init_n(bar(CEMPTY + c), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init_n(bar(TFULL + a), 1);
+      mbar_init_n(bar(TEMPTY + a), G3_EPI_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();  // barriers initialised
+  const int64_t tiles = ceil_div(p.M, G3_M);
+  if (warp == 0) {
+    // --------------------------------------------------------- producer --
+    if (lane == 0) {
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+        const int s = j % R;
+        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / R) & 1u) ^ 1u);
+        G3T(2 + 9 * j);
+        const int64_t r0 = t * G3_M;
+        const int rows = (int)(p.M - r0 < G3_M ? p.M - r0 : G3_M);
+        const uint32_t abytes = (uint32_t)(rows * p.lda * 4), mbytes = p.has_mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        char* slot = slots + s * slot_bytes;
+        mbar_arrive_expect_tx(bar(FULL + s), abytes + mbytes);
+        bulk_load(smem_u32(slot), p.A + r0 * p.lda, abytes, bar(FULL + s));
+        if (p.has_mask) bulk_load(smem_u32(slot + p.a_slot_bytes), p.mask + r0 * p.ldm, mbytes, bar(FULL + s));
+      }
+    }
+    return;
+  }
+  // TMEM allocation (warp 1), published to warps 1-15
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  tc_fence_after();
+  {
+    // weight operand B[n][k] split into tf32 hi / lo, K-major SWIZZLE_128B
+    // boxes of 32 K columns (conflict-free tensor-core reads), by warps 1-15
+    // while the producer already streams A: one batch of 16-byte W loads per
+    // thread, then scattered shared stores
+    const int nt = G3_THREADS - 32, t0 = tid - 32;
+    const int W4 = MODE == 0 ? (p.N + 3) / 4 : (p.K + 3) / 4;  // float4 per W row
+    const int Wrows = MODE == 0 ? p.K : p.N;
+    const int total4 = Wrows * W4;
+    const bool vec = p.w_vec;
+    const int rl = MODE == 0 ? p.N : p.K;
+    auto load4 = [&](int idx) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (idx < total4) {
+        const int r = idx / W4, c = 4 * (idx - r * W4);
+        const float* src = p.W + (int64_t)r * rl + c;
+        if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          v.x = __ldg(src);
+          if (c + 1 < rl) v.y = __ldg(src + 1);
+          if (c + 2 < rl) v.z = __ldg(src + 2);
+          if (c + 3 < rl) v.w = __ldg(src + 3);
+        }
+      }
+      return v;
+    };
+    auto scatter4 = [&](int idx, float4 v) {
+      if (idx >= total4) return;
+      const int r = idx / W4, c = 4 * (idx - r * W4);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int n = MODE == 0 ? c + q : r, k = MODE == 0 ? r : c + q;
+        if (n >= N_pad || k >= K_pad) continue;
+        const float h = tf32_hi(e[q]);
+        const uint32_t off = (uint32_t)((k >> 5) * b_box) + sw128_off(n, k & 31);
+        *reinterpret_cast<float*>(sB_hi + off) = h;
+        *reinterpret_cast<float*>(sB_lo + off) = __fsub_rn(e[q], h);
+      }
+    };
+    // first batch of loads in flight while both B images are zeroed (padding
+    // rows / K columns must be 0, not leftover shared memory)
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = load4(t0 + u * nt);
+    for (int z = t0; z < 2 * b_bytes / 16; z += nt) sts128(smem_u32(sB_hi) + 16 * z, make_float4(0.f, 0.f, 0.f, 0.f));
+    asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
+#pragma unroll
+    for (int u = 0; u < 4; ++u) scatter4(t0 + u * nt, v[u]);
+    for (int idx = t0 + 4 * nt; idx < total4; idx += nt) scatter4(idx, load4(idx));
+    fence_async_smem();
+    asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
+    if (tid == 32) G3T(1);
+  }
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: accumulators [0, 2 N_pad), A chunk c: hi at 2 N_pad + 64 c, lo at +32
+  auto acc_col = [&](int a) { return tmem + (uint32_t)(a * N_pad); };
+  auto ch_hi = [&](int c) { return tmem + (uint32_t)(2 * N_pad + 2 * G3_KCH * c); };
+
+  if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    // the whole warp runs the (warp-uniform) loop so descriptors live in
+    // uniform registers; one elected lane issues each tcgen05 instruction
+    const uint32_t idesc = idesc_tf32(G3_M, N_pad, 0, 0);
+    const uint32_t bh = smem_u32(sB_hi), bl = smem_u32(sB_lo);
+    int j = 0, cc = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      mbar_wait(bar(TEMPTY + a), ((uint32_t)(j >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      if (lane == 0) G3T(5 + 9 * j);
+      for (int c = 0; c < nch; ++c, ++cc) {
+        const int cs = cc % NC;
+        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / NC) & 1u);
+        tc_fence_after();
+        const int kst = min(G3_KCH, K_pad - c * G3_KCH) / 8;
+        const uint32_t ahi = ch_hi(cs), alo = ahi + G3_KCH;
+        const uint32_t bo0 = (uint32_t)(c * b_box);  // chunk c = SW128 box c of B
+        if (elect_one()) {
+          for (int st = 0; st < ((p.dbg & 2) ? 0 : kst); ++st) {
+            const uint32_t bo = bo0 + (uint32_t)(st * 32);
+            const uint64_t dbh = umma_desc_sw128(bh + bo), dbl = umma_desc_sw128(bl + bo);
+            const uint32_t acc = (c | st) != 0;
+            mma_tf32_ts(acc_col(a), alo + 8 * st, dbh, idesc, acc);
+            mma_tf32_ts(acc_col(a), ahi + 8 * st, dbl, idesc, 1);
+            mma_tf32_ts(acc_col(a), ahi + 8 * st, dbh, idesc, 1);
+          }
+          mma_commit(bar(CEMPTY + cs));
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(bar(TFULL + a));
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // -------------------------------------------------------- converters --
+    // warp -> (TMEM lane quarter, half of each 32-column chunk); thread = row
+    const int quarter = warp & 3, half = (warp - 4) >> 2, row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int j = 0, cc = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int s = j % R;
+      mbar_wait(bar(FULL + s), (uint32_t)(j / R) & 1u);
+      if (row == 0 && half == 0) G3T(3 + 9 * j);
+      const uint32_t xr = smem_u32(slots + s * slot_bytes) + (uint32_t)(row * p.lda * 4);
+      const uint32_t mr = smem_u32(slots + s * slot_bytes + p.a_slot_bytes) + (uint32_t)(row * p.ldm * 4);
+      for (int c = 0; c < nch; ++c, ++cc) {
+        const int cs = cc % NC;
+        const int k0 = c * G3_KCH + 16 * half;
+        // four 16-byte loads in flight before any conversion
+        float4 x[4], m[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = k0 + 4 * h;
+          x[h] = k < p.K ? lds128(xr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (MODE == 1 && p.has_mask) m[h] = k < p.K ? lds128(mr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        uint32_t hv[16], lv[16];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = k0 + 4 * h;
+          float xs[4] = {x[h].x, x[h].y, x[h].z, x[h].w};
+          if (MODE == 1 && p.has_mask) {
+            const float ms[4] = {m[h].x, m[h].y, m[h].z, m[h].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (!(ms[q] > 0.f)) xs[q] = 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (k + q >= p.K) xs[q] = 0.f;  // columns K..K_pad-1 are zero (row padding may hold anything)
+            const float hi = tf32_rna_finite(xs[q]);
+            hv[4 * h + q] = __float_as_uint(hi);
+            lv[4 * h + q] = __float_as_uint(__fsub_rn(xs[q], hi));
+          }
+        }
+        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / NC) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t hi_t = ch_hi(cs) + lane_off + (uint32_t)(16 * half);
+        if (!(p.dbg & 1)) {
+        tmem_st8(hi_t, *reinterpret_cast<uint32_t(*)[8]>(hv));
+        tmem_st8(hi_t + 8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8));
+        tmem_st8(hi_t + G3_KCH, *reinterpret_cast<uint32_t(*)[8]>(lv));
+        tmem_st8(hi_t + G3_KCH + 8, *reinterpret_cast<uint32_t(*)[8]>(lv + 8));
+        tmem_st_wait();
+        }
+        tc_fence_before();
+        mbar_arrive(bar(CFULL + cs));
+      }
+      if (row == 0 && half == 0) G3T(4 + 9 * j);
+      mbar_arrive(bar(EMPTY + s));  // raw slot consumed
+    }
+  } else if (warp >= 12) {
+    // ---------------------------------------------------------- epilogue --
+    // TMEM -> registers (thread = row) -> bias / ReLU -> shared staging tile
+    // in the SWIZZLE_128B box layout (conflict-free: a row's 16-byte chunks
+    // are XOR-permuted by row & 7) -> TMA tensor stores, one per 32 columns
+    const int quarter = warp & 3, et = tid - (G3_THREADS - G3_EPI_THREADS);
+    const bool tma_out = p.stage_off >= 0;
+    const uint32_t stg_u = tma_out ? smem_u32(smem + p.stage_off) : 0u;
+    for (int c = et; c < N_pad; c += G3_EPI_THREADS) sbias[c] = (MODE == 0 && p.bias && c < p.N) ? p.bias[c] : 0.f;
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      mbar_wait(bar(TFULL + a), (uint32_t)(j >> 1) & 1u);
+      tc_fence_after();
+      if (et == 0) G3T(6 + 9 * j);
+      const int r_loc = quarter * 32 + lane;
+      const int64_t row = t * G3_M + r_loc;
+      float* out = p.C + row * p.ldc;
+      if (tma_out && j > 0) {
+        // the previous tile's TMA stores must have finished reading staging
+        if (et == 0) bulk_wait_read0();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
+      for (int c0 = 0; c0 < N_pad; c0 += 32) {
+        uint32_t v[32];
+        if (p.dbg & 4) { for (int q = 0; q < 32; ++q) v[q] = 0; } else {
+        tmem_ld16_nowait(acc_col(a) + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+        if (c0 + 16 < N_pad)
+          tmem_ld16_nowait(acc_col(a) + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c0 + 16), v + 16);
+        tmem_ld_wait(); }
+        const int ncol = c0 + 16 < N_pad ? 32 : 16;
+        for (int h = 0; h < ncol; h += 16) {
+          float x[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float y = __uint_as_float(v[h + q]);
+            if (MODE == 0 && p.bias) y = __fadd_rn(y, sbias[c0 + h + q]);
+            if (p.relu) y = y > 0.f ? y : 0.f;
+            x[q] = y;
+          }
+          if (tma_out) {
+            // box (c0 / 32): 128 rows x 128 B; chunk cc of row r at (cc ^ (r & 7))
+            const uint32_t box = stg_u + (uint32_t)((c0 >> 5) * (G3_M * 128)) + (uint32_t)(r_loc * 128);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+              const int cc = (h + q) >> 2;
+              sts128(box + (uint32_t)(((cc ^ (r_loc & 7)) & 7) << 4), make_float4(x[q], x[q + 1], x[q + 2], x[q + 3]));
+            }
+          } else if (row < p.M) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c0 + h + q < p.N) out[c0 + h + q] = x[q];
+          }
+        }
+      }
+      if (et == 0) G3T(8 + 9 * j);
+      tc_fence_before();
+      mbar_arrive(bar(TEMPTY + a));  // accumulator drained: tile j+2's MMAs may start
+      if (tma_out) {
+        fence_async_smem();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (et == 0) {
+          for (int c0 = 0; c0 < N_pad; c0 += 32)
+            tma_store_2d(&tmC, stg_u + (uint32_t)((c0 >> 5) * (G3_M * 128)), c0, (int)(t * G3_M));
+          bulk_commit();
+        }
+      }
+      if (et == 0) G3T(7 + 9 * j);
+    }
+    if (tma_out && et == 0) bulk_wait0();
+  }
+  // warps 1-15 (warp 0 returned after issuing its copies)
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, p.tmem_cols);
+  }
+  if (tid == 32) G3T(G3_TR - 1);
+}
+
+// ------------------------------------------------------------ host side --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<EncodeTiledFn>(f);
+    return (EncodeTiledFn) nullptr;
+  }();
+  return fn;
+}
+
+// fp32 [rows, cols] row-major (ld floats) in 128-row x 32-column SWIZZLE_128B boxes
+bool make_map_sw128(CUtensorMap* m, const float* base, int64_t rows, int cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)G3_M};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t g3_fixed(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
+  return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 20) + 16 + 4 * N_pad;
+}
+int64_t g3_stage_bytes(int N_pad) { return (int64_t)G3_M * ((N_pad + 31) / 32) * 128; }  // SW128 boxes
+int64_t g3_smem(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
+  return g3_fixed(N_pad, K_pad, R, a_slot, m_slot) + 1024 + g3_stage_bytes(N_pad);
+}
+
+bool tc3_disabled() {
+  static const int v = [] {
+    const char* e = getenv("FGL_DENSE");
+    return (e && (e[0] == 's' || e[0] == 'v')) ? 1 : 0;  // simt / v2 force the older kernels
+  }();
+  return v != 0;
+}
+
+}  // namespace
+
+// Returns false if the shape is outside this kernel's envelope (caller falls
+// back); *err receives an FGL status otherwise.
+bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
+              const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, cudaStream_t st,
+              int* err) {
+  *err = 0;
+  if (tc3_disabled() || M < 1 || N < 1 || K < 1 || K > 128 || lda < K) return false;
+  if ((lda % 4) || (reinterpret_cast<uintptr_t>(A) & 15)) return false;
+  const int has_mask = (mode == 1 && mask) ? 1 : 0;
+  if (has_mask && ((ldm % 4) || ldm < K || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
+  const int N_pad = (N + 15) / 16 * 16;
+  const int K_pad = (K + 7) / 8 * 8;
+  if (N_pad > 256) return false;
+  // TMEM: two accumulators + a ring of NC A chunks (64 columns each)
+  const int NC = std::min(8, (512 - 2 * N_pad) / (2 * G3_KCH));
+  if (NC < 2) return false;
+  const int64_t a_slot = (int64_t)G3_M * lda * 4, m_slot = has_mask ? (int64_t)G3_M * ldm * 4 : 0;
+  int R = 0;
+  for (int r = G3_MAX_SLOTS; r >= 2; --r)
+    if (g3_smem(N_pad, K_pad, r, a_slot, m_slot) <= G3_MAX_SMEM) { R = r; break; }
+  if (R == 0) return false;
+  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
+  static const int rmax = getenv("FGL_G3SLOTS") ? atoi(getenv("FGL_G3SLOTS")) : G3_MAX_SLOTS;
+  if (R > rmax) R = rmax;
+  const int cols = 512;
+  // output through TMA tensor stores (SW128 boxes of 128 rows x 32 columns)
+  CUtensorMap mC;
+  std::memset(&mC, 0, sizeof(mC));
+  const bool coal = (ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15) && make_map_sw128(&mC, C, M, N, ldc);
+  const int64_t stage_off = (g3_fixed(N_pad, K_pad, R, a_slot, m_slot) - 1024 + 1023) / 1024 * 1024;
+  G3Args p{A, mask, W, bias, C, lda, ldm, ldc, M, N, K, N_pad, K_pad, R, NC, relu, has_mask, cols,
+           (int)a_slot, (int)m_slot, dbg, coal ? (int)stage_off : -1, 0,
+           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0)};
+  const int64_t smem = g3_smem(N_pad, K_pad, R, a_slot, m_slot);
+  static bool attr[2] = {false, false};
+  cudaError_t e;
+  if (!attr[mode]) {
+    e = mode == 0 ? cudaFuncSetAttribute(tc_gemm3_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM)
+                  : cudaFuncSetAttribute(tc_gemm3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_gemm3)"); return true; }
+    attr[mode] = true;
+  }
+  const int64_t tiles = ceil_div(M, G3_M);
+  const int grid = (int)std::min<int64_t>(tiles, kNumSMs);
+  if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, p);
+  else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) *err = cuda_status(e, "tc_gemm3_kernel");
+  return true;
+}
+
+}  // namespace fgl
+
+extern "C" int fgl_debug_g3_trace(int64_t* host, int64_t n) {
+  return cudaMemcpyFromSymbol(host, fgl::g3_trace, sizeof(int64_t) * (n < 148 * fgl::G3_TR ? n : 148 * fgl::G3_TR)) == cudaSuccess ? 0 : -1;
+}
