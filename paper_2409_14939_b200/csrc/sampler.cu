@@ -25,6 +25,7 @@
 // sources in `front`; (3) compaction of `front` -> next frontier (cleared as
 // it is read, OR-ed into `all`).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -735,6 +736,195 @@ __global__ void __launch_bounds__(256, 2) select_tau_kernel(SelectArgs a) {
 
 constexpr int kSelectSmem = 8 * kWarpBufWords * 8;  // 64 KB per 256-thread CTA
 
+// Balanced threshold-collect select (fanouts <= kTauMaxFan), the default.
+// Each warp takes a tile of 32 consecutive frontier entries and spreads the
+// Philox blocks of ALL its nodes evenly over its 32 lanes (lane g handles
+// blocks g, g+32, ... of the tile's concatenated block list), so no lane sits
+// idle while a neighbour draws a long node -- the per-node lane / warp paths
+// of select_tau_kernel left ~45% of the lanes idle on power-law degrees.
+// A drawn candidate survives if its key is below its node's threshold tau
+// (the f smallest of d uniform keys lie below ~(f + 3 sqrt f + 3)/d); the
+// survivor (key53 << 11 | slot) is appended to its node's segment of a
+// per-warp shared buffer (shared-memory atomic on the node's count).  Then
+// every survivor is ranked against its node's other survivors by counting,
+// and rank < min(d, f) is emitted at output position obase + rank: ascending
+// (key, slot) order, exactly np.lexsort's.  Nodes with d > kBalHub (slot does
+// not fit 11 bits), whose survivors overflow their segment, or with fewer
+// than min(d, f) survivors are redone exactly by the warp path
+// (tau_select_node: widened threshold / streaming fallback).
+constexpr int kBalHub = 2048;
+constexpr int kBalWarps = 4;
+constexpr int kBalTab = 80;  // bytes per node-table entry
+
+struct BalTab {
+  int64_t p0[32], e0[32], obase[32];
+  uint64_t tau[32], k0[32], k1[32];
+  int32_t d[32], seg[32], cnt[32], bs[32], u[32], b[32], fb[32];
+  int64_t idx[32];
+};
+
+inline int bal_cap(int fan) {
+  const double ex = fan + 3.0 * std::sqrt((double)fan) + 3.0;
+  return (int)std::ceil(ex + 3.5 * std::sqrt(ex) + 2.0);
+}
+inline int bal_sv_words(int fan) {  // survivors (32 caps) + emission queue (32 * fan u32)
+  return std::max(1024, (32 * bal_cap(fan) + 31) / 32 * 32) + 16 * fan;
+}
+inline int bal_smem(int fan) { return kBalWarps * (bal_sv_words(fan) * 8 + (int)sizeof(BalTab)); }
+
+__device__ __forceinline__ int bal_find(const int32_t* arr, int g) {
+  // largest n in [0, 32) with arr[n] <= g (arr non-decreasing, arr[0] = 0)
+  int n = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1)
+    if (arr[n + step < 32 ? n + step : 31] <= g && n + step < 32) n += step;
+  return n;
+}
+
+__global__ void __launch_bounds__(kBalWarps * 32, 6) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
+                                                                    int sv_words) {
+  extern __shared__ __align__(16) uint64_t sbuf[];
+  const int lane = lane_id(), wib = warp_id();
+  char* wbase = reinterpret_cast<char*>(sbuf) + (int64_t)wib * (sv_words * 8 + sizeof(BalTab));
+  uint64_t* sv = reinterpret_cast<uint64_t*>(wbase);
+  BalTab& T = *reinterpret_cast<BalTab*>(wbase + sv_words * 8);
+  const int64_t F = a.scal[kF];
+  const int64_t ebase = a.scal[kHopEdgeBase];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int fan = a.fan;
+  const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
+  uint32_t* bm_base = a.bm_front;
+  for (int64_t t0 = gw * 32; t0 < F; t0 += nwarps * 32) {
+    const int64_t i = t0 + lane;
+    int32_t u = 0, b = 0;
+    int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
+    if (i < F) {
+      u = a.front[i];
+      b = a.fb[i];
+      e0 = __ldg(a.off + u);
+      d = __ldg(a.off + u + 1) - e0;
+      p0 = a.hop_pos[b] + a.scan_deg[i];
+      obase = ebase + a.scan_sel[i];
+    }
+    bool elig = d > 0 && d <= kBalHub;
+    int cap = elig ? (int)(d < capn ? d : capn) : 0;
+    int seg = warp_incl_scan(cap) - cap;
+    if (seg + cap > sv_words - 16 * fan) { elig = false; cap = 0; }  // queue space after the survivors
+    const int nblk = elig ? (int)(((p0 + d - 1) >> 2) - (p0 >> 2) + 1) : 0;
+    const int bsum = warp_incl_scan(nblk);
+    const int bs = bsum - nblk;
+    const int TB = __shfl_sync(0xffffffffu, bsum, 31);
+    const int segtot = __shfl_sync(0xffffffffu, seg + cap, 31);
+    const uint64_t tau = (double)d <= expect ? kKeyOne
+                                             : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
+    T.p0[lane] = p0; T.e0[lane] = e0; T.obase[lane] = obase; T.tau[lane] = tau;
+    T.k0[lane] = a.keys[2 * b]; T.k1[lane] = a.keys[2 * b + 1];
+    T.d[lane] = (int32_t)(elig ? d : 0); T.seg[lane] = seg; T.cnt[lane] = 0; T.bs[lane] = bs;
+    T.u[lane] = u; T.b[lane] = b; T.idx[lane] = i;
+    __syncwarp();
+    // ---- balanced Philox over the tile's blocks, survivors into segments
+    for (int g = lane; g < TB; g += 32) {
+      const int n = bal_find(T.bs, g);
+      const int64_t np0 = T.p0[n];
+      const int nd = T.d[n];
+      const int64_t k = (np0 >> 2) + (g - T.bs[n]);
+      uint64_t w[4];
+      philox4x64_10((uint64_t)k + 1, T.k0[n], T.k1[n], w[0], w[1], w[2], w[3]);
+      const uint64_t ntau = T.tau[n];
+      const int ncap = nd < capn ? nd : capn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t slot = 4 * k + q - np0;
+        const uint64_t key = w[q] >> 11;
+        if (slot >= 0 && slot < nd && key < ntau) {
+          const int c = atomicAdd(&T.cnt[n], 1);
+          if (c < ncap) sv[T.seg[n] + c] = (key << 11) | (uint64_t)slot;
+        }
+      }
+    }
+    __syncwarp();
+    const int want = (int)(d < fan ? d : fan);
+    const int cnt = T.cnt[lane];
+    const bool fb = d > 0 && (!elig || cnt > cap || cnt < want);
+    // ranking runs over the survivors only: cs = exclusive scan of the
+    // survivor counts of the nodes that are not redone
+    const int live = fb ? 0 : cnt;
+    const int csum = warp_incl_scan(live);
+    T.bs[lane] = csum - live;  // block scan no longer needed: reuse as survivor scan
+    const int stot = __shfl_sync(0xffffffffu, csum, 31);
+    __syncwarp();
+    // ---- rank every survivor among its node's survivors by counting; the
+    // emitted (rank < want) ones are queued as (node, rank, slot) so that the
+    // col[] / weight gathers of a lane's emissions are issued back to back
+    uint32_t* q = reinterpret_cast<uint32_t*>(sv + segtot);  // emission queue after the survivors
+    int nq = 0;
+    for (int e0i = 0; e0i < stot; e0i += 32) {
+      const int e = e0i + lane;
+      uint32_t item = 0xffffffffu;
+      if (e < stot) {
+        const int n = bal_find(T.bs, e);
+        const int c = T.cnt[n];
+        const uint64_t* sg = sv + T.seg[n];
+        const uint64_t x = sg[e - T.bs[n]];
+        int rank = 0;
+        for (int jj = 0; jj < c; ++jj) rank += sg[jj] < x ? 1 : 0;
+        const int nd = T.d[n];
+        if (rank < (nd < fan ? nd : fan)) item = ((uint32_t)n << 24) | ((uint32_t)rank << 11) | (uint32_t)(x & 0x7FFu);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, item != 0xffffffffu);
+      if (item != 0xffffffffu) q[nq + __popc(m & ((1u << lane) - 1u))] = item;
+      nq += __popc(m);
+    }
+    __syncwarp();
+    for (int k0 = 0; k0 < nq; k0 += 128) {
+      uint32_t it[4];
+      int32_t sidx[4];
+      float wv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // four independent gathers in flight per lane
+        const int k = k0 + 32 * r + lane;
+        it[r] = k < nq ? q[k] : 0xffffffffu;
+        if (it[r] != 0xffffffffu) {
+          const int n = (int)(it[r] >> 24);
+          const int64_t ee = T.e0[n] + (int64_t)(it[r] & 0x7FFu);
+          sidx[r] = __ldg(a.col + ee);
+          wv[r] = a.ew ? __ldg(a.ew + ee) : 1.0f;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (it[r] == 0xffffffffu) continue;
+        const int n = (int)(it[r] >> 24);
+        const int64_t o = T.obase[n] + (int64_t)((it[r] >> 11) & 0x1FFFu);
+        a.tgt[o] = T.u[n];
+        a.src[o] = sidx[r];
+        a.wgt[o] = wv[r];
+        if (a.tgt_front) a.tgt_front[o] = (int32_t)T.idx[n];
+        atomicOr(bm_base + (int64_t)T.b[n] * a.words + (sidx[r] >> 5), 1u << (sidx[r] & 31));
+      }
+    }
+    __syncwarp();
+    // ---- exact warp path for hubs / overflow / too few survivors
+    unsigned big = __ballot_sync(0xffffffffu, fb);
+    uint32_t* wsl = reinterpret_cast<uint32_t*>(sv + kTauCap);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int64_t ii = t0 + src;
+      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+      const int64_t ee = __shfl_sync(0xffffffffu, e0, src);
+      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
+      const int bb = __shfl_sync(0xffffffffu, b, src);
+      const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
+      const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
+      if (dd <= 2048) tau_select_node<true>(a, sv, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+      else tau_select_node<false>(a, sv, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------ translate ----
 __device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
                                            const int32_t* __restrict__ wprefix, int64_t base_word,
@@ -943,7 +1133,25 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       const char* v = getenv("FGL_SELECT");
       return v && v[0] == 's';
     }();
-    if (fan <= kTauMaxFan && !force_stream)
+    static const bool force_tau = [] {
+      const char* v = getenv("FGL_SELECT");
+      return v && v[0] == 't';
+    }();
+    if (fan <= kTauMaxFan && bal_smem(fan) <= 200 * 1024 && !force_stream && !force_tau) {
+      const int bsm = bal_smem(fan);
+      static int bal_grid = 0, bal_smem_set = 0;
+      if (bsm > bal_smem_set) {
+        FGL_CUDA(cudaFuncSetAttribute(select_bal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal_kernel, kBalWarps * 32, bsm) !=
+                cudaSuccess || per_sm < 1)
+          per_sm = 2;
+        bal_grid = per_sm * kNumSMs;
+        bal_smem_set = bsm;
+      }
+      FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
+                                                                                  bal_sv_words(fan));
+    } else if (fan <= kTauMaxFan && !force_stream)
       FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, kSelectSmem, stream>>>(a);
     else if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);
     else if (fan <= 64) FGL_COUNT_LAUNCH(), select_kernel<2><<<select_grid(2), 256, 0, stream>>>(a);
