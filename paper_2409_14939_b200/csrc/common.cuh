@@ -70,6 +70,28 @@ __device__ __forceinline__ void philox4x64_10(uint64_t ctr, uint64_t k0, uint64_
   o0 = c0; o1 = c1; o2 = c2; o3 = c3;
 }
 
+// two independent Philox4x64-10 blocks, rounds interleaved (4 multiply chains)
+__device__ __forceinline__ void philox4x64_10_x2(uint64_t ctrA, uint64_t kA0, uint64_t kA1, uint64_t ctrB,
+                                                 uint64_t kB0, uint64_t kB1, uint64_t (&oA)[4],
+                                                 uint64_t (&oB)[4]) {
+  uint64_t a0 = ctrA, a1 = 0, a2 = 0, a3 = 0;
+  uint64_t b0 = ctrB, b1 = 0, b2 = 0, b3 = 0;
+  asm volatile("" : "+l"(kA0), "+l"(kA1), "+l"(kB0), "+l"(kB1));
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t ahi0 = __umul64hi(kPhiloxM0, a0), alo0 = kPhiloxM0 * a0;
+    const uint64_t ahi1 = __umul64hi(kPhiloxM1, a2), alo1 = kPhiloxM1 * a2;
+    const uint64_t bhi0 = __umul64hi(kPhiloxM0, b0), blo0 = kPhiloxM0 * b0;
+    const uint64_t bhi1 = __umul64hi(kPhiloxM1, b2), blo1 = kPhiloxM1 * b2;
+    a0 = ahi1 ^ a1 ^ kA0; a1 = alo1; a2 = ahi0 ^ a3 ^ kA1; a3 = alo0;
+    b0 = bhi1 ^ b1 ^ kB0; b1 = blo1; b2 = bhi0 ^ b3 ^ kB1; b3 = blo0;
+    kA0 += kPhiloxW0; kA1 += kPhiloxW1;
+    kB0 += kPhiloxW0; kB1 += kPhiloxW1;
+  }
+  oA[0] = a0; oA[1] = a1; oA[2] = a2; oA[3] = a3;
+  oB[0] = b0; oB[1] = b1; oB[2] = b2; oB[3] = b3;
+}
+
 // --------------------------------------------------------------- warp/block --
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }

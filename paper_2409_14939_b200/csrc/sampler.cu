@@ -758,9 +758,8 @@ constexpr int kBalTab = 80;  // bytes per node-table entry
 
 struct BalTab {
   int64_t p0[32], e0[32], obase[32];
-  uint64_t tau[32], k0[32], k1[32];
+  uint64_t tau[32];
   int32_t d[32], seg[32], cnt[32], bs[32], u[32], b[32], fb[32];
-  int64_t idx[32];
 };
 
 inline int bal_cap(int fan) {
@@ -781,7 +780,7 @@ __device__ __forceinline__ int bal_find(const int32_t* arr, int g) {
   return n;
 }
 
-__global__ void __launch_bounds__(kBalWarps * 32, 6) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
+__global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
                                                                     int sv_words) {
   extern __shared__ __align__(16) uint64_t sbuf[];
   const int lane = lane_id(), wib = warp_id();
@@ -819,18 +818,15 @@ __global__ void __launch_bounds__(kBalWarps * 32, 6) select_bal_kernel(const __g
     const uint64_t tau = (double)d <= expect ? kKeyOne
                                              : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
     T.p0[lane] = p0; T.e0[lane] = e0; T.obase[lane] = obase; T.tau[lane] = tau;
-    T.k0[lane] = a.keys[2 * b]; T.k1[lane] = a.keys[2 * b + 1];
     T.d[lane] = (int32_t)(elig ? d : 0); T.seg[lane] = seg; T.cnt[lane] = 0; T.bs[lane] = bs;
-    T.u[lane] = u; T.b[lane] = b; T.idx[lane] = i;
+    T.u[lane] = u; T.b[lane] = b;
     __syncwarp();
-    // ---- balanced Philox over the tile's blocks, survivors into segments
-    for (int g = lane; g < TB; g += 32) {
-      const int n = bal_find(T.bs, g);
+    // ---- balanced Philox over the tile's blocks, survivors into segments;
+    // two blocks per lane per step (g, g + 32) computed interleaved so that
+    // four independent multiply chains hide the IMAD latency
+    auto collect = [&](int n, int64_t k, const uint64_t (&w)[4]) {
       const int64_t np0 = T.p0[n];
       const int nd = T.d[n];
-      const int64_t k = (np0 >> 2) + (g - T.bs[n]);
-      uint64_t w[4];
-      philox4x64_10((uint64_t)k + 1, T.k0[n], T.k1[n], w[0], w[1], w[2], w[3]);
       const uint64_t ntau = T.tau[n];
       const int ncap = nd < capn ? nd : capn;
 #pragma unroll
@@ -842,39 +838,45 @@ __global__ void __launch_bounds__(kBalWarps * 32, 6) select_bal_kernel(const __g
           if (c < ncap) sv[T.seg[n] + c] = (key << 11) | (uint64_t)slot;
         }
       }
+    };
+    for (int g = lane; g < TB; g += 64) {
+      const int g2 = g + 32;
+      const bool two = g2 < TB;
+      const int n1 = bal_find(T.bs, g);
+      const int n2 = two ? bal_find(T.bs, g2) : n1;
+      const int64_t k1 = (T.p0[n1] >> 2) + (g - T.bs[n1]);
+      const int64_t k2 = two ? (T.p0[n2] >> 2) + (g2 - T.bs[n2]) : k1;
+      uint64_t w1[4], w2[4];
+      const int b1 = T.b[n1], b2 = T.b[n2];
+      philox4x64_10_x2((uint64_t)k1 + 1, __ldg(a.keys + 2 * b1), __ldg(a.keys + 2 * b1 + 1), (uint64_t)k2 + 1,
+                       __ldg(a.keys + 2 * b2), __ldg(a.keys + 2 * b2 + 1), w1, w2);
+      collect(n1, k1, w1);
+      if (two) collect(n2, k2, w2);
     }
     __syncwarp();
     const int want = (int)(d < fan ? d : fan);
     const int cnt = T.cnt[lane];
     const bool fb = d > 0 && (!elig || cnt > cap || cnt < want);
-    // ranking runs over the survivors only: cs = exclusive scan of the
-    // survivor counts of the nodes that are not redone
-    const int live = fb ? 0 : cnt;
-    const int csum = warp_incl_scan(live);
-    T.bs[lane] = csum - live;  // block scan no longer needed: reuse as survivor scan
-    const int stot = __shfl_sync(0xffffffffu, csum, 31);
-    __syncwarp();
-    // ---- rank every survivor among its node's survivors by counting; the
-    // emitted (rank < want) ones are queued as (node, rank, slot) so that the
-    // col[] / weight gathers of a lane's emissions are issued back to back
+    // ---- selection, lane = node: want passes of a minimum search over the
+    // node's survivors (strictly above the previous pick; all survivor words
+    // differ in their slot bits), picks queued as (node, rank, slot) so that
+    // the col[] / weight gathers of a lane's emissions are issued back to back
     uint32_t* q = reinterpret_cast<uint32_t*>(sv + segtot);  // emission queue after the survivors
-    int nq = 0;
-    for (int e0i = 0; e0i < stot; e0i += 32) {
-      const int e = e0i + lane;
-      uint32_t item = 0xffffffffu;
-      if (e < stot) {
-        const int n = bal_find(T.bs, e);
-        const int c = T.cnt[n];
-        const uint64_t* sg = sv + T.seg[n];
-        const uint64_t x = sg[e - T.bs[n]];
-        int rank = 0;
-        for (int jj = 0; jj < c; ++jj) rank += sg[jj] < x ? 1 : 0;
-        const int nd = T.d[n];
-        if (rank < (nd < fan ? nd : fan)) item = ((uint32_t)n << 24) | ((uint32_t)rank << 11) | (uint32_t)(x & 0x7FFu);
+    const int nsel = (!fb && d > 0) ? want : 0;
+    const int qbase = warp_incl_scan(nsel) - nsel;
+    const int nq = __shfl_sync(0xffffffffu, qbase + nsel, 31);
+    {
+      const uint64_t* sg = sv + seg;
+      uint64_t prev = 0;
+      for (int r = 0; r < nsel; ++r) {
+        uint64_t best = ~0ull;
+        for (int jj = 0; jj < cnt; ++jj) {
+          const uint64_t x = sg[jj];
+          if ((r == 0 || x > prev) && x < best) best = x;
+        }
+        prev = best;
+        q[qbase + r] = ((uint32_t)lane << 24) | ((uint32_t)r << 11) | (uint32_t)(best & 0x7FFu);
       }
-      const unsigned m = __ballot_sync(0xffffffffu, item != 0xffffffffu);
-      if (item != 0xffffffffu) q[nq + __popc(m & ((1u << lane) - 1u))] = item;
-      nq += __popc(m);
     }
     __syncwarp();
     for (int k0 = 0; k0 < nq; k0 += 128) {
@@ -900,7 +902,7 @@ __global__ void __launch_bounds__(kBalWarps * 32, 6) select_bal_kernel(const __g
         a.tgt[o] = T.u[n];
         a.src[o] = sidx[r];
         a.wgt[o] = wv[r];
-        if (a.tgt_front) a.tgt_front[o] = (int32_t)T.idx[n];
+        if (a.tgt_front) a.tgt_front[o] = (int32_t)(t0 + n);
         atomicOr(bm_base + (int64_t)T.b[n] * a.words + (sidx[r] >> 5), 1u << (sidx[r] & 31));
       }
     }
