@@ -51,7 +51,7 @@ struct SampleWs {
   int64_t* scal;       // [8]
 };
 
-enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5 };
+enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5, kTileCtr = 6 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -288,6 +288,7 @@ __global__ void hop_book_kernel(SampleWs w, const int64_t* __restrict__ fr_off, 
   const int64_t F = w.scal[kF];
   if (threadIdx.x == 0) {
     w.scal[kHopEdgeBase] = w.scal[kEdgeBase];
+    w.scal[kTileCtr] = 0;  // dynamic tile counter of this hop's select kernel
   }
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const int64_t f0 = fr_off[b], f1 = fr_off[b + 1];
@@ -389,6 +390,7 @@ struct SelectArgs {
   float* wgt;
   int32_t* tgt_front;
   int fan;
+  unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal_kernel)
 };
 
 template <int K>
@@ -794,7 +796,16 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
   const int fan = a.fan;
   const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
   uint32_t* bm_base = a.bm_front;
-  for (int64_t t0 = gw * 32; t0 < F; t0 += nwarps * 32) {
+  const int64_t ntiles = ceil_div(F, 32);
+  (void)gw; (void)nwarps;
+  for (;;) {
+    // dynamic tile scheduling: hub-heavy tiles cost ~10 normal ones, so a
+    // static grid stride leaves a long tail of busy warps
+    unsigned long long tix = 0;
+    if (lane == 0) tix = atomicAdd(a.tile_ctr, 1ull);
+    tix = __shfl_sync(0xffffffffu, tix, 0);
+    if ((int64_t)tix >= ntiles) break;
+    const int64_t t0 = (int64_t)tix * 32;
     const int64_t i = t0 + lane;
     int32_t u = 0, b = 0;
     int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
@@ -1129,7 +1140,8 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     FGL_LAUNCH_CHECK("degree scan");
     SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
                  w.scan_deg, w.scan_sel, fr_off(h), w.hop_pos, keys, w.scal,
-                 w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan};
+                 w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan,
+                 reinterpret_cast<unsigned long long*>(w.scal + kTileCtr)};
     // FGL_SELECT=stream forces the streaming top-list kernel (A/B parity tests)
     static const bool force_stream = [] {
       const char* v = getenv("FGL_SELECT");
