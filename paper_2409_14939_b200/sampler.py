@@ -207,6 +207,12 @@ class WindowSampler:
         self.seed_off = torch.empty(self.max_nb + 1, dtype=torch.int64, device=device)
         self.keys = torch.empty(2 * self.max_nb, dtype=torch.int64, device=device)
         self.counts = torch.empty(self.counts_len, dtype=torch.int64, device=device)
+        # pinned staging of a window's inputs (seeds | offsets | keys): one
+        # asynchronous host->device copy per stage(); the event guards reuse
+        pin = (lambda t: t.pin_memory()) if torch.cuda.is_available() else (lambda t: t)
+        self._pin_seeds = pin(torch.empty(nseed, dtype=torch.int32))
+        self._pin_meta = pin(torch.empty(3 * self.max_nb + 1, dtype=torch.int64))
+        self._pin_done = None
         self._fan = _lib.i32_array(self.fanouts.counts)
         ptr = lambda t: t.data_ptr() if t is not None else None
         self._out = _lib.FglSampleOut(
@@ -233,9 +239,18 @@ class WindowSampler:
             raise ValidationError("seed id out of range")
         keys = np.array([philox_key(s) for s in seeds_for_rng], dtype=np.uint64).reshape(-1)
         n = int(off[-1])
-        self.seeds_dev[:n].copy_(torch.from_numpy(flat.astype(np.int32)))
-        self.seed_off[: nb + 1].copy_(torch.from_numpy(off))
-        self.keys[: 2 * nb].copy_(torch.from_numpy(keys.view(np.int64)))
+        if self._pin_done is not None:
+            self._pin_done.synchronize()  # the previous window's copy has left the staging buffers
+        self._pin_seeds.numpy()[:n] = flat
+        meta = self._pin_meta.numpy()
+        meta[: nb + 1] = off
+        meta[nb + 1 : 3 * nb + 1] = keys.view(np.int64)
+        self.seeds_dev[:n].copy_(self._pin_seeds[:n], non_blocking=True)
+        self.seed_off[: nb + 1].copy_(self._pin_meta[: nb + 1], non_blocking=True)
+        self.keys[: 2 * nb].copy_(self._pin_meta[nb + 1 : 3 * nb + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pin_done = ev
         return nb, off
 
     def run(self, nb: int, seed_off_host: np.ndarray, stream=None) -> DeviceWindow:
