@@ -442,8 +442,12 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   if (n > 0) {
     int werr = 0;
     const int tc_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 128)));
+    const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(n, 64)));
     int used_chunks = chunks;
-    if (tc_wgrad(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc_chunks, st, &werr)) {
+    if (tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
+      if (werr) return werr;
+      used_chunks = tc3_chunks;
+    } else if (tc_wgrad(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc_chunks, st, &werr)) {
       if (werr) return werr;
       used_chunks = tc_chunks;
     } else {

@@ -370,6 +370,203 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
   if (tid == 32) G3T(G3_TR - 1);
 }
 
+// ------------------------------------------------------------------ wgrad --
+// Weight-gradient partials on the tensor cores: D[m][n] = sum_r A'[m][r] B'[n][r]
+// with A'[m][r] = H[r][m] (m < K), 1 (m == K: the db row), B'[n][r] =
+// dZ[r][n] * (mask[r][n] > 0).  The reduction dimension r (rows) is the MMA
+// K dimension, so both operands need a transpose, done by the converters on
+// their way into the MMA operands:
+//   warp 0      producer: bulk copies of 64-row tiles of H, dZ, mask;
+//   warps 4-11  converters: per 32-row chunk, thread = feature m = TMEM lane:
+//               16 rows of column m (conflict-free 4-byte shared loads) ->
+//               tf32 hi/lo -> tcgen05.st into the A chunk ring; and the dZ
+//               columns -> hi/lo K-major SWIZZLE_128B boxes in shared memory;
+//   warp 1      MMA: 4 K steps x 3 tcgen05.mma per chunk into ONE accumulator
+//               that lives for the CTA's whole row range;
+//   warps 12-15 epilogue: the CTA's [K+1][N] partial -> global (summed by
+//               reduce_partials_kernel, deterministic order).
+constexpr int WG3_MT = 64;   // rows per bulk-copied tile
+constexpr int WG3_NC = 4;    // A / B chunk ring depth (32 rows each)
+constexpr int WG3_R = 2;     // raw tile slots
+
+struct Wg3Args {
+  const float* H; const float* dZ; const float* mask;
+  int64_t ldh, ldz, ldm;
+  float* part;         // [gridDim.x][K+1][N]
+  int64_t M;
+  int K, N, N_pad, tmem_cols, h_bytes, z_bytes, m_bytes, dbg;
+};
+
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int N_pad = p.N_pad;
+  const int b_box = N_pad * 128;  // one SW128 box: N_pad rows x 32 K (rows r) fp32
+  char* sB = smem;                                  // [NC][hi, lo] boxes
+  char* slots = sB + WG3_NC * 2 * b_box;
+  const int slot_bytes = p.h_bytes + p.z_bytes + p.m_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + WG3_R * slot_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * WG3_R + 2 * WG3_NC + 1);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  const int FULL = 0, EMPTY = WG3_R, CFULL = 2 * WG3_R, CEMPTY = 2 * WG3_R + WG3_NC, TFULL = 2 * WG3_R + 2 * WG3_NC;
+  if (tid == 0) {
+    for (int s = 0; s < WG3_R; ++s) { mbar_init_n(bar(FULL + s), 1); mbar_init_n(bar(EMPTY + s), G3_CONV_THREADS); }
+    for (int c = 0; c < WG3_NC; ++c) { mbar_init_n(bar(CFULL + c), G3_CONV_THREADS); mbar_init_n(bar(CEMPTY + c), 1); }
+    mbar_init_n(bar(TFULL), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tiles = ceil_div(p.M, WG3_MT);
+  if (warp == 0) {
+    if (lane == 0) {
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+        const int s = j % WG3_R;
+        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / WG3_R) & 1u) ^ 1u);
+        const int64_t r0 = t * WG3_MT;
+        const int rows = (int)(p.M - r0 < WG3_MT ? p.M - r0 : WG3_MT);
+        const uint32_t hb = (uint32_t)(rows * p.ldh * 4), zb = (uint32_t)(rows * p.ldz * 4),
+                       mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        char* slot = slots + s * slot_bytes;
+        mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
+        bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
+        bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
+        if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
+      }
+    }
+    return;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto ch_hi = [&](int c) { return tmem + (uint32_t)(N_pad + 64 * c); };
+  const int my_tiles = (int)(tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+
+  if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(G3_M, N_pad, 0, 0);
+    const uint32_t sb = smem_u32(sB);
+    int cc = 0;
+    for (int j = 0; j < my_tiles; ++j) {
+      for (int c = 0; c < WG3_MT / 32; ++c, ++cc) {
+        const int cs = cc % WG3_NC;
+        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / WG3_NC) & 1u);
+        tc_fence_after();
+        const uint32_t ahi = ch_hi(cs), alo = ahi + 32;
+        const uint32_t bh = sb + (uint32_t)(cs * 2 * b_box), bl = bh + (uint32_t)b_box;
+        if (elect_one()) {
+#pragma unroll
+          for (int st = 0; st < ((p.dbg & 2) ? 0 : 4); ++st) {
+            const uint64_t dbh = umma_desc_sw128(bh + st * 32), dbl = umma_desc_sw128(bl + st * 32);
+            mma_tf32_ts(tmem, alo + 8 * st, dbh, idesc, (cc | st) != 0);
+            mma_tf32_ts(tmem, ahi + 8 * st, dbl, idesc, 1);
+            mma_tf32_ts(tmem, ahi + 8 * st, dbh, idesc, 1);
+          }
+          mma_commit(bar(CEMPTY + cs));
+        }
+        __syncwarp();
+      }
+    }
+    if (my_tiles > 0 && elect_one()) mma_commit(bar(TFULL));
+    __syncwarp();
+  } else if (warp >= 4 && warp < 12) {
+    const int ct = tid - 128;              // 0..255
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int m = quarter * 32 + lane;     // A' row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int cc = 0;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int s = j % WG3_R;
+      const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
+      const int rows = (int)(p.M - t * WG3_MT < WG3_MT ? p.M - t * WG3_MT : WG3_MT);
+      mbar_wait(bar(FULL + s), (uint32_t)(j / WG3_R) & 1u);
+      const uint32_t hs = smem_u32(slots + s * slot_bytes);
+      const uint32_t zs = hs + (uint32_t)p.h_bytes, ms = zs + (uint32_t)p.z_bytes;
+      for (int c = 0; c < WG3_MT / 32; ++c, ++cc) {
+        const int cs = cc % WG3_NC;
+        // A': column m of rows r = 32c + 16 half + [0, 16) (conflict-free:
+        // consecutive lanes read consecutive features of one row)
+        uint32_t hv[16], lv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int r = 32 * c + 16 * half + q;
+          float x = 0.f;
+          if (r < rows && !(p.dbg & 1)) {
+            if (m < p.K) x = lds32(hs + (uint32_t)((r * p.ldh + m) * 4));
+            else if (m == p.K) x = 1.f;
+          }
+          const float hi = tf32_rna_finite(x);
+          hv[q] = __float_as_uint(hi);
+          lv[q] = __float_as_uint(__fsub_rn(x, hi));
+        }
+        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / WG3_NC) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t hi_t = ch_hi(cs) + lane_off + (uint32_t)(16 * half);
+        tmem_st8(hi_t, *reinterpret_cast<uint32_t(*)[8]>(hv));
+        tmem_st8(hi_t + 8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8));
+        tmem_st8(hi_t + 32, *reinterpret_cast<uint32_t(*)[8]>(lv));
+        tmem_st8(hi_t + 40, *reinterpret_cast<uint32_t(*)[8]>(lv + 8));
+        // B': (n, 4 consecutive rows) groups -> SW128 box (row n, K = r);
+        // consecutive threads take consecutive n (conflict-free column loads)
+        const uint32_t bh = smem_u32(sB) + (uint32_t)(cs * 2 * b_box);
+        for (int idx = ct; idx < ((p.dbg & 4) ? 0 : N_pad * 8); idx += G3_CONV_THREADS) {
+          const int bn = idx % N_pad, br = idx / N_pad;
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+          if (bn < p.N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int r = 32 * c + 4 * br + q;
+              if (r < rows) {
+                const float z = lds32(zs + (uint32_t)((r * p.ldz + bn) * 4));
+                const float mk = p.mask ? lds32(ms + (uint32_t)((r * p.ldm + bn) * 4)) : 1.f;
+                e[q] = mk > 0.f ? z : 0.f;
+              }
+            }
+          }
+          float4 h4, l4;
+          h4.x = tf32_rna_finite(e[0]); l4.x = __fsub_rn(e[0], h4.x);
+          h4.y = tf32_rna_finite(e[1]); l4.y = __fsub_rn(e[1], h4.y);
+          h4.z = tf32_rna_finite(e[2]); l4.z = __fsub_rn(e[2], h4.z);
+          h4.w = tf32_rna_finite(e[3]); l4.w = __fsub_rn(e[3], h4.w);
+          const uint32_t off = sw128_off(bn, 4 * br);
+          sts128(bh + off, h4);
+          sts128(bh + (uint32_t)b_box + off, l4);
+        }
+        tmem_st_wait();
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(bar(CFULL + cs));
+      }
+      mbar_arrive(bar(EMPTY + s));
+    }
+  } else if (warp >= 12) {
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    float* out = p.part + (int64_t)blockIdx.x * (p.K + 1) * p.N;
+    if (my_tiles > 0) {
+      mbar_wait(bar(TFULL), 0);
+      tc_fence_after();
+    }
+    for (int c0 = 0; c0 < N_pad; c0 += 16) {
+      uint32_t v[16];
+      if (my_tiles > 0) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      if (m <= p.K) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (c0 + q < p.N) out[(int64_t)m * p.N + c0 + q] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
+      }
+    }
+  }
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, p.tmem_cols);
+  }
+}
+
 // ------------------------------------------------------------ host side --
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -466,6 +663,38 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_gemm3_kernel");
+  return true;
+}
+
+// Weight-gradient partials part[c][K+1][N] (row K = db) over `chunks` CTAs;
+// returns false outside the envelope (K + 1 <= 128, N <= 256, 16-byte rows).
+bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
+               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
+  *err = 0;
+  if (tc3_disabled() || M < 1 || K < 1 || K + 1 > G3_M || N < 1 || N > 256) return false;
+  if ((ldh % 4) || (ldz % 4) || (reinterpret_cast<uintptr_t>(H) & 15) || (reinterpret_cast<uintptr_t>(dZ) & 15))
+    return false;
+  if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
+  const int N_pad = (N + 15) / 16 * 16;
+  const int hb = WG3_MT * (int)ldh * 4, zb = WG3_MT * (int)ldz * 4, mb = mask ? WG3_MT * (int)ldm * 4 : 0;
+  const int64_t smem = 1024 + (int64_t)WG3_NC * 2 * N_pad * 128 + (int64_t)WG3_R * (hb + zb + mb) +
+                       8 * (2 * WG3_R + 2 * WG3_NC + 1) + 16;
+  if (smem > G3_MAX_SMEM) return false;
+  int cols = 32;
+  while (cols < N_pad + 64 * WG3_NC) cols <<= 1;
+  if (cols > 512) return false;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    e = cudaFuncSetAttribute(tc_wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad3)"); return true; }
+    attr = true;
+  }
+  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg};
+  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
   return true;
 }
 
