@@ -319,6 +319,18 @@ def main():
         torch.distributed.destroy_process_group()
 
 
+def _measured_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture
+    of `kernel` (same workload, committed under profiles/), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel, {}).get("traffic_bytes")
+    except Exception:
+        return None
+
+
 def stage_profile(pipe, mine, it, cfg, torch):
     """Per-stage device time of 2 windows (events between the stages; not part
     of the headline timing) and the roofline of the dominant stage."""
@@ -329,12 +341,19 @@ def stage_profile(pipe, mine, it, cfg, torch):
     acc = {"sample": 0.0, "schedule": 0.0, "prepare": 0.0, "compute": 0.0}
     draws = 0
     samp_bytes = 0.0
+    from paper_2409_14939_b200 import _lib as _l
+    sel = {"s": 0.0, "bytes": 0.0, "draws": 0.0}
     for k in range(2):
         seeds, rs = mine[(it + k) % len(mine)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        _l.call("fgl_profile_select", 1)
         ev[0].record()
         win = pipe.sampler.sample(seeds, rs)
         ev[1].record()
+        _l.call("fgl_profile_select", 0)
+        pms = np.zeros(16, dtype=np.float64)
+        nl = np.zeros(1, dtype=np.int64)
+        _l.call("fgl_profile_select_read", pms.ctypes.data, 16, nl.ctypes.data)
         win.host_counts()
         order = pipe.schedule(win, len(seeds))
         ev[2].record()
@@ -355,6 +374,17 @@ def stage_profile(pipe, mine, it, cfg, torch):
             e0, e1 = win.hop_edges(h)
             S = e1 - e0
             samp_bytes += (2 * 8 * F + S * 4 + S * (2 * 4 + 4)) / 2
+        # dominant launch: the last hop's select kernel (largest frontier).
+        # Algorithmic bytes: per frontier node its id, batch, two CSR offsets,
+        # the two scans (4+4+16+16); per sampled edge the chosen col entry and
+        # the (tgt, src, wgt, tgt_front) record (4 + 16); draws: one per candidate
+        hl = win.num_hops - 1
+        F = win.front_total(hl)
+        e0_, e1_ = win.hop_edges(hl)
+        S = e1_ - e0_
+        sel["s"] += float(pms[hl]) / 1e3 / 2
+        sel["bytes"] += (40.0 * F + 20.0 * S) / 2
+        sel["draws"] += win.hop_draws(hl) / 2
     t_s = acc["sample"] / 1e3
     # Philox ALU probe: draws/s of the bare Philox4x64-10 kernel on this GPU
     from paper_2409_14939_b200 import _lib
@@ -368,13 +398,16 @@ def stage_profile(pipe, mine, it, cfg, torch):
     torch.cuda.synchronize()
     peak_draws = 4 * nblk / (e0.elapsed_time(e1) / 1e3)
     roof = {
-        "kernel": "fgl_sample_window (select_kernel dominant)",
-        "bound": "hbm", "achieved": samp_bytes / t_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-        "frac": samp_bytes / t_s / 1e9 / hbm_peak, "traffic": None,
-        "peak_source": peak_src,
+        "kernel": "select_bal_kernel, the hop-2 launch of fgl_sample_window (largest select launch)",
+        "bound": "hbm", "achieved": sel["bytes"] / sel["s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
+        "frac": sel["bytes"] / sel["s"] / 1e9 / hbm_peak, "traffic": _measured_traffic("select_bal_kernel"),
+        "peak_source": peak_src, "launch_ms": sel["s"] * 1e3, "bytes_per_launch": sel["bytes"],
         "alu": {"bound": "philox4x64-10 draws (bit-exact sampling needs one per candidate edge)",
-                "achieved_draws_per_s": draws / t_s, "peak_draws_per_s": peak_draws,
-                "frac": draws / t_s / peak_draws},
+                "achieved_draws_per_s": sel["draws"] / sel["s"], "peak_draws_per_s": peak_draws,
+                "frac": sel["draws"] / sel["s"] / peak_draws,
+                "draws_per_launch": sel["draws"]},
+        "sampler_stage": {"ms_per_window": acc["sample"], "draws_per_s": draws / t_s,
+                          "alu_frac": draws / t_s / peak_draws},
     }
     return {"ms": acc, "roofline": roof}
 

@@ -128,6 +128,13 @@ int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uin
                      void* stream);
 /* Draws `count` Philox blocks and reduces them to one word (ALU roofline probe). */
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream);
+/* Measurement hook (bench.py roofline): while enabled, fgl_sample_window
+ * brackets every select-kernel launch with CUDA events on its stream;
+ * fgl_profile_select_read synchronises on them, writes up to `cap` per-launch
+ * device milliseconds (launch order: hop 0..H-1 of each window) and the
+ * launch count, then clears the record. */
+int fgl_profile_select(int32_t enable);
+int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches);
 
 /* ------------------------------------------------------------- prepare ---- */
 /* indptr[r] = base + (first e with rows[e] >= r), r in [0, num_rows]; `rows`

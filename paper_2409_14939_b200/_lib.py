@@ -61,6 +61,8 @@ SIGNATURES = {
         C.POINTER(FglSampleOut), vp, C.c_int64, vp]),
     "fgl_philox_words": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
+    "fgl_profile_select": (C.c_int, [C.c_int32]),
+    "fgl_profile_select_read": (C.c_int, [vp, C.c_int64, vp]),
     "fgl_csr_offsets_sorted": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_stable_group_ws_bytes": (C.c_int64, [C.c_int64]),
     "fgl_stable_group": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]),

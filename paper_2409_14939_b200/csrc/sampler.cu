@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -995,6 +996,11 @@ __global__ void translate_seeds_kernel(const int32_t* __restrict__ seeds,
   }
 }
 
+// measurement hook (fgl_profile_select): events around select launches
+std::mutex g_sel_mu;
+bool g_sel_prof = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_sel_ev;
+
 int select_grid(int K) {
   static int cache[9] = {0};
   if (cache[K]) return cache[K];
@@ -1022,6 +1028,28 @@ int select_grid(int K) {
 using namespace fgl;
 
 extern "C" {
+
+int fgl_profile_select(int32_t enable) {
+  g_sel_prof = enable != 0;
+  return FGL_OK;
+}
+
+int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_sel_mu);
+  int64_t k = 0;
+  for (auto& pr : g_sel_ev) {
+    float ms = 0.f;
+    FGL_CUDA(cudaEventSynchronize(pr.second));
+    FGL_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    if (ms_out && k < cap) ms_out[k] = ms;
+    ++k;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  if (launches) *launches = k;
+  g_sel_ev.clear();
+  return FGL_OK;
+}
 
 int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t nb,
                       const int32_t* fanouts, int32_t H, int64_t* out) {
@@ -1163,8 +1191,19 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
         bal_grid = per_sm * kNumSMs;
         bal_smem_set = bsm;
       }
+      cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+      if (g_sel_prof) {
+        cudaEventCreate(&pe0);
+        cudaEventCreate(&pe1);
+        cudaEventRecord(pe0, stream);
+      }
       FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
                                                                                   bal_sv_words(fan));
+      if (g_sel_prof) {
+        cudaEventRecord(pe1, stream);
+        std::lock_guard<std::mutex> lk(g_sel_mu);
+        g_sel_ev.emplace_back(pe0, pe1);
+      }
     } else if (fan <= kTauMaxFan && !force_stream)
       FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, kSelectSmem, stream>>>(a);
     else if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);

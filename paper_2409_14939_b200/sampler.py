@@ -145,6 +145,13 @@ class DeviceWindow:
     def total_edges(self) -> int:
         return int(self.host_counts()[self.num_hops * self.num_batches])
 
+    def hop_draws(self, hop: int) -> int:
+        """Philox draws (= candidates = sum of frontier degrees) of one hop;
+        measurement helper, computed on the device."""
+        f = self.frontier(hop).long()
+        off = self.s.g.row_offsets
+        return int((off[f + 1] - off[f]).sum().item())
+
     def frontier(self, hop: int):
         return self.s.frontier[hop * self.s.fcap : hop * self.s.fcap + self.front_total(hop)]
 
