@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--profile", action="store_true", help="stop after warm-up + 2 steps (for ncu)")
+    ap.add_argument("--cache-ratio", type=float, default=0.0,
+                    help="static-degree HBM feature cache in front of a host-resident store (configs *_host, papers)")
     args = ap.parse_args()
 
     import torch
@@ -233,7 +235,8 @@ def main():
                                batch_size=cfg["bs"], window_n=cfg["window"], lr=0.1, seed=0)
     pipe = trainer.Pipeline(dg, feats, labels, mcfg, trainer.PipelineFlags(), device=device,
                             feature_store=cfg["store"], dist=fdist.GradAllReduce(world),
-                            direct_x0=cfg.get("direct_x0", True))
+                            direct_x0=cfg.get("direct_x0", True),
+                            cache_ratio=args.cache_ratio if cfg["store"] == "host" else 0.0)
     lib = _lib.lib()
     W, K = max(args.warmup, 0), max(args.steps, 1)
     if args.profile:
@@ -296,7 +299,9 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (fp64 loss; int32/int64 sampling)",
         "data": "synthetic (seeded Chung-Lu power-law graph, random f32 features, random labels)",
-        "config": {"workload": cfg["desc"], "global_batch": cfg["bs"] * world,
+        "config": {"workload": cfg["desc"] + (f", static-degree HBM cache ratio {args.cache_ratio}"
+                                              if args.cache_ratio and cfg["store"] == "host" else ""),
+                   "global_batch": cfg["bs"] * world,
                    "windows_per_step_per_rank": 1, "mini_batches_per_step": batches_per_step,
                    "parallelism": f"dp{world}", "l2": "inputs (CSR 0.27 GB + features) larger than the 126 MB L2",
                    "epoch_batches": nbatches},

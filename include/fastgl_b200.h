@@ -254,6 +254,16 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
                     const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
                     const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
                     void* stream);
+/* fgl_gather_rows with a static HBM feature cache (memsim.py:110-186,
+ * static-degree policy): after the Match test, a node with cache_slot[g] >= 0
+ * is copied from cache_x[cache_slot[g] * ldc] (HBM) instead of the store;
+ * `hits` (optional) accumulates those rows, `loaded` the rows read from the
+ * store. cache_slot has one int32 per graph node (-1 = not cached). */
+int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
+                           const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
+                           const float* prev_x, int64_t ldp, const int32_t* cache_slot, const float* cache_x,
+                           int64_t ldc, float* out, int64_t ldo, uint64_t* loaded, uint64_t* hits,
+                           void* stream);
 
 #ifdef __cplusplus
 }

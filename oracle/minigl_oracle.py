@@ -26,7 +26,7 @@ __all__ = [
     "idmap_lookup", "layer_edge_weights", "edges_to_csr", "csr_transpose",
     "prepare_batch", "tile_plan_error", "aggregate", "dense", "softmax_xent",
     "init_params", "forward", "backward", "sgd_step", "match_matrix",
-    "greedy_order", "window_schedule", "epoch_h2d_bytes", "train_split",
+    "greedy_order", "window_schedule", "epoch_h2d_bytes", "cache_mask", "train_split",
     "train", "train_step", "evaluate_params", "two_cluster_task",
 ]
 
@@ -463,6 +463,17 @@ def window_schedule(node_sets, reorder: bool, dim: int):
     ex = [node_sets[i] for i in order]
     loads = [ex[0]] + [np.setdiff1d(b, a, assume_unique=True) for a, b in zip(ex, ex[1:])]
     return order, ex, loads, 4 * dim * sum(len(x) for x in loads)
+
+
+def cache_mask(num_nodes, cache_ratio, degrees):
+    """Static-degree feature cache (``memsim.py:110-126``): the floor(ratio * N)
+    highest-degree nodes, ties broken by lower node id."""
+    mask = np.zeros(num_nodes, dtype=bool)
+    k = int(np.floor(cache_ratio * num_nodes))
+    if k > 0:
+        ranked = np.lexsort((np.arange(num_nodes), -np.asarray(degrees).astype(np.int64)))
+        mask[ranked[:k]] = True
+    return mask
 
 
 def epoch_h2d_bytes(windows_exec, windows_loads, dim, match=True, cached=None):

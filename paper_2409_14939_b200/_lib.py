@@ -94,6 +94,8 @@ SIGNATURES = {
     "fgl_bitmap_test": (C.c_int, [vp, C.c_int64, vp, vp, vp]),
     "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
                                   vp, C.c_int64, vp, C.c_int64, vp, vp]),
+    "fgl_gather_rows_cached": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
+                                         vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp]),
 }
 
 _lib = None

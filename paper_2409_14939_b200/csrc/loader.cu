@@ -13,6 +13,11 @@
 //    HBM.  Rows are moved with 16-byte vector loads, one warp per row.  The
 //    count of rows read from the store is accumulated for the IO accounting
 //    of memsim.simulate_epoch_io (memsim.py:129-186).
+//  * fgl_gather_rows_cached -- the same with a static HBM feature cache
+//    (memsim.py:110-126 static-degree policy made real): a row the previous
+//    batch does not hold is read from the cache table when its node has a
+//    cache slot, else from the store; cache hits are counted separately
+//    (bytes_served_by_cache of simulate_epoch_io).
 #include <algorithm>
 
 #include "common.cuh"
@@ -65,14 +70,15 @@ template <bool VEC>
 __global__ void __launch_bounds__(256) gather_rows_kernel(
     const float* __restrict__ feats, int64_t ldf, int d, const int32_t* __restrict__ ids, int64_t n,
     const uint32_t* __restrict__ prev_bm, const int32_t* __restrict__ prev_prefix, int64_t prev_base,
-    const float* __restrict__ prev_x, int64_t ldp, float* __restrict__ out, int64_t ldo,
-    unsigned long long* __restrict__ loaded) {
+    const float* __restrict__ prev_x, int64_t ldp, const int32_t* __restrict__ cache_slot,
+    const float* __restrict__ cache_x, int64_t ldc, float* __restrict__ out, int64_t ldo,
+    unsigned long long* __restrict__ loaded, unsigned long long* __restrict__ hits) {
   constexpr int R = 4;
   const int lane = threadIdx.x & 31;
   const int w = VEC ? (d + 3) >> 2 : d;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t my_loaded = 0;
+  uint32_t my_loaded = 0, my_hits = 0;
   for (int64_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
     // lanes 0..R-1 resolve the R rows' sources, then broadcast
     const float* mine = nullptr;
@@ -86,6 +92,14 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
           const int64_t pr = __ldg(prev_prefix + (g >> 5)) + __popc(word & ((1u << (g & 31)) - 1u)) - prev_base;
           mine = prev_x + pr * ldp;
           store = false;
+        }
+      }
+      if (store && cache_slot) {  // static HBM cache (memsim.py:110-186): after Match
+        const int32_t cs = __ldg(cache_slot + g);
+        if (cs >= 0) {
+          mine = cache_x + (int64_t)cs * ldc;
+          store = false;
+          ++my_hits;
         }
       }
       my_loaded += store ? 1u : 0u;
@@ -126,6 +140,10 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
   if (loaded) {
     my_loaded = warp_sum(my_loaded);
     if (lane == 0 && my_loaded) atomicAdd(loaded, (unsigned long long)my_loaded);
+  }
+  if (hits) {
+    my_hits = warp_sum(my_hits);
+    if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
   }
 }
 
@@ -208,29 +226,41 @@ int fgl_bitmap_test(const int32_t* ids, int64_t n, const uint32_t* bitmap, int8_
   return FGL_OK;
 }
 
-int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
-                    const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
-                    const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
-                    void* stream) {
+int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
+                           const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
+                           const float* prev_x, int64_t ldp, const int32_t* cache_slot, const float* cache_x,
+                           int64_t ldc, float* out, int64_t ldo, uint64_t* loaded, uint64_t* hits,
+                           void* stream) {
   if (n < 0 || d < 1 || ldf < d || ldo < d || !feats || !out || (n > 0 && !ids) ||
-      (prev_bitmap && (!prev_prefix || !prev_x || ldp < d))) {
+      (prev_bitmap && (!prev_prefix || !prev_x || ldp < d)) || (cache_slot && (!cache_x || ldc < d))) {
     set_error("fgl_gather_rows: bad arguments");
     return FGL_E_INVALID;
   }
   if (n == 0) return FGL_OK;
-  const bool vec = ((ldf | ldo | (prev_bitmap ? ldp : 0)) % 4 == 0) &&
+  const bool vec = ((ldf | ldo | (prev_bitmap ? ldp : 0) | (cache_slot ? ldc : 0)) % 4 == 0) &&
                    !((reinterpret_cast<uintptr_t>(feats) | reinterpret_cast<uintptr_t>(out) |
-                      reinterpret_cast<uintptr_t>(prev_x)) & 15);
+                      reinterpret_cast<uintptr_t>(prev_x) | reinterpret_cast<uintptr_t>(cache_x)) & 15);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8 * 4), 148 * 16));
   auto* ld = reinterpret_cast<unsigned long long*>(loaded);
+  auto* ht = reinterpret_cast<unsigned long long*>(hits);
   if (vec)
     FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, out, ldo, ld);
+        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, cache_slot, cache_x, ldc, out,
+        ldo, ld, ht);
   else
     FGL_COUNT_LAUNCH(), gather_rows_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, out, ldo, ld);
+        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, cache_slot, cache_x, ldc, out,
+        ldo, ld, ht);
   FGL_LAUNCH_CHECK("gather_rows_kernel");
   return FGL_OK;
+}
+
+int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
+                    const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
+                    const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
+                    void* stream) {
+  return fgl_gather_rows_cached(feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, nullptr,
+                                nullptr, 0, out, ldo, loaded, nullptr, stream);
 }
 
 }  // extern "C"

@@ -33,7 +33,7 @@ from .graph import device_graph
 from .sampler import Fanouts, WindowSampler, derive_seed, make_epoch_batches
 
 __all__ = ["ModelConfig", "PipelineFlags", "EpochStats", "TrainReport", "train", "derive_seed",
-           "init_params", "DeviceModel", "Pipeline", "phase_breakdown", "PHASES"]
+           "init_params", "DeviceModel", "Pipeline", "StaticFeatureCache", "phase_breakdown", "PHASES"]
 
 PHASES = ("sample", "map", "io_sim", "compute")
 
@@ -191,6 +191,46 @@ def greedy_order(m: np.ndarray) -> list:
     return order
 
 
+class StaticFeatureCache:
+    """Static-degree feature cache in HBM (memsim.py:110-126 made real): the
+    floor(ratio * N) highest-degree nodes (ties: lower node id) keep their
+    feature rows in an HBM table; ``slot[g]`` is the row of node g in that
+    table or -1.  The loader (fgl_gather_rows_cached) serves a row that Match
+    does not cover from the table instead of the host link, and counts the
+    hits (bytes_served_by_cache of simulate_epoch_io, memsim.py:129-186)."""
+
+    POLICIES = ("none", "static-degree")
+
+    def __init__(self, dg, host_feats, d, ld, cache_ratio: float, policy: str = "static-degree",
+                 device="cuda"):
+        import torch
+        if not 0.0 <= cache_ratio <= 1.0:
+            raise ValidationError("cache_ratio must be within [0, 1]")
+        if policy not in self.POLICIES:
+            raise ValidationError(f"unknown cache policy {policy!r}")
+        n = int(dg.num_nodes)
+        self.k = int(np.floor(cache_ratio * n)) if policy == "static-degree" else 0
+        self.ratio, self.policy, self.ld = cache_ratio, policy, ld
+        self.slot = torch.full((n,), -1, dtype=torch.int32, device=device)
+        self.table = torch.zeros((max(self.k, 1), ld), dtype=torch.float32, device=device)
+        if self.k > 0:
+            off = dg.row_offsets
+            deg = (off[1:] - off[:-1]).to(torch.int64)
+            # stable sort on -degree: equal degrees keep ascending node id
+            top = torch.argsort(-deg, stable=True)[: self.k].to(torch.int32).contiguous()
+            self.slot[top.long()] = torch.arange(self.k, dtype=torch.int32, device=device)
+            self.nodes = top
+            _lib.call("fgl_gather_rows", host_feats.data_ptr(), ld, d, top.data_ptr(), self.k, None, None, 0,
+                      None, ld, self.table.data_ptr(), ld, None, torch.cuda.current_stream().cuda_stream)
+        else:
+            self.nodes = torch.zeros(0, dtype=torch.int32, device=device)
+
+    def mask_numpy(self, n):
+        m = np.zeros(n, dtype=bool)
+        m[self.nodes.cpu().numpy()] = True
+        return m
+
+
 class Pipeline:
     """Device-resident training pipeline for one graph / feature store / model.
 
@@ -200,7 +240,8 @@ class Pipeline:
     """
 
     def __init__(self, g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None,
-                 device="cuda", feature_store="device", params=None, dist=None, direct_x0=None):
+                 device="cuda", feature_store="device", params=None, dist=None, direct_x0=None,
+                 cache_ratio: float = 0.0, cache_policy: str = "static-degree"):
         import torch
         self.torch = torch
         self.cfg = cfg
@@ -247,6 +288,13 @@ class Pipeline:
         self.direct_x0 = bool(direct_x0) and feature_store == "device" and self.compact
         self.pairs = torch.zeros(120, dtype=torch.int64, device=device)
         self.loaded = torch.zeros(1, dtype=torch.int64, device=device)
+        self.cache_hits = torch.zeros(1, dtype=torch.int64, device=device)
+        self.cache = None
+        if cache_ratio > 0.0 or cache_policy not in StaticFeatureCache.POLICIES:
+            if feature_store != "host":
+                raise ValidationError("the static feature cache fronts a host-resident feature store")
+            self.cache = StaticFeatureCache(self.dg, self.feats, self.d0, self.ldf, cache_ratio, cache_policy,
+                                            device)
         self.loss_dev = torch.zeros(max(cfg.window_n, 1), dtype=torch.float64, device=device)
         dims = cfg.layer_dims
         self.bwd_ws = torch.empty(max(_lib.lib().fgl_dense_bwd_ws_bytes(a, b) for a, b in zip(dims, dims[1:])),
@@ -366,7 +414,12 @@ class Pipeline:
             prev_x = self._bufs[f"x0_{1 - x0_slot}"].data_ptr()
         else:
             p0, prev_bm, prev_pf, prev_x = 0, None, None, None
-        if not self.direct_x0:
+        if not self.direct_x0 and self.cache is not None and self.cache.k > 0:
+            self._call("fgl_gather_rows_cached", self.feats.data_ptr(), self.ldf, self.d0,
+                       s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
+                       self.cache.slot.data_ptr(), self.cache.table.data_ptr(), self.ldf,
+                       x0.data_ptr(), self.ldf, self.loaded.data_ptr(), self.cache_hits.data_ptr(), st)
+        elif not self.direct_x0:
             self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0,
                        s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
                        x0.data_ptr(), self.ldf, self.loaded.data_ptr(), st)
@@ -514,7 +567,8 @@ class Pipeline:
 
 
 def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None, *,
-          train_ids=None, val_ids=None, cost_params=None, feature_store="device") -> TrainReport:
+          train_ids=None, val_ids=None, cost_params=None, feature_store="device",
+          cache_ratio: float = 0.0, cache_policy: str = "static-degree") -> TrainReport:
     """Drop-in for trainer.train (trainer.py:246-349): same batch stream, same
     schedule, per-batch SGD; loss/accuracy per epoch; IO accounting from the
     loader's real row counts."""
@@ -541,7 +595,10 @@ def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None
     val_ids = np.asarray(val_ids, dtype=np.uint64)
     if train_ids.size == 0:
         raise ValidationError("training split is empty")
-    pipe = Pipeline(g, feats, labels_np, cfg, flags, feature_store=feature_store)
+    if cache_ratio > 0.0:
+        feature_store = "host"  # the cache fronts the host-resident store (memsim.py:129-186)
+    pipe = Pipeline(g, feats, labels_np, cfg, flags, feature_store=feature_store, cache_ratio=cache_ratio,
+                    cache_policy=cache_policy)
     seed_batches = make_epoch_batches(g, train_ids, cfg.batch_size, derive_seed(cfg.seed, 11))
     windows = [seed_batches[i : i + cfg.window_n] for i in range(0, len(seed_batches), cfg.window_n)]
     report = TrainReport(config=cfg, flags=flags)
@@ -549,6 +606,7 @@ def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None
     for _ in range(cfg.epochs):
         phase = dict.fromkeys(PHASES, 0.0)
         pipe.loaded.zero_()
+        pipe.cache_hits.zero_()
         loss_sum, seen, base, total_rows = 0.0, 0, 0, 0
         for win_seeds in windows:
             rs = [derive_seed(cfg.seed, 13, base + j) for j in range(len(win_seeds))]
@@ -561,7 +619,12 @@ def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None
             win = pipe.last_window
             total_rows += win.unique_total()
         loaded = int(pipe.loaded.item())
-        if flags.match:
+        hits = int(pipe.cache_hits.item())
+        if pipe.cache is not None and pipe.cache.k > 0:
+            # real counts: rows over the host link, rows from the HBM cache, rest Match
+            traffic = {"bytes_host_to_device": loaded * 4 * d, "bytes_served_by_cache": hits * 4 * d,
+                       "bytes_served_by_match": (total_rows - loaded - hits) * 4 * d}
+        elif flags.match:
             traffic = {"bytes_host_to_device": loaded * 4 * d,
                        "bytes_served_by_match": (total_rows - loaded) * 4 * d,
                        "bytes_served_by_cache": 0}

@@ -164,6 +164,21 @@ def test_schedule_windows(golden, golden_meta):
         assert list(got) == io[f"{match}_0.0"]
 
 
+def test_static_cache_io(golden, golden_meta, powerlaw_10k):
+    """Static-degree cache ratio 0.1 (memsim.py:110-186) on window 0 of the
+    schedule fixture: host-link / Match / cache bytes equal the reference's."""
+    st = golden("schedule")
+    sets = [st[f"w0_b{j}"] for j in range(6)]
+    _, ex, loads, _ = oracle.window_schedule(sets, True, 32)
+    deg = np.diff(powerlaw_10k.row_offsets.astype(np.int64))
+    mask = oracle.cache_mask(powerlaw_10k.num_nodes, 0.1, deg)
+    assert mask.sum() == 1000
+    io = golden_meta["schedule"]["io"]
+    for match in (True, False):
+        got = oracle.epoch_h2d_bytes([ex], [loads], 32, match=match, cached=mask)
+        assert list(got) == io[f"{match}_0.1"]
+
+
 @pytest.mark.parametrize("name", ["gcn", "gin", "gcn_noreorder", "gcn3"])
 def test_train_trajectory(golden_meta, name):
     g, x, labels = oracle.two_cluster_task(200, 16, 0)
