@@ -133,6 +133,21 @@ int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, vo
  * fgl_profile_select_read synchronises on them, writes up to `cap` per-launch
  * device milliseconds (launch order: hop 0..H-1 of each window) and the
  * launch count, then clears the record. */
+/* Random-walk sampler, drop-in for sampler.sample_random_walk
+ * (sampler.py:142-186), bit-exact against the reference's Philox(seed) stream
+ * (key0, key1 = SeedSequence(seed).generate_state(2)).  One walk of `length`
+ * steps per seed; sinks stop early.  Edges (tgt, src, wgt) are step-major,
+ * seed order within a step; step_off[0..length] are the step offsets
+ * (step_off[length] = edges).  unique_nodes = sorted unique of seeds and
+ * every visited node; counts[0] = its size, counts[1] = status (0 or an
+ * FGL_E_* code written by the device).  Asynchronous on `stream`.
+ * Replaces sampler.py:142-186 (the reference's pure-numpy walk). */
+int64_t fgl_walk_ws_bytes(int64_t num_nodes, int64_t num_seeds);
+int fgl_sample_walk(const fgl_graph* g, const int32_t* seeds, int64_t num_seeds, int32_t length, uint64_t key0,
+                    uint64_t key1, int32_t* tgt, int32_t* src, float* wgt, int64_t edge_cap, int64_t* step_off,
+                    int32_t* unique_nodes, int64_t unique_cap, int64_t* counts, void* ws, int64_t ws_bytes,
+                    void* stream);
+
 int fgl_profile_select(int32_t enable);
 int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches);
 

@@ -22,7 +22,7 @@ FIB = np.uint64(0x9E3779B97F4A7C15)
 
 __all__ = [
     "SENTINEL", "CSRGraph", "graph_from_edges", "gen_power_law", "derive_seed",
-    "Batch", "sample_khop", "epoch_seed_batches", "IdTable", "idmap_build",
+    "Batch", "sample_khop", "sample_random_walk", "epoch_seed_batches", "IdTable", "idmap_build",
     "idmap_lookup", "layer_edge_weights", "edges_to_csr", "csr_transpose",
     "prepare_batch", "tile_plan_error", "aggregate", "dense", "softmax_xent",
     "init_params", "forward", "backward", "sgd_step", "match_matrix",
@@ -176,6 +176,49 @@ def sample_khop(g: CSRGraph, seeds, fanouts, seed: int) -> Batch:
         seen += [tgt, src]
         frontier = np.unique(src)
     return Batch(seeds=seeds, layers=layers, unique_nodes=np.unique(np.concatenate(seen)),
+                 draws=pos)
+
+
+def sample_random_walk(g: CSRGraph, seeds, length: int, seed: int) -> Batch:
+    """Uniform random walk (``sampler.py:142-186``): at each step the alive
+    walkers whose node has out-degree > 0, in seed order, take consecutive
+    draws u of the Philox(seed) stream and move to
+    col[off[v] + floor(u * deg)] (float64 product, truncation); a sink ends
+    its walk without a draw.  Edges step-major; unique over seeds, targets and
+    sources."""
+    seeds = np.asarray(seeds, dtype=U64)
+    if seeds.size == 0 or int(seeds.max()) >= g.num_nodes:
+        raise ValueError("bad seeds")
+    if length < 1:
+        raise ValueError("walk length must be >= 1")
+    key = philox.key_for_seed(seed)
+    off = g.row_offsets.astype(np.int64)
+    cur = seeds.astype(np.int64).copy()
+    alive = np.ones(len(seeds), dtype=bool)
+    pos = 0
+    ts, ss, ws = [], [], []
+    for _ in range(length):
+        idx = np.flatnonzero(alive)
+        if idx.size == 0:
+            break
+        deg = off[cur[idx] + 1] - off[cur[idx]]
+        alive[idx[deg == 0]] = False
+        idx = idx[deg > 0]
+        deg = deg[deg > 0]
+        if idx.size == 0:
+            break
+        u = philox.keys53(key, pos, len(idx)).astype(np.float64) * 2.0 ** -53
+        pos += len(idx)
+        edge = off[cur[idx]] + (u * deg).astype(np.int64)
+        nxt = g.col_indices[edge].astype(np.int64)
+        ts.append(cur[idx].astype(U64))
+        ss.append(nxt.astype(U64))
+        ws.append(g.edge_weights[edge] if g.edge_weights is not None else np.ones(len(idx), dtype=np.float32))
+        cur[idx] = nxt
+    t = np.concatenate(ts) if ts else np.empty(0, dtype=U64)
+    s = np.concatenate(ss) if ss else np.empty(0, dtype=U64)
+    w = np.concatenate(ws) if ws else np.empty(0, dtype=np.float32)
+    return Batch(seeds=seeds, layers=[(t, s, w)], unique_nodes=np.unique(np.concatenate([seeds, t, s])),
                  draws=pos)
 
 

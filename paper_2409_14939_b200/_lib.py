@@ -62,6 +62,9 @@ SIGNATURES = {
     "fgl_philox_words": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
     "fgl_profile_select": (C.c_int, [C.c_int32]),
+    "fgl_walk_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
+    "fgl_sample_walk": (C.c_int, [C.POINTER(FglGraph), vp, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, vp, vp, vp, C.c_int64,
+                                  vp, vp, C.c_int64, vp, vp, C.c_int64, vp]),
     "fgl_profile_select_read": (C.c_int, [vp, C.c_int64, vp]),
     "fgl_csr_offsets_sorted": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_stable_group_ws_bytes": (C.c_int64, [C.c_int64]),

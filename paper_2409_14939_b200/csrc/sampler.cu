@@ -996,6 +996,78 @@ __global__ void translate_seeds_kernel(const int32_t* __restrict__ seeds,
   }
 }
 
+// ----------------------------------------------------------- random walk --
+// sampler.sample_random_walk (sampler.py:142-186): one uniform walk of
+// `length` steps per seed, one Philox stream for the batch.  At each step the
+// walkers still alive whose node has out-degree > 0, in seed order, consume
+// consecutive draws u (random() doubles = word >> 11 scaled by 2^-53) and step
+// to col[off[v] + floor(u * deg)] (an IEEE double multiply then truncation,
+// exactly numpy's (rng.random(n) * deg).astype(int64)); sinks stop their walk
+// without a draw.  Edges are emitted step-major, seed order within a step.
+// One CTA per batch: the per-step ranks of the stepping walkers come from a
+// block-wide scan, so the whole walk is a single launch with no host sync;
+// every visited node is marked in a bitmap whose compaction is the sorted
+// unique_nodes.
+constexpr int kWalkThreads = 1024;
+
+__global__ void __launch_bounds__(kWalkThreads) walk_kernel(const int64_t* __restrict__ off,
+                                                            const int32_t* __restrict__ col,
+                                                            const float* __restrict__ ew,
+                                                            const int32_t* __restrict__ seeds, int64_t n,
+                                                            int length, uint64_t k0, uint64_t k1,
+                                                            int64_t num_nodes, int32_t* __restrict__ cur,
+                                                            int32_t* __restrict__ tgt, int32_t* __restrict__ src,
+                                                            float* __restrict__ wgt,
+                                                            int64_t* __restrict__ step_off,
+                                                            uint32_t* __restrict__ bm, int64_t* status) {
+  __shared__ int64_t sm[33];
+  const int tid = threadIdx.x;
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    const int32_t sd = seeds[i];
+    if (sd < 0 || sd >= num_nodes) { set_status(status, FGL_E_INVALID); cur[i] = -1; continue; }
+    cur[i] = sd;
+    atomicOr(bm + (sd >> 5), 1u << (sd & 31));
+  }
+  __syncthreads();
+  if (tid == 0) step_off[0] = 0;
+  int64_t pos = 0;  // Philox stream position = edges emitted so far
+  for (int step = 0; step < length; ++step) {
+    int64_t running = 0;
+    for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
+      const int64_t i = c0 + tid;
+      const int32_t u = i < n ? cur[i] : -1;
+      int64_t e0 = 0, d = 0;
+      if (u >= 0) {
+        e0 = __ldg(off + u);
+        d = __ldg(off + u + 1) - e0;
+        if (d == 0) cur[i] = -1;  // sink: the walk stops, no draw
+      }
+      const int64_t flag = (u >= 0 && d > 0) ? 1 : 0;
+      int64_t tot;
+      const int64_t rank = running + block_excl_scan<int64_t>(flag, sm, &tot);
+      if (flag) {
+        const int64_t p = pos + rank;
+        uint64_t w[4];
+        philox4x64_10((uint64_t)(p >> 2) + 1, k0, k1, w[0], w[1], w[2], w[3]);
+        const uint64_t word = w[p & 3];
+        const double r = (double)(word >> 11) * 0x1.0p-53;
+        const int64_t pick = (int64_t)__dmul_rn(r, (double)d);
+        const int64_t e = e0 + pick;
+        const int32_t nxt = __ldg(col + e);
+        tgt[p] = u;
+        src[p] = nxt;
+        wgt[p] = ew ? __ldg(ew + e) : 1.0f;
+        cur[i] = nxt;
+        atomicOr(bm + (nxt >> 5), 1u << (nxt & 31));
+      }
+      running += tot;
+    }
+    pos += running;
+    if (tid == 0) step_off[step + 1] = pos;
+    __syncthreads();
+  }
+}
+
 // measurement hook (fgl_profile_select): events around select launches
 std::mutex g_sel_mu;
 bool g_sel_prof = false;
@@ -1244,6 +1316,57 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     }
     FGL_LAUNCH_CHECK("translate");
   }
+  return FGL_OK;
+}
+
+
+int64_t fgl_walk_ws_bytes(int64_t num_nodes, int64_t num_seeds) {
+  const int64_t words = align_up(ceil_div(num_nodes, 32), 4);
+  return align_up(4 * words, 256) + align_up(4 * std::max<int64_t>(num_seeds, 1), 256) +
+         align_up(8 * (2 * kPersistentCTAs + 2), 256) + 256;
+}
+
+int fgl_sample_walk(const fgl_graph* g, const int32_t* seeds, int64_t num_seeds, int32_t length, uint64_t key0,
+                    uint64_t key1, int32_t* tgt, int32_t* src, float* wgt, int64_t edge_cap, int64_t* step_off,
+                    int32_t* unique_nodes, int64_t unique_cap, int64_t* counts, void* ws, int64_t ws_bytes,
+                    void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!g || !seeds || num_seeds < 1 || length < 1 || !tgt || !src || !wgt || !step_off || !unique_nodes ||
+      !counts || !ws) {
+    set_error("fgl_sample_walk: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (edge_cap < num_seeds * (int64_t)length) {
+    set_error("fgl_sample_walk: edge buffer below num_seeds * length");
+    return FGL_E_CAPACITY;
+  }
+  if (ws_bytes < fgl_walk_ws_bytes(g->num_nodes, num_seeds)) {
+    set_error("fgl_sample_walk: workspace too small");
+    return FGL_E_CAPACITY;
+  }
+  const int64_t words = align_up(ceil_div(g->num_nodes, 32), 4);
+  char* p = static_cast<char*>(ws);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(p);
+  p += align_up(4 * words, 256);
+  int32_t* cur = reinterpret_cast<int32_t*>(p);
+  p += align_up(4 * std::max<int64_t>(num_seeds, 1), 256);
+  int64_t* part = reinterpret_cast<int64_t*>(p);
+  p += align_up(8 * (2 * kPersistentCTAs + 2), 256);
+  int64_t* scal = reinterpret_cast<int64_t*>(p);
+  // counts: [0] unique total, [1] status
+  FGL_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), stream));
+  FGL_CUDA(cudaMemsetAsync(bm, 0, 4 * words, stream));
+  FGL_COUNT_LAUNCH(), walk_kernel<<<1, kWalkThreads, 0, stream>>>(
+      g->row_offsets, g->col_indices, g->edge_weights, seeds, num_seeds, length, key0, key1, g->num_nodes, cur,
+      tgt, src, wgt, step_off, bm, counts + 1);
+  FGL_LAUNCH_CHECK("walk_kernel");
+  const int G = kPersistentCTAs;
+  FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(bm, words, part);
+  FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(part, G, scal, counts);
+  FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(bm, words, words, part, unique_nodes, nullptr,
+                                                                       nullptr, nullptr, nullptr, 0, unique_cap,
+                                                                       counts + 1);
+  FGL_LAUNCH_CHECK("walk unique compaction");
   return FGL_OK;
 }
 

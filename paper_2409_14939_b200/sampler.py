@@ -19,8 +19,8 @@ from . import _lib
 from .errors import ValidationError
 from .graph import device_graph
 
-__all__ = ["Fanouts", "SubgraphBatch", "sample_khop", "make_epoch_batches", "philox_key",
-           "derive_seed", "WindowSampler", "DeviceWindow"]
+__all__ = ["Fanouts", "SubgraphBatch", "sample_khop", "sample_random_walk", "make_epoch_batches",
+           "philox_key", "derive_seed", "WindowSampler", "DeviceWindow", "WalkSampler"]
 
 
 def derive_seed(base: int, *parts: int) -> int:
@@ -300,6 +300,73 @@ def sample_khop(g, seeds, fanouts, seed: int) -> SubgraphBatch:
     b.local_layers = []
     b.num_local = 0
     return b
+
+
+class WalkSampler:
+    """Device random-walk sampler (fgl_sample_walk) for batches of up to
+    ``max_seeds`` seeds and walks of ``length`` steps; buffers are allocated
+    once and results stay in HBM until the next call."""
+
+    def __init__(self, dgraph, max_seeds: int, length: int, device="cuda"):
+        import torch
+        if length < 1:
+            raise ValidationError("walk length must be >= 1")
+        self.torch, self.g, self.length, self.max_seeds = torch, dgraph, int(length), int(max_seeds)
+        e = self.max_seeds * self.length
+        i32 = dict(dtype=torch.int32, device=device)
+        self.tgt, self.src = torch.empty(e, **i32), torch.empty(e, **i32)
+        self.wgt = torch.empty(e, dtype=torch.float32, device=device)
+        self.step_off = torch.empty(self.length + 1, dtype=torch.int64, device=device)
+        self.ucap = min(int(dgraph.num_nodes), self.max_seeds * (self.length + 1))
+        self.unique = torch.empty(max(self.ucap, 1), **i32)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=device)
+        self.seeds_dev = torch.empty(self.max_seeds, **i32)
+        wsb = _lib.lib().fgl_walk_ws_bytes(dgraph.num_nodes, self.max_seeds)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+
+    def run(self, seeds: np.ndarray, seed: int, stream=None):
+        torch = self.torch
+        n = len(seeds)
+        if n > self.max_seeds:
+            raise ValidationError("batch exceeds max_seeds")
+        self.seeds_dev[:n].copy_(torch.from_numpy(np.asarray(seeds).astype(np.int32)))
+        k0, k1 = philox_key(seed)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        _lib.call("fgl_sample_walk", self.g.struct, self.seeds_dev.data_ptr(), n, self.length, k0, k1,
+                  self.tgt.data_ptr(), self.src.data_ptr(), self.wgt.data_ptr(), self.tgt.numel(),
+                  self.step_off.data_ptr(), self.unique.data_ptr(), self.ucap, self.counts.data_ptr(),
+                  self.ws.data_ptr(), self.ws.numel(), st)
+
+    def to_batch(self, seeds: np.ndarray) -> SubgraphBatch:
+        c = self.counts.cpu().numpy()
+        _lib.status_error(int(c[1]), "fgl_sample_walk")
+        ne = int(self.step_off[self.length].item())
+        t = self.tgt[:ne].cpu().numpy().astype(np.uint64)
+        s = self.src[:ne].cpu().numpy().astype(np.uint64)
+        w = self.wgt[:ne].cpu().numpy()
+        u = self.unique[: int(c[0])].cpu().numpy().astype(np.uint64)
+        return SubgraphBatch(seeds=seeds, layers=[(t, s, w)], unique_nodes=u)
+
+
+_WALKERS: dict = {}
+
+
+def sample_random_walk(g, seeds, length: int, seed: int) -> SubgraphBatch:
+    """One uniform random walk of ``length`` steps per seed; sinks stop early.
+
+    Drop-in for sampler.py:142-186 (bit-exact, Philox(seed) stream): the walk
+    runs as one GPU launch (fgl_sample_walk)."""
+    seeds = _validate_seeds(g.num_nodes, seeds)
+    if length < 1:
+        raise ValidationError("walk length must be >= 1")
+    dg = device_graph(g)
+    key = (id(dg), int(length))
+    ws = _WALKERS.get(key)
+    if ws is None or ws.max_seeds < len(seeds):
+        ws = WalkSampler(dg, max(len(seeds), 1024), length)
+        _WALKERS[key] = ws
+    ws.run(seeds, seed)
+    return ws.to_batch(seeds)
 
 
 def make_epoch_batches(g, train_ids, batch_size: int, shuffle_seed: int):

@@ -309,7 +309,26 @@ def train_fixture():
     return out
 
 
+def walk_fixture():
+    """Random walks (sampler.py:142-186) on the 10K power-law graph: varied
+    seed counts (incl. duplicates), lengths and stream seeds."""
+    g = graph.generate(graph.GraphGenSpec("power-law", 10_000, avg_degree=16, seed=7))
+    rng = np.random.default_rng(31)
+    store = {}
+    cases = [(1, 1), (5, 3), (64, 4), (700, 2), (2000, 6), (3000, 1)]
+    for c, (n, length) in enumerate(cases):
+        seeds = rng.integers(0, 10_000, size=n).astype(np.uint64)
+        s = int(rng.integers(0, 2**62))
+        b = sampler.sample_random_walk(g, seeds, length, s)
+        t, src, w = b.layers[0]
+        store.update({f"c{c}_seeds": seeds, f"c{c}_len": np.int64(length), f"c{c}_seed": np.uint64(s),
+                      f"c{c}_t": t, f"c{c}_s": src, f"c{c}_w": w, f"c{c}_u": b.unique_nodes})
+    store["ncases"] = np.int64(len(cases))
+    np.savez_compressed(OUT / "walk.npz", **store)
+
+
 def main():
+    walk_fixture()
     philox_fixture()
     meta, g10k = sampler_fixture()
     meta["idmap_traces"] = idmap_fixture()
@@ -322,4 +341,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "walk":
+        walk_fixture()  # regenerate only the random-walk fixture
+    else:
+        main()

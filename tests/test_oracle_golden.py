@@ -195,3 +195,14 @@ def test_train_trajectory(golden_meta, name):
     assert [r["accuracy"] for r in rep] == want["accuracy"]
     assert [r["bytes_h2d"] for r in rep] == want["bytes_h2d"]
     assert [r["bytes_match"] for r in rep] == want["bytes_match"]
+
+
+def test_random_walk_golden(golden, powerlaw_10k):
+    """oracle.sample_random_walk == the reference's sample_random_walk
+    (sampler.py:142-186) on the golden walk cases (incl. duplicate seeds)."""
+    st = golden("walk")
+    for c in range(int(st["ncases"])):
+        b = oracle.sample_random_walk(powerlaw_10k, st[f"c{c}_seeds"], int(st[f"c{c}_len"]), int(st[f"c{c}_seed"]))
+        t, s, w = b.layers[0]
+        assert np.array_equal(t, st[f"c{c}_t"]) and np.array_equal(s, st[f"c{c}_s"])
+        assert np.array_equal(w, st[f"c{c}_w"]) and np.array_equal(b.unique_nodes, st[f"c{c}_u"])
