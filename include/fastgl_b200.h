@@ -128,11 +128,6 @@ int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uin
                      void* stream);
 /* Draws `count` Philox blocks and reduces them to one word (ALU roofline probe). */
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream);
-/* Measurement hook (bench.py roofline): while enabled, fgl_sample_window
- * brackets every select-kernel launch with CUDA events on its stream;
- * fgl_profile_select_read synchronises on them, writes up to `cap` per-launch
- * device milliseconds (launch order: hop 0..H-1 of each window) and the
- * launch count, then clears the record. */
 /* Random-walk sampler, drop-in for sampler.sample_random_walk
  * (sampler.py:142-186), bit-exact against the reference's Philox(seed) stream
  * (key0, key1 = SeedSequence(seed).generate_state(2)).  One walk of `length`
@@ -148,6 +143,11 @@ int fgl_sample_walk(const fgl_graph* g, const int32_t* seeds, int64_t num_seeds,
                     int32_t* unique_nodes, int64_t unique_cap, int64_t* counts, void* ws, int64_t ws_bytes,
                     void* stream);
 
+/* Measurement hook (bench.py roofline): while enabled, fgl_sample_window
+ * brackets every select-kernel launch with CUDA events on its stream;
+ * fgl_profile_select_read synchronises on them, writes up to `cap` per-launch
+ * device milliseconds (launch order: hop 0..H-1 of each window) and the
+ * launch count, then clears the record. */
 int fgl_profile_select(int32_t enable);
 int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches);
 

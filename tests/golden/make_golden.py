@@ -327,7 +327,35 @@ def walk_fixture():
     np.savez_compressed(OUT / "walk.npz", **store)
 
 
+def graph_io_fixture():
+    """graph.from_edges (graph.py:151-183) on edge lists with duplicates and
+    self loops (weighted / unweighted), and an MGL1 file written by
+    graph.save_binary (graph.py:293-307)."""
+    rng = np.random.default_rng(41)
+    store = {}
+    cases = [(50, 400, False), (300, 3000, True), (1000, 20000, False), (7, 0, False)]
+    for c, (n, m, weighted) in enumerate(cases):
+        src = rng.integers(0, n, size=m).astype(np.uint64)
+        dst = rng.integers(0, n, size=m).astype(np.uint64)
+        if m:
+            src[: m // 10] = src[m // 10 : 2 * (m // 10)]   # exact duplicate pairs
+            dst[: m // 10] = dst[m // 10 : 2 * (m // 10)]
+            dst[2 * (m // 10) : 2 * (m // 10) + 5] = src[2 * (m // 10) : 2 * (m // 10) + 5]  # self loops
+        w = rng.standard_normal(m).astype(np.float32) if weighted else None
+        g = graph.from_edges(n, src, dst, w)
+        store.update({f"c{c}_n": np.int64(n), f"c{c}_src": src, f"c{c}_dst": dst,
+                      f"c{c}_ro": g.row_offsets, f"c{c}_ci": g.col_indices, f"c{c}_tro": g.t_row_offsets,
+                      f"c{c}_tci": g.t_col_indices})
+        if weighted:
+            store.update({f"c{c}_w": w, f"c{c}_ew": g.edge_weights, f"c{c}_tew": g.t_edge_weights})
+    store["ncases"] = np.int64(len(cases))
+    np.savez_compressed(OUT / "graph_io.npz", **store)
+    g = graph.from_edges(300, store["c1_src"], store["c1_dst"], store["c1_w"])
+    graph.save_binary(g, OUT / "small_weighted.mgl1")
+
+
 def main():
+    graph_io_fixture()
     walk_fixture()
     philox_fixture()
     meta, g10k = sampler_fixture()
@@ -343,5 +371,7 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "walk":
         walk_fixture()  # regenerate only the random-walk fixture
+    elif len(sys.argv) > 1 and sys.argv[1] == "graph_io":
+        graph_io_fixture()
     else:
         main()
