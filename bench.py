@@ -45,6 +45,11 @@ CONFIGS = {
              "602-d features in HBM, GCN (602,64,64,41), fanouts [15,10,5], batch 1024, window 8",
         nodes=233_000, edges=114_600_000, exponent=4.0, dims=(602, 64, 64, 41),
         fanouts=[15, 10, 5], bs=1024, window=8, arch="gcn", store="device"),
+    "products_sage": dict(
+        desc="products-shaped graph (BASELINE config 3 model), GraphSAGE-mean (1/indeg aggregation + root "
+             "term, shared weight; SURVEY 8(c) extension) (100,64,64,47), fanouts [15,10,5], batch 1024, window 8",
+        nodes=2_450_000, edges=61_900_000, exponent=3.0, dims=(100, 64, 64, 47),
+        fanouts=[15, 10, 5], bs=1024, window=8, arch="sage", store="device"),
     "gin": dict(
         desc="products-shaped graph, GIN 3-layer (100,64,64,47), fanouts [15,10,5], batch 1024, window 8",
         nodes=2_450_000, edges=61_900_000, exponent=3.0, dims=(100, 64, 64, 47),

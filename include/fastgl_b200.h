@@ -173,8 +173,9 @@ int fgl_gather_i32_f32(const int32_t* perm, int64_t n, const int32_t* a, const f
 /* One model layer's block CSR (trainer._prepare_batch, trainer.py:165-179):
  * lt (non-decreasing, in [0,num_rows)) / ls (in [0,num_cols)) are the hop's
  * edge endpoints in the layer's row / column index spaces.  Outputs:
- * indptr[num_rows+1], w[nnz] (GCN 1/sqrt(indeg*outdeg) in fp64 -> f32,
- * trainer.py:156-162, or 1.0 when arch_gcn == 0), and the stable transpose
+ * indptr[num_rows+1], w[nnz] (arch_gcn == 1: GCN 1/sqrt(indeg*outdeg) in fp64
+ * -> f32, trainer.py:156-162; 0: GIN 1.0; 2: SAGE mean 1/indeg in fp64 -> f32,
+ * the GraphSAGE extension of SURVEY 8(c)), and the stable transpose
  * t_indptr[num_cols+1], t_col[nnz] (= lt), t_w[nnz] (compute.py:233-239). */
 int64_t fgl_prepare_layer_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_cols);
 int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,

@@ -308,9 +308,15 @@ def idmap_lookup(t: IdTable, ids) -> np.ndarray:
 
 def layer_edge_weights(arch, lt, ls, n):
     """GCN 1/sqrt(indeg_t * outdeg_s) over per-hop local degrees, fp64 -> f32;
-    GIN unit weights (``trainer.py:156-162``)."""
+    GIN unit weights (``trainer.py:156-162``).  "sage" (EXTENSION, SURVEY
+    8(c): the reference has no GraphSAGE; oracle = this restatement): mean
+    aggregation 1/indeg_t in fp64 -> f32, with the GIN-style root term added
+    in forward / backward."""
     if arch == "gin":
         return np.ones(len(lt), dtype=np.float32)
+    if arch == "sage":
+        indeg = np.bincount(lt, minlength=n).astype(np.int64)
+        return (1.0 / indeg[lt].astype(np.float64)).astype(np.float32)
     indeg = np.bincount(lt, minlength=n).astype(np.int64)
     outdeg = np.bincount(ls, minlength=n).astype(np.int64)
     prod = (indeg[lt] * outdeg[ls]).astype(np.float64)
@@ -426,7 +432,7 @@ def forward(x0, csr, params, arch="gcn"):
     last = len(params) - 1
     for i, ((ip, ix, cw, *_), (w, b)) in enumerate(zip(csr, params)):
         h = aggregate(ip, ix, cw, x)
-        if arch == "gin":
+        if arch in ("gin", "sage"):  # root / self term
             h = h + x
         z = dense(h, w, b)
         caches.append((x, h, z))
@@ -445,7 +451,7 @@ def backward(dout, caches, csr, params, arch="gcn"):
         grads[i] = [h.T @ dz, dz.sum(axis=0)]
         dh = dz @ params[i][0].T
         dx = aggregate(*csr[i][3:6], dh)
-        if arch == "gin":
+        if arch in ("gin", "sage"):
             dx = dx + dh
     return grads
 

@@ -258,9 +258,13 @@ __global__ void layer_weights_kernel(const int32_t* __restrict__ lt, const int32
                                      float* __restrict__ w) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (!gcn) { w[e] = 1.0f; continue; }
+    if (gcn == 0) { w[e] = 1.0f; continue; }  // GIN
     const int32_t t = lt[e];
     const int64_t indeg = indptr[t + 1] - indptr[t];
+    if (gcn == 2) {  // SAGE mean: f32(1 / indeg) from fp64
+      w[e] = __double2float_rn(__ddiv_rn(1.0, (double)indeg));
+      continue;
+    }
     w[e] = gcn_weight(indeg, outdeg[ls[e]]);
   }
 }

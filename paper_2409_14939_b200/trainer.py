@@ -61,7 +61,7 @@ class ModelConfig:
         if not isinstance(self.fanouts, Fanouts):
             self.fanouts = Fanouts(self.fanouts)
         self.layer_dims = tuple(int(d) for d in self.layer_dims)
-        if self.arch not in ("gcn", "gin"):
+        if self.arch not in ("gcn", "gin", "sage"):
             raise ValidationError(f"unknown arch {self.arch!r}")
         if len(self.layer_dims) < 2 or any(d < 1 for d in self.layer_dims):
             raise ValidationError("layer_dims needs input dim, optional hiddens, and classes")
@@ -371,7 +371,7 @@ class Pipeline:
             wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
             pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
             self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
-                       cols, 1 if self.cfg.arch == "gcn" else 0, lay["indptr"].data_ptr(),
+                       cols, {"gin": 0, "gcn": 1, "sage": 2}[self.cfg.arch], lay["indptr"].data_ptr(),
                        lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
                        lay["t_w"].data_ptr(), pws.data_ptr(), wsb, self.stream)
             layers[self.H - 1 - h] = lay

@@ -206,3 +206,19 @@ def test_random_walk_golden(golden, powerlaw_10k):
         t, s, w = b.layers[0]
         assert np.array_equal(t, st[f"c{c}_t"]) and np.array_equal(s, st[f"c{c}_s"])
         assert np.array_equal(w, st[f"c{c}_w"]) and np.array_equal(b.unique_nodes, st[f"c{c}_u"])
+
+
+def test_sage_extension_restatement():
+    """GraphSAGE-mean is an extension (the reference has none):
+    its edge weights are 1/indeg in fp64 -> f32 and each layer adds the root
+    term, i.e. h = mean_{u in N(v)} x_u + x_v before the dense transform."""
+    lt = np.array([0, 0, 0, 1, 2, 2])
+    ls = np.array([1, 2, 3, 0, 0, 3])
+    w = oracle.layer_edge_weights("sage", lt, ls, 4)
+    assert w.dtype == np.float32
+    assert np.array_equal(w, np.array([1 / 3, 1 / 3, 1 / 3, 1, 0.5, 0.5], dtype=np.float32))
+    ip, ix, cw, *_ = oracle.edges_to_csr(4, lt, ls, w) + (None,) * 0
+    x = np.arange(8, dtype=np.float32).reshape(4, 2)
+    h = oracle.aggregate(ip, ix, cw, x) + x
+    want_row0 = (x[1] * np.float32(1 / 3) + x[2] * np.float32(1 / 3)) + x[3] * np.float32(1 / 3) + x[0]
+    np.testing.assert_allclose(h[0], want_row0, rtol=1e-6)
