@@ -183,6 +183,37 @@ int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t
                       int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
                       void* stream);
 
+/* ------------------------------------------------------- fused layers ---- */
+/* Upper model layers 1..L-1 of a COMPACT GCN batch (rows of layer i = hop
+ * H-1-i frontier), trained by ONE persistent kernel (trainer.py:182-228 for
+ * those layers): forward aggregation (bit-identical to fgl_spmm) + dense,
+ * fp64 softmax cross entropy (same as fgl_softmax_xent), dense backward,
+ * transposed aggregation, deterministic dW/db reductions.  Layer k of the
+ * struct is model layer k+1.  indptr / t_indptr point at the batch's first
+ * row (absolute edge offsets); col / t_col values minus col_base / t_base
+ * index the input / output rows.  X1 = layer-0 output (input of layer 1);
+ * dX1 receives its gradient, or is NULL: then the layer-1 -> layer-0
+ * transposed aggregation is left to the caller (fgl_spmm on dH of layer 1). */
+typedef struct fgl_upper_layer {
+  const int64_t* indptr; const int32_t* col; int64_t col_base; const float* w; int64_t rows;
+  const int64_t* t_indptr; const int32_t* t_col; int64_t t_base; const float* t_w; int64_t prev_rows;
+  int32_t din, dout;
+  const float* W; const float* b; float* dW; float* db;
+  float* H; int64_t ldh; float* Y; int64_t ldy; float* dH; float* dY;
+} fgl_upper_layer;
+
+typedef struct fgl_upper_args {
+  int32_t num_upper;
+  fgl_upper_layer layer[3];
+  const float* X1; int64_t ldx1; float* dX1;
+  const int32_t* seed_rows; int64_t seed_row_base; const int32_t* seed_ids; const int64_t* labels;
+  int64_t num_seeds; int32_t num_classes;
+  double* loss_sum;
+} fgl_upper_args;
+
+int64_t fgl_upper_ws_bytes(const fgl_upper_args* a);
+int fgl_upper_layers(const fgl_upper_args* a, void* ws, int64_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------- compute ---- */
 /* Memory-Aware CSR aggregation (compute.py:115-195):
  * Y[r] = sum_{e in [indptr[r], indptr[r+1])} w[e] * X[col[e] - col_base]

@@ -49,6 +49,25 @@ class FglSampleOut(C.Structure):
     ]
 
 
+class FglUpperLayer(C.Structure):
+    _fields_ = [
+        ("indptr", vp), ("col", vp), ("col_base", C.c_int64), ("w", vp), ("rows", C.c_int64),
+        ("t_indptr", vp), ("t_col", vp), ("t_base", C.c_int64), ("t_w", vp), ("prev_rows", C.c_int64),
+        ("din", C.c_int32), ("dout", C.c_int32),
+        ("W", vp), ("b", vp), ("dW", vp), ("db", vp),
+        ("H", vp), ("ldh", C.c_int64), ("Y", vp), ("ldy", C.c_int64), ("dH", vp), ("dY", vp),
+    ]
+
+
+class FglUpperArgs(C.Structure):
+    _fields_ = [
+        ("num_upper", C.c_int32), ("layer", FglUpperLayer * 3),
+        ("X1", vp), ("ldx1", C.c_int64), ("dX1", vp),
+        ("seed_rows", vp), ("seed_row_base", C.c_int64), ("seed_ids", vp), ("labels", vp),
+        ("num_seeds", C.c_int64), ("num_classes", C.c_int32), ("loss_sum", vp),
+    ]
+
+
 # name -> (restype, argtypes); every entry is declared in include/fastgl_b200.h
 SIGNATURES = {
     "fgl_last_error": (C.c_char_p, []),
@@ -62,6 +81,8 @@ SIGNATURES = {
     "fgl_philox_words": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
     "fgl_profile_select": (C.c_int, [C.c_int32]),
+    "fgl_upper_ws_bytes": (C.c_int64, [C.POINTER(FglUpperArgs)]),
+    "fgl_upper_layers": (C.c_int, [C.POINTER(FglUpperArgs), vp, C.c_int64, vp]),
     "fgl_walk_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
     "fgl_sample_walk": (C.c_int, [C.POINTER(FglGraph), vp, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, vp, vp, vp, C.c_int64,
                                   vp, vp, C.c_int64, vp, vp, C.c_int64, vp]),

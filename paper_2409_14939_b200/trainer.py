@@ -302,6 +302,7 @@ class Pipeline:
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
         self.gpu_launches = 0
+        self.fused_upper = self._fused_upper_ok()
 
     # ------------------------------------------------------------ buffers --
     def _buf(self, name, rows, cols, dtype=None):
@@ -426,7 +427,7 @@ class Pipeline:
         # forward
         X, ldx = x0, self.ldf
         H_bufs, Y_bufs, ns = [], [], []
-        for i in range(self.L):
+        for i in range(1 if self.fused_upper else self.L):
             din, dout = dims[i], dims[i + 1]
             r0, r1 = self._rows(win, i, b)
             n = r1 - r0
@@ -445,8 +446,11 @@ class Pipeline:
             Y_bufs.append(Yb)
             ns.append(n)
             X, ldx = Yb, _ld(dout)
-        # loss over the seed rows of the last layer
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
+        if self.fused_upper:
+            self._fused_upper_step(win, b, layers, H_bufs, Y_bufs, ns, s0, s1, slot)
+            return
+        # loss over the seed rows of the last layer
         C = dims[-1]
         r0, _ = self._rows(win, self.L - 1, b)
         dY = self._buf("dy_last", ns[-1], _ld(C))
@@ -479,6 +483,69 @@ class Pipeline:
                            lay["t_w"].data_ptr(), nx, col_base, dH.data_ptr(), _ld(din), self_x,
                            _ld(din), dXn.data_ptr(), _ld(din), din, st)
                 dX, lddx = dXn, _ld(din)
+        if self.dist is not None:
+            self.dist.allreduce_mean(self.model.grad)
+        self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+
+    # ------------------------------------------------------ fused upper --
+    def _fused_upper_ok(self) -> bool:
+        import os
+        dims = self.cfg.layer_dims
+        # opt-in (FGL_FUSED=1): correct, but this round's persistent kernel is
+        # latency bound (~200 us per batch vs ~140 us for the separate kernels)
+        if os.environ.get("FGL_FUSED", "0") != "1" or not self.compact or self.L < 2 or self.L > 4:
+            return False
+        return all(1 <= dims[i] <= 128 and dims[i + 1] <= 192 and (dims[i] + 1) * dims[i + 1] <= 24 * 256
+                   for i in range(1, self.L))
+
+    def _fused_upper_step(self, win, b, layers, H_bufs, Y_bufs, ns, s0, s1, slot):
+        """Layers 1..L-1 forward, fp64 loss and backward in ONE persistent
+        kernel (fgl_upper_layers), then layer 0's backward (tcgen05 wgrad)
+        and SGD."""
+        s, m, dims, st = self.sampler, self.model, self.cfg.layer_dims, self.stream
+        a = _lib.FglUpperArgs()
+        a.num_upper = self.L - 1
+        for i in range(1, self.L):
+            din, dout = dims[i], dims[i + 1]
+            r0, r1 = self._rows(win, i, b)
+            q0, q1 = self._rows(win, i - 1, b)
+            n = r1 - r0
+            lay = layers[i]
+            l = a.layer[i - 1]
+            l.indptr = lay["indptr"].data_ptr() + 8 * r0
+            l.col, l.col_base, l.w, l.rows = lay["col"], self._in_base(win, i, b), lay["w"].data_ptr(), n
+            l.t_indptr = lay["t_indptr"].data_ptr() + 8 * q0
+            l.t_col, l.t_base, l.t_w, l.prev_rows = lay["t_col"].data_ptr(), r0, lay["t_w"].data_ptr(), q1 - q0
+            l.din, l.dout = din, dout
+            l.W, l.b, l.dW, l.db = m.W(i), m.b(i), m.dW(i), m.db(i)
+            l.H, l.ldh = self._buf(f"h{i}", n, _ld(din)).data_ptr(), _ld(din)
+            l.Y, l.ldy = self._buf(f"y{i}", n, _ld(dout)).data_ptr(), _ld(dout)
+            l.dH = self._buf(f"dh{i}", n, _ld(din)).data_ptr()
+            l.dY = self._buf(f"dyu{i}", n, _ld(dout)).data_ptr()
+        n0 = ns[0]
+        d1 = dims[1]
+        dY0 = self._buf("dy0", n0, _ld(d1))
+        a.X1, a.ldx1, a.dX1 = Y_bufs[0].data_ptr(), _ld(d1), None
+        a.seed_rows = s.seed_front.data_ptr() + 4 * s0
+        a.seed_row_base = self._rows(win, self.L - 1, b)[0]
+        a.seed_ids = s.seeds_dev.data_ptr() + 4 * s0
+        a.labels = self.labels.data_ptr()
+        a.num_seeds, a.num_classes = s1 - s0, dims[-1]
+        a.loss_sum = self.loss_dev.data_ptr() + 8 * slot
+        wsb = _lib.lib().fgl_upper_ws_bytes(a)
+        ws = self._buf("upper_ws", wsb, 1, self.torch.uint8)
+        self._call("fgl_upper_layers", a, ws.data_ptr(), wsb, st)
+        # dY0 = A_1^T dH_1 over layer 0's (wide) row space: the standalone SpMM
+        lay1 = layers[1]
+        q0 = self._rows(win, 0, b)[0]
+        r0 = self._rows(win, 1, b)[0]
+        self._call("fgl_spmm", lay1["t_indptr"].data_ptr() + 8 * q0, lay1["t_col"].data_ptr(),
+                   lay1["t_w"].data_ptr(), n0, r0, a.layer[0].dH, _ld(d1), None, _ld(d1), dY0.data_ptr(), _ld(d1),
+                   d1, st)
+        # layer 0 backward: dW0 / db0 from H0 and dY0 * relu'(Y0)
+        self._call("fgl_dense_bwd", H_bufs[0].data_ptr(), _ld(dims[0]), n0, dims[0], m.W(0), d1,
+                   dY0.data_ptr(), _ld(d1), Y_bufs[0].data_ptr(), _ld(d1), m.dW(0), m.db(0), None, _ld(dims[0]),
+                   self.bwd_ws.data_ptr(), self.bwd_ws.numel(), st)
         if self.dist is not None:
             self.dist.allreduce_mean(self.model.grad)
         self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)

@@ -158,3 +158,30 @@ def test_batch_gradients_match_oracle(cfg1_graph, arch):
     for (gw, gb), (ww, wb) in zip(got, want):
         np.testing.assert_allclose(gw, ww, rtol=1e-5, atol=1e-5 * float(np.abs(ww).max()))
         np.testing.assert_allclose(gb, wb, rtol=1e-5, atol=1e-5 * float(np.abs(wb).max()))
+
+
+def test_fused_upper_layers_match_separate_kernels(cfg1_graph):
+    """The opt-in fused upper-layer kernel (FGL_FUSED=1, fgl_upper_layers) gives
+    the same losses and parameters as the separate kernels within 1e-5."""
+    import os
+    from paper_2409_14939_b200 import trainer
+    g = cfg1_graph
+    rng = np.random.default_rng(4)
+    dims, fan = (64, 48, 32, 7), [8, 4, 3]
+    feats = rng.standard_normal((g.num_nodes, dims[0])).astype(np.float32)
+    labels = rng.integers(0, dims[-1], size=g.num_nodes)
+    cfg = trainer.ModelConfig(layer_dims=dims, fanouts=fan, batch_size=300, window_n=3, lr=0.1, seed=2)
+    seeds = [rng.choice(g.num_nodes, 300, replace=False) for _ in range(3)]
+    rs = [oracle.derive_seed(2, 13, j) for j in range(3)]
+    out = []
+    for fused in ("0", "1"):
+        os.environ["FGL_FUSED"] = fused
+        try:
+            pipe = trainer.Pipeline(g, feats, labels, cfg)
+            assert pipe.fused_upper == (fused == "1")
+            _, lo = pipe.run_window(seeds, rs)
+            out.append((lo.cpu().numpy().copy(), pipe.model.flat.cpu().numpy()))
+        finally:
+            os.environ.pop("FGL_FUSED", None)
+    np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-5)
+    np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5, atol=1e-6)
