@@ -303,6 +303,9 @@ class Pipeline:
         self._bufs = {}
         self.gpu_launches = 0
         self.fused_upper = self._fused_upper_ok()
+        self._pre_h0 = None
+        self._pre_h0_win = None
+        self._agg_stream = None
 
     # ------------------------------------------------------------ buffers --
     def _buf(self, name, rows, cols, dtype=None):
@@ -432,13 +435,20 @@ class Pipeline:
             r0, r1 = self._rows(win, i, b)
             n = r1 - r0
             lay = layers[i]
-            Hb = self._buf(f"h{i}", n, _ld(din))
-            self_x = X.data_ptr() if not self.compact else None
-            col, base = lay["col"], self._in_base(win, i, b)
-            if i == 0 and self.direct_x0:
-                col, base = lay["col_global"], 0
-            self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
-                       base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
+            pre = (self._pre_h0.get(b) if (i == 0 and self._pre_h0 is not None and self._pre_h0_win is win)
+                   else None)
+            if pre is not None:
+                # layer-0 aggregation was run ahead on the aggregation stream
+                Hb, ev = pre
+                torch.cuda.current_stream().wait_event(ev)
+            else:
+                Hb = self._buf(f"h{i}", n, _ld(din))
+                self_x = X.data_ptr() if not self.compact else None
+                col, base = lay["col"], self._in_base(win, i, b)
+                if i == 0 and self.direct_x0:
+                    col, base = lay["col_global"], 0
+                self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
+                           base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
             Yb = self._buf(f"y{i}", n, _ld(dout))
             self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout,
                        Yb.data_ptr(), _ld(dout), 1 if i < self.L - 1 else 0, st)
@@ -486,6 +496,41 @@ class Pipeline:
         if self.dist is not None:
             self.dist.allreduce_mean(self.model.grad)
         self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+
+    # --------------------------------------------- layer-0 run-ahead --
+    def _launch_l0_aggs(self, win, order, layers):
+        """Layer 0's aggregation H0 = A_0 X (features straight from the HBM
+        table) depends on the sampled window only, not on the weights, so
+        the aggregations of ALL batches of the window are issued up front on a
+        separate stream; each batch step waits for its own event.  The wide
+        random-gather SpMMs then overlap the latency-bound dense / backward
+        kernels of earlier batches.  Results are identical (same kernel, same
+        inputs).  Only for the direct-x0 compact layout (features in HBM)."""
+        torch = self.torch
+        if not (self.direct_x0 and self.compact):
+            self._pre_h0 = None
+            return
+        if self._agg_stream is None:
+            self._agg_stream = torch.cuda.Stream(device=self.device)
+        ready = torch.cuda.Event()
+        ready.record()  # prepare of this window (and every earlier batch step) is ordered before
+        self._agg_stream.wait_event(ready)
+        lay = layers[0]
+        din = self.cfg.layer_dims[0]
+        pre = {}
+        with torch.cuda.stream(self._agg_stream):
+            st = self._agg_stream.cuda_stream
+            for j, b in enumerate(order):
+                r0, r1 = self._rows(win, 0, b)
+                n = r1 - r0
+                Hb = self._buf(f"h0_run{j}", n, _ld(din))
+                self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
+                           n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din, st)
+                ev = torch.cuda.Event()
+                ev.record(self._agg_stream)
+                pre[b] = (Hb, ev)
+        self._pre_h0 = pre
+        self._pre_h0_win = win
 
     # ------------------------------------------------------ fused upper --
     def _fused_upper_ok(self) -> bool:
@@ -565,6 +610,7 @@ class Pipeline:
         order = self.schedule(win, nb)
         t2 = tick() if tick else 0.0
         layers = self.prepare(win)
+        self._launch_l0_aggs(win, order, layers)
         t3 = tick() if tick else 0.0
         for j, b in enumerate(order):
             prev = order[j - 1] if (j > 0 and self.flags.match) else None
@@ -620,6 +666,7 @@ class Pipeline:
                 pending = self._sample_async(*windows[w + 1], slot=(w + 1) % 2)
             self.sampler = win.s
             layers = self.prepare(win)
+            self._launch_l0_aggs(win, order, layers)
             for j, b in enumerate(order):
                 prev = order[j - 1] if (j > 0 and self.flags.match) else None
                 self.batch_step(win, b, prev, j, layers, j % 2)
