@@ -353,6 +353,8 @@ def stage_profile(pipe, mine, it, cfg, torch):
     samp_bytes = 0.0
     from paper_2409_14939_b200 import _lib as _l
     sel = {"s": 0.0, "bytes": 0.0, "draws": 0.0}
+    pipe.loaded.zero_()
+    pipe.cache_hits.zero_()
     for k in range(2):
         seeds, rs = mine[(it + k) % len(mine)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
@@ -419,6 +421,28 @@ def stage_profile(pipe, mine, it, cfg, torch):
         "sampler_stage": {"ms_per_window": acc["sample"], "draws_per_s": draws / t_s,
                           "alu_frac": draws / t_s / peak_draws},
     }
+    if pipe.feature_store == "host":
+        # IO stage: feature rows that cross the host link per
+        # window vs the measured pinned host->device copy peak of this box
+        loaded = int(pipe.loaded.item()) / 2
+        hits = int(pipe.cache_hits.item()) / 2
+        link_bytes = loaded * 4 * pipe.d0
+        hb = torch.empty(1 << 28, dtype=torch.float32).pin_memory()
+        db = torch.empty(1 << 28, dtype=torch.float32, device=pipe.device)
+        db.copy_(hb, non_blocking=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        db.copy_(hb, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        link_peak = hb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del hb, db
+        achieved = link_bytes / (acc["compute"] / 1e3) / 1e9
+        roof["io"] = {"bound": "host link (pinned zero-copy row gathers)", "rows_per_window": loaded,
+                      "cache_rows_per_window": hits, "bytes_per_window": link_bytes,
+                      "achieved": achieved, "peak": link_peak, "unit": "GB/s", "frac": achieved / link_peak,
+                      "peak_source": "measured: pinned host->device cudaMemcpy of 1 GiB on this box",
+                      "note": "achieved = host-link bytes / whole compute stage time (lower bound for the gather)"}
     return {"ms": acc, "roofline": roof}
 
 
