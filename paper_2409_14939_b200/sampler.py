@@ -183,7 +183,7 @@ class WindowSampler:
     next call."""
 
     def __init__(self, dgraph, fanouts, max_batch_size: int, max_batches: int = 1,
-                 local_ids: bool = True, device="cuda"):
+                 local_ids: bool = True, device="cuda", window_rows: bool = True):
         import torch
         self.torch = torch
         self.g = dgraph
@@ -203,12 +203,16 @@ class WindowSampler:
         self.tgt = torch.empty(e, **i32)
         self.src = torch.empty(e, **i32)
         self.wgt = torch.empty(e, dtype=torch.float32, device=device)
-        self.tgt_row, self.src_row = opt(e), opt(e)
+        # window rows (unique-rank IDs) are only needed by the all-rows layout
+        # (GIN / SAGE) and the drop-in API; the compact GCN layout uses the
+        # frontier indices alone, and skipping the rows saves a rank lookup per edge
+        optr = opt if window_rows else (lambda n: None)
+        self.tgt_row, self.src_row = optr(e), optr(e)
         self.tgt_front, self.src_front = opt(e), opt(e)
         self.unique = torch.empty(self.uniq_cap, **i32)
         self.frontier = torch.empty(self.H * self.fcap, **i32)
         nseed = self.max_nb * self.max_bs
-        self.seed_rows, self.seed_front = opt(nseed), opt(nseed)
+        self.seed_rows, self.seed_front = optr(nseed), opt(nseed)
         self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=device)
         self.seeds_dev = torch.empty(nseed, **i32)
         self.seed_off = torch.empty(self.max_nb + 1, dtype=torch.int64, device=device)

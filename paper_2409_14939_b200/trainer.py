@@ -269,7 +269,8 @@ class Pipeline:
             self.feats = dev
         lab = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(np.asarray(labels, dtype=np.int64))
         self.labels = lab.to(device=device, dtype=torch.int64)
-        self.sampler = WindowSampler(self.dg, cfg.fanouts, cfg.batch_size, cfg.window_n, device=device)
+        self.sampler = WindowSampler(self.dg, cfg.fanouts, cfg.batch_size, cfg.window_n, device=device,
+                                     window_rows=cfg.arch != "gcn")
         out = _lib.i64_array([0, 0, 0])
         _lib.call("fgl_sample_ws_bitmaps", self.dg.num_nodes, cfg.window_n, self.sampler.fcap,
                   self.sampler.uniq_cap, out)
@@ -632,7 +633,8 @@ class Pipeline:
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(device=self.device)
             self._samplers = [self.sampler, WindowSampler(self.dg, self.cfg.fanouts, self.cfg.batch_size,
-                                                          self.cfg.window_n, device=self.device)]
+                                                          self.cfg.window_n, device=self.device,
+                                                          window_rows=self.cfg.arch != "gcn")]
         smp = self._samplers[slot]
         done = getattr(self, "_slot_done", {}).get(slot)
         if done is not None:  # the compute of the window that last used this slot
