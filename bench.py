@@ -410,7 +410,7 @@ def stage_profile(pipe, mine, it, cfg, torch):
     torch.cuda.synchronize()
     peak_draws = 4 * nblk / (e0.elapsed_time(e1) / 1e3)
     roof = {
-        "kernel": "select_bal_kernel, the hop-2 launch of fgl_sample_window (largest select launch)",
+        "kernel": "select_bal_kernel + select_hub_kernel (hop-2 selection of fgl_sample_window, the largest select launch)",
         "bound": "hbm", "achieved": sel["bytes"] / sel["s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
         "frac": sel["bytes"] / sel["s"] / 1e9 / hbm_peak, "traffic": _measured_traffic("select_bal_kernel"),
         "peak_source": peak_src, "launch_ms": sel["s"] * 1e3, "bytes_per_launch": sel["bytes"],

@@ -50,16 +50,18 @@ struct SampleWs {
   int64_t* pos;        // [nb]   running Philox position per batch
   int64_t* hop_pos;    // [nb]   position at the start of the current hop
   int64_t* scal;       // [8]
+  int32_t* hub_list;   // [fcap] hub frontier entries of the current hop
 };
 
-enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5, kTileCtr = 6 };
+enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5, kTileCtr = 6,
+            kHubCnt = 7 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
   int64_t words, fcap, bytes;
   int64_t off_front_bm, off_all_bm, off_wprefix, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
-      off_pos, off_hoppos, off_scal;
+      off_pos, off_hoppos, off_scal, off_hub;
 };
 
 WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
@@ -79,6 +81,7 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_pos = take(8 * nb);
   L.off_hoppos = take(8 * nb);
   L.off_scal = take(8 * 8);
+  L.off_hub = take(4 * L.fcap);
   L.bytes = o;
   return L;
 }
@@ -97,6 +100,7 @@ SampleWs carve(void* base, const WsLayout& L) {
   w.pos = reinterpret_cast<int64_t*>(p + L.off_pos);
   w.hop_pos = reinterpret_cast<int64_t*>(p + L.off_hoppos);
   w.scal = reinterpret_cast<int64_t*>(p + L.off_scal);
+  w.hub_list = reinterpret_cast<int32_t*>(p + L.off_hub);
   return w;
 }
 
@@ -290,6 +294,7 @@ __global__ void hop_book_kernel(SampleWs w, const int64_t* __restrict__ fr_off, 
   if (threadIdx.x == 0) {
     w.scal[kHopEdgeBase] = w.scal[kEdgeBase];
     w.scal[kTileCtr] = 0;  // dynamic tile counter of this hop's select kernel
+    w.scal[kHubCnt] = 0;   // hub nodes deferred to select_hub_kernel
   }
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const int64_t f0 = fr_off[b], f1 = fr_off[b + 1];
@@ -392,6 +397,8 @@ struct SelectArgs {
   int32_t* tgt_front;
   int fan;
   unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal_kernel)
+  unsigned long long* hub_cnt;   // hub nodes (d > kBalHub) deferred to select_hub_kernel
+  int32_t* hub_list;             // their frontier indices
 };
 
 template <int K>
@@ -783,9 +790,18 @@ __device__ __forceinline__ int bal_find(const int32_t* arr, int g) {
   return n;
 }
 
+// debug (FGL_SELDBG): per-warp finish times of the last launch
+__device__ int64_t g_sel_finish[4096];
+__device__ __forceinline__ int64_t sel_gtime() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
-                                                                    int sv_words) {
+                                                                    int sv_words, int dbg) {
   extern __shared__ __align__(16) uint64_t sbuf[];
+  const int64_t t_start = dbg ? sel_gtime() : 0;
   const int lane = lane_id(), wib = warp_id();
   char* wbase = reinterpret_cast<char*>(sbuf) + (int64_t)wib * (sv_words * 8 + sizeof(BalTab));
   uint64_t* sv = reinterpret_cast<uint64_t*>(wbase);
@@ -805,7 +821,13 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
     unsigned long long tix = 0;
     if (lane == 0) tix = atomicAdd(a.tile_ctr, 1ull);
     tix = __shfl_sync(0xffffffffu, tix, 0);
-    if ((int64_t)tix >= ntiles) break;
+    if ((int64_t)tix >= ntiles) {
+      if (dbg && lane == 0 && gw < 4095) {
+        g_sel_finish[gw + 1] = sel_gtime();
+        if (gw == 0) g_sel_finish[0] = t_start;
+      }
+      break;
+    }
     const int64_t t0 = (int64_t)tix * 32;
     const int64_t i = t0 + lane;
     int32_t u = 0, b = 0;
@@ -868,13 +890,15 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
     __syncwarp();
     const int want = (int)(d < fan ? d : fan);
     const int cnt = T.cnt[lane];
-    const bool fb = d > 0 && (!elig || cnt > cap || cnt < want);
+    const bool hub = d > kBalHub && a.hub_list;
+    if (hub) a.hub_list[atomicAdd(a.hub_cnt, 1ull)] = (int32_t)i;  // one CTA per hub, later
+    const bool fb = d > 0 && !hub && (!elig || cnt > cap || cnt < want);
     // ---- selection, lane = node: want passes of a minimum search over the
     // node's survivors (strictly above the previous pick; all survivor words
     // differ in their slot bits), picks queued as (node, rank, slot) so that
     // the col[] / weight gathers of a lane's emissions are issued back to back
     uint32_t* q = reinterpret_cast<uint32_t*>(sv + segtot);  // emission queue after the survivors
-    const int nsel = (!fb && d > 0) ? want : 0;
+    const int nsel = (!fb && !hub && d > 0) ? want : 0;  // hubs: select_hub_kernel
     const int qbase = warp_incl_scan(nsel) - nsel;
     const int nq = __shfl_sync(0xffffffffu, qbase + nsel, 31);
     {
@@ -936,6 +960,78 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
       else tau_select_node<false>(a, sv, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
     }
     __syncwarp();
+  }
+}
+
+// Hub nodes (d > kBalHub) of a hop, one CTA each (select_bal_kernel queues
+// them): all 512 threads draw the hub's Philox blocks, survivors below the
+// threshold go to shared memory, and the want smallest (key, slot) pairs are
+// ranked by counting -- a 19K-degree hub takes one CTA a few microseconds
+// instead of one warp ~100 us at the end of the select launch.  Overflow or
+// too few survivors: the exact warp path (tau_select_node) of warp 0.
+constexpr int kHubThreads = 512;
+constexpr int kHubCap = 2048;
+
+__global__ void __launch_bounds__(kHubThreads) select_hub_kernel(const __grid_constant__ SelectArgs a) {
+  __shared__ uint64_t skey[kHubCap];
+  __shared__ uint32_t sslot[kHubCap];
+  __shared__ int scnt;
+  const int tid = threadIdx.x;
+  const int64_t nh = (int64_t)*a.hub_cnt;
+  const int64_t ebase = a.scal[kHopEdgeBase];
+  const int fan = a.fan;
+  const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
+  for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int64_t i = a.hub_list[h];
+    const int32_t u = a.front[i];
+    const int b = a.fb[i];
+    const int64_t e0 = __ldg(a.off + u);
+    const int64_t d = __ldg(a.off + u + 1) - e0;
+    const int64_t p0 = a.hop_pos[b] + a.scan_deg[i];
+    const int64_t obase = ebase + a.scan_sel[i];
+    const uint64_t k0 = a.keys[2 * b], k1 = a.keys[2 * b + 1];
+    const int want = (int)(d < fan ? d : fan);
+    const uint64_t tau = (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
+    if (tid == 0) scnt = 0;
+    __syncthreads();
+    const int64_t blk0 = p0 >> 2, blk_last = (p0 + d - 1) >> 2;
+    for (int64_t blk = blk0 + tid; blk <= blk_last; blk += kHubThreads) {
+      uint64_t w[4];
+      philox4x64_10((uint64_t)blk + 1, k0, k1, w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t slot = 4 * blk + q - p0;
+        const uint64_t key = w[q] >> 11;
+        if (slot >= 0 && slot < d && key < tau) {
+          const int c = atomicAdd(&scnt, 1);
+          if (c < kHubCap) { skey[c] = key; sslot[c] = (uint32_t)slot; }
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = scnt;
+    if (cnt >= want && cnt <= kHubCap) {
+      uint32_t* bm = a.bm_front + (int64_t)b * a.words;
+      for (int c = tid; c < cnt; c += kHubThreads) {
+        const uint64_t ck = skey[c];
+        const uint32_t cs = sslot[c];
+        int rank = 0;
+        for (int j = 0; j < cnt; ++j) rank += key_less(skey[j], sslot[j], ck, cs) ? 1 : 0;
+        if (rank < want) {
+          const int64_t e = e0 + cs;
+          const int32_t sidx = __ldg(a.col + e);
+          const int64_t o = obase + rank;
+          a.tgt[o] = u;
+          a.src[o] = sidx;
+          a.wgt[o] = a.ew ? __ldg(a.ew + e) : 1.0f;
+          if (a.tgt_front) a.tgt_front[o] = (int32_t)i;
+          atomicOr(bm + (sidx >> 5), 1u << (sidx & 31));
+        }
+      }
+    } else if (tid < 32) {  // exact warp path (widened threshold / streaming fallback)
+      tau_select_node<false>(a, skey, sslot, i, u, e0, d, b, p0, obase, expect);
+    }
+    __syncthreads();
   }
 }
 
@@ -1101,6 +1197,10 @@ using namespace fgl;
 
 extern "C" {
 
+int fgl_debug_select_finish(int64_t* host, int64_t n) {
+  return cudaMemcpyFromSymbol(host, g_sel_finish, sizeof(int64_t) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
+}
+
 int fgl_profile_select(int32_t enable) {
   g_sel_prof = enable != 0;
   return FGL_OK;
@@ -1241,7 +1341,8 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
                  w.scan_deg, w.scan_sel, fr_off(h), w.hop_pos, keys, w.scal,
                  w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan,
-                 reinterpret_cast<unsigned long long*>(w.scal + kTileCtr)};
+                 reinterpret_cast<unsigned long long*>(w.scal + kTileCtr),
+                 reinterpret_cast<unsigned long long*>(w.scal + kHubCnt), w.hub_list};
     // FGL_SELECT=stream forces the streaming top-list kernel (A/B parity tests)
     static const bool force_stream = [] {
       const char* v = getenv("FGL_SELECT");
@@ -1253,25 +1354,32 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     }();
     if (fan <= kTauMaxFan && bal_smem(fan) <= 200 * 1024 && !force_stream && !force_tau) {
       const int bsm = bal_smem(fan);
-      static int bal_grid = 0, bal_smem_set = 0;
-      if (bsm > bal_smem_set) {
+      // grid per fanout: the survivor buffers (and so the CTAs per SM) depend on it
+      static int bal_attr = 0;
+      static int bal_grid_of[kTauMaxFan + 1] = {0};
+      if (bsm > bal_attr) {
         FGL_CUDA(cudaFuncSetAttribute(select_bal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
+        bal_attr = bsm;
+      }
+      if (!bal_grid_of[fan]) {
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal_kernel, kBalWarps * 32, bsm) !=
                 cudaSuccess || per_sm < 1)
           per_sm = 2;
-        bal_grid = per_sm * kNumSMs;
-        bal_smem_set = bsm;
+        bal_grid_of[fan] = per_sm * kNumSMs;
       }
+      const int bal_grid = bal_grid_of[fan];
       cudaEvent_t pe0 = nullptr, pe1 = nullptr;
       if (g_sel_prof) {
         cudaEventCreate(&pe0);
         cudaEventCreate(&pe1);
         cudaEventRecord(pe0, stream);
       }
+      static const int seldbg = getenv("FGL_SELDBG") ? 1 : 0;
       FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
-                                                                                  bal_sv_words(fan));
-      if (g_sel_prof) {
+                                                                                  bal_sv_words(fan), seldbg);
+      FGL_COUNT_LAUNCH(), select_hub_kernel<<<4 * kNumSMs, kHubThreads, 0, stream>>>(a);
+      if (g_sel_prof) {  // the events bracket both launches: together they are the hop's selection
         cudaEventRecord(pe1, stream);
         std::lock_guard<std::mutex> lk(g_sel_mu);
         g_sel_ev.emplace_back(pe0, pe1);
