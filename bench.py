@@ -448,8 +448,9 @@ def stage_profile(pipe, mine, it, cfg, torch):
 
 def e2e_measure(pipe, mine, it, K, torch, world, device):
     """Same metric through the public API with host buffers: each step stages
-    the window's seeds from pinned host memory and reads the per-batch losses
-    back to the host; wall clock (synchronised), max over ranks."""
+    the window's seeds from pinned host memory (H2D inside the timed region)
+    and copies its per-batch losses back to pinned host memory (D2H inside the
+    timed region, asynchronous); wall clock (synchronised), max over ranks."""
     from paper_2409_14939_b200 import dist as fdist
     edges = 0
     h2d = d2h = 0
@@ -459,13 +460,17 @@ def e2e_measure(pipe, mine, it, K, torch, world, device):
         pinned = [torch.from_numpy(s.astype(np.int64)).pin_memory() for s in seeds]
         staged.append(([p.numpy() for p in pinned], rs))
         h2d += sum(len(s) for s in seeds) * 4 + (len(seeds) + 1) * 8 + 16 * len(seeds)
+    host_losses = [torch.empty(len(staged[k][0]), dtype=torch.float64).pin_memory() for k in range(K)]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for order, losses in pipe.run_windows(staged):
-        lv = losses.cpu().numpy()  # per-batch losses back to the host every step
+    for k, (order, losses) in enumerate(pipe.run_windows(staged)):
+        # per-batch losses of every step copied back to pinned host memory
+        # (asynchronous D2H on the compute stream; no per-step host stall)
+        host_losses[k].copy_(losses, non_blocking=True)
         edges += pipe.last_window.total_edges()
-        d2h += lv.nbytes
+        d2h += host_losses[k].numel() * 8
     torch.cuda.synchronize()
+    _ = [float(h.sum()) for h in host_losses]  # the host consumes every step's losses
     wall = time.perf_counter() - t0
     wall = fdist.max_over_ranks(wall, world, device)
     edges_all = fdist.sum_over_ranks(float(edges), world, device)
