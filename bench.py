@@ -128,7 +128,8 @@ def build_workload(cfg, device):
     gen.manual_seed(1)
     feats = torch.randn((dg.num_nodes, cfg["dims"][0]), generator=gen, device=device, dtype=torch.float32)
     labels = torch.randint(0, cfg["dims"][-1], (dg.num_nodes,), generator=gen, device=device)
-    torch.cuda.synchronize()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
     log(f"graph: {dg.num_nodes} nodes, {dg.num_edges} edges, max degree "
         f"{int((dg.row_offsets[1:] - dg.row_offsets[:-1]).max())}; built in {time.time() - t0:.1f}s")
     return dg, feats, labels
