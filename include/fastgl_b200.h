@@ -183,6 +183,26 @@ int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t
                       int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
                       void* stream);
 
+/* --------------------------------------------------- depth layout ---- */
+/* Depth-major window rows for the all-rows layouts (GIN / GraphSAGE,
+ * trainer.py:182-195): rewrites a window sampled by fgl_sample_window (its
+ * counts vector, frontier lists, and the `all` bitmap + word prefix of its
+ * workspace, offsets from fgl_sample_ws_bitmaps) so that each batch's unique
+ * rows are ordered by (depth, node id), depth = first hop whose frontier
+ * holds the node (seeds 0, last-hop-only sources H).  Every R_i (rows model
+ * layer i needs) is then a prefix of the batch's block.  Rewrites
+ * unique_nodes, tgt_row / src_row (either may be NULL), seed_rows; writes
+ * row_map[old window row] = new row and depth_cnt[b * (H + 1) + h] (int64).
+ * No host synchronisation. */
+int64_t fgl_depth_relayout_ws_bytes(int64_t unique_cap);
+int fgl_depth_relayout(const int64_t* counts, int32_t H, int32_t nb, const int32_t* frontier,
+                       int64_t frontier_stride, const uint32_t* bm_all, const int32_t* wprefix, int64_t words,
+                       int32_t* unique_nodes, int64_t unique_cap, int32_t* tgt_row, int32_t* src_row,
+                       int32_t* seed_rows, int64_t num_seeds, int32_t* row_map, int64_t* depth_cnt, void* ws,
+                       int64_t ws_bytes, void* stream);
+/* Y[r] += X[r] for r < nrows (one rounded add per element). */
+int fgl_add_rows(float* Y, int64_t ldy, const float* X, int64_t ldx, int64_t nrows, int32_t d, void* stream);
+
 /* ------------------------------------------------------- fused layers ---- */
 /* Upper model layers 1..L-1 of a COMPACT GCN batch (rows of layer i = hop
  * H-1-i frontier), trained by ONE persistent kernel (trainer.py:182-228 for
@@ -213,6 +233,15 @@ typedef struct fgl_upper_args {
 
 int64_t fgl_upper_ws_bytes(const fgl_upper_args* a);
 int fgl_upper_layers(const fgl_upper_args* a, void* ws, int64_t ws_bytes, void* stream);
+
+/* fgl_prepare_layer for targets grouped but not ascending (depth-major rows
+ * of fgl_depth_relayout): stable grouping by target (compute.py:219-230)
+ * first; col_out receives the forward CSR's columns. */
+int64_t fgl_prepare_layer_grouped_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_cols);
+int fgl_prepare_layer_grouped(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
+                              int64_t num_cols, int32_t arch, int64_t* indptr, int32_t* col_out, float* w,
+                              int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
+                              void* stream);
 
 /* ------------------------------------------------------------- compute ---- */
 /* Memory-Aware CSR aggregation (compute.py:115-195):
@@ -305,12 +334,14 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
  * static-degree policy): after the Match test, a node with cache_slot[g] >= 0
  * is copied from cache_x[cache_slot[g] * ldc] (HBM) instead of the store;
  * `hits` (optional) accumulates those rows, `loaded` the rows read from the
- * store. cache_slot has one int32 per graph node (-1 = not cached). */
+ * store. cache_slot has one int32 per graph node (-1 = not cached).
+ * prev_row_map (optional): the previous batch's rows are in depth-major order
+ * (fgl_depth_relayout); its bitmap rank r maps to row prev_row_map[r]. */
 int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
                            const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
-                           const float* prev_x, int64_t ldp, const int32_t* cache_slot, const float* cache_x,
-                           int64_t ldc, float* out, int64_t ldo, uint64_t* loaded, uint64_t* hits,
-                           void* stream);
+                           const float* prev_x, int64_t ldp, const int32_t* prev_row_map,
+                           const int32_t* cache_slot, const float* cache_x, int64_t ldc, float* out, int64_t ldo,
+                           uint64_t* loaded, uint64_t* hits, void* stream);
 
 #ifdef __cplusplus
 }

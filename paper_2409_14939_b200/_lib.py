@@ -82,6 +82,10 @@ SIGNATURES = {
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
     "fgl_profile_select": (C.c_int, [C.c_int32]),
     "fgl_upper_ws_bytes": (C.c_int64, [C.POINTER(FglUpperArgs)]),
+    "fgl_depth_relayout_ws_bytes": (C.c_int64, [C.c_int64]),
+    "fgl_depth_relayout": (C.c_int, [vp, C.c_int32, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
+                                     vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp]),
+    "fgl_add_rows": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int32, vp]),
     "fgl_upper_layers": (C.c_int, [C.POINTER(FglUpperArgs), vp, C.c_int64, vp]),
     "fgl_walk_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
     "fgl_sample_walk": (C.c_int, [C.POINTER(FglGraph), vp, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, vp, vp, vp, C.c_int64,
@@ -92,6 +96,9 @@ SIGNATURES = {
     "fgl_stable_group": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]),
     "fgl_gather_i32_f32": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp]),
     "fgl_prepare_layer_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64]),
+    "fgl_prepare_layer_grouped_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64]),
+    "fgl_prepare_layer_grouped": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp, vp, vp, vp,
+                                            vp, vp, vp, C.c_int64, vp]),
     "fgl_prepare_layer": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp, vp,
                                     vp, vp, vp, vp, C.c_int64, vp]),
     "fgl_spmm": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64,
@@ -119,7 +126,7 @@ SIGNATURES = {
     "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
                                   vp, C.c_int64, vp, C.c_int64, vp, vp]),
     "fgl_gather_rows_cached": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
-                                         vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp]),
+                                         vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp]),
 }
 
 _lib = None

@@ -70,9 +70,10 @@ template <bool VEC>
 __global__ void __launch_bounds__(256) gather_rows_kernel(
     const float* __restrict__ feats, int64_t ldf, int d, const int32_t* __restrict__ ids, int64_t n,
     const uint32_t* __restrict__ prev_bm, const int32_t* __restrict__ prev_prefix, int64_t prev_base,
-    const float* __restrict__ prev_x, int64_t ldp, const int32_t* __restrict__ cache_slot,
-    const float* __restrict__ cache_x, int64_t ldc, float* __restrict__ out, int64_t ldo,
-    unsigned long long* __restrict__ loaded, unsigned long long* __restrict__ hits) {
+    const float* __restrict__ prev_x, int64_t ldp, const int32_t* __restrict__ prev_row_map,
+    const int32_t* __restrict__ cache_slot, const float* __restrict__ cache_x, int64_t ldc,
+    float* __restrict__ out, int64_t ldo, unsigned long long* __restrict__ loaded,
+    unsigned long long* __restrict__ hits) {
   constexpr int R = 4;
   const int lane = threadIdx.x & 31;
   const int w = VEC ? (d + 3) >> 2 : d;
@@ -89,7 +90,8 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(
       if (prev_bm) {
         const uint32_t word = __ldg(prev_bm + (g >> 5));
         if ((word >> (g & 31)) & 1u) {
-          const int64_t pr = __ldg(prev_prefix + (g >> 5)) + __popc(word & ((1u << (g & 31)) - 1u)) - prev_base;
+          int64_t pr = __ldg(prev_prefix + (g >> 5)) + __popc(word & ((1u << (g & 31)) - 1u)) - prev_base;
+          if (prev_row_map) pr = __ldg(prev_row_map + pr + prev_base) - prev_base;  // depth-major rows
           mine = prev_x + pr * ldp;
           store = false;
         }
@@ -228,9 +230,9 @@ int fgl_bitmap_test(const int32_t* ids, int64_t n, const uint32_t* bitmap, int8_
 
 int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int32_t* ids, int64_t n,
                            const uint32_t* prev_bitmap, const int32_t* prev_prefix, int64_t prev_base,
-                           const float* prev_x, int64_t ldp, const int32_t* cache_slot, const float* cache_x,
-                           int64_t ldc, float* out, int64_t ldo, uint64_t* loaded, uint64_t* hits,
-                           void* stream) {
+                           const float* prev_x, int64_t ldp, const int32_t* prev_row_map,
+                           const int32_t* cache_slot, const float* cache_x, int64_t ldc, float* out, int64_t ldo,
+                           uint64_t* loaded, uint64_t* hits, void* stream) {
   if (n < 0 || d < 1 || ldf < d || ldo < d || !feats || !out || (n > 0 && !ids) ||
       (prev_bitmap && (!prev_prefix || !prev_x || ldp < d)) || (cache_slot && (!cache_x || ldc < d))) {
     set_error("fgl_gather_rows: bad arguments");
@@ -245,12 +247,12 @@ int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int
   auto* ht = reinterpret_cast<unsigned long long*>(hits);
   if (vec)
     FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, cache_slot, cache_x, ldc, out,
-        ldo, ld, ht);
+        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, prev_row_map, cache_slot, cache_x,
+        ldc, out, ldo, ld, ht);
   else
     FGL_COUNT_LAUNCH(), gather_rows_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, cache_slot, cache_x, ldc, out,
-        ldo, ld, ht);
+        feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, prev_row_map, cache_slot, cache_x,
+        ldc, out, ldo, ld, ht);
   FGL_LAUNCH_CHECK("gather_rows_kernel");
   return FGL_OK;
 }
@@ -260,7 +262,7 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
                     const float* prev_x, int64_t ldp, float* out, int64_t ldo, uint64_t* loaded,
                     void* stream) {
   return fgl_gather_rows_cached(feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, nullptr,
-                                nullptr, 0, out, ldo, loaded, nullptr, stream);
+                                nullptr, nullptr, 0, out, ldo, loaded, nullptr, stream);
 }
 
 }  // extern "C"

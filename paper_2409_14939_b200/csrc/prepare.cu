@@ -60,6 +60,21 @@ __global__ void offsets_from_sorted_kernel(const int32_t* __restrict__ rows, int
   }
 }
 
+// row-parallel variant for sparse targets (long runs of rows without edges,
+// e.g. the depth-major rows of the GIN / SAGE layout): lower_bound per row
+__global__ void offsets_bsearch_kernel(const int32_t* __restrict__ rows, int64_t nnz, int64_t num_rows,
+                                       int64_t base, int64_t* __restrict__ indptr) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= num_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nnz;  // first e with rows[e] >= r
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(rows + mid) < r) lo = mid + 1; else hi = mid;
+    }
+    indptr[r] = base + lo;
+  }
+}
+
 __global__ void histogram_kernel(const int32_t* __restrict__ keys, int64_t n, int32_t* counts) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
@@ -373,10 +388,23 @@ int64_t fgl_prepare_layer_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_co
          fgl_stable_group_ws_bytes(num_cols);
 }
 
+static int prepare_layer_impl(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
+                              int64_t num_cols, int32_t arch_gcn, int64_t* indptr, float* w,
+                              int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
+                              void* stream_, bool sparse_rows);
+
 int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
                       int64_t num_cols, int32_t arch_gcn, int64_t* indptr, float* w,
                       int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
                       void* stream_) {
+  return prepare_layer_impl(lt, ls, nnz, num_rows, num_cols, arch_gcn, indptr, w, t_indptr, t_col, t_w, ws,
+                            ws_bytes, stream_, false);
+}
+
+static int prepare_layer_impl(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
+                              int64_t num_cols, int32_t arch_gcn, int64_t* indptr, float* w,
+                              int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
+                              void* stream_, bool sparse_rows) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (nnz < 0 || num_rows < 1 || num_cols < 1 || nnz >= (1ll << 31) || !indptr || !w ||
       !t_indptr || (nnz > 0 && (!lt || !ls || !t_col || !t_w))) {
@@ -391,7 +419,10 @@ int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t
   int32_t* perm = reinterpret_cast<int32_t*>(p);
   int32_t* outdeg = reinterpret_cast<int32_t*>(p + al(4 * std::max<int64_t>(nnz, 1)));
   void* gws = p + al(4 * std::max<int64_t>(nnz, 1)) + al(4 * std::max<int64_t>(num_cols, 1));
-  FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
+  if (sparse_rows)
+    FGL_COUNT_LAUNCH(), offsets_bsearch_kernel<<<grid_for(num_rows + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
+  else
+    FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
   int rc = stable_group_impl(ls, nnz, num_cols, 0, t_indptr, perm, outdeg, gws,
                              fgl_stable_group_ws_bytes(num_cols), st);
   if (rc) return rc;
@@ -401,6 +432,45 @@ int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t
   }
   FGL_LAUNCH_CHECK("prepare_layer");
   return FGL_OK;
+}
+
+int64_t fgl_prepare_layer_grouped_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_cols) {
+  const int64_t n = std::max<int64_t>(nnz, 1);
+  return 2 * al(4 * n) + std::max(fgl_stable_group_ws_bytes(num_rows), fgl_prepare_layer_ws_bytes(nnz, num_rows, num_cols));
+}
+
+// fgl_prepare_layer for targets that are grouped but NOT ascending (the
+// depth-major rows of fgl_depth_relayout): a stable grouping by target first
+// (compute.edges_to_csr's stable argsort, compute.py:219-230), then the
+// sorted-target path; col_out receives the forward CSR's column array.
+int fgl_prepare_layer_grouped(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
+                              int64_t num_cols, int32_t arch, int64_t* indptr, int32_t* col_out, float* w,
+                              int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
+                              void* stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (nnz < 0 || num_rows < 1 || num_cols < 1 || nnz >= (1ll << 31) || !indptr || !w || !t_indptr ||
+      (nnz > 0 && (!lt || !ls || !col_out || !t_col || !t_w))) {
+    set_error("fgl_prepare_layer_grouped: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (ws_bytes < fgl_prepare_layer_grouped_ws_bytes(nnz, num_rows, num_cols)) {
+    set_error("fgl_prepare_layer_grouped: workspace too small");
+    return FGL_E_CAPACITY;
+  }
+  char* p = static_cast<char*>(ws);
+  const int64_t n = std::max<int64_t>(nnz, 1);
+  int32_t* perm = reinterpret_cast<int32_t*>(p);
+  int32_t* lt_s = reinterpret_cast<int32_t*>(p + al(4 * n));
+  void* rest = p + 2 * al(4 * n);
+  const int64_t rest_bytes = ws_bytes - 2 * al(4 * n);
+  int rc = stable_group_impl(lt, nnz, num_rows, 0, indptr, perm, nullptr, rest, rest_bytes, st);
+  if (rc) return rc;
+  if (nnz > 0) {
+    FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, lt, nullptr, lt_s, nullptr);
+    FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, ls, nullptr, col_out, nullptr);
+  }
+  return prepare_layer_impl(lt_s, col_out, nnz, num_rows, num_cols, arch, indptr, w, t_indptr, t_col, t_w, rest,
+                            rest_bytes, stream_, true);
 }
 
 }  // extern "C"

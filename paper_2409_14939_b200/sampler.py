@@ -105,9 +105,13 @@ class DeviceWindow:
     _host_counts: np.ndarray | None = None
 
     def host_counts(self) -> np.ndarray:
-        """One device->host read of the counts vector (the window's only sync)."""
+        """One device->host read of the counts vector (the window's only sync);
+        with the depth layout the per-(batch, depth) counts follow it."""
         if self._host_counts is None:
-            c = self.s.counts[: counts_layout(self.num_hops, self.num_batches)["len"]].cpu().numpy()
+            n = counts_layout(self.num_hops, self.num_batches)["len"]
+            if self.s.depth_layout:
+                n += self.num_batches * (self.num_hops + 1)
+            c = self.s.counts[:n].cpu().numpy()
             _lib.status_error(int(c[counts_layout(self.num_hops, self.num_batches)["status"]]),
                               "fgl_sample_window")
             self._host_counts = c
@@ -144,6 +148,13 @@ class DeviceWindow:
 
     def total_edges(self) -> int:
         return int(self.host_counts()[self.num_hops * self.num_batches])
+
+    def prefix_rows(self, layer: int, b: int) -> int:
+        """Depth layout: rows of model layer `layer` for batch b = nodes of
+        depth <= H-1-layer (a prefix of the batch's block)."""
+        c = self.host_counts()
+        o = counts_layout(self.num_hops, self.num_batches)["len"] + b * (self.num_hops + 1)
+        return int(c[o : o + self.num_hops - layer].sum())
 
     def hop_draws(self, hop: int) -> int:
         """Philox draws (= candidates = sum of frontier degrees) of one hop;
@@ -183,7 +194,7 @@ class WindowSampler:
     next call."""
 
     def __init__(self, dgraph, fanouts, max_batch_size: int, max_batches: int = 1,
-                 local_ids: bool = True, device="cuda", window_rows: bool = True):
+                 local_ids: bool = True, device="cuda", window_rows: bool = True, depth_layout: bool = False):
         import torch
         self.torch = torch
         self.g = dgraph
@@ -217,7 +228,17 @@ class WindowSampler:
         self.seeds_dev = torch.empty(nseed, **i32)
         self.seed_off = torch.empty(self.max_nb + 1, dtype=torch.int64, device=device)
         self.keys = torch.empty(2 * self.max_nb, dtype=torch.int64, device=device)
-        self.counts = torch.empty(self.counts_len, dtype=torch.int64, device=device)
+        # counts vector + per-(batch, depth) counts of the depth layout right after it
+        self.counts = torch.empty(self.counts_len + self.max_nb * (self.H + 1), dtype=torch.int64, device=device)
+        self.depth_layout = bool(depth_layout and window_rows and local_ids)
+        self.row_map = None
+        if self.depth_layout:
+            self.row_map = torch.empty(max(self.uniq_cap, 1), dtype=torch.int32, device=device)
+            rb = _lib.lib().fgl_depth_relayout_ws_bytes(self.uniq_cap)
+            self.relayout_ws = torch.empty(rb, dtype=torch.uint8, device=device)
+            out3 = _lib.i64_array([0, 0, 0])
+            _lib.call("fgl_sample_ws_bitmaps", dgraph.num_nodes, self.max_nb, self.fcap, self.uniq_cap, out3)
+            self._bm_all_off, self._prefix_off, self._words = int(out3[0]), int(out3[1]), int(out3[2])
         # pinned staging of a window's inputs (seeds | offsets | keys): one
         # asynchronous host->device copy per stage(); the event guards reuse
         pin = (lambda t: t.pin_memory()) if torch.cuda.is_available() else (lambda t: t)
@@ -270,6 +291,15 @@ class WindowSampler:
         _lib.call("fgl_sample_window", self.g.struct, self.seeds_dev.data_ptr(),
                   self.seed_off.data_ptr(), int(seed_off_host[-1]), nb, self.keys.data_ptr(),
                   self._fan, self.H, self._out, self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+        if self.depth_layout:
+            # rows of every batch in (depth, node id) order: each layer's rows become a prefix
+            ws = self.ws.data_ptr()
+            dc = self.counts.data_ptr() + 8 * counts_layout(self.H, nb)["len"]
+            _lib.call("fgl_depth_relayout", self.counts.data_ptr(), self.H, nb, self.frontier.data_ptr(), self.fcap,
+                      ws + self._bm_all_off, ws + self._prefix_off, self._words, self.unique.data_ptr(),
+                      self.uniq_cap, self.tgt_row.data_ptr(), self.src_row.data_ptr(),
+                      self.seed_rows.data_ptr(), int(seed_off_host[-1]), self.row_map.data_ptr(), dc,
+                      self.relayout_ws.data_ptr(), self.relayout_ws.numel(), st.cuda_stream)
         return DeviceWindow(nb, self.H, self, seed_off_host)
 
     def sample(self, seed_lists, seeds_for_rng) -> DeviceWindow:

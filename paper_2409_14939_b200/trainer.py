@@ -270,7 +270,7 @@ class Pipeline:
         lab = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(np.asarray(labels, dtype=np.int64))
         self.labels = lab.to(device=device, dtype=torch.int64)
         self.sampler = WindowSampler(self.dg, cfg.fanouts, cfg.batch_size, cfg.window_n, device=device,
-                                     window_rows=cfg.arch != "gcn")
+                                     window_rows=cfg.arch != "gcn", depth_layout=cfg.arch != "gcn")
         out = _lib.i64_array([0, 0, 0])
         _lib.call("fgl_sample_ws_bitmaps", self.dg.num_nodes, cfg.window_n, self.sampler.fcap,
                   self.sampler.uniq_cap, out)
@@ -362,6 +362,7 @@ class Pipeline:
             else:
                 lt, ls = s.tgt_row, s.src_row
                 rows = cols = win.unique_total()
+            grouped = (not self.compact) and s.depth_layout
             rows, cols = max(rows, 1), max(cols, 1)
             lay = {
                 "indptr": self._buf(f"ip{h}", rows + 1, 1, torch.int64),
@@ -373,12 +374,23 @@ class Pipeline:
                 "col_global": s.src.data_ptr() + 4 * e0,
                 "nnz": nnz,
             }
-            wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
-            pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
-            self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
-                       cols, {"gin": 0, "gcn": 1, "sage": 2}[self.cfg.arch], lay["indptr"].data_ptr(),
-                       lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
-                       lay["t_w"].data_ptr(), pws.data_ptr(), wsb, self.stream)
+            arch_code = {"gin": 0, "gcn": 1, "sage": 2}[self.cfg.arch]
+            if grouped:  # depth-major targets are grouped but not ascending
+                colb = self._buf(f"colg{h}", max(nnz, 1), 1, torch.int32)
+                lay["col"] = colb.data_ptr()
+                wsb = _lib.lib().fgl_prepare_layer_grouped_ws_bytes(nnz, rows, cols)
+                pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
+                self._call("fgl_prepare_layer_grouped", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
+                           cols, arch_code, lay["indptr"].data_ptr(), colb.data_ptr(), lay["w"].data_ptr(),
+                           lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(), lay["t_w"].data_ptr(),
+                           pws.data_ptr(), wsb, self.stream)
+            else:
+                wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
+                pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
+                self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
+                           cols, arch_code, lay["indptr"].data_ptr(),
+                           lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
+                           lay["t_w"].data_ptr(), pws.data_ptr(), wsb, self.stream)
             layers[self.H - 1 - h] = lay
         return layers
 
@@ -387,7 +399,10 @@ class Pipeline:
         """(first, last) row of batch b in model layer i's output row space."""
         if self.compact:
             return win.front_range(self.H - 1 - i, b)
-        return win.unique_range(b)
+        u0, u1 = win.unique_range(b)
+        if win.s.depth_layout:  # depth-major rows: layer i needs a prefix
+            return u0, u0 + win.prefix_rows(i, b)
+        return u0, u1
 
     def _in_base(self, win, i, b):
         """Row of batch b's first input row in layer i's input index space."""
@@ -422,12 +437,14 @@ class Pipeline:
         if not self.direct_x0 and self.cache is not None and self.cache.k > 0:
             self._call("fgl_gather_rows_cached", self.feats.data_ptr(), self.ldf, self.d0,
                        s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
+                       s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None,
                        self.cache.slot.data_ptr(), self.cache.table.data_ptr(), self.ldf,
                        x0.data_ptr(), self.ldf, self.loaded.data_ptr(), self.cache_hits.data_ptr(), st)
         elif not self.direct_x0:
-            self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0,
+            self._call("fgl_gather_rows_cached", self.feats.data_ptr(), self.ldf, self.d0,
                        s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
-                       x0.data_ptr(), self.ldf, self.loaded.data_ptr(), st)
+                       s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None,
+                       None, None, self.ldf, x0.data_ptr(), self.ldf, self.loaded.data_ptr(), None, st)
         # forward
         X, ldx = x0, self.ldf
         H_bufs, Y_bufs, ns = [], [], []
@@ -489,10 +506,13 @@ class Pipeline:
                 nx = q1 - q0
                 dXn = self._buf(f"dx{i}", nx, _ld(din))
                 col_base = self._rows(win, i, b)[0]
-                self_x = dH.data_ptr() if not self.compact else None
+                prefix = (not self.compact) and s.depth_layout
+                self_x = dH.data_ptr() if (not self.compact and not prefix) else None
                 self._call("fgl_spmm", lay["t_indptr"].data_ptr() + 8 * q0, lay["t_col"].data_ptr(),
                            lay["t_w"].data_ptr(), nx, col_base, dH.data_ptr(), _ld(din), self_x,
                            _ld(din), dXn.data_ptr(), _ld(din), din, st)
+                if prefix:  # root term dx += dh on the layer's own (prefix) rows only
+                    self._call("fgl_add_rows", dXn.data_ptr(), _ld(din), dH.data_ptr(), _ld(din), n, din, st)
                 dX, lddx = dXn, _ld(din)
         if self.dist is not None:
             self.dist.allreduce_mean(self.model.grad)
@@ -634,7 +654,8 @@ class Pipeline:
             self._side = torch.cuda.Stream(device=self.device)
             self._samplers = [self.sampler, WindowSampler(self.dg, self.cfg.fanouts, self.cfg.batch_size,
                                                           self.cfg.window_n, device=self.device,
-                                                          window_rows=self.cfg.arch != "gcn")]
+                                                          window_rows=self.cfg.arch != "gcn",
+                                                          depth_layout=self.cfg.arch != "gcn")]
         smp = self._samplers[slot]
         done = getattr(self, "_slot_done", {}).get(slot)
         if done is not None:  # the compute of the window that last used this slot
