@@ -302,6 +302,7 @@ class Pipeline:
                                   dtype=torch.uint8, device=device)
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
+        self._graveyard = []
         self.gpu_launches = 0
         self.fused_upper = self._fused_upper_ok()
         self._pre_h0 = None
@@ -315,6 +316,10 @@ class Pipeline:
         need = max(int(rows), 1) * int(cols)
         t = self._bufs.get(name)
         if t is None or t.numel() < need or t.dtype != dtype:
+            if t is not None:
+                # buffers are used from two streams: a replaced one may still be
+                # read by queued kernels, so it is kept alive, never recycled
+                self._graveyard.append(t)
             t = torch.empty(int(need * 1.25) + 64, dtype=dtype, device=self.device)
             self._bufs[name] = t
         return t
@@ -346,9 +351,10 @@ class Pipeline:
         return greedy_order(m)
 
     # ------------------------------------------------------------ prepare --
-    def prepare(self, win) -> list:
+    def prepare(self, win, slot: int = 0) -> list:
         """Block CSR (+ stable transpose, GCN weights) of every model layer for
-        the whole window (trainer.py:165-179)."""
+        the whole window (trainer.py:165-179).  `slot` selects one of two
+        buffer sets, so the next window can be prepared while this one trains."""
         torch = self.torch
         s = self.sampler
         layers = [None] * self.L
@@ -365,28 +371,28 @@ class Pipeline:
             grouped = (not self.compact) and s.depth_layout
             rows, cols = max(rows, 1), max(cols, 1)
             lay = {
-                "indptr": self._buf(f"ip{h}", rows + 1, 1, torch.int64),
-                "w": self._buf(f"w{h}", max(nnz, 1), 1),
-                "t_indptr": self._buf(f"tip{h}", cols + 1, 1, torch.int64),
-                "t_col": self._buf(f"tc{h}", max(nnz, 1), 1, torch.int32),
-                "t_w": self._buf(f"tw{h}", max(nnz, 1), 1),
+                "indptr": self._buf(f"ip{h}s{slot}", rows + 1, 1, torch.int64),
+                "w": self._buf(f"w{h}s{slot}", max(nnz, 1), 1),
+                "t_indptr": self._buf(f"tip{h}s{slot}", cols + 1, 1, torch.int64),
+                "t_col": self._buf(f"tc{h}s{slot}", max(nnz, 1), 1, torch.int32),
+                "t_w": self._buf(f"tw{h}s{slot}", max(nnz, 1), 1),
                 "col": ls.data_ptr() + 4 * e0,
                 "col_global": s.src.data_ptr() + 4 * e0,
                 "nnz": nnz,
             }
             arch_code = {"gin": 0, "gcn": 1, "sage": 2}[self.cfg.arch]
             if grouped:  # depth-major targets are grouped but not ascending
-                colb = self._buf(f"colg{h}", max(nnz, 1), 1, torch.int32)
+                colb = self._buf(f"colg{h}s{slot}", max(nnz, 1), 1, torch.int32)
                 lay["col"] = colb.data_ptr()
                 wsb = _lib.lib().fgl_prepare_layer_grouped_ws_bytes(nnz, rows, cols)
-                pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
+                pws = self._buf(f"pws{h}s{slot}", wsb, 1, torch.uint8)
                 self._call("fgl_prepare_layer_grouped", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
                            cols, arch_code, lay["indptr"].data_ptr(), colb.data_ptr(), lay["w"].data_ptr(),
                            lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(), lay["t_w"].data_ptr(),
                            pws.data_ptr(), wsb, self.stream)
             else:
                 wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
-                pws = self._buf(f"pws{h}", wsb, 1, torch.uint8)
+                pws = self._buf(f"pws{h}s{slot}", wsb, 1, torch.uint8)
                 self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
                            cols, arch_code, lay["indptr"].data_ptr(),
                            lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
@@ -519,7 +525,7 @@ class Pipeline:
         self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
 
     # --------------------------------------------- layer-0 run-ahead --
-    def _launch_l0_aggs(self, win, order, layers):
+    def _launch_l0_aggs(self, win, order, layers, slot: int = 0, stream=None):
         """Layer 0's aggregation H0 = A_0 X (features straight from the HBM
         table) depends on the sampled window only, not on the weights, so
         the aggregations of ALL batches of the window are issued up front on a
@@ -531,24 +537,26 @@ class Pipeline:
         if not (self.direct_x0 and self.compact):
             self._pre_h0 = None
             return
-        if self._agg_stream is None:
-            self._agg_stream = torch.cuda.Stream(device=self.device)
-        ready = torch.cuda.Event()
-        ready.record()  # prepare of this window (and every earlier batch step) is ordered before
-        self._agg_stream.wait_event(ready)
+        if stream is None:
+            if self._agg_stream is None:
+                self._agg_stream = torch.cuda.Stream(device=self.device)
+            stream = self._agg_stream
+            ready = torch.cuda.Event()
+            ready.record()  # prepare of this window (and every earlier batch step) is ordered before
+            stream.wait_event(ready)
         lay = layers[0]
         din = self.cfg.layer_dims[0]
         pre = {}
-        with torch.cuda.stream(self._agg_stream):
-            st = self._agg_stream.cuda_stream
+        with torch.cuda.stream(stream):
+            st = stream.cuda_stream
             for j, b in enumerate(order):
                 r0, r1 = self._rows(win, 0, b)
                 n = r1 - r0
-                Hb = self._buf(f"h0_run{j}", n, _ld(din))
+                Hb = self._buf(f"h0_run{j}s{slot}", n, _ld(din))
                 self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
                            n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din, st)
                 ev = torch.cuda.Event()
-                ev.record(self._agg_stream)
+                ev.record(stream)
                 pre[b] = (Hb, ev)
         self._pre_h0 = pre
         self._pre_h0_win = win
@@ -680,16 +688,23 @@ class Pipeline:
         for w in range(len(windows)):
             win = pending
             nb = win.num_batches
+            slot = w % 2
+            self.sampler = win.s
             with torch.cuda.stream(self._side):
                 win.host_counts()  # window w's sampling is complete
                 # match counts ride the side stream too, so their read-back does
                 # not wait for window w-1's compute on the main stream
                 order = self.schedule(win, nb)
+                # the weight-independent work of window w -- block CSRs and the
+                # layer-0 aggregations -- also runs on the side stream, under
+                # window w-1's compute; its buffers alternate between two slots
+                layers = self.prepare(win, slot)
+                self._launch_l0_aggs(win, order, layers, slot, stream=self._side)
+                prepped = torch.cuda.Event()
+                prepped.record(self._side)
             if w + 1 < len(windows):
                 pending = self._sample_async(*windows[w + 1], slot=(w + 1) % 2)
-            self.sampler = win.s
-            layers = self.prepare(win)
-            self._launch_l0_aggs(win, order, layers)
+            torch.cuda.current_stream().wait_event(prepped)
             for j, b in enumerate(order):
                 prev = order[j - 1] if (j > 0 and self.flags.match) else None
                 self.batch_step(win, b, prev, j, layers, j % 2)
