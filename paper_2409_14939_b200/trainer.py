@@ -684,36 +684,56 @@ class Pipeline:
         windows = list(windows)
         if not windows:
             return
+        # the weight-dependent chain (dense / backward / SGD, many short
+        # kernels) is the critical path: it runs on a HIGH-priority stream so
+        # its CTAs are scheduled ahead of the wide sampling / aggregation
+        # kernels of the side streams whenever SMs free up
+        caller = torch.cuda.current_stream()
+        if not hasattr(self, "_main"):
+            try:
+                lo, hi = torch.cuda.Stream.priority_range()
+            except Exception:  # noqa: BLE001 - no priority support: default priority
+                lo = hi = 0
+            self._main = torch.cuda.Stream(device=self.device, priority=min(lo, hi))
+        self._main.wait_stream(caller)
         pending = self._sample_async(*windows[0], slot=0)
         for w in range(len(windows)):
             win = pending
             nb = win.num_batches
             slot = w % 2
             self.sampler = win.s
-            with torch.cuda.stream(self._side):
+            if not hasattr(self, "_prep"):
+                self._prep = torch.cuda.Stream(device=self.device)
+            sampled = torch.cuda.Event()
+            sampled.record(self._side)
+            self._prep.wait_event(sampled)
+            with torch.cuda.stream(self._prep):
                 win.host_counts()  # window w's sampling is complete
-                # match counts ride the side stream too, so their read-back does
+                # match counts ride the prepare stream, so their read-back does
                 # not wait for window w-1's compute on the main stream
                 order = self.schedule(win, nb)
                 # the weight-independent work of window w -- block CSRs and the
-                # layer-0 aggregations -- also runs on the side stream, under
-                # window w-1's compute; its buffers alternate between two slots
+                # layer-0 aggregations -- runs on a third stream, under window
+                # w-1's compute and concurrently with the sampling of window
+                # w+1; its buffers alternate between two slots
                 layers = self.prepare(win, slot)
-                self._launch_l0_aggs(win, order, layers, slot, stream=self._side)
+                self._launch_l0_aggs(win, order, layers, slot, stream=self._prep)
                 prepped = torch.cuda.Event()
-                prepped.record(self._side)
+                prepped.record(self._prep)
             if w + 1 < len(windows):
                 pending = self._sample_async(*windows[w + 1], slot=(w + 1) % 2)
-            torch.cuda.current_stream().wait_event(prepped)
-            for j, b in enumerate(order):
-                prev = order[j - 1] if (j > 0 and self.flags.match) else None
-                self.batch_step(win, b, prev, j, layers, j % 2)
-            ev = torch.cuda.Event()
-            ev.record()
+            with torch.cuda.stream(self._main):
+                self._main.wait_event(prepped)
+                for j, b in enumerate(order):
+                    prev = order[j - 1] if (j > 0 and self.flags.match) else None
+                    self.batch_step(win, b, prev, j, layers, j % 2)
+                ev = torch.cuda.Event()
+                ev.record(self._main)
             if not hasattr(self, "_slot_done"):
                 self._slot_done = {}
             self._slot_done[w % 2] = ev
             self.last_window = win
+            caller.wait_stream(self._main)  # the caller's stream sees this window's losses / weights
             yield order, self.loss_dev[:nb]
         self.sampler = self._samplers[0]
 
