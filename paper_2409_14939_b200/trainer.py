@@ -654,16 +654,18 @@ class Pipeline:
         return order, self.loss_dev[:nb]
 
     # --------------------------------------------------------- pipelined --
+    LOOKAHEAD = 2  # windows sampled ahead of the one being trained
+
     def _sample_async(self, seed_lists, rng_seeds, slot):
-        """Stage + launch the window sampler of ping-pong slot `slot` on the
-        side stream (asynchronous)."""
+        """Stage + launch the window sampler of slot `slot` (LOOKAHEAD + 1
+        samplers in rotation) on the sampling stream (asynchronous)."""
         torch = self.torch
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(device=self.device)
-            self._samplers = [self.sampler, WindowSampler(self.dg, self.cfg.fanouts, self.cfg.batch_size,
-                                                          self.cfg.window_n, device=self.device,
-                                                          window_rows=self.cfg.arch != "gcn",
-                                                          depth_layout=self.cfg.arch != "gcn")]
+            self._samplers = [self.sampler] + [
+                WindowSampler(self.dg, self.cfg.fanouts, self.cfg.batch_size, self.cfg.window_n, device=self.device,
+                              window_rows=self.cfg.arch != "gcn", depth_layout=self.cfg.arch != "gcn")
+                for _ in range(self.LOOKAHEAD)]
         smp = self._samplers[slot]
         done = getattr(self, "_slot_done", {}).get(slot)
         if done is not None:  # the compute of the window that last used this slot
@@ -671,15 +673,19 @@ class Pipeline:
         with torch.cuda.stream(self._side):
             nb, off = smp.stage(seed_lists, rng_seeds)
             win = smp.run(nb, off, stream=self._side)
+            win.sampled = torch.cuda.Event()
+            win.sampled.record(self._side)
         self.gpu_launches += 1
         return win
 
     def run_windows(self, windows):
-        """Train a sequence of windows [(seed_lists, rng_seeds), ...] with the
-        sampling of window w+1 (side stream, second sampler) overlapping the
-        schedule / prepare / compute of window w (current stream).  Yields
-        (order, device losses) per window; numerically identical to
-        run_window applied in sequence."""
+        """Train a sequence of windows [(seed_lists, rng_seeds), ...] on three
+        streams: sampling runs LOOKAHEAD windows ahead, the block CSRs and
+        layer-0 aggregations of window w run on a prepare stream under window
+        w-1's compute, and the weight-dependent chain runs on a high-priority
+        stream.  Yields (order, device losses) per window; numerically
+        identical to run_window applied in sequence."""
+        import collections
         torch = self.torch
         windows = list(windows)
         if not windows:
@@ -695,33 +701,40 @@ class Pipeline:
             except Exception:  # noqa: BLE001 - no priority support: default priority
                 lo = hi = 0
             self._main = torch.cuda.Stream(device=self.device, priority=min(lo, hi))
+            self._prep = torch.cuda.Stream(device=self.device)
+            self._io = torch.cuda.Stream(device=self.device)
+            self._prep_done = {}
         self._main.wait_stream(caller)
-        pending = self._sample_async(*windows[0], slot=0)
+        nsmp = self.LOOKAHEAD + 1
+        pending = collections.deque()
+        for k in range(min(self.LOOKAHEAD, len(windows))):
+            pending.append(self._sample_async(*windows[k], slot=k % nsmp))
         for w in range(len(windows)):
-            win = pending
+            win = pending.popleft()
             nb = win.num_batches
             slot = w % 2
             self.sampler = win.s
-            if not hasattr(self, "_prep"):
-                self._prep = torch.cuda.Stream(device=self.device)
-            sampled = torch.cuda.Event()
-            sampled.record(self._side)
-            self._prep.wait_event(sampled)
-            with torch.cuda.stream(self._prep):
-                win.host_counts()  # window w's sampling is complete
-                # match counts ride the prepare stream, so their read-back does
-                # not wait for window w-1's compute on the main stream
+            # the window's sizes and match counts are read on a small stream
+            # that waits for this window's sampling only (not for the prepare
+            # or sampling work queued behind it)
+            self._io.wait_event(win.sampled)
+            with torch.cuda.stream(self._io):
+                win.host_counts()
                 order = self.schedule(win, nb)
+            self._prep.wait_event(win.sampled)
+            if slot in self._prep_done:  # prepare buffers of this slot: window w-2 has trained
+                self._prep.wait_event(self._prep_done[slot])
+            with torch.cuda.stream(self._prep):
                 # the weight-independent work of window w -- block CSRs and the
-                # layer-0 aggregations -- runs on a third stream, under window
-                # w-1's compute and concurrently with the sampling of window
-                # w+1; its buffers alternate between two slots
+                # layer-0 aggregations -- runs under window w-1's compute and
+                # the sampling of later windows; buffers alternate between slots
                 layers = self.prepare(win, slot)
                 self._launch_l0_aggs(win, order, layers, slot, stream=self._prep)
                 prepped = torch.cuda.Event()
                 prepped.record(self._prep)
-            if w + 1 < len(windows):
-                pending = self._sample_async(*windows[w + 1], slot=(w + 1) % 2)
+            if w + self.LOOKAHEAD < len(windows):
+                k = w + self.LOOKAHEAD
+                pending.append(self._sample_async(*windows[k], slot=k % nsmp))
             with torch.cuda.stream(self._main):
                 self._main.wait_event(prepped)
                 for j, b in enumerate(order):
@@ -731,7 +744,8 @@ class Pipeline:
                 ev.record(self._main)
             if not hasattr(self, "_slot_done"):
                 self._slot_done = {}
-            self._slot_done[w % 2] = ev
+            self._slot_done[w % nsmp] = ev
+            self._prep_done[slot] = ev
             self.last_window = win
             caller.wait_stream(self._main)  # the caller's stream sees this window's losses / weights
             yield order, self.loss_dev[:nb]
