@@ -103,6 +103,8 @@ SIGNATURES = {
                                     vp, vp, vp, vp, C.c_int64, vp]),
     "fgl_spmm": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64,
                            vp, C.c_int64, C.c_int32, vp]),
+    "fgl_spmm_gather": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int64,
+                                  C.c_int32, C.c_int32, vp]),
     "fgl_dense_fwd": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, vp, C.c_int32, vp,
                                 C.c_int64, C.c_int32, vp]),
     "fgl_dense_bwd_ws_bytes": (C.c_int64, [C.c_int32, C.c_int32]),

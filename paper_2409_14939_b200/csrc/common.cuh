@@ -169,6 +169,8 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
               cudaStream_t st, int* err);
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
                int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
+bool tc_wgrad4(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
+               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
 // tcgen05 3xTF32 weight gradient partials: part[c][K+1][N] (row K = db).
 bool tc_wgrad(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);

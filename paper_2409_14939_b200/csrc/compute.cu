@@ -274,21 +274,38 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(
 
 // Sum partials over chunks in a fixed order (deterministic): each CTA owns 32
 // outputs; 8 thread groups sum interleaved chunks, then a fixed-order combine.
+// dW / db from per-CTA partials, summed in a fixed order (deterministic).
+// kp1 == 0: partial element i is output i (dW row-major, then db); kp1 = K+1:
+// partials are stored feature-major ([N][K+1], coalesced tensor-core
+// epilogue), element j = n*(K+1) + k is output k*N + n (k == K: db[n]).
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int chunks, int64_t n,
-                                       float* __restrict__ out, int64_t split, float* __restrict__ out2) {
+                                       float* __restrict__ out, int64_t split, float* __restrict__ out2, int kp1) {
   __shared__ float sm[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t i = blockIdx.x * 32 + lane;
   float s = 0.f;
-  if (i < n)
-    for (int c = grp; c < chunks; c += 8) s = __fadd_rn(s, part[(int64_t)c * n + i]);
+  if (i < n) {
+    const float* q = part + i;
+    int c = grp;
+    for (; c + 24 < chunks; c += 32) {  // four independent loads in flight
+      const float a = q[(int64_t)c * n], b = q[(int64_t)(c + 8) * n], d = q[(int64_t)(c + 16) * n],
+                  e = q[(int64_t)(c + 24) * n];
+      s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, a), b), d), e);
+    }
+    for (; c < chunks; c += 8) s = __fadd_rn(s, q[(int64_t)c * n]);
+  }
   sm[grp][lane] = s;
   __syncthreads();
   if (grp == 0 && i < n) {
     float t = sm[0][lane];
 #pragma unroll
     for (int g = 1; g < 8; ++g) t = __fadd_rn(t, sm[g][lane]);
-    if (i < split) out[i] = t; else out2[i - split] = t;
+    int64_t o = i;
+    if (kp1 > 0) {
+      const int64_t nn = i / kp1, k = i - nn * kp1;
+      o = k * (n / kp1) + nn;
+    }
+    if (o < split) out[o] = t; else out2[o - split] = t;
   }
 }
 
@@ -443,10 +460,12 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     int werr = 0;
     const int tc_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 128)));
     const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(n, 64)));
-    int used_chunks = chunks;
-    if (tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
+    int used_chunks = chunks, kp1 = 0;
+    if (tc_wgrad4(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr) ||
+        tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
       if (werr) return werr;
       used_chunks = tc3_chunks;
+      kp1 = din + 1;
     } else if (tc_wgrad(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc_chunks, st, &werr)) {
       if (werr) return werr;
       used_chunks = tc_chunks;
@@ -457,7 +476,7 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
                                                                   rows_per, pw, vec);
     }
     FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
-        pw, used_chunks, outs, dW, (int64_t)din * dout, db);
+        pw, used_chunks, outs, dW, (int64_t)din * dout, db, kp1);
     int err = 0;
     if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
       if (err) return err;

@@ -386,15 +386,17 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
 //   warps 12-15 epilogue: the CTA's [K+1][N] partial -> global (summed by
 //               reduce_partials_kernel, deterministic order).
 constexpr int WG3_MT = 64;   // rows per bulk-copied tile
-constexpr int WG3_NC = 4;    // A / B chunk ring depth (32 rows each)
-constexpr int WG3_R = 2;     // raw tile slots
+constexpr int WG3_NC = 3;    // A / B chunk ring depth (32 rows each; 3 leaves room for 3 raw slots)
+constexpr int WG3_R_MAX = 4; // raw tile slots (as many as fit)
 
 struct Wg3Args {
   const float* H; const float* dZ; const float* mask;
   int64_t ldh, ldz, ldm;
-  float* part;         // [gridDim.x][K+1][N]
+  float* part;         // [gridDim.x][N][K+1] (feature-major)
   int64_t M;
   int K, N, N_pad, tmem_cols, h_bytes, z_bytes, m_bytes, dbg;
+  int R, NC;  // raw tile slots, A/B chunk ring depth
+  int piece;  // bulk-copy request size (bytes, multiple of 16)
 };
 
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
@@ -404,35 +406,43 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
   const int N_pad = p.N_pad;
   const int b_box = N_pad * 128;  // one SW128 box: N_pad rows x 32 K (rows r) fp32
   char* sB = smem;                                  // [NC][hi, lo] boxes
-  char* slots = sB + WG3_NC * 2 * b_box;
+  char* slots = sB + p.NC * 2 * b_box;
   const int slot_bytes = p.h_bytes + p.z_bytes + p.m_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + WG3_R * slot_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * WG3_R + 2 * WG3_NC + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + p.R * slot_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.R + 2 * p.NC + 1);
   auto bar = [&](int i) { return smem_u32(bars + i); };
-  const int FULL = 0, EMPTY = WG3_R, CFULL = 2 * WG3_R, CEMPTY = 2 * WG3_R + WG3_NC, TFULL = 2 * WG3_R + 2 * WG3_NC;
+  const int FULL = 0, EMPTY = p.R, CFULL = 2 * p.R, CEMPTY = 2 * p.R + p.NC, TFULL = 2 * p.R + 2 * p.NC;
   if (tid == 0) {
-    for (int s = 0; s < WG3_R; ++s) { mbar_init_n(bar(FULL + s), 1); mbar_init_n(bar(EMPTY + s), G3_CONV_THREADS); }
-    for (int c = 0; c < WG3_NC; ++c) { mbar_init_n(bar(CFULL + c), G3_CONV_THREADS); mbar_init_n(bar(CEMPTY + c), 1); }
+    for (int s = 0; s < p.R; ++s) { mbar_init_n(bar(FULL + s), 1); mbar_init_n(bar(EMPTY + s), G3_CONV_THREADS); }
+    for (int c = 0; c < p.NC; ++c) { mbar_init_n(bar(CFULL + c), G3_CONV_THREADS / 2); mbar_init_n(bar(CEMPTY + c), 1); }
     mbar_init_n(bar(TFULL), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (tid == 0) G3T(0);
   const int64_t tiles = ceil_div(p.M, WG3_MT);
   if (warp == 0) {
     if (lane == 0) {
       int j = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
-        const int s = j % WG3_R;
-        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / WG3_R) & 1u) ^ 1u);
+        const int s = j % p.R;
+        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / p.R) & 1u) ^ 1u);
+        if (j < 8) G3T(58 + j);
         const int64_t r0 = t * WG3_MT;
         const int rows = (int)(p.M - r0 < WG3_MT ? p.M - r0 : WG3_MT);
         const uint32_t hb = (uint32_t)(rows * p.ldh * 4), zb = (uint32_t)(rows * p.ldz * 4),
                        mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
-        bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
-        bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
-        if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
+        auto load = [&](uint32_t dst, const float* src, uint32_t bytes) {
+          for (uint32_t o = 0; o < bytes; o += (uint32_t)p.piece) {
+            const uint32_t b = bytes - o < (uint32_t)p.piece ? bytes - o : (uint32_t)p.piece;
+            bulk_load(dst + o, reinterpret_cast<const char*>(src) + o, b, bar(FULL + s));
+          }
+        };
+        load(smem_u32(slot), p.H + r0 * p.ldh, hb);
+        load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb);
+        if (p.mask) load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb);
       }
     }
     return;
@@ -449,10 +459,11 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
     const uint32_t idesc = idesc_tf32(G3_M, N_pad, 0, 0);
     const uint32_t sb = smem_u32(sB);
     int cc = 0;
-    for (int j = 0; j < my_tiles; ++j) {
+    for (int j = 0; j < ((p.dbg & 16) ? 0 : my_tiles); ++j) {
       for (int c = 0; c < WG3_MT / 32; ++c, ++cc) {
-        const int cs = cc % WG3_NC;
-        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / WG3_NC) & 1u);
+        const int cs = cc % p.NC;
+        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / p.NC) & 1u);
+        if (cc < 8 && lane == 0) G3T(50 + cc);
         tc_fence_after();
         const uint32_t ahi = ch_hi(cs), alo = ahi + 32;
         const uint32_t bh = sb + (uint32_t)(cs * 2 * b_box), bl = bh + (uint32_t)b_box;
@@ -471,27 +482,295 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
     }
     if (my_tiles > 0 && elect_one()) mma_commit(bar(TFULL));
     __syncwarp();
+  } else if (warp >= 4) {
+    // three groups of 4 warps (4-7, 8-11, 12-15) take every third 32-row
+    // chunk, so one group's TMEM-store / fence latency overlaps the others'
+    // shared-memory work; warps 12-15 then also run the epilogue
+    const int grp = (warp - 4) >> 2;
+    const int ct = tid - 128 - 128 * grp;  // 0..127 within the group
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;     // A' row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int kk = 0;
+    for (int cc = grp; cc < 2 * my_tiles; cc += 3, ++kk) {
+      const int j = cc >> 1, c = cc & 1;
+      const int s = j % p.R;
+      const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
+      const int rows = (int)(p.M - t * WG3_MT < WG3_MT ? p.M - t * WG3_MT : WG3_MT);
+      mbar_wait(bar(FULL + s), (uint32_t)(j / p.R) & 1u);
+      const bool trc = ct == 0 && grp == 0 && kk < 8;
+      if (trc) G3T(2 + 6 * kk);
+      const uint32_t hs = smem_u32(slots + s * slot_bytes);
+      const uint32_t zs = hs + (uint32_t)p.h_bytes, ms = zs + (uint32_t)p.z_bytes;
+      {
+        const int cs = cc % p.NC;
+        // A': column m of rows r = 32c + [0, 32) (conflict-free: consecutive
+        // lanes read consecutive features of one row)
+        // branch-free: all 32 loads issue back to back (rows past the tile
+        // end read stale in-bounds slot data and are zeroed after)
+        uint32_t hv[32], lv[32];
+        {
+          const int nrow = rows - 32 * c;
+          const uint32_t a0 = hs + (uint32_t)((32 * c * p.ldh + (m < p.K ? m : 0)) * 4);
+          const uint32_t rs = (uint32_t)(p.ldh * 4);
+          float xs[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) xs[q] = lds32(a0 + (uint32_t)q * rs);
+          const float one = m == p.K ? 1.f : 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float x = q < nrow ? (m < p.K ? xs[q] : one) : 0.f;
+            const float hi = tf32_rna_finite(x);
+            hv[q] = __float_as_uint(hi);
+            lv[q] = __float_as_uint(__fsub_rn(x, hi));
+          }
+        }
+        if (trc) G3T(3 + 6 * kk);
+        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / p.NC) & 1u) ^ 1u);
+        if (trc) G3T(4 + 6 * kk);
+        tc_fence_after();
+        const uint32_t hi_t = ch_hi(cs) + lane_off;
+        tmem_st32(hi_t, hv);
+        tmem_st32(hi_t + 32, lv);
+        // B': 4x4 blocks (rows 4rq..4rq+3 of the chunk x features 4n4..4n4+3):
+        // four 16-byte row loads, a register transpose, four 16-byte stores
+        // into the SW128 box (row n, K = r).  Item -> (n4, rq) is chosen so
+        // that each 8-lane phase hits 8 distinct bank groups on both sides:
+        // loads by n4 mod 8, stores by rq ^ (n & 7).
+        const uint32_t bh = smem_u32(sB) + (uint32_t)(cs * 2 * b_box);
+        const int n4s = N_pad >> 2;
+        const int items = ((n4s + 7) >> 3) * 64;
+        for (int t = ct; t < ((p.dbg & 4) ? 0 : items); t += G3_CONV_THREADS / 2) {
+          const int ph = t & 7, hi_ = t >> 3;
+          const int n4 = ph + 8 * (hi_ >> 3);
+          const int rq = (((ph >> 1) + (hi_ & 3)) & 3) + 4 * ((hi_ >> 2) & 1);
+          if (n4 >= n4s) continue;
+          const int rb = 32 * c + 4 * rq;
+          float4 e[4];
+          if (rb + 4 <= rows && 4 * n4 + 4 <= p.N && p.mask) {
+            // interior block (the common case): no row / feature predicates
+            float4 mk[4];
+            const uint32_t za = zs + (uint32_t)((rb * p.ldz + 4 * n4) * 4), zr = (uint32_t)(p.ldz * 4);
+            const uint32_t ma = ms + (uint32_t)((rb * p.ldm + 4 * n4) * 4), mr = (uint32_t)(p.ldm * 4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[i] = lds128(za + (uint32_t)i * zr);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mk[i] = lds128(ma + (uint32_t)i * mr);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              e[i].x = mk[i].x > 0.f ? e[i].x : 0.f;
+              e[i].y = mk[i].y > 0.f ? e[i].y : 0.f;
+              e[i].z = mk[i].z > 0.f ? e[i].z : 0.f;
+              e[i].w = mk[i].w > 0.f ? e[i].w : 0.f;
+            }
+          } else {
+            const int nn = 4 * n4 < p.N ? 4 * n4 : 0;
+            float4 mk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[i] = lds128(zs + (uint32_t)(((rb + i) * p.ldz + nn) * 4));
+            if (p.mask) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) mk[i] = lds128(ms + (uint32_t)(((rb + i) * p.ldm + nn) * 4));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+            }
+            // keep feature f < N of row r < rows with a positive mask
+            const int nv = 4 * n4 < p.N ? min(p.N - 4 * n4, 4) : 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const bool rv = rb + i < rows;
+              e[i].x = (rv && nv > 0 && mk[i].x > 0.f) ? e[i].x : 0.f;
+              e[i].y = (rv && nv > 1 && mk[i].y > 0.f) ? e[i].y : 0.f;
+              e[i].z = (rv && nv > 2 && mk[i].z > 0.f) ? e[i].z : 0.f;
+              e[i].w = (rv && nv > 3 && mk[i].w > 0.f) ? e[i].w : 0.f;
+            }
+          }
+          const float4 col[4] = {make_float4(e[0].x, e[1].x, e[2].x, e[3].x), make_float4(e[0].y, e[1].y, e[2].y, e[3].y),
+                                 make_float4(e[0].z, e[1].z, e[2].z, e[3].z), make_float4(e[0].w, e[1].w, e[2].w, e[3].w)};
+#pragma unroll
+          for (int jn = 0; jn < 4; ++jn) {
+            float4 h4, l4;
+            h4.x = tf32_rna_finite(col[jn].x); l4.x = __fsub_rn(col[jn].x, h4.x);
+            h4.y = tf32_rna_finite(col[jn].y); l4.y = __fsub_rn(col[jn].y, h4.y);
+            h4.z = tf32_rna_finite(col[jn].z); l4.z = __fsub_rn(col[jn].z, h4.z);
+            h4.w = tf32_rna_finite(col[jn].w); l4.w = __fsub_rn(col[jn].w, h4.w);
+            const uint32_t off = sw128_off(4 * n4 + jn, 4 * rq);
+            sts128(bh + off, h4);
+            sts128(bh + (uint32_t)b_box + off, l4);
+          }
+        }
+        if (trc) G3T(5 + 6 * kk);
+        tmem_st_wait();
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(bar(CFULL + cs));
+        if (trc) G3T(6 + 6 * kk);
+      }
+      mbar_arrive(bar(EMPTY + s));
+      if (trc) G3T(7 + 6 * kk);
+    }
+  }
+  if (warp >= 12) {
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    float* out = p.part + (int64_t)blockIdx.x * (p.K + 1) * p.N;
+    if (my_tiles > 0) {
+      mbar_wait(bar(TFULL), 0);
+      tc_fence_after();
+    }
+    if (tid == 384) G3T(70);
+    for (int c0 = 0; c0 < N_pad; c0 += 16) {
+      uint32_t v[16];
+      if (my_tiles > 0) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      if (m <= p.K) {  // feature-major partials: a warp stores 32 consecutive floats per column
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
+      }
+    }
+    if (tid == 384) G3T(71);
+  }
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, p.tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------- wgrad v4 --
+// Same partials as tc_wgrad3_kernel, with B' = masked dZ fed to the MMA as an
+// MN-major swizzled operand: the producer's TMA tensor copies land dZ (and
+// the mask) in 64-row x 32-column swizzled boxes that ARE the operand layout,
+// so the converters only split them in place (hi) and beside (lo) with
+// 16-byte shared accesses -- no transpose.  A' = H^T still goes through TMEM
+// (K-major, thread = feature = TMEM lane), and the raw slot is released by
+// the MMA's commit once both of its chunks have been multiplied.
+constexpr int WG4_MT = 64;
+
+struct Wg4Args {
+  const float* H;
+  int64_t ldh;
+  float* part;         // [gridDim.x][N][K+1] (feature-major)
+  int64_t M;
+  int K, N, N_mma, nblk, has_mask, tmem_cols, h_bytes, slot_bytes, R, NC, dbg;
+};
+
+// MN-major tf32 operand: the only smem layout the MMA takes for 32-bit MN-major
+// data is SWIZZLE_128B_BASE32B (layout type 1: 32-byte granules of each
+// 128-byte row XOR-ed with the row index mod 4; atoms of 32 MN elements x 4 K
+// rows), which is what a CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B TMA copy writes.
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128_32b(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;   // stride between 32-element MN atoms
+  d |= (uint64_t)(512 >> 4) << 32;               // stride between 4-row K groups
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad4_kernel(const __grid_constant__ CUtensorMap tmZ,
+                                                                  const __grid_constant__ CUtensorMap tmM, Wg4Args p) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int zbox = WG4_MT * 128;                    // one 64-row x 32-column SW128 box
+  const int zreg = p.nblk * zbox;                   // dZ (or mask, or lo) region of a slot
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.R * p.slot_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.R + 2 * p.NC + 1);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  // slot layout: [H raw rows | dZ (hi after the split) | lo | mask]
+  auto slot_h = [&](int s) { return smem_u32(smem + s * p.slot_bytes); };
+  auto slot_z = [&](int s) { return slot_h(s) + (uint32_t)p.h_bytes; };
+  const int FULL = 0, EMPTY = p.R, CFULL = 2 * p.R, CEMPTY = 2 * p.R + p.NC, TFULL = 2 * p.R + 2 * p.NC;
+  if (tid == 0) {
+    for (int s = 0; s < p.R; ++s) { mbar_init_n(bar(FULL + s), 1); mbar_init_n(bar(EMPTY + s), 1); }
+    for (int c = 0; c < p.NC; ++c) { mbar_init_n(bar(CFULL + c), G3_CONV_THREADS / 2); mbar_init_n(bar(CEMPTY + c), 1); }
+    mbar_init_n(bar(TFULL), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tiles = ceil_div(p.M, WG4_MT);
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmZ);
+      if (p.has_mask) tma_prefetch_desc(&tmM);
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+        const int s = j % p.R;
+        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / p.R) & 1u) ^ 1u);
+        const int64_t r0 = t * WG4_MT;
+        const int rows = (int)(p.M - r0 < WG4_MT ? p.M - r0 : WG4_MT);
+        const uint32_t hb = (uint32_t)(rows * p.ldh * 4);
+        mbar_arrive_expect_tx(bar(FULL + s), hb + (uint32_t)(zreg * (1 + p.has_mask)));
+        bulk_load(slot_h(s), p.H + r0 * p.ldh, hb, bar(FULL + s));
+        for (int nb = 0; nb < p.nblk; ++nb) {
+          tma_load_2d(slot_z(s) + (uint32_t)(nb * zbox), &tmZ, 32 * nb, (int)r0, bar(FULL + s));
+          if (p.has_mask)
+            tma_load_2d(slot_z(s) + (uint32_t)(2 * zreg + nb * zbox), &tmM, 32 * nb, (int)r0, bar(FULL + s));
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto ch_hi = [&](int c) { return tmem + (uint32_t)(p.N_mma + 64 * c); };
+  const int my_tiles = (int)(tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+
+  if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(G3_M, p.N_mma, 0, 1);
+    int cc = 0;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int s = j % p.R;
+      for (int c = 0; c < WG4_MT / 32; ++c, ++cc) {
+        const int cs = cc % p.NC;
+        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / p.NC) & 1u);
+        tc_fence_after();
+        const uint32_t ahi = ch_hi(cs), alo = ahi + 32;
+        if (elect_one()) {
+#pragma unroll
+          for (int st = 0; st < ((p.dbg & 2) ? 0 : 4); ++st) {
+            const uint32_t kg = (uint32_t)((4 * c + st) * 1024);
+            const uint64_t dbh = umma_desc_mn_sw128_32b(slot_z(s) + kg, (uint32_t)zbox);
+            const uint64_t dbl = umma_desc_mn_sw128_32b(slot_z(s) + (uint32_t)zreg + kg, (uint32_t)zbox);
+            mma_tf32_ts(tmem, alo + 8 * st, dbh, idesc, (cc | st) != 0);
+            mma_tf32_ts(tmem, ahi + 8 * st, dbl, idesc, 1);
+            mma_tf32_ts(tmem, ahi + 8 * st, dbh, idesc, 1);
+          }
+          mma_commit(bar(CEMPTY + cs));
+          if (c == WG4_MT / 32 - 1) mma_commit(bar(EMPTY + s));
+        }
+        __syncwarp();
+      }
+    }
+    if (my_tiles > 0 && elect_one()) mma_commit(bar(TFULL));
+    __syncwarp();
   } else if (warp >= 4 && warp < 12) {
-    const int ct = tid - 128;              // 0..255
-    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    // two groups of 4 warps take alternate 32-row chunks
+    const int grp = (warp - 4) >> 2;
+    const int ct = tid - 128 - 128 * grp;  // 0..127 within the group
+    const int quarter = warp & 3;
     const int m = quarter * 32 + lane;     // A' row = TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int cc = 0;
     for (int j = 0; j < my_tiles; ++j) {
-      const int s = j % WG3_R;
+      const int s = j % p.R;
       const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
-      const int rows = (int)(p.M - t * WG3_MT < WG3_MT ? p.M - t * WG3_MT : WG3_MT);
-      mbar_wait(bar(FULL + s), (uint32_t)(j / WG3_R) & 1u);
-      const uint32_t hs = smem_u32(slots + s * slot_bytes);
-      const uint32_t zs = hs + (uint32_t)p.h_bytes, ms = zs + (uint32_t)p.z_bytes;
-      for (int c = 0; c < WG3_MT / 32; ++c, ++cc) {
-        const int cs = cc % WG3_NC;
-        // A': column m of rows r = 32c + 16 half + [0, 16) (conflict-free:
-        // consecutive lanes read consecutive features of one row)
-        uint32_t hv[16], lv[16];
+      const int rows = (int)(p.M - t * WG4_MT < WG4_MT ? p.M - t * WG4_MT : WG4_MT);
+      mbar_wait(bar(FULL + s), (uint32_t)(j / p.R) & 1u);
+      const uint32_t hs = slot_h(s), zs = slot_z(s);
+      for (int c = 0; c < WG4_MT / 32; ++c, ++cc) {
+        if (c != grp) continue;
+        const int cs = cc % p.NC;
+        uint32_t hv[32], lv[32];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int r = 32 * c + 16 * half + q;
+        for (int q = 0; q < 32; ++q) {
+          const int r = 32 * c + q;
           float x = 0.f;
           if (r < rows && !(p.dbg & 1)) {
             if (m < p.K) x = lds32(hs + (uint32_t)((r * p.ldh + m) * 4));
@@ -501,45 +780,42 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
           hv[q] = __float_as_uint(hi);
           lv[q] = __float_as_uint(__fsub_rn(x, hi));
         }
-        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / WG3_NC) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t hi_t = ch_hi(cs) + lane_off + (uint32_t)(16 * half);
-        tmem_st8(hi_t, *reinterpret_cast<uint32_t(*)[8]>(hv));
-        tmem_st8(hi_t + 8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8));
-        tmem_st8(hi_t + 32, *reinterpret_cast<uint32_t(*)[8]>(lv));
-        tmem_st8(hi_t + 40, *reinterpret_cast<uint32_t(*)[8]>(lv + 8));
-        // B': (n, 4 consecutive rows) groups -> SW128 box (row n, K = r);
-        // consecutive threads take consecutive n (conflict-free column loads)
-        const uint32_t bh = smem_u32(sB) + (uint32_t)(cs * 2 * b_box);
-        for (int idx = ct; idx < ((p.dbg & 4) ? 0 : N_pad * 8); idx += G3_CONV_THREADS) {
-          const int bn = idx % N_pad, br = idx / N_pad;
-          float e[4] = {0.f, 0.f, 0.f, 0.f};
-          if (bn < p.N) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int r = 32 * c + 4 * br + q;
-              if (r < rows) {
-                const float z = lds32(zs + (uint32_t)((r * p.ldz + bn) * 4));
-                const float mk = p.mask ? lds32(ms + (uint32_t)((r * p.ldm + bn) * 4)) : 1.f;
-                e[q] = mk > 0.f ? z : 0.f;
-              }
+        // B': split this chunk's 32 rows of every 32-column box in place; the
+        // boxes' rows past M are zero-filled by the TMA, columns past N too
+        if (!(p.dbg & 4)) {
+          const int per = p.nblk * 256;  // 16-byte units: nblk boxes x 32 rows x 8
+          for (int u = ct; u < per; u += G3_CONV_THREADS / 2) {
+            const uint32_t off = (uint32_t)((u >> 8) * zbox + c * 4096 + (u & 255) * 16);
+            float4 z = lds128(zs + off);
+            if (p.has_mask) {
+              const float4 mk = lds128(zs + (uint32_t)(2 * zreg) + off);
+              z.x = mk.x > 0.f ? z.x : 0.f;
+              z.y = mk.y > 0.f ? z.y : 0.f;
+              z.z = mk.z > 0.f ? z.z : 0.f;
+              z.w = mk.w > 0.f ? z.w : 0.f;
             }
+            float4 h4, l4;
+            h4.x = tf32_rna_finite(z.x); l4.x = __fsub_rn(z.x, h4.x);
+            h4.y = tf32_rna_finite(z.y); l4.y = __fsub_rn(z.y, h4.y);
+            h4.z = tf32_rna_finite(z.z); l4.z = __fsub_rn(z.z, h4.z);
+            h4.w = tf32_rna_finite(z.w); l4.w = __fsub_rn(z.w, h4.w);
+            sts128(zs + off, h4);
+            sts128(zs + (uint32_t)zreg + off, l4);
           }
-          float4 h4, l4;
-          h4.x = tf32_rna_finite(e[0]); l4.x = __fsub_rn(e[0], h4.x);
-          h4.y = tf32_rna_finite(e[1]); l4.y = __fsub_rn(e[1], h4.y);
-          h4.z = tf32_rna_finite(e[2]); l4.z = __fsub_rn(e[2], h4.z);
-          h4.w = tf32_rna_finite(e[3]); l4.w = __fsub_rn(e[3], h4.w);
-          const uint32_t off = sw128_off(bn, 4 * br);
-          sts128(bh + off, h4);
-          sts128(bh + (uint32_t)b_box + off, l4);
+        }
+        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / p.NC) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t hi_t = ch_hi(cs) + lane_off;
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          tmem_st8(hi_t + 8 * q8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8 * q8));
+          tmem_st8(hi_t + 32 + 8 * q8, *reinterpret_cast<uint32_t(*)[8]>(lv + 8 * q8));
         }
         tmem_st_wait();
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(bar(CFULL + cs));
       }
-      mbar_arrive(bar(EMPTY + s));
     }
   } else if (warp >= 12) {
     const int quarter = warp & 3;
@@ -549,13 +825,14 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
       mbar_wait(bar(TFULL), 0);
       tc_fence_after();
     }
-    for (int c0 = 0; c0 < N_pad; c0 += 16) {
+    for (int c0 = 0; c0 < p.N_mma; c0 += 16) {
+      if (c0 >= p.N) break;
       uint32_t v[16];
       if (my_tiles > 0) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-      if (m <= p.K) {
+      if (m <= p.K) {  // feature-major partials: a warp stores 32 consecutive floats per column
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          if (c0 + q < p.N) out[(int64_t)m * p.N + c0 + q] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
+          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
       }
     }
   }
@@ -666,6 +943,58 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   return true;
 }
 
+// fp32 [rows, cols] (ld floats) in 64-row x 32-column 128B_ATOM_32B-swizzled boxes,
+// columns past `cols` and rows past `rows` zero-filled
+bool make_map_wg4(CUtensorMap* m, const float* base, int64_t rows, int cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)WG4_MT};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tc_wgrad4(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
+               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
+  *err = 0;
+  static const int off = getenv("FGL_WGRAD") ? atoi(getenv("FGL_WGRAD")) : 3;  // opt-in (FGL_WGRAD=4): slower than v3
+  if (off != 4 || tc3_disabled() || M < 1 || K < 1 || K + 1 > G3_M || N < 1 || N > 256) return false;
+  if ((ldh % 4) || (reinterpret_cast<uintptr_t>(H) & 15) || (ldz % 4) || (reinterpret_cast<uintptr_t>(dZ) & 15))
+    return false;
+  if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
+  const int N_mma = (N + 31) / 32 * 32, nblk = N_mma / 32;
+  const int h_bytes = WG4_MT * (int)ldh * 4;  // multiple of 1024 (ldh % 4 == 0)
+  const int has_mask = mask ? 1 : 0;
+  const int slot = h_bytes + nblk * WG4_MT * 128 * (2 + has_mask);
+  const int NC = std::min(4, (512 - N_mma) / 64);
+  if (NC < 1) return false;
+  int R = 4;
+  auto smem_of = [&](int r) { return (int64_t)1024 + (int64_t)r * slot + 8 * (2 * r + 2 * NC + 1) + 16; };
+  while (R > 2 && smem_of(R) > G3_MAX_SMEM) --R;
+  if (smem_of(R) > G3_MAX_SMEM) return false;
+  CUtensorMap mZ, mM;
+  std::memset(&mZ, 0, sizeof(mZ));
+  std::memset(&mM, 0, sizeof(mM));
+  if (!make_map_wg4(&mZ, dZ, M, N, ldz)) return false;
+  if (mask && !make_map_wg4(&mM, mask, M, N, ldm)) return false;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    e = cudaFuncSetAttribute(tc_wgrad4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad4)"); return true; }
+    attr = true;
+  }
+  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
+  Wg4Args p{H, ldh, part, M, K, N, N_mma, nblk, has_mask, 512, h_bytes, slot, R, NC, dbg};
+  FGL_COUNT_LAUNCH(), tc_wgrad4_kernel<<<chunks, G3_THREADS, smem_of(R), st>>>(mZ, mM, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad4_kernel");
+  return true;
+}
+
 // Weight-gradient partials part[c][K+1][N] (row K = db) over `chunks` CTAs;
 // returns false outside the envelope (K + 1 <= 128, N <= 256, 16-byte rows).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
@@ -677,11 +1006,20 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
   const int N_pad = (N + 15) / 16 * 16;
   const int hb = WG3_MT * (int)ldh * 4, zb = WG3_MT * (int)ldz * 4, mb = mask ? WG3_MT * (int)ldm * 4 : 0;
-  const int64_t smem = 1024 + (int64_t)WG3_NC * 2 * N_pad * 128 + (int64_t)WG3_R * (hb + zb + mb) +
-                       8 * (2 * WG3_R + 2 * WG3_NC + 1) + 16;
+  // deepest raw-tile ring that fits next to the chunk ring: the kernel is a
+  // stream over H / dZ / mask, so bytes in flight per SM set its speed
+  static const int env_r = getenv("FGL_WG3_R") ? atoi(getenv("FGL_WG3_R")) : 0;
+  static const int env_nc = getenv("FGL_WG3_NC") ? atoi(getenv("FGL_WG3_NC")) : 0;
+  const int NC = env_nc > 0 ? env_nc : WG3_NC;
+  auto smem_of = [&](int R) {
+    return 1024 + (int64_t)NC * 2 * N_pad * 128 + (int64_t)R * (hb + zb + mb) + 8 * (2 * R + 2 * NC + 1) + 16;
+  };
+  int R = env_r > 0 ? env_r : WG3_R_MAX;
+  while (R > 2 && smem_of(R) > G3_MAX_SMEM) --R;
+  const int64_t smem = smem_of(R);
   if (smem > G3_MAX_SMEM) return false;
   int cols = 32;
-  while (cols < N_pad + 64 * WG3_NC) cols <<= 1;
+  while (cols < N_pad + 64 * NC) cols <<= 1;
   if (cols > 512) return false;
   static bool attr = false;
   cudaError_t e;
@@ -691,7 +1029,8 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg};
+  static const int piece = getenv("FGL_WG3_PIECE") ? atoi(getenv("FGL_WG3_PIECE")) : (1 << 30);
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, piece};
   FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
