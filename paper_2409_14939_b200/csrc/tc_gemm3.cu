@@ -88,11 +88,12 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
   char* slots = sB_lo + b_bytes;
   const int slot_bytes = p.a_slot_bytes + p.m_slot_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(slots + R * slot_bytes);
-  // full[R] empty[R] cfull[8] cempty[8] tfull[2] tempty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * R + 20);
+  // full[R] empty[R] cfull[8] cempty[8] tfull[2] tempty[2] bready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * R + 21);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
   auto bar = [&](int i) { return smem_u32(bars + i); };
-  const int FULL = 0, EMPTY = R, CFULL = 2 * R, CEMPTY = 2 * R + 8, TFULL = 2 * R + 16, TEMPTY = 2 * R + 18;
+  const int FULL = 0, EMPTY = R, CFULL = 2 * R, CEMPTY = 2 * R + 8, TFULL = 2 * R + 16, TEMPTY = 2 * R + 18,
+            BREADY = 2 * R + 20;
 
   if (tid == 0) {
     G3T(0);
@@ -101,13 +102,14 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       mbar_init_n(bar(EMPTY + s), G3_CONV_THREADS);
     }
     for (int c = 0; c < 8; ++c) {
-      mbar_init_n(bar(CFULL + c), G3_CONV_THREADS);
+      mbar_init_n(bar(CFULL + c), G3_CONV_THREADS / 2);
       mbar_init_n(bar(CEMPTY + c), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init_n(bar(TFULL + a), 1);
       mbar_init_n(bar(TEMPTY + a), G3_EPI_THREADS);
     }
+    mbar_init_n(bar(BREADY), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // barriers initialised
@@ -136,21 +138,23 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
   tc_fence_before();
   asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
   tc_fence_after();
-  {
+  if (warp == 2 || warp == 3 || warp >= 12) {
     // weight operand B[n][k] split into tf32 hi / lo, K-major SWIZZLE_128B
-    // boxes of 32 K columns (conflict-free tensor-core reads), by warps 1-15
-    // while the producer already streams A: one batch of 16-byte W loads per
-    // thread, then scattered shared stores
-    const int nt = G3_THREADS - 32, t0 = tid - 32;
-    const int W4 = MODE == 0 ? (p.N + 3) / 4 : (p.K + 3) / 4;  // float4 per W row
-    const int Wrows = MODE == 0 ? p.K : p.N;
-    const int total4 = Wrows * W4;
+    // boxes of 32 K columns (conflict-free tensor-core reads), by warps 2-3
+    // and the epilogue warps 12-15 while the producer streams A and the
+    // converters already convert it; the MMA issuer waits on BREADY.  Work
+    // item = 4x4 block (n 4n4.., k 4k4..) over [N_pad x K_pad] (covers every
+    // element the MMA reads, padding included, so no zeroing pass): four
+    // 16-byte W loads, a register transpose (mode 0: B = W^T), eight 16-byte
+    // shared stores; consecutive threads take consecutive k4 (conflict-free).
+    const int nt = 192, t0 = warp < 4 ? tid - 64 : tid - 384 + 64;
+    const int K4 = K_pad >> 2, N4 = N_pad >> 2, nblk = K4 * N4;
     const bool vec = p.w_vec;
-    const int rl = MODE == 0 ? p.N : p.K;
-    auto load4 = [&](int idx) {
+    const int rl = MODE == 0 ? p.N : p.K;  // W row length
+    const int wr = MODE == 0 ? p.K : p.N;  // W rows
+    auto wload = [&](int r, int c) {      // W[r][c..c+3], zero outside
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (idx < total4) {
-        const int r = idx / W4, c = 4 * (idx - r * W4);
+      if (r < wr && c < rl) {
         const float* src = p.W + (int64_t)r * rl + c;
         if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
         else {
@@ -162,33 +166,53 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       }
       return v;
     };
-    auto scatter4 = [&](int idx, float4 v) {
-      if (idx >= total4) return;
-      const int r = idx / W4, c = 4 * (idx - r * W4);
-      const float e[4] = {v.x, v.y, v.z, v.w};
+    constexpr int PER = 3;  // blocks per thread with all loads in flight
+    for (int b0 = t0; b0 < nblk; b0 += PER * nt) {
+      float4 w[PER][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int n = MODE == 0 ? c + q : r, k = MODE == 0 ? r : c + q;
-        if (n >= N_pad || k >= K_pad) continue;
-        const float h = tf32_hi(e[q]);
-        const uint32_t off = (uint32_t)((k >> 5) * b_box) + sw128_off(n, k & 31);
-        *reinterpret_cast<float*>(sB_hi + off) = h;
-        *reinterpret_cast<float*>(sB_lo + off) = __fsub_rn(e[q], h);
+      for (int u = 0; u < PER; ++u) {
+        const int b = b0 + u * nt;
+        const int k4 = b % K4, n4 = b / K4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          w[u][i] = b < nblk ? (MODE == 0 ? wload(4 * k4 + i, 4 * n4) : wload(4 * n4 + i, 4 * k4))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    };
-    // first batch of loads in flight while both B images are zeroed (padding
-    // rows / K columns must be 0, not leftover shared memory)
-    float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = load4(t0 + u * nt);
-    for (int z = t0; z < 2 * b_bytes / 16; z += nt) sts128(smem_u32(sB_hi) + 16 * z, make_float4(0.f, 0.f, 0.f, 0.f));
-    asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
+      for (int u = 0; u < PER; ++u) {
+        const int b = b0 + u * nt;
+        if (b >= nblk) break;
+        const int k4 = b % K4, n4 = b / K4;
+        float4 r4[4];  // r4[jn] = B[4 n4 + jn][4 k4 .. 4 k4 + 3]
+        if (MODE == 0) {
+          r4[0] = make_float4(w[u][0].x, w[u][1].x, w[u][2].x, w[u][3].x);
+          r4[1] = make_float4(w[u][0].y, w[u][1].y, w[u][2].y, w[u][3].y);
+          r4[2] = make_float4(w[u][0].z, w[u][1].z, w[u][2].z, w[u][3].z);
+          r4[3] = make_float4(w[u][0].w, w[u][1].w, w[u][2].w, w[u][3].w);
+        } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) scatter4(t0 + u * nt, v[u]);
-    for (int idx = t0 + 4 * nt; idx < total4; idx += nt) scatter4(idx, load4(idx));
+          for (int jn = 0; jn < 4; ++jn) r4[jn] = w[u][jn];
+        }
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) {
+          const int n = 4 * n4 + jn, k = 4 * k4;
+          float4 h4, l4;
+          h4.x = tf32_hi(r4[jn].x); l4.x = __fsub_rn(r4[jn].x, h4.x);
+          h4.y = tf32_hi(r4[jn].y); l4.y = __fsub_rn(r4[jn].y, h4.y);
+          h4.z = tf32_hi(r4[jn].z); l4.z = __fsub_rn(r4[jn].z, h4.z);
+          h4.w = tf32_hi(r4[jn].w); l4.w = __fsub_rn(r4[jn].w, h4.w);
+          const uint32_t off = (uint32_t)((k >> 5) * b_box) + sw128_off(n, k & 31);
+          sts128(smem_u32(sB_hi) + off, h4);
+          sts128(smem_u32(sB_lo) + off, l4);
+        }
+      }
+    }
     fence_async_smem();
     asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
-    if (tid == 32) G3T(1);
+    if (t0 == 0) {
+      G3T(1);
+      mbar_arrive(bar(BREADY));
+    }
   }
   const uint32_t tmem = *tmem_slot;
   // TMEM columns: accumulators [0, 2 N_pad), A chunk c: hi at 2 N_pad + 64 c, lo at +32
@@ -201,6 +225,8 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
     // uniform registers; one elected lane issues each tcgen05 instruction
     const uint32_t idesc = idesc_tf32(G3_M, N_pad, 0, 0);
     const uint32_t bh = smem_u32(sB_hi), bl = smem_u32(sB_lo);
+    mbar_wait(bar(BREADY), 0);  // weight images split
+    tc_fence_after();
     int j = 0, cc = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
       const int a = j & 1;
@@ -210,6 +236,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       for (int c = 0; c < nch; ++c, ++cc) {
         const int cs = cc % NC;
         mbar_wait(bar(CFULL + cs), (uint32_t)(cc / NC) & 1u);
+        if (j == 1 && c < 4 && lane == 0) G3T(65 + c);
         tc_fence_after();
         const int kst = min(G3_KCH, K_pad - c * G3_KCH) / 8;
         const uint32_t ahi = ch_hi(cs), alo = ahi + G3_KCH;
@@ -219,9 +246,11 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
             const uint32_t bo = bo0 + (uint32_t)(st * 32);
             const uint64_t dbh = umma_desc_sw128(bh + bo), dbl = umma_desc_sw128(bl + bo);
             const uint32_t acc = (c | st) != 0;
-            mma_tf32_ts(acc_col(a), alo + 8 * st, dbh, idesc, acc);
-            mma_tf32_ts(acc_col(a), ahi + 8 * st, dbl, idesc, 1);
-            mma_tf32_ts(acc_col(a), ahi + 8 * st, dbh, idesc, 1);
+            if (!(p.dbg & 32)) {
+              mma_tf32_ts(acc_col(a), alo + 8 * st, dbh, idesc, acc);
+              mma_tf32_ts(acc_col(a), ahi + 8 * st, dbl, idesc, 1);
+            }
+            mma_tf32_ts(acc_col(a), ahi + 8 * st, dbh, idesc, (p.dbg & 32) ? acc : 1u);
           }
           mma_commit(bar(CEMPTY + cs));
         }
@@ -232,60 +261,63 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
     }
   } else if (warp >= 4 && warp < 12) {
     // -------------------------------------------------------- converters --
-    // warp -> (TMEM lane quarter, half of each 32-column chunk); thread = row
-    const int quarter = warp & 3, half = (warp - 4) >> 2, row = quarter * 32 + lane;
+    // two groups of 4 warps (thread = row = TMEM lane) take alternate 32-column
+    // chunks, so one group's TMEM-store latency overlaps the other's loads
+    const int quarter = warp & 3, grp = (warp - 4) >> 2, row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int j = 0, cc = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
       const int s = j % R;
       mbar_wait(bar(FULL + s), (uint32_t)(j / R) & 1u);
-      if (row == 0 && half == 0) G3T(3 + 9 * j);
+      if (row == 0 && grp == 0) G3T(3 + 9 * j);
       const uint32_t xr = smem_u32(slots + s * slot_bytes) + (uint32_t)(row * p.lda * 4);
       const uint32_t mr = smem_u32(slots + s * slot_bytes + p.a_slot_bytes) + (uint32_t)(row * p.ldm * 4);
       for (int c = 0; c < nch; ++c, ++cc) {
+        if ((cc & 1) != grp) continue;
         const int cs = cc % NC;
-        const int k0 = c * G3_KCH + 16 * half;
-        // four 16-byte loads in flight before any conversion
-        float4 x[4], m[4];
+        uint32_t hv[32], lv[32];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int k = k0 + 4 * h;
-          x[h] = k < p.K ? lds128(xr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (MODE == 1 && p.has_mask) m[h] = k < p.K ? lds128(mr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        uint32_t hv[16], lv[16];
+        for (int hh = 0; hh < 2; ++hh) {
+          const int k0 = c * G3_KCH + 16 * hh;
+          // four 16-byte loads in flight before any conversion
+          float4 x[4], m[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int k = k0 + 4 * h;
-          float xs[4] = {x[h].x, x[h].y, x[h].z, x[h].w};
-          if (MODE == 1 && p.has_mask) {
-            const float ms[4] = {m[h].x, m[h].y, m[h].z, m[h].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (!(ms[q] > 0.f)) xs[q] = 0.f;
+          for (int h = 0; h < 4; ++h) {
+            const int k = k0 + 4 * h;
+            x[h] = k < p.K ? lds128(xr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (MODE == 1 && p.has_mask) m[h] = k < p.K ? lds128(mr + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (k + q >= p.K) xs[q] = 0.f;  // columns K..K_pad-1 are zero (row padding may hold anything)
-            const float hi = tf32_rna_finite(xs[q]);
-            hv[4 * h + q] = __float_as_uint(hi);
-            lv[4 * h + q] = __float_as_uint(__fsub_rn(xs[q], hi));
+          for (int h = 0; h < 4; ++h) {
+            const int k = k0 + 4 * h;
+            float xs[4] = {x[h].x, x[h].y, x[h].z, x[h].w};
+            if (MODE == 1 && p.has_mask) {
+              const float ms[4] = {m[h].x, m[h].y, m[h].z, m[h].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (!(ms[q] > 0.f)) xs[q] = 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (k + q >= p.K) xs[q] = 0.f;  // columns K..K_pad-1 are zero (row padding may hold anything)
+              const float hi = tf32_rna_finite(xs[q]);
+              hv[16 * hh + 4 * h + q] = __float_as_uint(hi);
+              lv[16 * hh + 4 * h + q] = __float_as_uint(__fsub_rn(xs[q], hi));
+            }
           }
         }
         mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / NC) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t hi_t = ch_hi(cs) + lane_off + (uint32_t)(16 * half);
+        const uint32_t hi_t = ch_hi(cs) + lane_off;
         if (!(p.dbg & 1)) {
-        tmem_st8(hi_t, *reinterpret_cast<uint32_t(*)[8]>(hv));
-        tmem_st8(hi_t + 8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8));
-        tmem_st8(hi_t + G3_KCH, *reinterpret_cast<uint32_t(*)[8]>(lv));
-        tmem_st8(hi_t + G3_KCH + 8, *reinterpret_cast<uint32_t(*)[8]>(lv + 8));
-        tmem_st_wait();
+          tmem_st32(hi_t, hv);
+          tmem_st32(hi_t + G3_KCH, lv);
+          tmem_st_wait();
         }
         tc_fence_before();
         mbar_arrive(bar(CFULL + cs));
       }
-      if (row == 0 && half == 0) G3T(4 + 9 * j);
+      if (row == 0 && grp == 0) G3T(4 + 9 * j);
       mbar_arrive(bar(EMPTY + s));  // raw slot consumed
     }
   } else if (warp >= 12) {
@@ -338,9 +370,20 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
               sts128(box + (uint32_t)(((cc ^ (r_loc & 7)) & 7) << 4), make_float4(x[q], x[q + 1], x[q + 2], x[q + 3]));
             }
           } else if (row < p.M) {
+            if (((reinterpret_cast<uintptr_t>(p.C) | (uintptr_t)(p.ldc * 4)) & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (c0 + h + q < p.N) out[c0 + h + q] = x[q];
+              for (int q = 0; q < 16; q += 4) {
+                const int col = c0 + h + q;
+                if (col + 3 < p.N) *reinterpret_cast<float4*>(out + col) = make_float4(x[q], x[q + 1], x[q + 2], x[q + 3]);
+                else
+                  for (int u = 0; u < 4; ++u)
+                    if (col + u < p.N) out[col + u] = x[q + u];
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (c0 + h + q < p.N) out[c0 + h + q] = x[q];
+            }
           }
         }
       }
@@ -875,7 +918,7 @@ bool make_map_sw128(CUtensorMap* m, const float* base, int64_t rows, int cols, i
 }
 
 int64_t g3_fixed(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
-  return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 20) + 16 + 4 * N_pad;
+  return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 21) + 16 + 4 * N_pad;
 }
 int64_t g3_stage_bytes(int N_pad) { return (int64_t)G3_M * ((N_pad + 31) / 32) * 128; }  // SW128 boxes
 int64_t g3_smem(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
@@ -909,23 +952,34 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   const int NC = std::min(8, (512 - 2 * N_pad) / (2 * G3_KCH));
   if (NC < 2) return false;
   const int64_t a_slot = (int64_t)G3_M * lda * 4, m_slot = has_mask ? (int64_t)G3_M * ldm * 4 : 0;
+  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
+  static const int rmax = getenv("FGL_G3SLOTS") ? atoi(getenv("FGL_G3SLOTS")) : G3_MAX_SLOTS;
+  // stage mode: 1 (default) = stage the epilogue for TMA tensor stores; 0 =
+  // trade the staging tile for a third raw slot and direct row stores
+  // (measured slower: 28.3 vs 26.6 us at the products layer-0 shape)
+  static const int stage_pref = getenv("FGL_G3STAGE") ? atoi(getenv("FGL_G3STAGE")) : 1;
   int R = 0;
   for (int r = G3_MAX_SLOTS; r >= 2; --r)
     if (g3_smem(N_pad, K_pad, r, a_slot, m_slot) <= G3_MAX_SMEM) { R = r; break; }
+  bool stage = true;
+  if (stage_pref == 0 && R < 3 && rmax >= 3 &&
+      g3_fixed(N_pad, K_pad, 3, a_slot, m_slot) <= G3_MAX_SMEM) {
+    R = 3;
+    stage = false;
+  }
   if (R == 0) return false;
-  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  static const int rmax = getenv("FGL_G3SLOTS") ? atoi(getenv("FGL_G3SLOTS")) : G3_MAX_SLOTS;
   if (R > rmax) R = rmax;
   const int cols = 512;
   // output through TMA tensor stores (SW128 boxes of 128 rows x 32 columns)
   CUtensorMap mC;
   std::memset(&mC, 0, sizeof(mC));
-  const bool coal = (ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15) && make_map_sw128(&mC, C, M, N, ldc);
+  const bool coal = stage && (ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15) &&
+                    make_map_sw128(&mC, C, M, N, ldc);
   const int64_t stage_off = (g3_fixed(N_pad, K_pad, R, a_slot, m_slot) - 1024 + 1023) / 1024 * 1024;
   G3Args p{A, mask, W, bias, C, lda, ldm, ldc, M, N, K, N_pad, K_pad, R, NC, relu, has_mask, cols,
            (int)a_slot, (int)m_slot, dbg, coal ? (int)stage_off : -1, 0,
            !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0)};
-  const int64_t smem = g3_smem(N_pad, K_pad, R, a_slot, m_slot);
+  const int64_t smem = coal ? g3_smem(N_pad, K_pad, R, a_slot, m_slot) : g3_fixed(N_pad, K_pad, R, a_slot, m_slot);
   static bool attr[2] = {false, false};
   cudaError_t e;
   if (!attr[mode]) {

@@ -16,12 +16,14 @@ torch.cuda.synchronize()
 buf = np.zeros(148 * 72, dtype=np.int64)
 _lib.lib().fgl_debug_g3_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
 tr = buf.reshape(148, 72)
-t0 = tr[:, 0].min()
+t0 = tr[:, 0][tr[:, 0] > 0].min()
 for c in (0, 1, 74, 147):
+    if tr[c, 0] == 0: continue
     r = tr[c]
     print(f"CTA {c}: start {(r[0]-t0)/1e3:.2f} prologue_done {(r[1]-t0)/1e3:.2f} end {(r[71]-t0)/1e3:.2f} us")
     for j in range(7):
         v = r[2 + 9 * j: 11 + 9 * j]
         if v[0] == 0: break
         print("   tile", j, " ".join(f"{nm}={(x-t0)/1e3:6.2f}" for nm, x in zip(("load", "conv0", "conv1", "mma", "epi0", "epi1", "staged", "bar", "copied"), v)))
+print("tile-1 chunk CFULL seen by MMA (CTA 147):", " ".join(f"{(x - t0) / 1e3:6.2f}" for x in tr[147, 65:69]))
 print("kernel span", (tr[:, 71].max() - t0) / 1e3, "us")
