@@ -139,6 +139,91 @@ __global__ void __launch_bounds__(32 * (1 + ST_CONS)) spmm_tma_kernel(const __gr
   }
 }
 
+// ------------------------------------------------ software-pipelined rows --
+// One warp per row, lane = 16-byte feature chunk (d <= 128).  Three-stage
+// pipeline over the warp's rows so that one row costs about one memory
+// latency instead of four: while row i's (<= 8) neighbour rows are being
+// gathered, row i+1's column / weight lists and row i+2's offsets are already
+// in flight.  Accumulation is in CSR order with a rounded multiply then a
+// rounded add (bit-identical to fgl_spmm); rows longer than SP_MAXE take a
+// plain in-order loop.
+__device__ __forceinline__ float4 fmadd4(float4 acc, float w, float4 x) {
+  acc.x = __fadd_rn(acc.x, __fmul_rn(w, x.x));
+  acc.y = __fadd_rn(acc.y, __fmul_rn(w, x.y));
+  acc.z = __fadd_rn(acc.z, __fmul_rn(w, x.z));
+  acc.w = __fadd_rn(acc.w, __fmul_rn(w, x.w));
+  return acc;
+}
+
+constexpr int SP_MAXE = 8;
+
+__global__ void __launch_bounds__(256) spmm_pipe_kernel(const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const float* __restrict__ w, int64_t nrows, int64_t col_base,
+                                                        const float* __restrict__ X, int64_t ldx,
+                                                        float* __restrict__ Y, int64_t ldy, int d4) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= nrows) return;
+  auto ip_pair = [&](int64_t row, int64_t& b, int64_t& e) {
+    int64_t v = 0;
+    if (row < nrows && lane < 2) v = indptr[row + lane];
+    b = __shfl_sync(0xffffffffu, v, 0);
+    e = __shfl_sync(0xffffffffu, v, 1);
+  };
+  auto lists = [&](int64_t b, int64_t e, int32_t& cl, float& wl) {
+    const int n = (int)(e - b);
+    cl = 0;
+    wl = 0.f;
+    if (lane < n && lane < SP_MAXE) {
+      cl = (int32_t)(col[b + lane] - col_base);
+      wl = w[b + lane];
+    }
+  };
+  int64_t b0, e0, b1, e1;
+  ip_pair(r, b0, e0);
+  ip_pair(r + nw, b1, e1);
+  int32_t cl0;
+  float wl0;
+  lists(b0, e0, cl0, wl0);
+  while (r < nrows) {
+    const int n = (int)(e0 - b0);
+    // stage 1: gather row r's neighbour feature rows
+    float4 x[SP_MAXE];
+#pragma unroll
+    for (int u = 0; u < SP_MAXE; ++u) {
+      const int32_t c = __shfl_sync(0xffffffffu, cl0, u);
+      x[u] = (u < n && lane < d4) ? __ldg(reinterpret_cast<const float4*>(X + (int64_t)c * ldx) + lane)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // stage 2 / 3: next row's lists, the row after that's offsets
+    int32_t cl1;
+    float wl1;
+    lists(b1, e1, cl1, wl1);
+    int64_t b2, e2;
+    ip_pair(r + 2 * nw, b2, e2);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n <= SP_MAXE) {
+#pragma unroll
+      for (int u = 0; u < SP_MAXE; ++u) {
+        const float wk = __shfl_sync(0xffffffffu, wl0, u);
+        if (u < n) acc = fmadd4(acc, wk, x[u]);
+      }
+    } else {
+      for (int64_t e = b0; e < e0; ++e) {
+        const int32_t c = (int32_t)(col[e] - col_base);
+        const float wk = w[e];
+        if (lane < d4) acc = fmadd4(acc, wk, __ldg(reinterpret_cast<const float4*>(X + (int64_t)c * ldx) + lane));
+      }
+    }
+    if (lane < d4) reinterpret_cast<float4*>(Y + r * ldy)[lane] = acc;
+    r += nw;
+    b0 = b1; e0 = e1; cl0 = cl1; wl0 = wl1;
+    b1 = b2; e1 = e2;
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -205,6 +290,18 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
     return FGL_E_UNSUPPORTED;
   }
   if (num_rows == 0) return FGL_OK;
+  static const int use_tma = getenv("FGL_GATHER_TMA") ? atoi(getenv("FGL_GATHER_TMA")) : 0;
+  if (!use_tma && d <= 128) {
+    static int per_sm = 0;
+    if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_pipe_kernel, 256, 0) != cudaSuccess ||
+                    per_sm < 1))
+      per_sm = 2;
+    const int grid = (int)std::min<int64_t>(ceil_div(num_rows, 8), (int64_t)kNumSMs * per_sm);
+    FGL_COUNT_LAUNCH(), spmm_pipe_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, col, w, num_rows, col_base, X,
+                                                                                ldx, Y, ldy, (d + 3) / 4);
+    FGL_LAUNCH_CHECK("spmm_pipe_kernel");
+    return FGL_OK;
+  }
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     set_error("fgl_spmm_gather: cuTensorMapEncodeTiled unavailable");

@@ -278,6 +278,7 @@ class Pipeline:
         self.model = DeviceModel(cfg.layer_dims, params if params is not None else init_params(cfg.layer_dims, cfg.seed), device)
         self.L = cfg.num_layers
         self.H = len(cfg.fanouts)
+        self._max_fan = min(16, max(int(f) for f in cfg.fanouts))
         self.compact = cfg.arch == "gcn"
         # direct_x0: with the feature table resident in HBM, the layer-0
         # aggregation gathers neighbour rows straight from the table (the x0
@@ -553,8 +554,16 @@ class Pipeline:
                 r0, r1 = self._rows(win, 0, b)
                 n = r1 - r0
                 Hb = self._buf(f"h0_run{j}s{slot}", n, _ld(din))
-                self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
-                           n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din, st)
+                if self.ldf <= 128:
+                    # rows hold <= fanout edges: the software-pipelined short-row
+                    # kernel (bit-identical to fgl_spmm)
+                    self._call("fgl_spmm_gather", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"],
+                               lay["w"].data_ptr(), n, 0, self.feats.data_ptr(), self.ldf, int(self.feats.shape[0]),
+                               Hb.data_ptr(), _ld(din), din, self._max_fan, st)
+                else:
+                    self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
+                               n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din,
+                               st)
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 pre[b] = (Hb, ev)
