@@ -280,6 +280,12 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
  * row r_i = rows[i] - row_base, label y_i = labels[seed_ids[i]] (or labels[i]
  * when seed_ids is NULL); dlogits[r_i] = (softmax - onehot(y_i)) / B as f32;
  * *loss_sum = sum_i -log(p_i + 1e-30) (device double; mean = loss_sum / B). */
+/* dH = (dX * (Xout > 0)) W^T alone (the dgrad half of fgl_dense_bwd,
+ * trainer.py:212-228), so the trainer can run a layer's weight gradient on a
+ * second stream while the backward chain continues. */
+int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ldxo, int64_t n, const float* W,
+                    int32_t din, int32_t dout, float* dH, int64_t lddh, void* stream);
+
 int64_t fgl_softmax_xent_ws_bytes(void);
 int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,
                      const int32_t* seed_ids, const int64_t* labels, int64_t B, int32_t C,

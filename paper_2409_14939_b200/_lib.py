@@ -111,6 +111,8 @@ SIGNATURES = {
     "fgl_dense_bwd": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, C.c_int32, vp,
                                 C.c_int64, vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64,
                                 vp]),
+    "fgl_dense_dgrad": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int32, C.c_int32, vp, C.c_int64,
+                                  vp]),
     "fgl_softmax_xent_ws_bytes": (C.c_int64, []),
     "fgl_softmax_xent": (C.c_int, [vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, C.c_int32,
                                    vp, C.c_int64, vp, vp, C.c_int64, vp]),

@@ -493,6 +493,23 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   return FGL_OK;
 }
 
+int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ldxo, int64_t n, const float* W,
+                    int32_t din, int32_t dout, float* dH, int64_t lddh, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || din < 1 || dout < 1 || !W || !dH || lddx < dout || (Xout && ldxo < dout) || lddh < din) {
+    set_error("fgl_dense_dgrad: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (n == 0) return FGL_OK;
+  int err = 0;
+  if (tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) return err;
+  dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
+  FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0, Xout,
+                                                        ldxo);
+  FGL_LAUNCH_CHECK("dense_dgrad");
+  return FGL_OK;
+}
+
 int64_t fgl_softmax_xent_ws_bytes(void) { return 8 * (148 * 8 * 8 + 1); }
 
 int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,

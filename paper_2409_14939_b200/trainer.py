@@ -299,8 +299,12 @@ class Pipeline:
                                             device)
         self.loss_dev = torch.zeros(max(cfg.window_n, 1), dtype=torch.float64, device=device)
         dims = cfg.layer_dims
-        self.bwd_ws = torch.empty(max(_lib.lib().fgl_dense_bwd_ws_bytes(a, b) for a, b in zip(dims, dims[1:])),
-                                  dtype=torch.uint8, device=device)
+        # one weight-gradient workspace per layer: the upper layers' weight
+        # gradients run on a side stream concurrently with the backward chain
+        self.bwd_ws_l = [torch.empty(_lib.lib().fgl_dense_bwd_ws_bytes(a, b), dtype=torch.uint8, device=device)
+                         for a, b in zip(dims, dims[1:])]
+        self.bwd_ws = self.bwd_ws_l[0]
+        self._wg_stream = None
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
         self._graveyard = []
@@ -496,17 +500,36 @@ class Pipeline:
                    s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), s1 - s0, C,
                    dY.data_ptr(), _ld(C), self.loss_dev.data_ptr() + 8 * slot,
                    self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
-        # backward
+        # backward.  Layer i > 0: its weight gradient (dW, db) only feeds the
+        # SGD step, so it runs on a side stream while the chain continues with
+        # dH = dZ W^T -> transposed aggregation -> layer i-1; the SGD waits for
+        # all of them.  Same kernels and inputs: results are unchanged.
         dX, lddx = dY, _ld(C)
+        wg_done = []
+        side = self._side_wgrad_stream()
         for i in range(self.L - 1, -1, -1):
             din, dout = dims[i], dims[i + 1]
             n = ns[i]
             mask = Y_bufs[i].data_ptr() if i < self.L - 1 else None
             dH = self._buf(f"dh{i}", n, _ld(din)) if i > 0 else None
-            self._call("fgl_dense_bwd", H_bufs[i].data_ptr(), _ld(din), n, din, m.W(i), dout,
-                       dX.data_ptr(), lddx, mask, _ld(dout), m.dW(i), m.db(i),
-                       dH.data_ptr() if dH is not None else None, _ld(din), self.bwd_ws.data_ptr(),
-                       self.bwd_ws.numel(), st)
+            ws_i = self.bwd_ws_l[i]
+            if i > 0 and side is not None:
+                ready = torch.cuda.Event()
+                ready.record()
+                side.wait_event(ready)
+                self._call("fgl_dense_bwd", H_bufs[i].data_ptr(), _ld(din), n, din, m.W(i), dout,
+                           dX.data_ptr(), lddx, mask, _ld(dout), m.dW(i), m.db(i), None, _ld(din),
+                           ws_i.data_ptr(), ws_i.numel(), side.cuda_stream)
+                done = torch.cuda.Event()
+                done.record(side)
+                wg_done.append(done)
+                self._call("fgl_dense_dgrad", dX.data_ptr(), lddx, mask, _ld(dout), n, m.W(i), din, dout,
+                           dH.data_ptr(), _ld(din), st)
+            else:
+                self._call("fgl_dense_bwd", H_bufs[i].data_ptr(), _ld(din), n, din, m.W(i), dout,
+                           dX.data_ptr(), lddx, mask, _ld(dout), m.dW(i), m.db(i),
+                           dH.data_ptr() if dH is not None else None, _ld(din), ws_i.data_ptr(),
+                           ws_i.numel(), st)
             if i > 0:
                 lay = layers[i]
                 q0, q1 = self._rows(win, i - 1, b)
@@ -521,9 +544,25 @@ class Pipeline:
                 if prefix:  # root term dx += dh on the layer's own (prefix) rows only
                     self._call("fgl_add_rows", dXn.data_ptr(), _ld(din), dH.data_ptr(), _ld(din), n, din, st)
                 dX, lddx = dXn, _ld(din)
+        cur = torch.cuda.current_stream()
+        for ev in wg_done:
+            cur.wait_event(ev)
         if self.dist is not None:
             self.dist.allreduce_mean(self.model.grad)
         self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+
+    def _side_wgrad_stream(self):
+        import os
+        if os.environ.get("FGL_SIDE_WGRAD", "1") == "0" or self.dist is not None:
+            return None
+        if self._wg_stream is None:
+            torch = self.torch
+            try:
+                lo, hi = torch.cuda.Stream.priority_range()
+                self._wg_stream = torch.cuda.Stream(device=self.device, priority=min(lo, hi))
+            except Exception:  # noqa: BLE001 - no priority support
+                self._wg_stream = torch.cuda.Stream(device=self.device)
+        return self._wg_stream
 
     # --------------------------------------------- layer-0 run-ahead --
     def _launch_l0_aggs(self, win, order, layers, slot: int = 0, stream=None):
