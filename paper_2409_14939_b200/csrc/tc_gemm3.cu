@@ -971,10 +971,24 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   if (R > rmax) R = rmax;
   const int cols = 512;
   // output through TMA tensor stores (SW128 boxes of 128 rows x 32 columns)
+  // tensor-map encodes cost host microseconds per call; the trainer reuses
+  // the same output buffers every batch, so keep the last few maps
+  struct MapCache { const float* C; int64_t M, ldc; int N; CUtensorMap m; };
+  static thread_local MapCache cache[8];
+  static thread_local int cache_next = 0;
   CUtensorMap mC;
   std::memset(&mC, 0, sizeof(mC));
-  const bool coal = stage && (ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15) &&
-                    make_map_sw128(&mC, C, M, N, ldc);
+  bool coal = false;
+  if (stage && (ldc % 4 == 0) && !(reinterpret_cast<uintptr_t>(C) & 15)) {
+    for (auto& c : cache)
+      if (c.C == C && c.M == M && c.N == N && c.ldc == ldc) { mC = c.m; coal = true; break; }
+    if (!coal && make_map_sw128(&mC, C, M, N, ldc)) {
+      MapCache& c = cache[cache_next];
+      cache_next = (cache_next + 1) % 8;
+      c.C = C; c.M = M; c.N = N; c.ldc = ldc; c.m = mC;
+      coal = true;
+    }
+  }
   const int64_t stage_off = (g3_fixed(N_pad, K_pad, R, a_slot, m_slot) - 1024 + 1023) / 1024 * 1024;
   G3Args p{A, mask, W, bias, C, lda, ldm, ldc, M, N, K, N_pad, K_pad, R, NC, relu, has_mask, cols,
            (int)a_slot, (int)m_slot, dbg, coal ? (int)stage_off : -1, 0,

@@ -305,6 +305,7 @@ class Pipeline:
                          for a, b in zip(dims, dims[1:])]
         self.bwd_ws = self.bwd_ws_l[0]
         self._wg_stream = None
+        self._cs = None  # stream being issued on inside run_windows
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
         self._graveyard = []
@@ -331,7 +332,14 @@ class Pipeline:
 
     @property
     def stream(self):
-        return self.torch.cuda.current_stream().cuda_stream
+        cs = self._cs
+        return cs.cuda_stream if cs is not None else self.torch.cuda.current_stream().cuda_stream
+
+    def _cur(self):
+        """The stream work is being issued on (cached inside run_windows: a
+        torch.cuda.current_stream() call costs ~10 us of host time)."""
+        cs = self._cs
+        return cs if cs is not None else self.torch.cuda.current_stream()
 
     def _call(self, name, *args):
         _lib.call(name, *args)
@@ -469,7 +477,7 @@ class Pipeline:
             if pre is not None:
                 # layer-0 aggregation was run ahead on the aggregation stream
                 Hb, ev = pre
-                torch.cuda.current_stream().wait_event(ev)
+                self._cur().wait_event(ev)
             else:
                 Hb = self._buf(f"h{i}", n, _ld(din))
                 self_x = X.data_ptr() if not self.compact else None
@@ -515,7 +523,7 @@ class Pipeline:
             ws_i = self.bwd_ws_l[i]
             if i > 0 and side is not None:
                 ready = torch.cuda.Event()
-                ready.record()
+                ready.record(self._cur())
                 side.wait_event(ready)
                 self._call("fgl_dense_bwd", H_bufs[i].data_ptr(), _ld(din), n, din, m.W(i), dout,
                            dX.data_ptr(), lddx, mask, _ld(dout), m.dW(i), m.db(i), None, _ld(din),
@@ -544,7 +552,7 @@ class Pipeline:
                 if prefix:  # root term dx += dh on the layer's own (prefix) rows only
                     self._call("fgl_add_rows", dXn.data_ptr(), _ld(din), dH.data_ptr(), _ld(din), n, din, st)
                 dX, lddx = dXn, _ld(din)
-        cur = torch.cuda.current_stream()
+        cur = self._cur()
         for ev in wg_done:
             cur.wait_event(ev)
         if self.dist is not None:
@@ -767,12 +775,15 @@ class Pipeline:
             # or sampling work queued behind it)
             self._io.wait_event(win.sampled)
             with torch.cuda.stream(self._io):
+                self._cs = self._io
                 win.host_counts()
                 order = self.schedule(win, nb)
+                self._cs = None
             self._prep.wait_event(win.sampled)
             if slot in self._prep_done:  # prepare buffers of this slot: window w-2 has trained
                 self._prep.wait_event(self._prep_done[slot])
             with torch.cuda.stream(self._prep):
+                self._cs = self._prep
                 # the weight-independent work of window w -- block CSRs and the
                 # layer-0 aggregations -- runs under window w-1's compute and
                 # the sampling of later windows; buffers alternate between slots
@@ -780,16 +791,19 @@ class Pipeline:
                 self._launch_l0_aggs(win, order, layers, slot, stream=self._prep)
                 prepped = torch.cuda.Event()
                 prepped.record(self._prep)
+                self._cs = None
             if w + self.LOOKAHEAD < len(windows):
                 k = w + self.LOOKAHEAD
                 pending.append(self._sample_async(*windows[k], slot=k % nsmp))
             with torch.cuda.stream(self._main):
+                self._cs = self._main
                 self._main.wait_event(prepped)
                 for j, b in enumerate(order):
                     prev = order[j - 1] if (j > 0 and self.flags.match) else None
                     self.batch_step(win, b, prev, j, layers, j % 2)
                 ev = torch.cuda.Event()
                 ev.record(self._main)
+            self._cs = None
             if not hasattr(self, "_slot_done"):
                 self._slot_done = {}
             self._slot_done[w % nsmp] = ev
