@@ -561,7 +561,7 @@ class Pipeline:
 
     def _side_wgrad_stream(self):
         import os
-        if os.environ.get("FGL_SIDE_WGRAD", "1") == "0" or self.dist is not None:
+        if os.environ.get("FGL_SIDE_WGRAD", "1") == "0":
             return None
         if self._wg_stream is None:
             torch = self.torch
