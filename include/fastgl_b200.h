@@ -286,6 +286,16 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
 int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ldxo, int64_t n, const float* W,
                     int32_t din, int32_t dout, float* dH, int64_t lddh, void* stream);
 
+/* CUDA-graph replay of a per-batch chain: begin a
+ * thread-local capture on `stream`; end it and launch it through the slot's
+ * executable graph (cudaGraphExecUpdate when the topology matches, else a
+ * fresh instantiation); or abort it (the caller then runs the work eagerly).
+ * fgl_capture_stats: {graph launches, updates, instantiations}. */
+int fgl_capture_begin(void* stream);
+int fgl_capture_end_launch(int32_t slot, void* stream);
+int fgl_capture_abort(void* stream);
+int fgl_capture_stats(int64_t* out3);
+
 int64_t fgl_softmax_xent_ws_bytes(void);
 int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,
                      const int32_t* seed_ids, const int64_t* labels, int64_t B, int32_t C,

@@ -113,6 +113,10 @@ SIGNATURES = {
                                 vp]),
     "fgl_dense_dgrad": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int32, C.c_int32, vp, C.c_int64,
                                   vp]),
+    "fgl_capture_begin": (C.c_int, [vp]),
+    "fgl_capture_end_launch": (C.c_int, [C.c_int32, vp]),
+    "fgl_capture_abort": (C.c_int, [vp]),
+    "fgl_capture_stats": (C.c_int, [vp]),
     "fgl_softmax_xent_ws_bytes": (C.c_int64, []),
     "fgl_softmax_xent": (C.c_int, [vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, C.c_int32,
                                    vp, C.c_int64, vp, vp, C.c_int64, vp]),

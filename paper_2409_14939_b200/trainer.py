@@ -42,6 +42,10 @@ def _ld(d: int) -> int:
     return (int(d) + 3) // 4 * 4
 
 
+class _NeedAlloc(RuntimeError):
+    """A work buffer must grow while a CUDA graph is being captured."""
+
+
 @dataclass
 class ModelConfig:
     """Architecture and schedule knobs (trainer.py:45-79)."""
@@ -306,6 +310,8 @@ class Pipeline:
         self.bwd_ws = self.bwd_ws_l[0]
         self._wg_stream = None
         self._cs = None  # stream being issued on inside run_windows
+        self._capturing = False
+        self.graph_fallbacks = 0
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
         self._graveyard = []
@@ -322,6 +328,8 @@ class Pipeline:
         need = max(int(rows), 1) * int(cols)
         t = self._bufs.get(name)
         if t is None or t.numel() < need or t.dtype != dtype:
+            if self._capturing:
+                raise _NeedAlloc(name)  # no allocation inside a graph capture: run this batch eagerly
             if t is not None:
                 # buffers are used from two streams: a replaced one may still be
                 # read by queued kernels, so it is kept alive, never recycled
@@ -430,8 +438,40 @@ class Pipeline:
         return win.front_range(self.H - i, b)[0]
 
     # -------------------------------------------------------------- batch --
+    def _graph_mode(self) -> bool:
+        import os
+        return (os.environ.get("FGL_GRAPH", "1") != "0" and self._cs is not None and not self.fused_upper
+                and (self.dist is None or getattr(self.dist, "world", 1) <= 1))
+
     def batch_step(self, win, b, prev, slot, layers, x0_slot):
-        """Load x0, forward, loss, backward, SGD for batch b of the window."""
+        """Load x0, forward, loss, backward, SGD for batch b of the window.
+
+        Inside run_windows the batch's chain is captured and replayed as one
+        CUDA graph (fgl_capture_*): the same kernels with the same arguments,
+        fewer host calls and shorter launch gaps.  A capture that fails (a
+        buffer has to grow, an unexpected path) is aborted and the batch runs
+        eagerly."""
+        if not self._graph_mode():
+            return self._batch_step_body(win, b, prev, slot, layers, x0_slot)
+        cur = self._cs
+        # dependencies on other streams are taken before the capture starts
+        pre = (self._pre_h0.get(b) if (self._pre_h0 is not None and self._pre_h0_win is win) else None)
+        if pre is not None:
+            cur.wait_event(pre[1])
+        st = cur.cuda_stream
+        _lib.call("fgl_capture_begin", st)
+        self._capturing = True
+        try:
+            self._batch_step_body(win, b, prev, slot, layers, x0_slot, external_done=True)
+        except Exception:  # noqa: BLE001 - any failure: discard the capture, run eagerly
+            self._capturing = False
+            _lib.lib().fgl_capture_abort(st)
+            self.graph_fallbacks += 1
+            return self._batch_step_body(win, b, prev, slot, layers, x0_slot, external_done=True)
+        self._capturing = False
+        _lib.call("fgl_capture_end_launch", 0, st)
+
+    def _batch_step_body(self, win, b, prev, slot, layers, x0_slot, external_done=False):
         torch = self.torch
         s = self.sampler
         m = self.model
@@ -477,7 +517,8 @@ class Pipeline:
             if pre is not None:
                 # layer-0 aggregation was run ahead on the aggregation stream
                 Hb, ev = pre
-                self._cur().wait_event(ev)
+                if not external_done:
+                    self._cur().wait_event(ev)
             else:
                 Hb = self._buf(f"h{i}", n, _ld(din))
                 self_x = X.data_ptr() if not self.compact else None

@@ -185,3 +185,34 @@ def test_fused_upper_layers_match_separate_kernels(cfg1_graph):
             os.environ.pop("FGL_FUSED", None)
     np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-5)
     np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("arch,direct", [("gcn", True), ("gcn", False), ("gin", False), ("sage", False)])
+def test_graph_replay_bit_identical(cfg1_graph, arch, direct, monkeypatch):
+    """The per-batch chain replayed as CUDA graphs (fgl_capture_*) gives
+    exactly the parameters and losses of eager launches, and graphs are used."""
+    import ctypes
+    from paper_2409_14939_b200 import _lib, trainer
+    g = cfg1_graph
+    rng = np.random.default_rng(11)
+    feats = rng.standard_normal((g.num_nodes, 20)).astype(np.float32)
+    labels = rng.integers(0, 4, size=g.num_nodes)
+    cfg = trainer.ModelConfig(layer_dims=(20, 16, 16, 4), fanouts=[6, 4, 3], batch_size=200, window_n=4, lr=0.2,
+                              arch=arch)
+    wins = [([rng.choice(g.num_nodes, 200, replace=False) for _ in range(4)], [100 * w + j for j in range(4)])
+            for w in range(5)]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FGL_GRAPH", mode)
+        stats0 = (ctypes.c_int64 * 3)()
+        _lib.call("fgl_capture_stats", ctypes.cast(stats0, ctypes.c_void_p))
+        pipe = trainer.Pipeline(g, feats, labels, cfg, direct_x0=direct)
+        losses = [lo.cpu().numpy().copy() for _, lo in pipe.run_windows(wins)]
+        stats1 = (ctypes.c_int64 * 3)()
+        _lib.call("fgl_capture_stats", ctypes.cast(stats1, ctypes.c_void_p))
+        out[mode] = (pipe.model.flat.cpu().numpy(), losses, stats1[0] - stats0[0], pipe.graph_fallbacks)
+    assert out["0"][2] == 0
+    assert out["1"][2] >= 15  # 20 batches; a few may fall back (first-use buffer growth)
+    assert np.array_equal(out["0"][0], out["1"][0])
+    for a, b in zip(out["0"][1], out["1"][1]):
+        assert np.array_equal(a, b)
