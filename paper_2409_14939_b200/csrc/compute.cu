@@ -107,6 +107,60 @@ __global__ void __launch_bounds__(256) spmm_kernel(
   }
 }
 
+// d <= 64 (one float4 per lane, half a warp per row): the row's offsets and
+// each edge's (col, w) are lane-uniform loads (broadcast, no shuffles), the
+// next row's offsets are fetched while the current row gathers, and up to 4
+// neighbour rows are in flight per step.  Same CSR-order arithmetic as
+// spmm_kernel (bit-identical); lean enough for the transposed aggregation's
+// ~1-edge rows, which made spmm_kernel instruction/latency bound.
+__global__ void __launch_bounds__(256) spmm_half_kernel(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+    const float* __restrict__ w, int64_t nrows, int64_t col_base, const float* __restrict__ X,
+    int64_t ldx, const float* __restrict__ self_x, int64_t ld_self, float* __restrict__ Y,
+    int64_t ldy, int d4) {
+  const int lane = threadIdx.x & 15;
+  const int64_t hw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;  // half-warp id
+  const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
+  int64_t r = hw;
+  int64_t e0 = 0, e1 = 0;
+  if (r < nrows) { e0 = indptr[r]; e1 = indptr[r + 1]; }
+  while (r < nrows) {
+    const int64_t rn = r + nhw;
+    int64_t f0 = 0, f1 = 0;
+    if (rn < nrows) { f0 = indptr[rn]; f1 = indptr[rn + 1]; }  // next row's offsets, in flight
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t e = e0; e < e1; e += 4) {
+      const int n = (int)(e1 - e < 4 ? e1 - e : 4);
+      int32_t c[4];
+      float wk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = u < n ? (int32_t)(__ldg(col + e + u) - col_base) : 0;
+        wk[u] = u < n ? __ldg(w + e + u) : 0.f;
+      }
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        x[u] = (u < n && lane < d4) ? __ldg(reinterpret_cast<const float4*>(X + (int64_t)c[u] * ldx) + lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < n) acc = fmadd4(acc, wk[u], x[u]);
+    }
+    if (lane < d4) {
+      if (self_x) {  // GIN: h = aggregate + x, one rounded add (trainer.py:189-190)
+        const float4 sx = reinterpret_cast<const float4*>(self_x + r * ld_self)[lane];
+        acc.x = __fadd_rn(acc.x, sx.x); acc.y = __fadd_rn(acc.y, sx.y);
+        acc.z = __fadd_rn(acc.z, sx.z); acc.w = __fadd_rn(acc.w, sx.w);
+      }
+      reinterpret_cast<float4*>(Y + r * ldy)[lane] = acc;
+    }
+    r = rn;
+    e0 = f0;
+    e1 = f1;
+  }
+}
+
 template <int L, int CPL>
 void launch_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows,
                  int64_t col_base, const float* X, int64_t ldx, const float* self_x,
@@ -402,7 +456,17 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
   else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 4) launch_spmm<4, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 8) launch_spmm<8, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 16) launch_spmm<16, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 16) {
+    static const int half = getenv("FGL_SPMM_HALF") ? atoi(getenv("FGL_SPMM_HALF")) : 1;
+    if (half) {
+      static const int bps = getenv("FGL_SPMM_GRID") ? atoi(getenv("FGL_SPMM_GRID")) : 8;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_rows, 16), (int64_t)148 * bps));
+      FGL_COUNT_LAUNCH(), spmm_half_kernel<<<grid, 256, 0, st>>>(indptr, col, w, num_rows, col_base, X, ldx, self_x,
+                                                                  ld_self, Y, ldy, d4);
+    } else {
+      launch_spmm<16, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+    }
+  }
   else if (d4 <= 32) launch_spmm<32, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 64) launch_spmm<32, 2>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 128) launch_spmm<32, 4>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);

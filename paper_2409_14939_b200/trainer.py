@@ -443,6 +443,32 @@ class Pipeline:
         return (os.environ.get("FGL_GRAPH", "1") != "0" and self._cs is not None and not self.fused_upper
                 and (self.dist is None or getattr(self.dist, "world", 1) <= 1))
 
+    def _graphs_on(self) -> bool:
+        import os
+        return (os.environ.get("FGL_GRAPH", "1") != "0"
+                and (self.dist is None or getattr(self.dist, "world", 1) <= 1))
+
+    def _graphed(self, stream, slot: int, fn):
+        """Run fn() -- work issued on `stream` only, no host reads of device
+        data, no cross-stream events leaving it -- as one CUDA graph through
+        executable-graph slot `slot`; eager fallback if the capture fails."""
+        import os
+        if not self._graphs_on() or str(slot) not in os.environ.get("FGL_GRAPH_SLOTS", "0,1,2").split(","):
+            return fn()
+        st = stream.cuda_stream
+        _lib.call("fgl_capture_begin", st)
+        self._capturing = True
+        try:
+            r = fn()
+        except Exception:  # noqa: BLE001 - discard the capture, run eagerly
+            self._capturing = False
+            _lib.lib().fgl_capture_abort(st)
+            self.graph_fallbacks += 1
+            return fn()
+        self._capturing = False
+        _lib.call("fgl_capture_end_launch", slot, st)
+        return r
+
     def batch_step(self, win, b, prev, slot, layers, x0_slot):
         """Load x0, forward, loss, backward, SGD for batch b of the window.
 
@@ -456,7 +482,7 @@ class Pipeline:
         cur = self._cs
         # dependencies on other streams are taken before the capture starts
         pre = (self._pre_h0.get(b) if (self._pre_h0 is not None and self._pre_h0_win is win) else None)
-        if pre is not None:
+        if pre is not None and pre[1] is not None:
             cur.wait_event(pre[1])
         st = cur.cuda_stream
         _lib.call("fgl_capture_begin", st)
@@ -517,7 +543,7 @@ class Pipeline:
             if pre is not None:
                 # layer-0 aggregation was run ahead on the aggregation stream
                 Hb, ev = pre
-                if not external_done:
+                if not external_done and ev is not None:
                     self._cur().wait_event(ev)
             else:
                 Hb = self._buf(f"h{i}", n, _ld(din))
@@ -652,9 +678,12 @@ class Pipeline:
                     self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
                                n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din,
                                st)
-                ev = torch.cuda.Event()
-                ev.record(stream)
-                pre[b] = (Hb, ev)
+                if self._capturing:  # graph-captured: the window's `prepped` event orders it
+                    pre[b] = (Hb, None)
+                else:
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    pre[b] = (Hb, ev)
         self._pre_h0 = pre
         self._pre_h0_win = win
 
@@ -769,7 +798,7 @@ class Pipeline:
             self._side.wait_event(done)
         with torch.cuda.stream(self._side):
             nb, off = smp.stage(seed_lists, rng_seeds)
-            win = smp.run(nb, off, stream=self._side)
+            win = self._graphed(self._side, 2, lambda: smp.run(nb, off, stream=self._side))
             win.sampled = torch.cuda.Event()
             win.sampled.record(self._side)
         self.gpu_launches += 1
@@ -828,8 +857,11 @@ class Pipeline:
                 # the weight-independent work of window w -- block CSRs and the
                 # layer-0 aggregations -- runs under window w-1's compute and
                 # the sampling of later windows; buffers alternate between slots
-                layers = self.prepare(win, slot)
-                self._launch_l0_aggs(win, order, layers, slot, stream=self._prep)
+                def _prep_work():
+                    lay = self.prepare(win, slot)
+                    self._launch_l0_aggs(win, order, lay, slot, stream=self._prep)
+                    return lay
+                layers = self._graphed(self._prep, 1, _prep_work)
                 prepped = torch.cuda.Event()
                 prepped.record(self._prep)
                 self._cs = None

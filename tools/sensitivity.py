@@ -39,5 +39,10 @@ t0 = time.perf_counter()
 for _ in pipe.run_windows(wins[3:3 + K]): pass
 torch.cuda.synchronize()
 tot = (time.perf_counter() - t0) / K * 1e3
+import ctypes
+from paper_2409_14939_b200 import _lib as _L
+st3 = (ctypes.c_int64 * 3)()
+_L.call("fgl_capture_stats", ctypes.cast(st3, ctypes.c_void_p))
+print(f"graphs: launches {st3[0]} updates {st3[1]} instantiations {st3[2]}, eager fallbacks {pipe.graph_fallbacks}")
 print(f"skip={sorted(skip)}: wall {tot:.3f} ms/window, host blocked {blocked[0] / K * 1e3:.3f}, "
       f"issuing {tot - blocked[0] / K * 1e3:.3f}", flush=True)
