@@ -176,7 +176,9 @@ int fgl_gather_i32_f32(const int32_t* perm, int64_t n, const int32_t* a, const f
  * indptr[num_rows+1], w[nnz] (arch_gcn == 1: GCN 1/sqrt(indeg*outdeg) in fp64
  * -> f32, trainer.py:156-162; 0: GIN 1.0; 2: SAGE mean 1/indeg in fp64 -> f32,
  * the GraphSAGE extension of SURVEY 8(c)), and the stable transpose
- * t_indptr[num_cols+1], t_col[nnz] (= lt), t_w[nnz] (compute.py:233-239). */
+ * t_indptr[num_cols+1], t_col[nnz] (= lt), t_w[nnz] (compute.py:233-239).
+ * t_indptr = t_col = t_w = NULL skips the transpose (model layer 0: the input
+ * features need no gradient, so the backward never aggregates through it). */
 int64_t fgl_prepare_layer_ws_bytes(int64_t nnz, int64_t num_rows, int64_t num_cols);
 int fgl_prepare_layer(const int32_t* lt, const int32_t* ls, int64_t nnz, int64_t num_rows,
                       int64_t num_cols, int32_t arch_gcn, int64_t* indptr, float* w,

@@ -406,8 +406,12 @@ static int prepare_layer_impl(const int32_t* lt, const int32_t* ls, int64_t nnz,
                               int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
                               void* stream_, bool sparse_rows) {
   cudaStream_t st = (cudaStream_t)stream_;
+  // t_indptr == t_col == t_w == NULL: no transpose (model layer 0 -- the input
+  // features need no gradient); only the source degrees for the weights
+  const bool transpose = t_indptr != nullptr;
   if (nnz < 0 || num_rows < 1 || num_cols < 1 || nnz >= (1ll << 31) || !indptr || !w ||
-      !t_indptr || (nnz > 0 && (!lt || !ls || !t_col || !t_w))) {
+      (nnz > 0 && (!lt || !ls)) || (transpose && nnz > 0 && (!t_col || !t_w)) ||
+      (!transpose && (t_col || t_w))) {
     set_error("fgl_prepare_layer: bad arguments");
     return FGL_E_INVALID;
   }
@@ -423,12 +427,18 @@ static int prepare_layer_impl(const int32_t* lt, const int32_t* ls, int64_t nnz,
     FGL_COUNT_LAUNCH(), offsets_bsearch_kernel<<<grid_for(num_rows + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
   else
     FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
-  int rc = stable_group_impl(ls, nnz, num_cols, 0, t_indptr, perm, outdeg, gws,
-                             fgl_stable_group_ws_bytes(num_cols), st);
-  if (rc) return rc;
+  if (transpose) {
+    int rc = stable_group_impl(ls, nnz, num_cols, 0, t_indptr, perm, outdeg, gws,
+                               fgl_stable_group_ws_bytes(num_cols), st);
+    if (rc) return rc;
+  } else {
+    FGL_CUDA(cudaMemsetAsync(outdeg, 0, 4 * num_cols, st));
+    if (nnz > 0) FGL_COUNT_LAUNCH(), histogram_kernel<<<grid_for(nnz), kThreads, 0, st>>>(ls, nnz, outdeg);
+  }
   if (nnz > 0) {
     FGL_COUNT_LAUNCH(), layer_weights_kernel<<<grid_for(nnz), kThreads, 0, st>>>(lt, ls, nnz, indptr, outdeg, arch_gcn, w);
-    FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, lt, w, t_col, t_w);
+    if (transpose)
+      FGL_COUNT_LAUNCH(), gather_i32_f32_kernel<<<grid_for(nnz), kThreads, 0, st>>>(perm, nnz, lt, w, t_col, t_w);
   }
   FGL_LAUNCH_CHECK("prepare_layer");
   return FGL_OK;
@@ -448,8 +458,9 @@ int fgl_prepare_layer_grouped(const int32_t* lt, const int32_t* ls, int64_t nnz,
                               int64_t* t_indptr, int32_t* t_col, float* t_w, void* ws, int64_t ws_bytes,
                               void* stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
-  if (nnz < 0 || num_rows < 1 || num_cols < 1 || nnz >= (1ll << 31) || !indptr || !w || !t_indptr ||
-      (nnz > 0 && (!lt || !ls || !col_out || !t_col || !t_w))) {
+  if (nnz < 0 || num_rows < 1 || num_cols < 1 || nnz >= (1ll << 31) || !indptr || !w ||
+      (nnz > 0 && (!lt || !ls || !col_out)) || (t_indptr && nnz > 0 && (!t_col || !t_w)) ||
+      (!t_indptr && (t_col || t_w))) {
     set_error("fgl_prepare_layer_grouped: bad arguments");
     return FGL_E_INVALID;
   }

@@ -312,6 +312,7 @@ class Pipeline:
         self._cs = None  # stream being issued on inside run_windows
         self._capturing = False
         self.graph_fallbacks = 0
+        self._keep_l0_transpose = False  # tests that inspect layer 0's transpose set this
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
         self._graveyard = []
@@ -391,16 +392,20 @@ class Pipeline:
                 rows = cols = win.unique_total()
             grouped = (not self.compact) and s.depth_layout
             rows, cols = max(rows, 1), max(cols, 1)
+            # model layer 0 (hop H-1, the largest) needs no transpose: nothing
+            # aggregates a gradient back into the input features
+            need_t = h != self.H - 1 or self._keep_l0_transpose
             lay = {
                 "indptr": self._buf(f"ip{h}s{slot}", rows + 1, 1, torch.int64),
                 "w": self._buf(f"w{h}s{slot}", max(nnz, 1), 1),
-                "t_indptr": self._buf(f"tip{h}s{slot}", cols + 1, 1, torch.int64),
-                "t_col": self._buf(f"tc{h}s{slot}", max(nnz, 1), 1, torch.int32),
-                "t_w": self._buf(f"tw{h}s{slot}", max(nnz, 1), 1),
+                "t_indptr": self._buf(f"tip{h}s{slot}", cols + 1, 1, torch.int64) if need_t else None,
+                "t_col": self._buf(f"tc{h}s{slot}", max(nnz, 1), 1, torch.int32) if need_t else None,
+                "t_w": self._buf(f"tw{h}s{slot}", max(nnz, 1), 1) if need_t else None,
                 "col": ls.data_ptr() + 4 * e0,
                 "col_global": s.src.data_ptr() + 4 * e0,
                 "nnz": nnz,
             }
+            tptr = (lambda k: lay[k].data_ptr() if lay[k] is not None else None)
             arch_code = {"gin": 0, "gcn": 1, "sage": 2}[self.cfg.arch]
             if grouped:  # depth-major targets are grouped but not ascending
                 colb = self._buf(f"colg{h}s{slot}", max(nnz, 1), 1, torch.int32)
@@ -409,15 +414,14 @@ class Pipeline:
                 pws = self._buf(f"pws{h}s{slot}", wsb, 1, torch.uint8)
                 self._call("fgl_prepare_layer_grouped", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
                            cols, arch_code, lay["indptr"].data_ptr(), colb.data_ptr(), lay["w"].data_ptr(),
-                           lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(), lay["t_w"].data_ptr(),
-                           pws.data_ptr(), wsb, self.stream)
+                           tptr("t_indptr"), tptr("t_col"), tptr("t_w"), pws.data_ptr(), wsb, self.stream)
             else:
                 wsb = _lib.lib().fgl_prepare_layer_ws_bytes(nnz, rows, cols)
                 pws = self._buf(f"pws{h}s{slot}", wsb, 1, torch.uint8)
                 self._call("fgl_prepare_layer", lt.data_ptr() + 4 * e0, ls.data_ptr() + 4 * e0, nnz, rows,
                            cols, arch_code, lay["indptr"].data_ptr(),
-                           lay["w"].data_ptr(), lay["t_indptr"].data_ptr(), lay["t_col"].data_ptr(),
-                           lay["t_w"].data_ptr(), pws.data_ptr(), wsb, self.stream)
+                           lay["w"].data_ptr(), tptr("t_indptr"), tptr("t_col"),
+                           tptr("t_w"), pws.data_ptr(), wsb, self.stream)
             layers[self.H - 1 - h] = lay
         return layers
 
