@@ -296,7 +296,11 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
     if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_pipe_kernel, 256, 0) != cudaSuccess ||
                     per_sm < 1))
       per_sm = 2;
-    const int grid = (int)std::min<int64_t>(ceil_div(num_rows, 8), (int64_t)kNumSMs * per_sm);
+    // rows per warp: 0 = persistent grid (one wave); > 0 = finite CTAs that
+    // retire, so a concurrent high-priority stream gets SM slots sooner
+    static const int rpw = getenv("FGL_PIPE_RPW") ? atoi(getenv("FGL_PIPE_RPW")) : 8;
+    const int64_t cap = rpw > 0 ? ceil_div(num_rows, 8LL * rpw) : (int64_t)kNumSMs * per_sm;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_rows, 8), cap));
     FGL_COUNT_LAUNCH(), spmm_pipe_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, col, w, num_rows, col_base, X,
                                                                                 ldx, Y, ldy, (d + 3) / 4);
     FGL_LAUNCH_CHECK("spmm_pipe_kernel");
