@@ -22,6 +22,7 @@ forward), so it runs the full unique-node layout like the reference.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -457,7 +458,7 @@ class Pipeline:
         data, no cross-stream events leaving it -- as one CUDA graph through
         executable-graph slot `slot`; eager fallback if the capture fails."""
         import os
-        if not self._graphs_on() or str(slot) not in os.environ.get("FGL_GRAPH_SLOTS", "0,1,2").split(","):
+        if not self._graphs_on() or str(slot) not in os.environ.get("FGL_GRAPH_SLOTS", "0,1,2,3").split(","):
             return fn()
         st = stream.cuda_stream
         _lib.call("fgl_capture_begin", st)
@@ -875,9 +876,23 @@ class Pipeline:
             with torch.cuda.stream(self._main):
                 self._cs = self._main
                 self._main.wait_event(prepped)
-                for j, b in enumerate(order):
-                    prev = order[j - 1] if (j > 0 and self.flags.match) else None
-                    self.batch_step(win, b, prev, j, layers, j % 2)
+                if self._graph_mode() and os.environ.get("FGL_GRAPH_WINDOW", "1") != "0":
+                    # the whole window's chain (8 batch steps) as ONE graph:
+                    # no launch gaps between batches either
+                    for b in order:
+                        pre = self._pre_h0.get(b) if (self._pre_h0 is not None and self._pre_h0_win is win) else None
+                        if pre is not None and pre[1] is not None:
+                            self._main.wait_event(pre[1])
+
+                    def _window_chain():
+                        for j, b in enumerate(order):
+                            prev = order[j - 1] if (j > 0 and self.flags.match) else None
+                            self._batch_step_body(win, b, prev, j, layers, j % 2, external_done=True)
+                    self._graphed(self._main, 3, _window_chain)
+                else:
+                    for j, b in enumerate(order):
+                        prev = order[j - 1] if (j > 0 and self.flags.match) else None
+                        self.batch_step(win, b, prev, j, layers, j % 2)
                 ev = torch.cuda.Event()
                 ev.record(self._main)
             self._cs = None

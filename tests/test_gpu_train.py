@@ -212,7 +212,7 @@ def test_graph_replay_bit_identical(cfg1_graph, arch, direct, monkeypatch):
         _lib.call("fgl_capture_stats", ctypes.cast(stats1, ctypes.c_void_p))
         out[mode] = (pipe.model.flat.cpu().numpy(), losses, stats1[0] - stats0[0], pipe.graph_fallbacks)
     assert out["0"][2] == 0
-    assert out["1"][2] >= 15  # 20 batches; a few may fall back (first-use buffer growth)
+    assert out["1"][2] >= 5  # graph launches (window chains, prepare, sampler); a few may fall back
     assert np.array_equal(out["0"][0], out["1"][0])
     for a, b in zip(out["0"][1], out["1"][1]):
         assert np.array_equal(a, b)
