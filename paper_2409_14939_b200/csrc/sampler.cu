@@ -799,8 +799,7 @@ __device__ __forceinline__ int64_t sel_gtime() {
 }
 
 __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
-                                                                    int sv_words, int dbg, int tile_limit,
-                                                                    int unlimited_from) {
+                                                                    int sv_words, int dbg) {
   extern __shared__ __align__(16) uint64_t sbuf[];
   const int64_t t_start = dbg ? sel_gtime() : 0;
   const int lane = lane_id(), wib = warp_id();
@@ -816,14 +815,7 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
   uint32_t* bm_base = a.bm_front;
   const int64_t ntiles = ceil_div(F, 32);
   (void)gw; (void)nwarps;
-  // CTAs below `unlimited_from` retire after `tile_limit` tiles per warp, so
-  // SM slots turn over while the sampler runs beside the training chain; the
-  // last wave of CTAs has no limit and finishes whatever is left
-  const bool limited = (int)blockIdx.x < unlimited_from;
-  int done_tiles = 0;
   for (;;) {
-    if (limited && done_tiles >= tile_limit) break;
-    ++done_tiles;
     // dynamic tile scheduling: hub-heavy tiles cost ~10 normal ones, so a
     // static grid stride leaves a long tail of busy warps
     unsigned long long tix = 0;
@@ -1376,10 +1368,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
           per_sm = 2;
         bal_grid_of[fan] = per_sm * kNumSMs;
       }
-      static const int rounds = getenv("FGL_SEL_ROUNDS") ? atoi(getenv("FGL_SEL_ROUNDS")) : 1;
-      static const int tlim = getenv("FGL_SEL_K") ? atoi(getenv("FGL_SEL_K")) : 2;
-      const int bal_grid = bal_grid_of[fan] * std::max(rounds, 1);
-      const int unlimited_from = bal_grid_of[fan] * (std::max(rounds, 1) - 1);
+      const int bal_grid = bal_grid_of[fan];
       cudaEvent_t pe0 = nullptr, pe1 = nullptr;
       if (g_sel_prof) {
         cudaEventCreate(&pe0);
@@ -1388,8 +1377,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       }
       static const int seldbg = getenv("FGL_SELDBG") ? 1 : 0;
       FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
-                                                                                  bal_sv_words(fan), seldbg, tlim,
-                                                                                  unlimited_from);
+                                                                                  bal_sv_words(fan), seldbg);
       FGL_COUNT_LAUNCH(), select_hub_kernel<<<4 * kNumSMs, kHubThreads, 0, stream>>>(a);
       if (g_sel_prof) {  // the events bracket both launches: together they are the hop's selection
         cudaEventRecord(pe1, stream);

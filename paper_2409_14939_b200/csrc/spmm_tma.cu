@@ -343,18 +343,7 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
   a.row_bytes = (int)(ldx * 4);
   a.max_len = max_row_len;
   a.g_stride = (4 * a.row_bytes + 127) / 128 * 128;  // gather4 destinations are 128-byte aligned
-  static const int cfg = [] {
-    const char* e = getenv("FGL_GATHER_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  int rc;
-  switch (cfg) {
-    case 1: rc = launch_gather<8, 3, 2>(*mp, a, (cudaStream_t)stream); break;
-    case 2: rc = launch_gather<8, 4, 2>(*mp, a, (cudaStream_t)stream); break;
-    case 3: rc = launch_gather<4, 4, 1>(*mp, a, (cudaStream_t)stream); break;
-    case 4: rc = launch_gather<16, 4, 4>(*mp, a, (cudaStream_t)stream); break;
-    default: rc = launch_gather<16, 3, 4>(*mp, a, (cudaStream_t)stream); break;
-  }
+  const int rc = launch_gather<16, 3, 4>(*mp, a, (cudaStream_t)stream);
   if (rc) return rc;
   return FGL_OK;
 }

@@ -439,7 +439,6 @@ struct Wg3Args {
   int64_t M;
   int K, N, N_pad, tmem_cols, h_bytes, z_bytes, m_bytes, dbg;
   int R, NC;  // raw tile slots, A/B chunk ring depth
-  int piece;  // bulk-copy request size (bytes, multiple of 16)
 };
 
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
@@ -477,15 +476,9 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
                        mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
-        auto load = [&](uint32_t dst, const float* src, uint32_t bytes) {
-          for (uint32_t o = 0; o < bytes; o += (uint32_t)p.piece) {
-            const uint32_t b = bytes - o < (uint32_t)p.piece ? bytes - o : (uint32_t)p.piece;
-            bulk_load(dst + o, reinterpret_cast<const char*>(src) + o, b, bar(FULL + s));
-          }
-        };
-        load(smem_u32(slot), p.H + r0 * p.ldh, hb);
-        load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb);
-        if (p.mask) load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb);
+        bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
+        bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
+        if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
       }
     }
     return;
@@ -1097,8 +1090,7 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  static const int piece = getenv("FGL_WG3_PIECE") ? atoi(getenv("FGL_WG3_PIECE")) : (1 << 30);
-  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, piece};
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC};
   FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
