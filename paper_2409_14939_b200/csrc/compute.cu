@@ -523,7 +523,11 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   if (n > 0) {
     int werr = 0;
     const int tc_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 128)));
-    const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(n, 64)));
+    // at least `tpc` 64-row tiles per CTA: small layers then use a few CTAs
+    // (fewer per-CTA prologues, fewer partials to reduce, fewer SMs taken
+    // from the concurrent chain); the large layer 0 still spans all SMs
+    static const int tpc = getenv("FGL_WG_TPC") ? std::max(1, atoi(getenv("FGL_WG_TPC"))) : 16;
+    const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(ceil_div(n, 64), tpc)));
     int used_chunks = chunks, kp1 = 0;
     if (tc_wgrad4(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr) ||
         tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
