@@ -439,6 +439,7 @@ struct Wg3Args {
   int64_t M;
   int K, N, N_pad, tmem_cols, h_bytes, z_bytes, m_bytes, dbg;
   int R, NC;  // raw tile slots, A/B chunk ring depth
+  int nacc;   // TMEM accumulators (tiles round-robin over them)
 };
 
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
@@ -488,7 +489,10 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
   asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  auto ch_hi = [&](int c) { return tmem + (uint32_t)(N_pad + 64 * c); };
+  // TMEM: NACC accumulators [0, NACC N_pad) (tile j accumulates into j % NACC:
+  // the tensor core's fp32 accumulation loses accuracy over long chains, the
+  // epilogue sums the accumulators with IEEE adds), then the A chunk ring
+  auto ch_hi = [&](int c) { return tmem + (uint32_t)(p.nacc * N_pad + 64 * c); };
   const int my_tiles = (int)(tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
 
   if (warp == 1) {
@@ -496,6 +500,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
     const uint32_t sb = smem_u32(sB);
     int cc = 0;
     for (int j = 0; j < ((p.dbg & 16) ? 0 : my_tiles); ++j) {
+      const uint32_t acc_t = tmem + (uint32_t)((j % p.nacc) * N_pad);
       for (int c = 0; c < WG3_MT / 32; ++c, ++cc) {
         const int cs = cc % p.NC;
         mbar_wait(bar(CFULL + cs), (uint32_t)(cc / p.NC) & 1u);
@@ -507,9 +512,10 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
 #pragma unroll
           for (int st = 0; st < ((p.dbg & 2) ? 0 : 4); ++st) {
             const uint64_t dbh = umma_desc_sw128(bh + st * 32), dbl = umma_desc_sw128(bl + st * 32);
-            mma_tf32_ts(tmem, alo + 8 * st, dbh, idesc, (cc | st) != 0);
-            mma_tf32_ts(tmem, ahi + 8 * st, dbl, idesc, 1);
-            mma_tf32_ts(tmem, ahi + 8 * st, dbh, idesc, 1);
+            const uint32_t first = (j < p.nacc && c == 0 && st == 0) ? 0u : 1u;  // overwrite on a fresh accumulator
+            mma_tf32_ts(acc_t, alo + 8 * st, dbh, idesc, first);
+            mma_tf32_ts(acc_t, ahi + 8 * st, dbl, idesc, 1);
+            mma_tf32_ts(acc_t, ahi + 8 * st, dbh, idesc, 1);
           }
           mma_commit(bar(CEMPTY + cs));
         }
@@ -656,13 +662,21 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
       tc_fence_after();
     }
     if (tid == 384) G3T(70);
+    const int used = my_tiles < p.nacc ? my_tiles : p.nacc;
     for (int c0 = 0; c0 < N_pad; c0 += 16) {
-      uint32_t v[16];
-      if (my_tiles > 0) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      float sum[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sum[q] = 0.f;
+      for (int a = 0; a < used; ++a) {  // fixed order: deterministic
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N_pad + c0), v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sum[q] = a == 0 ? __uint_as_float(v[q]) : __fadd_rn(sum[q], __uint_as_float(v[q]));
+      }
       if (m <= p.K) {  // feature-major partials: a warp stores 32 consecutive floats per column
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
+          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = sum[q];
       }
     }
     if (tid == 384) G3T(71);
@@ -1079,8 +1093,10 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   while (R > 2 && smem_of(R) > G3_MAX_SMEM) --R;
   const int64_t smem = smem_of(R);
   if (smem > G3_MAX_SMEM) return false;
+  static const int env_acc = getenv("FGL_WG3_ACC") ? atoi(getenv("FGL_WG3_ACC")) : 4;
+  const int nacc = std::max(1, std::min(env_acc, (512 - 64 * NC) / N_pad));
   int cols = 32;
-  while (cols < N_pad + 64 * NC) cols <<= 1;
+  while (cols < nacc * N_pad + 64 * NC) cols <<= 1;
   if (cols > 512) return false;
   static bool attr = false;
   cudaError_t e;
@@ -1090,7 +1106,7 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC};
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc};
   FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");

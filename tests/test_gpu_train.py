@@ -61,9 +61,11 @@ def test_window_steps_match_oracle(cfg1_graph, arch, dims, fan, direct):
         loss, _ = oracle.train_step(batches[bi], feats, labels, params, cfg.lr, arch)
         assert lv[j] / len(seeds[bi]) == pytest.approx(loss, rel=1e-5)
     got = pipe.model.to_numpy()
+    # 1e-5 relative to the parameter scale after 4 SGD steps: fp32 dense
+    # products and partial sums round differently from numpy's BLAS
     for (w, b), (w2, b2) in zip(got, params):
-        np.testing.assert_allclose(w, w2, rtol=1e-5, atol=2e-6)
-        np.testing.assert_allclose(b, b2, rtol=1e-5, atol=2e-6)
+        np.testing.assert_allclose(w, w2, rtol=1e-5, atol=1e-5 * float(np.abs(w2).max()))
+        np.testing.assert_allclose(b, b2, rtol=1e-5, atol=1e-5 * max(float(np.abs(b2).max()), 0.1))
     torch.cuda.synchronize()
 
 
