@@ -74,17 +74,46 @@ def log(*a):
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML in a
+    background thread every ~5 ms (the region is ~0.1 s), nvidia-smi -lms as
+    the fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.rows = []
+        self.nvml = None
 
     def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self._stop = threading.Event()
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), int(get_reasons(h))))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    time.sleep(0.005)
+            self._thr = threading.Thread(target=run, daemon=True)
+            self._thr.start()
+            return self
+        except Exception:  # noqa: BLE001 - no NVML: nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -95,6 +124,10 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         self.out = ""
+        if self.nvml is not None:
+            self._stop.set()
+            self._thr.join(timeout=1)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -103,6 +136,12 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None:
+            if not self.rows:
+                return {"sm_mhz": None, "sm_max_mhz": float(self.max_mhz), "reasons": ["unsampled"], "samples": 0}
+            reasons = sorted({name for _, r in self.rows for bit, name in self.REASONS.items() if r & bit})
+            return {"sm_mhz": statistics.median(float(c) for c, _ in self.rows), "sm_max_mhz": float(self.max_mhz),
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
         rows = []
         for line in (getattr(self, "out", "") or "").splitlines():
             p = [x.strip() for x in line.split(",")]
@@ -115,7 +154,7 @@ class ClockSampler:
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------- workload --
