@@ -166,7 +166,7 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
 // Warp-specialised TMA variant of tc_gemm (tc_gemm3.cu); same contract.
 bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
-              cudaStream_t st, int* err);
+              cudaStream_t st, int* err, int accum = 0);
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
                int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
 bool tc_wgrad4(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,

@@ -487,6 +487,20 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   }
   if (n == 0) return FGL_OK;
   int err = 0;
+  if (din > 128 && dout <= 256 && !(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15)) {
+    // wide inputs (Reddit: 602): K slices of 128 on the tensor cores, each
+    // adding into Z (bias / ReLU with the last slice); fp32 sums of slices
+    bool ok = true;
+    for (int k0 = 0; k0 < din && ok; k0 += 128) {
+      const int ks = din - k0 < 128 ? din - k0 : 128;
+      const bool last = k0 + ks >= din;
+      ok = tc_gemm3(0, H + k0, ldh, nullptr, 0, W + (int64_t)k0 * dout, last ? b : nullptr, Z, ldz, n, dout, ks,
+                    last ? relu : 0, (cudaStream_t)stream, &err, k0 > 0);
+      if (err) return err;
+    }
+    if (ok) return FGL_OK;
+    // a slice fell outside the envelope: the SIMT kernel below recomputes Z whole
+  }
   if (tc_gemm(0, H, ldh, nullptr, 0, W, b, Z, ldz, n, dout, din, relu, (cudaStream_t)stream, &err))
     return err;
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
@@ -529,7 +543,30 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     static const int tpc = getenv("FGL_WG_TPC") ? std::max(1, atoi(getenv("FGL_WG_TPC"))) : 16;
     const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(ceil_div(n, 64), tpc)));
     int used_chunks = chunks, kp1 = 0;
-    if (tc_wgrad4(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr) ||
+    bool split_done = false;
+    if (din + 1 > 128 && !(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15)) {
+      // wide inputs: feature slices of 124 rows of dW on the tensor cores; each
+      // slice's partials are reduced straight into its rows of dW (db from the
+      // first slice, the others' db rows land in scratch)
+      float* scratch_db = pw + (int64_t)tc3_chunks * 125 * dout;
+      float* slice_part = scratch_db + dout;
+      bool ok = true;
+      for (int k0 = 0; k0 < din && ok; k0 += 124) {
+        const int ks = din - k0 < 124 ? din - k0 : 124;
+        ok = tc_wgrad3(H + k0, ldh, dX, lddx, Xout, ldxo, n, ks, dout, slice_part, tc3_chunks, st, &werr);
+        if (werr) return werr;
+        if (ok) {
+          const int64_t o = (int64_t)(ks + 1) * dout;
+          FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(o, 32), 256, 0, st>>>(
+              slice_part, tc3_chunks, o, dW + (int64_t)k0 * dout, (int64_t)ks * dout, k0 == 0 ? db : scratch_db,
+              ks + 1);
+        }
+      }
+      split_done = ok;
+    }
+    if (split_done) {
+      // dW / db complete
+    } else if (tc_wgrad4(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr) ||
         tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
       if (werr) return werr;
       used_chunks = tc3_chunks;
@@ -543,8 +580,9 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
       FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
                                                                   rows_per, pw, vec);
     }
-    FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
-        pw, used_chunks, outs, dW, (int64_t)din * dout, db, kp1);
+    if (!split_done)
+      FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
+          pw, used_chunks, outs, dW, (int64_t)din * dout, db, kp1);
     int err = 0;
     if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
       if (err) return err;

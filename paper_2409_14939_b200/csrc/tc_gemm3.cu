@@ -50,6 +50,9 @@ struct G3Args {
   int64_t M;
   int N, K, N_pad, K_pad, R, NC, relu, has_mask, tmem_cols, a_slot_bytes, m_slot_bytes, dbg;
   int stage_off, stage_pitch, w_vec;  // coalesced-epilogue staging tile (byte offset in smem, pitch in floats), or -1
+  int accum;  // mode 0: C += A W (earlier K slices already in C)
+  int a_tma;  // A tiles by TMA tensor copies of a column slice (rows of a_lds floats in smem)
+  int a_lds;  // smem row stride of an A tile, floats (= lda for whole-row bulk copies)
 };
 
 // debug timeline (FGL_G3DBG & 8): per CTA, globaltimer stamps of each role's
@@ -75,7 +78,8 @@ __device__ __forceinline__ float tf32_rna_finite(float x) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmC, G3Args p) {
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmC,
+                                                                 const __grid_constant__ CUtensorMap tmA, G3Args p) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -88,12 +92,12 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
   char* slots = sB_lo + b_bytes;
   const int slot_bytes = p.a_slot_bytes + p.m_slot_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(slots + R * slot_bytes);
-  // full[R] empty[R] cfull[8] cempty[8] tfull[2] tempty[2] bready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * R + 21);
+  // full[R] empty[R] cfull[8] cempty[8] tfull[2] tempty[2] bready cacc
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * R + 22);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
   auto bar = [&](int i) { return smem_u32(bars + i); };
   const int FULL = 0, EMPTY = R, CFULL = 2 * R, CEMPTY = 2 * R + 8, TFULL = 2 * R + 16, TEMPTY = 2 * R + 18,
-            BREADY = 2 * R + 20;
+            BREADY = 2 * R + 20, CACC = 2 * R + 21;
 
   if (tid == 0) {
     G3T(0);
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       mbar_init_n(bar(TEMPTY + a), G3_EPI_THREADS);
     }
     mbar_init_n(bar(BREADY), 1);
+    mbar_init_n(bar(CACC), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // barriers initialised
@@ -124,10 +129,12 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
         G3T(2 + 9 * j);
         const int64_t r0 = t * G3_M;
         const int rows = (int)(p.M - r0 < G3_M ? p.M - r0 : G3_M);
-        const uint32_t abytes = (uint32_t)(rows * p.lda * 4), mbytes = p.has_mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        const uint32_t abytes = p.a_tma ? (uint32_t)(G3_M * p.a_lds * 4) : (uint32_t)(rows * p.lda * 4);
+        const uint32_t mbytes = p.has_mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), abytes + mbytes);
-        bulk_load(smem_u32(slot), p.A + r0 * p.lda, abytes, bar(FULL + s));
+        if (p.a_tma) tma_load_2d(smem_u32(slot), &tmA, 0, (int)r0, bar(FULL + s));  // OOB rows / cols: zeros
+        else bulk_load(smem_u32(slot), p.A + r0 * p.lda, abytes, bar(FULL + s));
         if (p.has_mask) bulk_load(smem_u32(slot + p.a_slot_bytes), p.mask + r0 * p.ldm, mbytes, bar(FULL + s));
       }
     }
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       const int s = j % R;
       mbar_wait(bar(FULL + s), (uint32_t)(j / R) & 1u);
       if (row == 0 && grp == 0) G3T(3 + 9 * j);
-      const uint32_t xr = smem_u32(slots + s * slot_bytes) + (uint32_t)(row * p.lda * 4);
+      const uint32_t xr = smem_u32(slots + s * slot_bytes) + (uint32_t)(row * p.a_lds * 4);
       const uint32_t mr = smem_u32(slots + s * slot_bytes + p.a_slot_bytes) + (uint32_t)(row * p.ldm * 4);
       for (int c = 0; c < nch; ++c, ++cc) {
         if ((cc & 1) != grp) continue;
@@ -344,6 +351,18 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
         if (et == 0) bulk_wait_read0();
         asm volatile("bar.sync 2, 128;" ::: "memory");
       }
+      const bool acc_stage = MODE == 0 && p.accum && tma_out;
+      if (acc_stage) {
+        // K split: the earlier slices' sum arrives in the staging boxes by TMA
+        // (same SW128 layout the stores use: conflict-free, coalesced)
+        if (et == 0) {
+          const int nbox = (N_pad + 31) / 32;
+          mbar_arrive_expect_tx(bar(CACC), (uint32_t)(nbox * G3_M * 128));
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(stg_u + (uint32_t)(b * G3_M * 128), &tmC, 32 * b, (int)(t * G3_M), bar(CACC));
+        }
+        mbar_wait(bar(CACC), (uint32_t)j & 1u);
+      }
       for (int c0 = 0; c0 < N_pad; c0 += 32) {
         uint32_t v[32];
         if (p.dbg & 4) { for (int q = 0; q < 32; ++q) v[q] = 0; } else {
@@ -354,9 +373,24 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
         const int ncol = c0 + 16 < N_pad ? 32 : 16;
         for (int h = 0; h < ncol; h += 16) {
           float x[16];
+          float prev[16];
+          if (acc_stage) {
+            const uint32_t box = stg_u + (uint32_t)((c0 >> 5) * (G3_M * 128)) + (uint32_t)(r_loc * 128);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+              const int cc = (h + q) >> 2;
+              const float4 pv = lds128(box + (uint32_t)(((cc ^ (r_loc & 7)) & 7) << 4));
+              prev[q] = pv.x; prev[q + 1] = pv.y; prev[q + 2] = pv.z; prev[q + 3] = pv.w;
+            }
+          } else if (MODE == 0 && p.accum) {  // K split without staging: row-contiguous loads
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              prev[q] = (row < p.M && c0 + h + q < p.N) ? out[c0 + h + q] : 0.f;
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             float y = __uint_as_float(v[h + q]);
+            if (MODE == 0 && p.accum) y = __fadd_rn(prev[q], y);
             if (MODE == 0 && p.bias) y = __fadd_rn(y, sbias[c0 + h + q]);
             if (p.relu) y = y > 0.f ? y : 0.f;
             x[q] = y;
@@ -440,9 +474,11 @@ struct Wg3Args {
   int K, N, N_pad, tmem_cols, h_bytes, z_bytes, m_bytes, dbg;
   int R, NC;  // raw tile slots, A/B chunk ring depth
   int nacc;   // TMEM accumulators (tiles round-robin over them)
+  int h_tma;  // H tiles by TMA tensor copies of a column slice (rows of h_lds floats in smem)
+  int h_lds;  // smem row stride of an H tile, floats (= ldh for whole-row bulk copies)
 };
 
-__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_constant__ CUtensorMap tmH, Wg3Args p) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -473,11 +509,12 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
         if (j < 8) G3T(58 + j);
         const int64_t r0 = t * WG3_MT;
         const int rows = (int)(p.M - r0 < WG3_MT ? p.M - r0 : WG3_MT);
-        const uint32_t hb = (uint32_t)(rows * p.ldh * 4), zb = (uint32_t)(rows * p.ldz * 4),
-                       mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        const uint32_t hb = p.h_tma ? (uint32_t)(WG3_MT * p.h_lds * 4) : (uint32_t)(rows * p.ldh * 4);
+        const uint32_t zb = (uint32_t)(rows * p.ldz * 4), mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
-        bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
+        if (p.h_tma) tma_load_2d(smem_u32(slot), &tmH, 0, (int)r0, bar(FULL + s));  // OOB rows / cols: zeros
+        else bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
         bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
         if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
       }
@@ -553,8 +590,8 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(Wg3Args p) {
         uint32_t hv[32], lv[32];
         {
           const int nrow = rows - 32 * c;
-          const uint32_t a0 = hs + (uint32_t)((32 * c * p.ldh + (m < p.K ? m : 0)) * 4);
-          const uint32_t rs = (uint32_t)(p.ldh * 4);
+          const uint32_t a0 = hs + (uint32_t)((32 * c * p.h_lds + (m < p.K ? m : 0)) * 4);
+          const uint32_t rs = (uint32_t)(p.h_lds * 4);
           float xs[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) xs[q] = lds32(a0 + (uint32_t)q * rs);
@@ -925,7 +962,7 @@ bool make_map_sw128(CUtensorMap* m, const float* base, int64_t rows, int cols, i
 }
 
 int64_t g3_fixed(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
-  return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 21) + 16 + 4 * N_pad;
+  return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 22) + 16 + 4 * N_pad;
 }
 int64_t g3_stage_bytes(int N_pad) { return (int64_t)G3_M * ((N_pad + 31) / 32) * 128; }  // SW128 boxes
 int64_t g3_smem(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
@@ -946,7 +983,7 @@ bool tc3_disabled() {
 // back); *err receives an FGL status otherwise.
 bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, cudaStream_t st,
-              int* err) {
+              int* err, int accum) {
   *err = 0;
   if (tc3_disabled() || M < 1 || N < 1 || K < 1 || K > 128 || lda < K) return false;
   if ((lda % 4) || (reinterpret_cast<uintptr_t>(A) & 15)) return false;
@@ -958,7 +995,11 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   // TMEM: two accumulators + a ring of NC A chunks (64 columns each)
   const int NC = std::min(8, (512 - 2 * N_pad) / (2 * G3_KCH));
   if (NC < 2) return false;
-  const int64_t a_slot = (int64_t)G3_M * lda * 4, m_slot = has_mask ? (int64_t)G3_M * ldm * 4 : 0;
+  // a column slice of a wide A (lda > 256 floats: whole-row bulk copies would
+  // not fit): 2-D TMA tensor copies of [128 rows x K_box] tiles instead
+  const int a_tma = (mode == 0 && lda > 256) ? 1 : 0;
+  const int a_lds = a_tma ? (K + 3) / 4 * 4 : (int)lda;
+  const int64_t a_slot = (int64_t)G3_M * a_lds * 4, m_slot = has_mask ? (int64_t)G3_M * ldm * 4 : 0;
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
   static const int rmax = getenv("FGL_G3SLOTS") ? atoi(getenv("FGL_G3SLOTS")) : G3_MAX_SLOTS;
   // stage mode: 1 (default) = stage the epilogue for TMA tensor stores; 0 =
@@ -999,7 +1040,7 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   const int64_t stage_off = (g3_fixed(N_pad, K_pad, R, a_slot, m_slot) - 1024 + 1023) / 1024 * 1024;
   G3Args p{A, mask, W, bias, C, lda, ldm, ldc, M, N, K, N_pad, K_pad, R, NC, relu, has_mask, cols,
            (int)a_slot, (int)m_slot, dbg, coal ? (int)stage_off : -1, 0,
-           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0)};
+           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0), accum, a_tma, a_lds};
   const int64_t smem = coal ? g3_smem(N_pad, K_pad, R, a_slot, m_slot) : g3_fixed(N_pad, K_pad, R, a_slot, m_slot);
   static bool attr[2] = {false, false};
   cudaError_t e;
@@ -1011,8 +1052,21 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   }
   const int64_t tiles = ceil_div(M, G3_M);
   const int grid = (int)std::min<int64_t>(tiles, kNumSMs);
-  if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, p);
-  else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, p);
+  CUtensorMap mA;
+  std::memset(&mA, 0, sizeof(mA));
+  if (a_tma) {
+    EncodeTiledFn fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+    cuuint32_t box[2] = {(cuuint32_t)a_lds, (cuuint32_t)G3_M};
+    cuuint32_t es[2] = {1, 1};
+    if (!fn || fn(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
+  else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_gemm3_kernel");
   return true;
@@ -1080,7 +1134,11 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     return false;
   if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
   const int N_pad = (N + 15) / 16 * 16;
-  const int hb = WG3_MT * (int)ldh * 4, zb = WG3_MT * (int)ldz * 4, mb = mask ? WG3_MT * (int)ldm * 4 : 0;
+  // a column slice of a wide H (ldh > 256 floats): 2-D TMA tensor copies of
+  // [64 rows x K_box] tiles instead of whole-row bulk copies
+  const int h_tma = ldh > 256 ? 1 : 0;
+  const int h_lds = h_tma ? (K + 3) / 4 * 4 : (int)ldh;
+  const int hb = WG3_MT * h_lds * 4, zb = WG3_MT * (int)ldz * 4, mb = mask ? WG3_MT * (int)ldm * 4 : 0;
   // deepest raw-tile ring that fits next to the chunk ring: the kernel is a
   // stream over H / dZ / mask, so bytes in flight per SM set its speed
   static const int env_r = getenv("FGL_WG3_R") ? atoi(getenv("FGL_WG3_R")) : 0;
@@ -1106,8 +1164,21 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc};
-  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(p);
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc, h_tma, h_lds};
+  CUtensorMap mH;
+  std::memset(&mH, 0, sizeof(mH));
+  if (h_tma) {
+    EncodeTiledFn fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)ldh * 4};
+    cuuint32_t box[2] = {(cuuint32_t)h_lds, (cuuint32_t)WG3_MT};
+    cuuint32_t es[2] = {1, 1};
+    if (!fn || fn(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(H), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(mH, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
   return true;
