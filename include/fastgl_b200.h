@@ -304,6 +304,21 @@ int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int6
                      float* dlogits, int64_t ldd, double* loss_sum, void* ws, int64_t ws_bytes,
                      void* stream);
 
+/* Top model layer of the compact GCN batch in one launch (its rows are the
+ * seeds): logits = H W + b, fp64 softmax cross entropy (trainer.py:198-209),
+ * dH = dY W^T, and per-CTA partials of dW, db and the loss; din <= 64, C <= 48.
+ * With reduce_stream == NULL (or == chain_stream) the partials are reduced
+ * right after on chain_stream; otherwise the caller orders
+ * fgl_top_layer_reduce on reduce_stream after the chain stream (off the
+ * critical path). */
+int64_t fgl_top_layer_ws_bytes(int64_t B, int32_t din, int32_t C);
+int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_base, const int32_t* seed_ids,
+                  const int64_t* labels, int64_t B, int32_t din, int32_t C, const float* W, const float* b,
+                  float* dH, int64_t lddh, float* dW, float* db, double* loss_sum, void* ws, int64_t ws_bytes,
+                  void* chain_stream, void* reduce_stream);
+int fgl_top_layer_reduce(int64_t B, int32_t din, int32_t C, float* dW, float* db, double* loss_sum, void* ws,
+                         void* stream);
+
 /* params -= f32(lr) * grads, separately rounded (trainer.py:321-323). */
 int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream);
 

@@ -424,6 +424,170 @@ __global__ void fill_rows_kernel(float* __restrict__ Y, int64_t ldy, int64_t nro
   }
 }
 
+// Top model layer in one launch (compact GCN: the layer's rows are exactly
+// the batch's seeds): logits Y = H W + b, fp64 softmax cross entropy
+// (trainer.py:198-209) with dY = (p - onehot)/B, dH = dY W^T, and per-CTA
+// partials of dW = H^T dY, db = sum dY and of the loss (reduced off the
+// critical chain).  Replaces the dense forward, the softmax, the loss sum
+// and the dgrad launches of the top layer.  32 seeds per CTA, din <= 64, C <= 48;
+// fp32 FMA in a fixed order (within 1e-5), fp64 loss.
+constexpr int TOP_ROWS = 8;  // one warp per seed row in the softmax; 128 CTAs for a 1024-seed batch
+
+__global__ void __launch_bounds__(256) top_layer_kernel(
+    const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ rows, int64_t row_base,
+    const int32_t* __restrict__ seed_ids, const int64_t* __restrict__ labels, int64_t B, int din, int C,
+    const float* __restrict__ W, const float* __restrict__ b, float* __restrict__ dH, int64_t lddh,
+    float* __restrict__ part, double* __restrict__ loss_part) {
+  __shared__ __align__(16) float Ws[64][64];   // [k][c]
+  __shared__ __align__(16) float WsT[48][64];  // [c][k]
+  __shared__ __align__(16) float Hs[TOP_ROWS][68];
+  __shared__ __align__(16) float Ys[TOP_ROWS][48];
+  __shared__ double lsum[TOP_ROWS];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * TOP_ROWS;
+  const int nr = (int)(B - i0 < TOP_ROWS ? B - i0 : TOP_ROWS);
+  for (int i = t; i < 64 * 64; i += 256) {
+    const int k = i >> 6, c = i & 63;
+    const float v = (k < din && c < C) ? __ldg(W + (int64_t)k * C + c) : 0.f;
+    Ws[k][c] = v;
+    if (c < 48) WsT[c][k] = v;
+  }
+  for (int i = t; i < TOP_ROWS * 68; i += 256) {
+    const int rr = i / 68, k = i - rr * 68;
+    float v = 0.f;
+    if (rr < nr) {
+      if (k < din) v = __ldg(H + (int64_t)(rows[i0 + rr] - row_base) * ldh + k);
+      else if (k == din) v = 1.f;
+    }
+    Hs[rr][k] = v;
+  }
+  __syncthreads();
+  const int rr = warp;  // every phase: warp = seed row of the CTA
+  // logits: lane -> columns 2 lane, 2 lane + 1
+  {
+    const int c0 = 2 * lane;
+    float a0 = 0.f, a1 = 0.f;
+    for (int k = 0; k < din; ++k) {
+      const float h = Hs[rr][k];
+      const float2 w = *reinterpret_cast<const float2*>(&Ws[k][c0]);
+      a0 = __fmaf_rn(h, w.x, a0);
+      a1 = __fmaf_rn(h, w.y, a1);
+    }
+    if (c0 < 48) Ys[rr][c0] = c0 < C ? (b ? __fadd_rn(a0, b[c0]) : a0) : 0.f;
+    if (c0 + 1 < 48) Ys[rr][c0 + 1] = c0 + 1 < C ? (b ? __fadd_rn(a1, b[c0 + 1]) : a1) : 0.f;
+  }
+  __syncwarp();
+  // softmax cross entropy of the warp's row (fp64); Ys <- dY
+  {
+    double l = 0.0;
+    if (rr < nr) {
+      double mx = -INFINITY;
+      for (int c = lane; c < C; c += 32) mx = fmax(mx, (double)Ys[rr][c]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double ex[2] = {0.0, 0.0};
+      double se = 0.0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+        if (c < C) { ex[u] = exp((double)Ys[rr][c] - mx); se += ex[u]; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      const int64_t y = labels[seed_ids ? (int64_t)seed_ids[i0 + rr] : i0 + rr];
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + 32 * u;
+        if (c < C) {
+          const double pc = ex[u] / se;
+          if (c == y) l += -log(pc + 1e-30);
+          Ys[rr][c] = (float)((c == y ? pc - 1.0 : pc) / (double)B);
+        }
+      }
+      l = warp_sum(l);
+    } else {
+      for (int c = lane; c < 48; c += 32) Ys[rr][c] = 0.f;
+    }
+    if (lane == 0) lsum[rr] = l;
+  }
+  __syncwarp();
+  // dH = dY W^T: lane -> input features 2 lane, 2 lane + 1
+  if (rr < nr) {
+    const int k0 = 2 * lane;
+    float a0 = 0.f, a1 = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float g = Ys[rr][c];
+      const float2 w = *reinterpret_cast<const float2*>(&WsT[c][k0]);
+      a0 = __fmaf_rn(g, w.x, a0);
+      a1 = __fmaf_rn(g, w.y, a1);
+    }
+    float* out = dH + (int64_t)(rows[i0 + rr] - row_base) * lddh;
+    if (k0 < din) out[k0] = a0;
+    if (k0 + 1 < din) out[k0 + 1] = a1;
+  }
+  __syncthreads();
+  // dW / db partials [(din + 1) x C] (row din = db): thread = 4 k x 4 c block
+  {
+    float* pp = part + (int64_t)blockIdx.x * (din + 1) * C;
+    const int kb = (din + 1 + 3) >> 2, cb = (C + 3) >> 2;
+    for (int blk = t; blk < kb * cb; blk += 256) {
+      const int k0 = (blk / cb) * 4, c0 = (blk % cb) * 4;
+      float a[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[u][v] = 0.f;
+      for (int r = 0; r < nr; ++r) {
+        const float4 h = *reinterpret_cast<const float4*>(&Hs[r][k0]);
+        const float4 g = *reinterpret_cast<const float4*>(&Ys[r][c0]);
+        const float hv[4] = {h.x, h.y, h.z, h.w}, gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) a[u][v] = __fmaf_rn(hv[u], gv[v], a[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (k0 + u <= din && c0 + v < C) pp[(int64_t)(k0 + u) * C + c0 + v] = a[u][v];
+    }
+  }
+  if (t == 0) {
+    double l = 0.0;
+    for (int r = 0; r < TOP_ROWS; ++r) l += lsum[r];
+    loss_part[blockIdx.x] = l;
+  }
+}
+
+// partials -> dW / db (fixed order, 4 independent accumulators per output
+// combined in a fixed tree: deterministic) and the batch loss (fp64)
+__global__ void top_reduce_kernel(const float* __restrict__ part, int chunks, int64_t outs, float* __restrict__ dW,
+                                  int64_t split, float* __restrict__ db, const double* __restrict__ loss_part,
+                                  double* __restrict__ loss_sum) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < outs) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int c = 0;
+    for (; c + 3 < chunks; c += 4) {
+      s0 = __fadd_rn(s0, part[(int64_t)c * outs + i]);
+      s1 = __fadd_rn(s1, part[(int64_t)(c + 1) * outs + i]);
+      s2 = __fadd_rn(s2, part[(int64_t)(c + 2) * outs + i]);
+      s3 = __fadd_rn(s3, part[(int64_t)(c + 3) * outs + i]);
+    }
+    for (; c < chunks; ++c) s0 = __fadd_rn(s0, part[(int64_t)c * outs + i]);
+    const float s = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+    if (i < split) dW[i] = s; else db[i - split] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    double l = 0.0;
+    for (int c = threadIdx.x; c < chunks; c += 32) l += loss_part[c];
+    l = warp_sum(l);
+    if (threadIdx.x == 0) *loss_sum = l;
+  }
+}
+
 int blocks_for(int64_t n, int t = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, t), 148 * 16));
 }
@@ -634,6 +798,50 @@ int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int6
                                               dlogits, ldd, part);
   FGL_COUNT_LAUNCH(), sum_doubles_kernel<<<1, 1024, 0, st>>>(part, blocks * 8, loss_sum);
   FGL_LAUNCH_CHECK("softmax_xent");
+  return FGL_OK;
+}
+
+int64_t fgl_top_layer_ws_bytes(int64_t B, int32_t din, int32_t C) {
+  const int64_t chunks = ceil_div(std::max<int64_t>(B, 1), TOP_ROWS);
+  return chunks * ((int64_t)(din + 1) * C * 4 + 8) + 64;
+}
+
+int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_base, const int32_t* seed_ids,
+                  const int64_t* labels, int64_t B, int32_t din, int32_t C, const float* W, const float* b,
+                  float* dH, int64_t lddh, float* dW, float* db, double* loss_sum, void* ws, int64_t ws_bytes,
+                  void* chain_stream, void* reduce_stream) {
+  if (B < 1 || din < 1 || din > 64 || C < 1 || C > 48 || !H || !rows || !labels || !W || !dH || !dW || !db ||
+      !loss_sum || ldh < din || lddh < din || ws_bytes < fgl_top_layer_ws_bytes(B, din, C)) {
+    set_error("fgl_top_layer: bad arguments (din <= 64, C <= 48)");
+    return FGL_E_INVALID;
+  }
+  const int chunks = (int)ceil_div(B, TOP_ROWS);
+  float* part = static_cast<float*>(ws);
+  double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
+  FGL_COUNT_LAUNCH(), top_layer_kernel<<<chunks, 256, 0, (cudaStream_t)chain_stream>>>(
+      H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp);
+  FGL_LAUNCH_CHECK("top_layer_kernel");
+  if (reduce_stream && reduce_stream != chain_stream) {
+    // the reduction is off the chain: the caller orders reduce_stream after
+    // chain_stream's top_layer_kernel with an event (fgl_top_layer_reduce)
+    return FGL_OK;
+  }
+  const int64_t outs = (int64_t)(din + 1) * C;
+  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 256), 256, 0, (cudaStream_t)chain_stream>>>(
+      part, chunks, outs, dW, (int64_t)din * C, db, lp, loss_sum);
+  FGL_LAUNCH_CHECK("top_reduce_kernel");
+  return FGL_OK;
+}
+
+int fgl_top_layer_reduce(int64_t B, int32_t din, int32_t C, float* dW, float* db, double* loss_sum, void* ws,
+                         void* stream) {
+  const int chunks = (int)ceil_div(B, TOP_ROWS);
+  float* part = static_cast<float*>(ws);
+  double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
+  const int64_t outs = (int64_t)(din + 1) * C;
+  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 256), 256, 0, (cudaStream_t)stream>>>(
+      part, chunks, outs, dW, (int64_t)din * C, db, lp, loss_sum);
+  FGL_LAUNCH_CHECK("top_reduce_kernel");
   return FGL_OK;
 }
 

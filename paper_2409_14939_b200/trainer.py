@@ -313,6 +313,7 @@ class Pipeline:
         self._cs = None  # stream being issued on inside run_windows
         self._capturing = False
         self.graph_fallbacks = 0
+        self._fuse_top = os.environ.get("FGL_FUSE_TOP", "1") != "0"
         self._keep_l0_transpose = False  # tests that inspect layer 0's transpose set this
         self.xent_ws = torch.empty(_lib.lib().fgl_softmax_xent_ws_bytes(), dtype=torch.uint8, device=device)
         self._bufs = {}
@@ -536,6 +537,10 @@ class Pipeline:
                        s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None,
                        None, None, self.ldf, x0.data_ptr(), self.ldf, self.loaded.data_ptr(), None, st)
         # forward
+        s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
+        top_fused = (self.compact and not self.fused_upper and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 48
+                     and self._fuse_top
+                     and (self._rows(win, self.L - 1, b)[1] - self._rows(win, self.L - 1, b)[0]) == s1 - s0)
         X, ldx = x0, self.ldf
         H_bufs, Y_bufs, ns = [], [], []
         for i in range(1 if self.fused_upper else self.L):
@@ -558,9 +563,12 @@ class Pipeline:
                     col, base = lay["col_global"], 0
                 self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
                            base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
-            Yb = self._buf(f"y{i}", n, _ld(dout))
-            self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout,
-                       Yb.data_ptr(), _ld(dout), 1 if i < self.L - 1 else 0, st)
+            if i == self.L - 1 and top_fused:
+                Yb = None  # the fused top-layer kernel computes the logits itself
+            else:
+                Yb = self._buf(f"y{i}", n, _ld(dout))
+                self._call("fgl_dense_fwd", Hb.data_ptr(), _ld(din), n, din, m.W(i), m.b(i), dout,
+                           Yb.data_ptr(), _ld(dout), 1 if i < self.L - 1 else 0, st)
             H_bufs.append(Hb)
             Y_bufs.append(Yb)
             ns.append(n)
@@ -569,31 +577,58 @@ class Pipeline:
         if self.fused_upper:
             self._fused_upper_step(win, b, layers, H_bufs, Y_bufs, ns, s0, s1, slot)
             return
-        # loss over the seed rows of the last layer
         C = dims[-1]
         r0, _ = self._rows(win, self.L - 1, b)
-        dY = self._buf("dy_last", ns[-1], _ld(C))
-        if not self.compact:
-            self._call("fgl_fill_rows", dY.data_ptr(), _ld(C), ns[-1], C, None, 0, st)
         rows_ptr = (s.seed_front if self.compact else s.seed_rows).data_ptr() + 4 * s0
-        self._call("fgl_softmax_xent", Y_bufs[-1].data_ptr(), _ld(C), rows_ptr, r0,
-                   s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), s1 - s0, C,
-                   dY.data_ptr(), _ld(C), self.loss_dev.data_ptr() + 8 * slot,
-                   self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
+        wg_done = []
+        side = self._side_wgrad_stream()
+        first_bwd = self.L - 1
+        if top_fused:
+            # top layer: logits, loss, dH and the weight-gradient partials in
+            # one launch; the partial reduction runs on the side stream
+            it = self.L - 1
+            din = dims[it]
+            dHt = self._buf(f"dh{it}", ns[it], _ld(din))
+            B = s1 - s0
+            wsb = _lib.lib().fgl_top_layer_ws_bytes(B, din, C)
+            tws = self._buf(f"top_ws{slot % 2}", wsb, 1, torch.uint8)
+            red = side.cuda_stream if side is not None else None
+            self._call("fgl_top_layer", H_bufs[it].data_ptr(), _ld(din), rows_ptr, r0,
+                       s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), B, din, C, m.W(it), m.b(it),
+                       dHt.data_ptr(), _ld(din), m.dW(it), m.db(it), self.loss_dev.data_ptr() + 8 * slot,
+                       tws.data_ptr(), wsb, st, red)
+            if side is not None:
+                ready = torch.cuda.Event()
+                ready.record(self._cur())
+                side.wait_event(ready)
+                self._call("fgl_top_layer_reduce", B, din, C, m.dW(it), m.db(it),
+                           self.loss_dev.data_ptr() + 8 * slot, tws.data_ptr(), side.cuda_stream)
+                done = torch.cuda.Event()
+                done.record(side)
+                wg_done.append(done)
+        else:
+            # loss over the seed rows of the last layer
+            dY = self._buf("dy_last", ns[-1], _ld(C))
+            if not self.compact:
+                self._call("fgl_fill_rows", dY.data_ptr(), _ld(C), ns[-1], C, None, 0, st)
+            self._call("fgl_softmax_xent", Y_bufs[-1].data_ptr(), _ld(C), rows_ptr, r0,
+                       s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), s1 - s0, C,
+                       dY.data_ptr(), _ld(C), self.loss_dev.data_ptr() + 8 * slot,
+                       self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
         # backward.  Layer i > 0: its weight gradient (dW, db) only feeds the
         # SGD step, so it runs on a side stream while the chain continues with
         # dH = dZ W^T -> transposed aggregation -> layer i-1; the SGD waits for
         # all of them.  Same kernels and inputs: results are unchanged.
-        dX, lddx = dY, _ld(C)
-        wg_done = []
-        side = self._side_wgrad_stream()
-        for i in range(self.L - 1, -1, -1):
+        dX, lddx = (None, 0) if top_fused else (dY, _ld(C))
+        for i in range(first_bwd, -1, -1):
             din, dout = dims[i], dims[i + 1]
             n = ns[i]
             mask = Y_bufs[i].data_ptr() if i < self.L - 1 else None
             dH = self._buf(f"dh{i}", n, _ld(din)) if i > 0 else None
             ws_i = self.bwd_ws_l[i]
-            if i > 0 and side is not None:
+            if top_fused and i == self.L - 1:
+                pass  # dH / dW / db of the top layer came from fgl_top_layer
+            elif i > 0 and side is not None:
                 ready = torch.cuda.Event()
                 ready.record(self._cur())
                 side.wait_event(ready)
