@@ -446,20 +446,35 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t i0 = (int64_t)blockIdx.x * TOP_ROWS;
   const int nr = (int)(B - i0 < TOP_ROWS ? B - i0 : TOP_ROWS);
-  for (int i = t; i < 64 * 64; i += 256) {
-    const int k = i >> 6, c = i & 63;
-    const float v = (k < din && c < C) ? __ldg(W + (int64_t)k * C + c) : 0.f;
-    Ws[k][c] = v;
-    if (c < 48) WsT[c][k] = v;
+  // every global load of the staging is issued before the first shared
+  // store (one memory latency, not one per element)
+  float wv[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = t + 256 * u, k = i >> 6, c = i & 63;
+    wv[u] = (k < din && c < C) ? __ldg(W + (int64_t)k * C + c) : 0.f;
   }
-  for (int i = t; i < TOP_ROWS * 68; i += 256) {
-    const int rr = i / 68, k = i - rr * 68;
+  float hv3[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int i = t + 256 * u, r = i / 68, k = i - r * 68;
     float v = 0.f;
-    if (rr < nr) {
-      if (k < din) v = __ldg(H + (int64_t)(rows[i0 + rr] - row_base) * ldh + k);
+    if (i < TOP_ROWS * 68 && r < nr) {
+      if (k < din) v = __ldg(H + (int64_t)(rows[i0 + r] - row_base) * ldh + k);
       else if (k == din) v = 1.f;
     }
-    Hs[rr][k] = v;
+    hv3[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = t + 256 * u, k = i >> 6, c = i & 63;
+    Ws[k][c] = wv[u];
+    if (c < 48) WsT[c][k] = wv[u];
+  }
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int i = t + 256 * u;
+    if (i < TOP_ROWS * 68) Hs[i / 68][i % 68] = hv3[u];
   }
   __syncthreads();
   const int rr = warp;  // every phase: warp = seed row of the CTA
