@@ -307,6 +307,9 @@ int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int6
 /* Top model layer of the compact GCN batch in one launch (its rows are the
  * seeds): logits = H W + b, fp64 softmax cross entropy (trainer.py:198-209),
  * dH = dY W^T, and per-CTA partials of dW, db and the loss; din <= 64, C <= 48.
+ * agg_indptr != NULL: H is not read but gathered in-kernel as A X with
+ * X = H (ldh), the layer's CSR (agg_indptr over the same rows, agg_col -
+ * agg_col_base, agg_w), fgl_spmm arithmetic (bit-identical).
  * With reduce_stream == NULL (or == chain_stream) the partials are reduced
  * right after on chain_stream; otherwise the caller orders
  * fgl_top_layer_reduce on reduce_stream after the chain stream (off the
@@ -315,6 +318,7 @@ int64_t fgl_top_layer_ws_bytes(int64_t B, int32_t din, int32_t C);
 int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_base, const int32_t* seed_ids,
                   const int64_t* labels, int64_t B, int32_t din, int32_t C, const float* W, const float* b,
                   float* dH, int64_t lddh, float* dW, float* db, double* loss_sum, void* ws, int64_t ws_bytes,
+                  const int64_t* agg_indptr, const int32_t* agg_col, const float* agg_w, int64_t agg_col_base,
                   void* chain_stream, void* reduce_stream);
 int fgl_top_layer_reduce(int64_t B, int32_t din, int32_t C, float* dW, float* db, double* loss_sum, void* ws,
                          void* stream);

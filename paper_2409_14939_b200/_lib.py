@@ -122,7 +122,7 @@ SIGNATURES = {
                                    vp, C.c_int64, vp, vp, C.c_int64, vp]),
     "fgl_top_layer_ws_bytes": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "fgl_top_layer": (C.c_int, [vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, C.c_int32, C.c_int32, vp, vp, vp,
-                                C.c_int64, vp, vp, vp, vp, C.c_int64, vp, vp]),
+                                C.c_int64, vp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp, vp]),
     "fgl_top_layer_reduce": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "fgl_sgd": (C.c_int, [vp, vp, C.c_int64, C.c_float, vp]),
     "fgl_fill_rows": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, vp, C.c_int32, vp]),

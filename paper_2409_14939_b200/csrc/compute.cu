@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
     const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ rows, int64_t row_base,
     const int32_t* __restrict__ seed_ids, const int64_t* __restrict__ labels, int64_t B, int din, int C,
     const float* __restrict__ W, const float* __restrict__ b, float* __restrict__ dH, int64_t lddh,
-    float* __restrict__ part, double* __restrict__ loss_part) {
+    float* __restrict__ part, double* __restrict__ loss_part, const int64_t* __restrict__ agg_indptr,
+    const int32_t* __restrict__ agg_col, const float* __restrict__ agg_w, int64_t agg_col_base) {
   __shared__ __align__(16) float Ws[64][64];   // [k][c]
   __shared__ __align__(16) float WsT[48][64];  // [c][k]
   __shared__ __align__(16) float Hs[TOP_ROWS][68];
@@ -454,27 +455,72 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
     const int i = t + 256 * u, k = i >> 6, c = i & 63;
     wv[u] = (k < din && c < C) ? __ldg(W + (int64_t)k * C + c) : 0.f;
   }
-  float hv3[3];
+  if (agg_indptr) {
+    // H = A X for this CTA's rows, gathered here (one warp per row, float4
+    // lanes, CSR order with a rounded multiply then a rounded add: the
+    // arithmetic of fgl_spmm, bit-identical); H never leaves the chip
+    const int rw = warp, ln = lane & 15, d4 = (din + 3) >> 2;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rw < nr) {
+      const int64_t r = rows[i0 + rw] - row_base;
+      const int64_t e0 = agg_indptr[r], e1 = agg_indptr[r + 1];
+      for (int64_t e = e0; e < e1; e += 4) {
+        const int n = (int)(e1 - e < 4 ? e1 - e : 4);
+        int32_t cc[4];
+        float ww[4];
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    const int i = t + 256 * u, r = i / 68, k = i - r * 68;
-    float v = 0.f;
-    if (i < TOP_ROWS * 68 && r < nr) {
-      if (k < din) v = __ldg(H + (int64_t)(rows[i0 + r] - row_base) * ldh + k);
-      else if (k == din) v = 1.f;
+        for (int u = 0; u < 4; ++u) {
+          cc[u] = u < n ? (int32_t)(__ldg(agg_col + e + u) - agg_col_base) : 0;
+          ww[u] = u < n ? __ldg(agg_w + e + u) : 0.f;
+        }
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = (u < n && lane < 16 && ln < d4)
+                     ? __ldg(reinterpret_cast<const float4*>(H + (int64_t)cc[u] * ldh) + ln)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < n) acc = fmadd4(acc, ww[u], x[u]);
+      }
     }
-    hv3[u] = v;
-  }
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int i = t + 256 * u, k = i >> 6, c = i & 63;
-    Ws[k][c] = wv[u];
-    if (c < 48) WsT[c][k] = wv[u];
-  }
+    for (int u = 0; u < 16; ++u) {
+      const int i = t + 256 * u, k = i >> 6, c = i & 63;
+      Ws[k][c] = wv[u];
+      if (c < 48) WsT[c][k] = wv[u];
+    }
+    for (int k = lane; k < 68; k += 32) Hs[rw][k] = (rw < nr && k == din) ? 1.f : 0.f;
+    __syncwarp();
+    if (lane < 16 && ln < d4 && rw < nr) {
+      Hs[rw][4 * ln] = acc.x;
+      if (4 * ln + 1 < din) Hs[rw][4 * ln + 1] = acc.y;
+      if (4 * ln + 2 < din) Hs[rw][4 * ln + 2] = acc.z;
+      if (4 * ln + 3 < din) Hs[rw][4 * ln + 3] = acc.w;
+    }
+  } else {
+    float hv3[3];
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    const int i = t + 256 * u;
-    if (i < TOP_ROWS * 68) Hs[i / 68][i % 68] = hv3[u];
+    for (int u = 0; u < 3; ++u) {
+      const int i = t + 256 * u, r = i / 68, k = i - r * 68;
+      float v = 0.f;
+      if (i < TOP_ROWS * 68 && r < nr) {
+        if (k < din) v = __ldg(H + (int64_t)(rows[i0 + r] - row_base) * ldh + k);
+        else if (k == din) v = 1.f;
+      }
+      hv3[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = t + 256 * u, k = i >> 6, c = i & 63;
+      Ws[k][c] = wv[u];
+      if (c < 48) WsT[c][k] = wv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int i = t + 256 * u;
+      if (i < TOP_ROWS * 68) Hs[i / 68][i % 68] = hv3[u];
+    }
   }
   __syncthreads();
   const int rr = warp;  // every phase: warp = seed row of the CTA
@@ -824,9 +870,11 @@ int64_t fgl_top_layer_ws_bytes(int64_t B, int32_t din, int32_t C) {
 int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_base, const int32_t* seed_ids,
                   const int64_t* labels, int64_t B, int32_t din, int32_t C, const float* W, const float* b,
                   float* dH, int64_t lddh, float* dW, float* db, double* loss_sum, void* ws, int64_t ws_bytes,
+                  const int64_t* agg_indptr, const int32_t* agg_col, const float* agg_w, int64_t agg_col_base,
                   void* chain_stream, void* reduce_stream) {
   if (B < 1 || din < 1 || din > 64 || C < 1 || C > 48 || !H || !rows || !labels || !W || !dH || !dW || !db ||
-      !loss_sum || ldh < din || lddh < din || ws_bytes < fgl_top_layer_ws_bytes(B, din, C)) {
+      !loss_sum || ldh < din || lddh < din || ws_bytes < fgl_top_layer_ws_bytes(B, din, C) ||
+      (agg_indptr && (!agg_col || !agg_w || (ldh % 4) || (reinterpret_cast<uintptr_t>(H) & 15)))) {
     set_error("fgl_top_layer: bad arguments (din <= 64, C <= 48)");
     return FGL_E_INVALID;
   }
@@ -834,7 +882,8 @@ int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_
   float* part = static_cast<float*>(ws);
   double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
   FGL_COUNT_LAUNCH(), top_layer_kernel<<<chunks, 256, 0, (cudaStream_t)chain_stream>>>(
-      H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp);
+      H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp, agg_indptr, agg_col, agg_w,
+      agg_col_base);
   FGL_LAUNCH_CHECK("top_layer_kernel");
   if (reduce_stream && reduce_stream != chain_stream) {
     // the reduction is off the chain: the caller orders reduce_stream after

@@ -555,6 +555,11 @@ class Pipeline:
                 Hb, ev = pre
                 if not external_done and ev is not None:
                     self._cur().wait_event(ev)
+            elif i == self.L - 1 and top_fused:
+                # the fused top-layer kernel gathers H = A X itself
+                Hb = None
+                top_agg = (lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(),
+                           self._in_base(win, i, b), X.data_ptr(), ldx)
             else:
                 Hb = self._buf(f"h{i}", n, _ld(din))
                 self_x = X.data_ptr() if not self.compact else None
@@ -593,10 +598,11 @@ class Pipeline:
             wsb = _lib.lib().fgl_top_layer_ws_bytes(B, din, C)
             tws = self._buf(f"top_ws{slot % 2}", wsb, 1, torch.uint8)
             red = side.cuda_stream if side is not None else None
-            self._call("fgl_top_layer", H_bufs[it].data_ptr(), _ld(din), rows_ptr, r0,
+            a_ip, a_col, a_w, a_base, a_x, a_ld = top_agg
+            self._call("fgl_top_layer", a_x, a_ld, rows_ptr, r0,
                        s.seeds_dev.data_ptr() + 4 * s0, self.labels.data_ptr(), B, din, C, m.W(it), m.b(it),
                        dHt.data_ptr(), _ld(din), m.dW(it), m.db(it), self.loss_dev.data_ptr() + 8 * slot,
-                       tws.data_ptr(), wsb, st, red)
+                       tws.data_ptr(), wsb, a_ip, a_col, a_w, a_base, st, red)
             if side is not None:
                 ready = torch.cuda.Event()
                 ready.record(self._cur())
