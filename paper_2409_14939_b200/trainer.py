@@ -826,7 +826,7 @@ class Pipeline:
         return order, self.loss_dev[:nb]
 
     # --------------------------------------------------------- pipelined --
-    LOOKAHEAD = 2  # windows sampled ahead of the one being trained
+    LOOKAHEAD = int(os.environ.get("FGL_LOOKAHEAD", "2"))  # windows sampled ahead of the one being trained
 
     def _sample_async(self, seed_lists, rng_seeds, slot):
         """Stage + launch the window sampler of slot `slot` (LOOKAHEAD + 1
