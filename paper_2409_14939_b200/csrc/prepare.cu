@@ -423,9 +423,10 @@ static int prepare_layer_impl(const int32_t* lt, const int32_t* ls, int64_t nnz,
   int32_t* perm = reinterpret_cast<int32_t*>(p);
   int32_t* outdeg = reinterpret_cast<int32_t*>(p + al(4 * std::max<int64_t>(nnz, 1)));
   void* gws = p + al(4 * std::max<int64_t>(nnz, 1)) + al(4 * std::max<int64_t>(num_cols, 1));
-  if (sparse_rows)
-    FGL_COUNT_LAUNCH(), offsets_bsearch_kernel<<<grid_for(num_rows + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
-  else
+  if (sparse_rows) {
+    // grouped path: the stable grouping by target already wrote these
+    // offsets (its exclusive scan of the per-row counts) -- nothing to do
+  } else
     FGL_COUNT_LAUNCH(), offsets_from_sorted_kernel<<<grid_for(nnz + 1), kThreads, 0, st>>>(lt, nnz, num_rows, 0, indptr);
   if (transpose) {
     int rc = stable_group_impl(ls, nnz, num_cols, 0, t_indptr, perm, outdeg, gws,
