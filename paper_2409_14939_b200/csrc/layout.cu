@@ -97,6 +97,103 @@ __global__ void depth_part_scan_kernel(int64_t* part, int n) {
   }
 }
 
+// All depths in one pass (instead of one count / scan / apply pass per depth).
+// Per-chunk counts of every depth: part[d * (G + 1) + blk].
+__global__ void depth_chunk_all_kernel(const int8_t* __restrict__ depth, const int64_t* __restrict__ uoff, int nb,
+                                       int D, int64_t* part) {
+  __shared__ unsigned int sc[8];
+  if (threadIdx.x < 8) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t U = uoff[nb];
+  const int64_t chunk = ceil_div(U, gridDim.x);
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(U, i0 + chunk);
+  unsigned int c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t u = i0 + threadIdx.x; u < i1; u += blockDim.x) {
+    const int d = depth[u];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] += (d == k) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    unsigned int v = c[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(sc + k, v);
+  }
+  __syncthreads();
+  if (threadIdx.x < D) part[(int64_t)threadIdx.x * (gridDim.x + 1) + blockIdx.x] = sc[threadIdx.x];
+}
+
+// block d: exclusive scan of depth d's chunk counts
+__global__ void depth_part_scan_all_kernel(int64_t* part, int n) {
+  __shared__ int64_t sm[33];
+  int64_t* q = part + (int64_t)blockIdx.x * (n + 1);
+  int64_t carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int64_t v = i < n ? q[i] : 0, tot;
+    const int64_t ex = block_excl_scan(v, sm, &tot);
+    if (i < n) q[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+// new row of every row, all depths at once: warp ballots give each row its
+// rank among same-depth rows of the tile; u0[b] + rows of smaller depth in
+// batch b + (same-depth rows of batch b before it)
+__global__ void __launch_bounds__(256) depth_apply_all_kernel(const int8_t* __restrict__ depth,
+                                                              const int64_t* __restrict__ uoff, int nb, int D,
+                                                              const int64_t* __restrict__ part,
+                                                              const unsigned long long* __restrict__ cnt,
+                                                              int32_t* __restrict__ row_map) {
+  __shared__ int64_t sbase[64 * 9], sbefore[64 * 9];
+  __shared__ int64_t srun[8], tot[8];
+  __shared__ int wcnt[8][8], wex[8][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = tid; k < nb * D; k += blockDim.x) {
+    const int b = k / D, d = k - b * D;
+    int64_t base = 0, before = 0;
+    for (int hh = 0; hh < d; ++hh) base += (int64_t)cnt[b * D + hh];
+    for (int bb = 0; bb < b; ++bb) before += (int64_t)cnt[bb * D + d];
+    sbase[k] = uoff[b] + base;
+    sbefore[k] = before;
+  }
+  if (tid < D) srun[tid] = part[(int64_t)tid * (gridDim.x + 1) + blockIdx.x];
+  __syncthreads();
+  const int64_t U = uoff[nb];
+  const int64_t chunk = ceil_div(U, gridDim.x);
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(U, i0 + chunk);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t t0 = i0; t0 < i1; t0 += blockDim.x) {
+    const int64_t u = t0 + tid;
+    const int dd = u < i1 ? (int)depth[u] : -1;
+    int mypre = 0;
+    for (int d = 0; d < D; ++d) {
+      const unsigned m = __ballot_sync(0xffffffffu, dd == d);
+      if (lane == 0) wcnt[warp][d] = __popc(m);
+      if (dd == d) mypre = __popc(m & lt_mask);
+    }
+    __syncthreads();
+    if (tid < D) {
+      int acc = 0;
+      for (int w = 0; w < 8; ++w) {
+        wex[w][tid] = acc;
+        acc += wcnt[w][tid];
+      }
+      tot[tid] = acc;
+    }
+    __syncthreads();
+    if (dd >= 0) {
+      const int b = seg_of(uoff, nb, u);
+      const int64_t ex = srun[dd] + wex[warp][dd] + mypre;
+      row_map[u] = (int32_t)(sbase[b * D + dd] + ex - sbefore[b * D + dd]);
+    }
+    __syncthreads();
+    if (tid < D) srun[tid] += tot[tid];
+    __syncthreads();
+  }
+}
+
 // new row of every depth-h row: u0[b] + (depth-h rows of batch b before it,
 // = global depth-h rank minus the depth-h rows of earlier batches) + the rows
 // of smaller depth in batch b
@@ -173,7 +270,7 @@ extern "C" {
 
 int64_t fgl_depth_relayout_ws_bytes(int64_t unique_cap) {
   const int64_t u = std::max<int64_t>(unique_cap, 1);
-  return (u + 255) / 256 * 256 + 4 * u + 8 * (2 * kPersistentCTAs + 2) + 256;
+  return (u + 255) / 256 * 256 + 4 * u + 8 * 8 * (kPersistentCTAs + 1) + 256;  // part: up to 8 depths x (G + 1)
 }
 
 int fgl_depth_relayout(const int64_t* counts, int32_t H, int32_t nb, const int32_t* frontier,
@@ -213,10 +310,17 @@ int fgl_depth_relayout(const int64_t* counts, int32_t H, int32_t nb, const int32
                                                             wprefix, words, h, depth);
   }
   FGL_COUNT_LAUNCH(), depth_count_kernel<<<TG, LT, 0, st>>>(depth, uoff, nb, H, cnt);
-  for (int h = 0; h <= H; ++h) {
-    FGL_COUNT_LAUNCH(), depth_chunk_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, h, part);
-    FGL_COUNT_LAUNCH(), depth_part_scan_kernel<<<1, 1024, 0, st>>>(part, G);
-    FGL_COUNT_LAUNCH(), depth_apply_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, H, h, part, cnt, row_map);
+  if (H + 1 <= 8 && LT == 256) {
+    // all depths in one count / scan / apply pass
+    FGL_COUNT_LAUNCH(), depth_chunk_all_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, H + 1, part);
+    FGL_COUNT_LAUNCH(), depth_part_scan_all_kernel<<<H + 1, 1024, 0, st>>>(part, G);
+    FGL_COUNT_LAUNCH(), depth_apply_all_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, H + 1, part, cnt, row_map);
+  } else {
+    for (int h = 0; h <= H; ++h) {
+      FGL_COUNT_LAUNCH(), depth_chunk_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, h, part);
+      FGL_COUNT_LAUNCH(), depth_part_scan_kernel<<<1, 1024, 0, st>>>(part, G);
+      FGL_COUNT_LAUNCH(), depth_apply_kernel<<<G, LT, 0, st>>>(depth, uoff, nb, H, h, part, cnt, row_map);
+    }
   }
   FGL_COUNT_LAUNCH(), permute_unique_kernel<<<TG, LT, 0, st>>>(unique_nodes, uoff, nb, row_map, tmp);
   FGL_COUNT_LAUNCH(), copy_i32_kernel<<<TG, LT, 0, st>>>(tmp, uoff, nb, unique_nodes);
