@@ -195,6 +195,14 @@ def epoch_windows(num_nodes, cfg, seed=0):
 _CPU = {}
 
 
+def _host_features(feats, cfg):
+    """[N, d] host array of the workload's features (a view for a pinned store)."""
+    table = getattr(feats, "table", None)
+    if table is not None:
+        return table[:, : cfg["dims"][0]].numpy()
+    return feats.cpu().numpy()
+
+
 def _cpu_batch(args):
     import oracle
     seeds, rs = args
@@ -217,7 +225,7 @@ def cpu_oracle_throughput(dg, feats, labels, cfg, windows, budget_s=25.0, worker
     from paper_2409_14939_b200.graph import to_host
     hg = to_host(dg)
     g = oracle.CSRGraph(hg.num_nodes, hg.row_offsets, hg.col_indices, None, None, None)
-    _CPU.update(g=g, feats=feats.cpu().numpy(), labels=labels.cpu().numpy(), dims=cfg["dims"],
+    _CPU.update(g=g, feats=_host_features(feats, cfg), labels=labels.cpu().numpy(), dims=cfg["dims"],
                 fanouts=cfg["fanouts"], arch=cfg["arch"], params=oracle.init_params(cfg["dims"], 0))
     workers = workers or max(1, min(os.cpu_count() or 1, 16))
     # one probe batch sizes the sample to the time budget
@@ -248,6 +256,70 @@ def cpu_oracle_throughput(dg, feats, labels, cfg, windows, budget_s=25.0, worker
 
 
 # ------------------------------------------------------------------- main --
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: launch the N ranks (one
+    process per GPU, NCCL over NVLink) through torch.distributed.run on
+    127.0.0.1 and return its exit code; rank 0 prints the JSON line."""
+    import torch
+    if args.impl == "ours" and args.dist_backend == "nccl" and torch.cuda.device_count() < args.gpus:
+        log(f"bench: --gpus {args.gpus} needs {args.gpus} visible GPUs for NCCL (found {torch.cuda.device_count()}); "
+            f"--dist-backend gloo runs the ranks on fewer GPUs (functional check, not a measurement)")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ)
+    if args.impl == "ours" and args.dist_backend == "nccl":
+        # the communicator's INIT lines (rings / NVLS / channels) on stderr
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    log("bench: spawning", " ".join(cmd))
+    return subprocess.call(cmd, env=env)
+
+
+def make_feature_store(cfg, dg, rank, world, device):
+    """BASELINE config 4: the feature table in pinned HOST memory, ONE copy
+    for all ranks of the node (HostFeatureStore.shared: rank 0 fills a
+    shared-memory table that every rank maps and page-locks).  Rank 0
+    generates the rows on its GPU chunk by chunk (seeded)."""
+    import torch
+    from paper_2409_14939_b200.store import HostFeatureStore
+    n, d = dg.num_nodes, cfg["dims"][0]
+
+    def fill(table):
+        gen = torch.Generator(device=device)
+        gen.manual_seed(1)
+        chunk = 1 << 22
+        for i in range(0, n, chunk):
+            m = min(chunk, n - i)
+            table[i : i + m, :d].copy_(torch.randn((m, d), generator=gen, device=device, dtype=torch.float32).cpu())
+    t0 = time.time()
+    st = HostFeatureStore.shared(n, d, fill, rank=rank, world=world)
+    log(f"rank {rank}: shared pinned feature store {n} x {st.ld} f32 ({n * st.ld * 4 / 2**30:.1f} GiB, "
+        f"one copy for {world} rank(s)) ready in {time.time() - t0:.1f}s")
+    return st
+
+
+def config_dict(cfg, args, world, nbatches):
+    """The `config` object of both arms (same keys, same workload string)."""
+    return {"workload": cfg["desc"] + (f", static-degree HBM cache ratio {args.cache_ratio}"
+                                       if args.cache_ratio and cfg["store"] == "host" else ""),
+            "batch_size": cfg["bs"], "global_batch": cfg["bs"] * world,
+            "windows_per_step_per_rank": 1, "mini_batches_per_step": cfg["window"] * world,
+            "parallelism": f"dp{world}" + ("" if world == 1 else f" ({args.dist_backend})"),
+            "l2": "inputs (CSR 0.27 GB + features) larger than the 126 MB L2",
+            "epoch_batches": nbatches}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,25 +327,42 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
+    ap.add_argument("--bs", type=int, default=0, help="batch size override (config 5 sweep: 512..8192)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share a GPU (functional check of the N-rank path, not a measurement)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--profile", action="store_true", help="stop after warm-up + 2 steps (for ncu)")
     ap.add_argument("--cache-ratio", type=float, default=0.0,
                     help="static-degree HBM feature cache in front of a host-resident store (configs *_host, papers)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
 
     import torch
     from paper_2409_14939_b200 import dist as fdist
-    cfg = CONFIGS[args.config]
-    rank, world = fdist.init("nccl") if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (0, 1)
+    cfg = dict(CONFIGS[args.config])
+    if args.bs:
+        cfg["bs"] = int(args.bs)
+        cfg["desc"] = cfg["desc"].replace("batch 1024", f"batch {args.bs}")
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
-        return run_reference(args, cfg, rank, world, local)
-    torch.cuda.set_device(local)
-    device = f"cuda:{local}"
+    if args.impl == "reference":  # CPU arm: rank 0 alone, no process group
+        return run_reference(args, cfg, int(os.environ.get("RANK", 0)), world_env, local)
+    rank, world = fdist.init(args.dist_backend) if world_env > 1 else (0, 1)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
+    device = f"cuda:{torch.cuda.current_device()}"
     from paper_2409_14939_b200 import _lib, trainer
 
-    dg, feats, labels = build_workload(cfg, device)
+    if cfg["store"] == "host":
+        from paper_2409_14939_b200.graph import chung_lu_graph
+        dg = chung_lu_graph(cfg["nodes"], cfg["edges"], exponent=cfg["exponent"], seed=0, device=device)
+        feats = make_feature_store(cfg, dg, rank, world, device)
+        gen = torch.Generator(device=device)
+        gen.manual_seed(2)
+        labels = torch.randint(0, cfg["dims"][-1], (dg.num_nodes,), generator=gen, device=device)
+    else:
+        dg, feats, labels = build_workload(cfg, device)
     windows, nbatches = epoch_windows(dg.num_nodes, cfg)
     mine = fdist.shard(windows, rank, world)
     mcfg = trainer.ModelConfig(layer_dims=cfg["dims"], fanouts=cfg["fanouts"], arch=cfg["arch"],
@@ -304,8 +393,9 @@ def main():
     edges = 0
     draws = 0
     l0 = lib.fgl_launch_count()
+    fb0 = lib.fgl_dense_fallback_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         if args.profile:  # ncu --profile-from-start off: capture only the timed steps
             torch.cuda.profiler.start()
@@ -319,6 +409,9 @@ def main():
         if args.profile:
             torch.cuda.profiler.stop()
     launches = lib.fgl_launch_count() - l0
+    fallbacks = lib.fgl_dense_fallback_count() - fb0
+    if fallbacks:
+        raise RuntimeError(f"{fallbacks} dense layers ran on the SIMT fallback inside the timed region")
     if world > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -333,32 +426,30 @@ def main():
         if rank == 0:
             print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step}), flush=True)
         return
-    # ---------------- stage breakdown + roofline (instrumented extra steps) --
-    stages = stage_profile(pipe, mine, it, cfg, torch)
-    it += 2
+    # ---------------- per-stage rooflines (live, instrumented extra steps) ----
+    stages = stage_profile(pipe, take(4), cfg, torch)
     # ---------------- end to end through the public API with host buffers ----
-    e2e = e2e_measure(pipe, mine, it, K, torch, world, device)
+    e2e = e2e_measure(pipe, take(K), torch, world, device)
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (fp64 loss; int32/int64 sampling)",
         "data": "synthetic (seeded Chung-Lu power-law graph, random f32 features, random labels)",
-        "config": {"workload": cfg["desc"] + (f", static-degree HBM cache ratio {args.cache_ratio}"
-                                              if args.cache_ratio and cfg["store"] == "host" else ""),
-                   "global_batch": cfg["bs"] * world,
-                   "windows_per_step_per_rank": 1, "mini_batches_per_step": batches_per_step,
-                   "parallelism": f"dp{world}", "l2": "inputs (CSR 0.27 GB + features) larger than the 126 MB L2",
-                   "epoch_batches": nbatches},
+        "config": config_dict(cfg, args, world, nbatches),
         "epoch_time_s": epoch_s,
         "sampled_edges_per_step": edges_all / K,
         "philox_draws_per_step": fdist.sum_over_ranks(float(draws), world, device) / K,
         "gpu_launches": int(launches),
+        "dense_fallbacks": int(fallbacks),
         "clocks": clk.summary(),
         "stages_ms_per_step": stages["ms"],
         "roofline": stages["roofline"],
+        "stage_rooflines": stages["stages"],
         "e2e": e2e,
     }
+    if world > 1:
+        out["allreduce"] = allreduce_probe(pipe, torch, world, device)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         v, cores, sample, wall = cpu_oracle_throughput(dg, feats, labels, cfg, mine, args.cpu_budget)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
@@ -381,112 +472,192 @@ def _measured_traffic(kernel):
         return None
 
 
-def stage_profile(pipe, mine, it, cfg, torch):
-    """Per-stage device time of 2 windows (events between the stages; not part
-    of the headline timing) and the roofline of the dominant stage."""
-    import json as _json
-    peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    acc = {"sample": 0.0, "schedule": 0.0, "prepare": 0.0, "compute": 0.0}
-    draws = 0
-    samp_bytes = 0.0
-    from paper_2409_14939_b200 import _lib as _l
-    sel = {"s": 0.0, "bytes": 0.0, "draws": 0.0}
-    pipe.loaded.zero_()
-    pipe.cache_hits.zero_()
-    for k in range(2):
-        seeds, rs = mine[(it + k) % len(mine)]
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        _l.call("fgl_profile_select", 1)
-        ev[0].record()
-        win = pipe.sampler.sample(seeds, rs)
-        ev[1].record()
-        _l.call("fgl_profile_select", 0)
-        pms = np.zeros(16, dtype=np.float64)
-        nl = np.zeros(1, dtype=np.int64)
-        _l.call("fgl_profile_select_read", pms.ctypes.data, 16, nl.ctypes.data)
-        win.host_counts()
-        order = pipe.schedule(win, len(seeds))
-        ev[2].record()
-        layers = pipe.prepare(win)
-        ev[3].record()
-        for j, b in enumerate(order):
-            pipe.batch_step(win, b, order[j - 1] if j else None, j, layers, j % 2)
-        ev[4].record()
-        torch.cuda.synchronize()
-        for i, name in enumerate(acc):
-            acc[name] += ev[i].elapsed_time(ev[i + 1]) / 2
-        nb = win.num_batches
-        draws += sum(win.draws(b) for b in range(nb)) / 2
-        # algorithmic sampler bytes (SURVEY 8(d)): offsets of each frontier node,
-        # chosen col (+weight) reads, (t, s, w) writes
-        for h in range(win.num_hops):
-            F = win.front_total(h)
-            e0, e1 = win.hop_edges(h)
-            S = e1 - e0
-            samp_bytes += (2 * 8 * F + S * 4 + S * (2 * 4 + 4)) / 2
-        # dominant launch: the last hop's select kernel (largest frontier).
-        # Algorithmic bytes: per frontier node its id, batch, two CSR offsets,
-        # the two scans (4+4+16+16); per sampled edge the chosen col entry and
-        # the (tgt, src, wgt, tgt_front) record (4 + 16); draws: one per candidate
-        hl = win.num_hops - 1
-        F = win.front_total(hl)
-        e0_, e1_ = win.hop_edges(hl)
-        S = e1_ - e0_
-        sel["s"] += float(pms[hl]) / 1e3 / 2
-        sel["bytes"] += (40.0 * F + 20.0 * S) / 2
-        sel["draws"] += win.hop_draws(hl) / 2
-    t_s = acc["sample"] / 1e3
-    # Philox ALU probe: draws/s of the bare Philox4x64-10 kernel on this GPU
+_TRAFFIC_KEYS = {"select": "select_bal_kernel", "aggregate_l0": "spmm_kernel_l0", "dense_fwd": "tc_gemm3_kernel_l0",
+                 "wgrad": "tc_wgrad3_kernel_l0", "gather": "gather_rows_kernel_host"}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(p.read_text()) if p.exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6540.8))
+    bf16 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1328.6)))
+    src = "MEASURED_PEAKS.json (driver-measured copy bandwidth / cuBLAS bf16, sustained)" if peaks else \
+        "fallback figures of B200_PROFILING.md"
+    return hbm, bf16, src
+
+
+def philox_peak(torch, device):
+    """Measured Philox4x64-10 throughput of this GPU (draws/s): the bare
+    counter-based generator with nothing else (fgl_philox_bench)."""
     from paper_2409_14939_b200 import _lib
-    buf = torch.empty(148 * 8 * 256, dtype=torch.int64, device=pipe.device)
+    buf = torch.empty(148 * 8 * 256, dtype=torch.int64, device=device)
     nblk = 1 << 27
-    _lib.call("fgl_philox_bench", 1, 2, nblk, buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("fgl_philox_bench", 1, 2, nblk, buf.data_ptr(), st)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    _lib.call("fgl_philox_bench", 3, 4, nblk, buf.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    _lib.call("fgl_philox_bench", 3, 4, nblk, buf.data_ptr(), st)
     e1.record()
     torch.cuda.synchronize()
-    peak_draws = 4 * nblk / (e0.elapsed_time(e1) / 1e3)
-    roof = {
-        "kernel": "select_bal_kernel + select_hub_kernel (hop-2 selection of fgl_sample_window, the largest select launch)",
-        "bound": "hbm", "achieved": sel["bytes"] / sel["s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
-        "frac": sel["bytes"] / sel["s"] / 1e9 / hbm_peak, "traffic": _measured_traffic("select_bal_kernel"),
-        "peak_source": peak_src, "launch_ms": sel["s"] * 1e3, "bytes_per_launch": sel["bytes"],
-        "alu": {"bound": "philox4x64-10 draws (bit-exact sampling needs one per candidate edge)",
-                "achieved_draws_per_s": sel["draws"] / sel["s"], "peak_draws_per_s": peak_draws,
-                "frac": sel["draws"] / sel["s"] / peak_draws,
-                "draws_per_launch": sel["draws"]},
-        "sampler_stage": {"ms_per_window": acc["sample"], "draws_per_s": draws / t_s,
-                          "alu_frac": draws / t_s / peak_draws},
-    }
-    if pipe.feature_store == "host":
-        # IO stage (SURVEY 8(d)): feature rows that cross the host link per
-        # window vs the measured pinned host->device copy peak of this box
-        loaded = int(pipe.loaded.item()) / 2
-        hits = int(pipe.cache_hits.item()) / 2
-        link_bytes = loaded * 4 * pipe.d0
-        hb = torch.empty(1 << 28, dtype=torch.float32).pin_memory()
-        db = torch.empty(1 << 28, dtype=torch.float32, device=pipe.device)
-        db.copy_(hb, non_blocking=True)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        db.copy_(hb, non_blocking=True)
-        e1.record()
+    return 4 * nblk / (e0.elapsed_time(e1) / 1e3)
+
+
+def host_link_peak(torch, device):
+    hb = torch.empty(1 << 28, dtype=torch.float32).pin_memory()
+    db = torch.empty(1 << 28, dtype=torch.float32, device=device)
+    db.copy_(hb, non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    db.copy_(hb, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return hb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+def _roof(bound, achieved, peak, unit, traffic_key=None, **extra):
+    out = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak if peak else None,
+           "traffic": _measured_traffic(traffic_key) if traffic_key else None}
+    out.update(extra)
+    return out
+
+
+def stage_profile(pipe, wins, cfg, torch):
+    """Per-stage rooflines from LIVE kernel times: the timed pipeline itself
+    (run_windows: CUDA graphs; sampling, prepare / layer-0 aggregation and
+    the model chain on their concurrent streams) runs extra windows with
+    fgl_profile on, so the library brackets its dominant launches with CUDA
+    events on their own streams (event-record nodes inside the graphs, timed
+    on every replay).  Each stage's achieved
+    rate = its ALGORITHMIC bytes or draws over those launches
+    / their summed device time; `bound` is the roof with the larger fraction.
+    The headline `roofline` is the stage whose kernels take the most device
+    time."""
+    import ctypes
+
+    from paper_2409_14939_b200 import _lib
+    lib = _lib.lib()
+    hbm_peak, bf16_peak, peak_src = _peaks()
+    tf32_peak = bf16_peak / 2  # dense tf32 rate of the tensor cores = half of bf16 (3xTF32 issues 3 MMAs)
+    device = pipe.device
+    d0 = cfg["dims"][0]
+    H = len(cfg["fanouts"])
+    weighted = pipe.dg.edge_weights is not None
+    pipe.loaded.zero_()
+    pipe.cache_hits.zero_()
+    hop = {h: {"F": 0, "S": 0} for h in range(H)}
+    l0 = {"n": 0, "E": 0, "launches": 0}
+    torch.cuda.synchronize()
+    lib.fgl_profile(1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    draws_total = 0
+    try:
+        for _ in pipe.run_windows(wins):
+            win = pipe.last_window
+            for h in range(H):  # host counts only: no device sync inside the loop
+                e0, e1 = win.hop_edges(h)
+                hop[h]["F"] += win.front_total(h)
+                hop[h]["S"] += e1 - e0
+            draws_total += sum(win.draws(b) for b in range(win.num_batches))
+            e0, e1 = win.hop_edges(H - 1)
+            l0["E"] += e1 - e0
+            l0["launches"] += win.num_batches
+        ev1.record()
         torch.cuda.synchronize()
-        link_peak = hb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
-        del hb, db
-        achieved = link_bytes / (acc["compute"] / 1e3) / 1e9
-        roof["io"] = {"bound": "host link (pinned zero-copy row gathers)", "rows_per_window": loaded,
-                      "cache_rows_per_window": hits, "bytes_per_window": link_bytes,
-                      "achieved": achieved, "peak": link_peak, "unit": "GB/s", "frac": achieved / link_peak,
-                      "peak_source": "measured: pinned host->device cudaMemcpy of 1 GiB on this box",
-                      "note": "achieved = host-link bytes / whole compute stage time (lower bound for the gather)"}
-    return {"ms": acc, "roofline": roof}
+    finally:
+        lib.fgl_profile(0)
+    loaded = int(pipe.loaded.sum().item())
+    cap = 1 << 16
+    ids = np.zeros(cap, np.int32)
+    args3 = np.zeros(3 * cap, np.int64)
+    ms = np.zeros(cap, np.float64)
+    cnt = ctypes.c_int64()
+    _lib.call("fgl_profile_read", cap, ids.ctypes.data, args3.ctypes.data, ms.ctypes.data, ctypes.byref(cnt))
+    k = min(int(cnt.value), cap)
+    ids, args3, ms = ids[:k], args3[: 3 * k].reshape(k, 3), ms[:k]
+    nwin = len(wins)
+    window_ms = ev0.elapsed_time(ev1) / nwin
+
+    def tot(mask):
+        return float(ms[mask].sum()) / 1e3, int(mask.sum())
+
+    stages = {}
+    # --- sample: select_bal + select_hub per hop; INT-ALU (Philox) and HBM roofs
+    t, n = tot(ids == 1)
+    if n:
+        draws = draws_total
+        bytes_ = sum(2 * 8 * v["F"] + v["S"] * (4 + 4 * weighted) + v["S"] * (2 * 4 + 4) for v in hop.values())
+        peak_draws = philox_peak(torch, device)
+        alu = draws / t / peak_draws
+        hbmf = bytes_ / t / 1e9 / hbm_peak
+        stages["sample"] = _roof("alu" if alu >= hbmf else "hbm", draws / t, peak_draws, "draws/s", "select",
+                                 kernel="select_bal_kernel + select_hub_kernel (every hop)", launches=n,
+                                 ms_per_window=t * 1e3 / nwin, draws_per_launch=draws / n,
+                                 hbm={"achieved": bytes_ / t / 1e9, "peak": hbm_peak, "unit": "GB/s", "frac": hbmf,
+                                      "bytes_per_launch": bytes_ / n,
+                                      "model": "SURVEY 8(d): 16 B offsets per frontier node, chosen col (+w) read, "
+                                               "(t, s, w) written per sampled edge"},
+                                 peak_source="measured: fgl_philox_bench, bare Philox4x64-10 on this GPU")
+    # --- layer-0 aggregation (the largest SpMM): HBM, reference byte model
+    agg_id = 2 if (ids == 2).any() else 3
+    mask = (ids == agg_id) & (args3[:, 1] == d0)
+    t, n = tot(mask)
+    if n:
+        rows = int(args3[mask, 0].sum())
+        E = l0["E"] if agg_id == 2 or n == l0["launches"] else None
+        if E is not None:
+            bytes_ = 8 * (rows + n) + E * (4 + 4) + 4 * E * d0 + 4 * rows * d0
+            stages["aggregate_l0"] = _roof(
+                "hbm", bytes_ / t / 1e9, hbm_peak, "GB/s", "aggregate_l0",
+                kernel="spmm_pipe_kernel (fgl_spmm_gather)" if agg_id == 2 else "spmm_kernel (fgl_spmm)",
+                launches=n, ms_per_window=t * 1e3 / nwin, bytes_per_launch=bytes_ / n,
+                model="memsim.py:96 / Eq. 3: 8(n+1) + E(4+4) + 4 E d + 4 n d", peak_source=peak_src,
+                flops_per_launch=2 * E * d0 / n)
+    # --- dense forward / dgrad / weight gradient: HBM (intensity below the ridge); tensor pipe reported
+    for name, pid, byte_fn, flop_fn, kname in [
+            ("dense_fwd", 4, lambda M, N, K: 4 * (M * K + K * N + 2 * M * N), lambda M, N, K: 2 * M * N * K,
+             "tc_gemm3_kernel<0> (all layers)"),
+            ("dgrad", 5, lambda M, N, K: 4 * (2 * M * K + K * N + M * N), lambda M, N, K: 2 * M * N * K,
+             "tc_gemm3_kernel<1> (all layers)"),
+            ("wgrad", 6, lambda M, K, N: 4 * (M * K + 2 * M * N), lambda M, K, N: 2 * M * K * N,
+             "tc_wgrad3_kernel + reduce_partials (all layers)")]:
+        mask = ids == pid
+        t, n = tot(mask)
+        if not n:
+            continue
+        a = args3[mask]
+        bytes_ = float(sum(byte_fn(*map(int, r)) for r in a))
+        flops = float(sum(flop_fn(*map(int, r)) for r in a))
+        stages[name] = _roof("hbm", bytes_ / t / 1e9, hbm_peak, "GB/s", name if name != "dgrad" else None,
+                             kernel=kname, launches=n, ms_per_window=t * 1e3 / nwin, bytes_per_launch=bytes_ / n,
+                             tensor={"achieved_tflops": flops / t / 1e12, "peak_tflops": tf32_peak,
+                                     "frac": flops / t / 1e12 / tf32_peak,
+                                     "note": "fp32-accurate 3xTF32: 3 tf32 MMAs per product; peak = dense tf32 "
+                                             "(half of the measured bf16)"},
+                             peak_source=peak_src)
+    # --- IO: x0 rows over the host link (host-resident feature store)
+    mask = ids == 7
+    t, n = tot(mask)
+    if n and pipe.feature_store == "host":
+        link = host_link_peak(torch, device)
+        link_bytes = loaded * 4 * d0
+        stages["io"] = _roof("host_link", link_bytes / t / 1e9, link, "GB/s", "gather",
+                             kernel="gather_rows_kernel (Match delta + cache + zero-copy host rows)", launches=n,
+                             ms_per_window=t * 1e3 / nwin, rows_per_window=loaded / nwin,
+                             bytes_per_launch=link_bytes / n,
+                             peak_source="measured: pinned host->device cudaMemcpy of 1 GiB on this box")
+    per_stage_ms = {k: v["ms_per_window"] for k, v in stages.items()}
+    per_stage_ms["window"] = window_ms
+    dom = max(stages, key=lambda k: stages[k]["ms_per_window"]) if stages else None
+    head = dict(stages[dom]) if dom else {}
+    if head:
+        head["stage"] = dom
+        head["why_dominant"] = (f"largest summed device time of the profiled launches per window "
+                                f"({head['ms_per_window']:.3f} ms); live times (graph replays, concurrent streams)")
+    return {"ms": per_stage_ms, "roofline": head, "stages": stages}
 
 
-def e2e_measure(pipe, mine, it, K, torch, world, device):
+def e2e_measure(pipe, wins, torch, world, device):
     """Same metric through the public API with host buffers: each step stages
     the window's seeds from pinned host memory (H2D inside the timed region)
     and copies its per-batch losses back to pinned host memory (D2H inside the
@@ -495,8 +666,8 @@ def e2e_measure(pipe, mine, it, K, torch, world, device):
     edges = 0
     h2d = d2h = 0
     staged = []
-    for k in range(K):  # the caller's inputs live in pinned host memory before the clock starts
-        seeds, rs = mine[(it + k) % len(mine)]
+    K = len(wins)
+    for seeds, rs in wins:  # the caller's inputs live in pinned host memory before the clock starts
         pinned = [torch.from_numpy(s.astype(np.int64)).pin_memory() for s in seeds]
         staged.append(([p.numpy() for p in pinned], rs))
         h2d += sum(len(s) for s in seeds) * 4 + (len(seeds) + 1) * 8 + 16 * len(seeds)
@@ -505,7 +676,7 @@ def e2e_measure(pipe, mine, it, K, torch, world, device):
     t0 = time.perf_counter()
     for k, (order, losses) in enumerate(pipe.run_windows(staged)):
         # per-batch losses of every step copied back to pinned host memory
-        # (asynchronous D2H on the compute stream; no per-step host stall)
+        # (asynchronous D2H on the caller's stream; no per-step host stall)
         host_losses[k].copy_(losses, non_blocking=True)
         edges += pipe.last_window.total_edges()
         d2h += host_losses[k].numel() * 8
@@ -516,6 +687,32 @@ def e2e_measure(pipe, mine, it, K, torch, world, device):
     edges_all = fdist.sum_over_ranks(float(edges), world, device)
     return {"value": edges_all / wall, "unit": UNIT, "h2d_bytes_per_step": h2d // K,
             "d2h_bytes_per_step": d2h // K}
+
+
+def allreduce_probe(pipe, torch, world, device):
+    """NVLink all-reduce of this job's gradient bucket (latency) and of a
+    64 MiB buffer (bus bandwidth), CUDA events, max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2409_14939_b200 import dist as fdist
+    out = {"backend": str(dist.get_backend())}
+    for name, numel in (("bucket", pipe.model.grad.numel()), ("64MiB", 16 << 20)):
+        buf = torch.ones(numel, dtype=torch.float32, device=device)
+        for _ in range(5):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50 if name == "bucket" else 10
+        e0.record()
+        for _ in range(reps):
+            dist.all_reduce(buf)
+        e1.record()
+        torch.cuda.synchronize()
+        t = fdist.max_over_ranks(e0.elapsed_time(e1) / reps / 1e3, world, device)
+        nbytes = numel * 4
+        out[name] = {"bytes": nbytes, "us": t * 1e6, "busbw_gbs": 2 * (world - 1) / world * nbytes / t / 1e9}
+    return out
 
 
 def cpu_reference_steps(dg, feats, labels, cfg, windows, steps, warmup, budget_s):
@@ -529,7 +726,7 @@ def cpu_reference_steps(dg, feats, labels, cfg, windows, steps, warmup, budget_s
     from paper_2409_14939_b200.graph import to_host
     hg = to_host(dg)
     g = oracle.CSRGraph(hg.num_nodes, hg.row_offsets, hg.col_indices, None, None, None)
-    _CPU.update(g=g, feats=feats.cpu().numpy(), labels=labels.cpu().numpy(), dims=cfg["dims"],
+    _CPU.update(g=g, feats=_host_features(feats, cfg), labels=labels.cpu().numpy(), dims=cfg["dims"],
                 fanouts=cfg["fanouts"], arch=cfg["arch"], params=oracle.init_params(cfg["dims"], 0))
     workers = max(1, min(os.cpu_count() or 1, 16))
     jobs = [(s, r) for w_seeds, w_rs in windows for s, r in zip(w_seeds, w_rs)]
@@ -576,7 +773,7 @@ def run_reference(args, cfg, rank, world, local):
         "steps_requested": args.steps, "warmup": max(1, min(args.warmup, 2)),
         "ms_per_step": wall / rounds * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "impl": "reference", "dtype": "f32 (fp64 loss)", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "global_batch": cfg["bs"], "parallelism": f"{cores} cpu processes"},
+        "config": dict(config_dict(cfg, args, world, nbatches), host_processes=cores),
         "epoch_time_s": None,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

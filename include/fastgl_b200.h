@@ -12,8 +12,13 @@
  *    per thread in fgl_last_error().  The Python layer maps the codes to the
  *    reference's exception types (errors.py:1-35).
  *  - Node IDs on device are int32 (N < 2^31); CSR offsets are int64.
- *  - No global mutable state; calls on distinct streams/buffers are
- *    independent and thread-safe.
+ *  - Caller-owned state only (graph handles, executable graphs, work
+ *    buffers), with these process-wide exceptions: a launch counter and
+ *    CUDA-graph counters (atomics), the per-thread last error, per-thread
+ *    caches of TMA tensor maps keyed by buffer address, one-time kernel
+ *    attribute settings (max dynamic shared memory), the profiling switch
+ *    and its event record (fgl_profile), and A/B switches read once from
+ *    the environment.  Calls on distinct streams/buffers are independent.
  */
 #ifndef FASTGL_B200_H
 #define FASTGL_B200_H
@@ -39,6 +44,9 @@ const char* fgl_last_error(void);
 int fgl_version(void);
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t fgl_launch_count(void);
+/* Dense layer calls (fgl_dense_fwd / _bwd / _dgrad) whose shape fell outside
+ * the tcgen05 kernels' envelope and ran on the SIMT fallback kernels. */
+int64_t fgl_dense_fallback_count(void);
 /* Device properties the build was compiled for; returns FGL_E_CUDA without a GPU. */
 int fgl_device_check(int device);
 
@@ -143,13 +151,18 @@ int fgl_sample_walk(const fgl_graph* g, const int32_t* seeds, int64_t num_seeds,
                     int32_t* unique_nodes, int64_t unique_cap, int64_t* counts, void* ws, int64_t ws_bytes,
                     void* stream);
 
-/* Measurement hook (bench.py roofline): while enabled, fgl_sample_window
- * brackets every select-kernel launch with CUDA events on its stream;
- * fgl_profile_select_read synchronises on them, writes up to `cap` per-launch
- * device milliseconds (launch order: hop 0..H-1 of each window) and the
- * launch count, then clears the record. */
-int fgl_profile_select(int32_t enable);
-int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches);
+/* Measurement hook (bench.py per-stage rooflines): while enabled, the
+ * dominant launch of every stage -- select (id 1, a = {hop}), layer-0 block
+ * aggregation (2, {rows, d}), fgl_spmm (3, {rows, d}), dense forward (4,
+ * {M, N, K}), dgrad (5, {M, N, K}), weight gradient (6, {M, K, N}), x0
+ * gather (7, {rows, d}) -- is bracketed by CUDA events on its own stream;
+ * inside a stream capture they become external event-record nodes, timed on
+ * every replay of the graph.
+ * fgl_profile_read synchronises on them and writes up to `cap` records
+ * (ids, args3[3*k..], device ms) in issue order plus the record count, then
+ * clears the record. */
+int fgl_profile(int32_t enable);
+int fgl_profile_read(int64_t cap, int32_t* ids, int64_t* args3, double* ms, int64_t* count);
 
 /* ------------------------------------------------------------- prepare ---- */
 /* indptr[r] = base + (first e with rows[e] >= r), r in [0, num_rows]; `rows`
@@ -206,36 +219,6 @@ int fgl_depth_relayout(const int64_t* counts, int32_t H, int32_t nb, const int32
 int fgl_add_rows(float* Y, int64_t ldy, const float* X, int64_t ldx, int64_t nrows, int32_t d, void* stream);
 
 /* ------------------------------------------------------- fused layers ---- */
-/* Upper model layers 1..L-1 of a COMPACT GCN batch (rows of layer i = hop
- * H-1-i frontier), trained by ONE persistent kernel (trainer.py:182-228 for
- * those layers): forward aggregation (bit-identical to fgl_spmm) + dense,
- * fp64 softmax cross entropy (same as fgl_softmax_xent), dense backward,
- * transposed aggregation, deterministic dW/db reductions.  Layer k of the
- * struct is model layer k+1.  indptr / t_indptr point at the batch's first
- * row (absolute edge offsets); col / t_col values minus col_base / t_base
- * index the input / output rows.  X1 = layer-0 output (input of layer 1);
- * dX1 receives its gradient, or is NULL: then the layer-1 -> layer-0
- * transposed aggregation is left to the caller (fgl_spmm on dH of layer 1). */
-typedef struct fgl_upper_layer {
-  const int64_t* indptr; const int32_t* col; int64_t col_base; const float* w; int64_t rows;
-  const int64_t* t_indptr; const int32_t* t_col; int64_t t_base; const float* t_w; int64_t prev_rows;
-  int32_t din, dout;
-  const float* W; const float* b; float* dW; float* db;
-  float* H; int64_t ldh; float* Y; int64_t ldy; float* dH; float* dY;
-} fgl_upper_layer;
-
-typedef struct fgl_upper_args {
-  int32_t num_upper;
-  fgl_upper_layer layer[3];
-  const float* X1; int64_t ldx1; float* dX1;
-  const int32_t* seed_rows; int64_t seed_row_base; const int32_t* seed_ids; const int64_t* labels;
-  int64_t num_seeds; int32_t num_classes;
-  double* loss_sum;
-} fgl_upper_args;
-
-int64_t fgl_upper_ws_bytes(const fgl_upper_args* a);
-int fgl_upper_layers(const fgl_upper_args* a, void* ws, int64_t ws_bytes, void* stream);
-
 /* fgl_prepare_layer for targets grouped but not ascending (depth-major rows
  * of fgl_depth_relayout): stable grouping by target (compute.py:219-230)
  * first; col_out receives the forward CSR's columns. */
@@ -289,12 +272,17 @@ int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ld
                     int32_t din, int32_t dout, float* dH, int64_t lddh, void* stream);
 
 /* CUDA-graph replay of a per-batch chain: begin a
- * thread-local capture on `stream`; end it and launch it through the slot's
- * executable graph (cudaGraphExecUpdate when the topology matches, else a
- * fresh instantiation); or abort it (the caller then runs the work eagerly).
- * fgl_capture_stats: {graph launches, updates, instantiations}. */
+ * thread-local capture on `stream`; end it and launch it through a
+ * caller-owned executable-graph handle (cudaGraphExecUpdate when the topology
+ * matches, else a fresh instantiation); or abort it (the caller then runs the
+ * work eagerly).  A handle belongs to the device current at fgl_exec_create
+ * and is rejected on any other.  fgl_capture_stats: process-wide {graph
+ * launches, updates, instantiations}. */
+typedef struct fgl_exec fgl_exec;
+int fgl_exec_create(fgl_exec** out);
+int fgl_exec_destroy(fgl_exec* h);
 int fgl_capture_begin(void* stream);
-int fgl_capture_end_launch(int32_t slot, void* stream);
+int fgl_capture_end_launch(fgl_exec* h, void* stream);
 int fgl_capture_abort(void* stream);
 int fgl_capture_stats(int64_t* out3);
 
@@ -390,6 +378,12 @@ int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int
                            const float* prev_x, int64_t ldp, const int32_t* prev_row_map,
                            const int32_t* cache_slot, const float* cache_x, int64_t ldc, float* out, int64_t ldo,
                            uint64_t* loaded, uint64_t* hits, void* stream);
+
+/* Page-lock and map a caller-allocated host feature table (e.g. one shared
+ * by every rank of a node); *dev_ptr = its device address for
+ * the loader.  Synchronous.  fgl_host_unregister undoes it. */
+int fgl_host_register(void* host, int64_t bytes, void** dev_ptr);
+int fgl_host_unregister(void* host);
 
 #ifdef __cplusplus
 }

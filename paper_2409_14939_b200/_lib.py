@@ -49,25 +49,6 @@ class FglSampleOut(C.Structure):
     ]
 
 
-class FglUpperLayer(C.Structure):
-    _fields_ = [
-        ("indptr", vp), ("col", vp), ("col_base", C.c_int64), ("w", vp), ("rows", C.c_int64),
-        ("t_indptr", vp), ("t_col", vp), ("t_base", C.c_int64), ("t_w", vp), ("prev_rows", C.c_int64),
-        ("din", C.c_int32), ("dout", C.c_int32),
-        ("W", vp), ("b", vp), ("dW", vp), ("db", vp),
-        ("H", vp), ("ldh", C.c_int64), ("Y", vp), ("ldy", C.c_int64), ("dH", vp), ("dY", vp),
-    ]
-
-
-class FglUpperArgs(C.Structure):
-    _fields_ = [
-        ("num_upper", C.c_int32), ("layer", FglUpperLayer * 3),
-        ("X1", vp), ("ldx1", C.c_int64), ("dX1", vp),
-        ("seed_rows", vp), ("seed_row_base", C.c_int64), ("seed_ids", vp), ("labels", vp),
-        ("num_seeds", C.c_int64), ("num_classes", C.c_int32), ("loss_sum", vp),
-    ]
-
-
 # name -> (restype, argtypes); every entry is declared in include/fastgl_b200.h
 SIGNATURES = {
     "fgl_last_error": (C.c_char_p, []),
@@ -80,17 +61,15 @@ SIGNATURES = {
         C.POINTER(FglSampleOut), vp, C.c_int64, vp]),
     "fgl_philox_words": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_philox_bench": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, vp, vp]),
-    "fgl_profile_select": (C.c_int, [C.c_int32]),
-    "fgl_upper_ws_bytes": (C.c_int64, [C.POINTER(FglUpperArgs)]),
+    "fgl_profile": (C.c_int, [C.c_int32]),
     "fgl_depth_relayout_ws_bytes": (C.c_int64, [C.c_int64]),
     "fgl_depth_relayout": (C.c_int, [vp, C.c_int32, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
                                      vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp]),
     "fgl_add_rows": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int32, vp]),
-    "fgl_upper_layers": (C.c_int, [C.POINTER(FglUpperArgs), vp, C.c_int64, vp]),
     "fgl_walk_ws_bytes": (C.c_int64, [C.c_int64, C.c_int64]),
     "fgl_sample_walk": (C.c_int, [C.POINTER(FglGraph), vp, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, vp, vp, vp, C.c_int64,
                                   vp, vp, C.c_int64, vp, vp, C.c_int64, vp]),
-    "fgl_profile_select_read": (C.c_int, [vp, C.c_int64, vp]),
+    "fgl_profile_read": (C.c_int, [C.c_int64, vp, vp, vp, vp]),
     "fgl_csr_offsets_sorted": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, vp, vp]),
     "fgl_stable_group_ws_bytes": (C.c_int64, [C.c_int64]),
     "fgl_stable_group": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]),
@@ -113,8 +92,11 @@ SIGNATURES = {
                                 vp]),
     "fgl_dense_dgrad": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int32, C.c_int32, vp, C.c_int64,
                                   vp]),
+    "fgl_dense_fallback_count": (C.c_int64, []),
     "fgl_capture_begin": (C.c_int, [vp]),
-    "fgl_capture_end_launch": (C.c_int, [C.c_int32, vp]),
+    "fgl_capture_end_launch": (C.c_int, [vp, vp]),
+    "fgl_exec_create": (C.c_int, [vp]),
+    "fgl_exec_destroy": (C.c_int, [vp]),
     "fgl_capture_abort": (C.c_int, [vp]),
     "fgl_capture_stats": (C.c_int, [vp]),
     "fgl_softmax_xent_ws_bytes": (C.c_int64, []),
@@ -137,6 +119,8 @@ SIGNATURES = {
     "fgl_bitmap_test": (C.c_int, [vp, C.c_int64, vp, vp, vp]),
     "fgl_gather_rows": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
                                   vp, C.c_int64, vp, C.c_int64, vp, vp]),
+    "fgl_host_register": (C.c_int, [vp, C.c_int64, vp]),
+    "fgl_host_unregister": (C.c_int, [vp]),
     "fgl_gather_rows_cached": (C.c_int, [vp, C.c_int64, C.c_int32, vp, C.c_int64, vp, vp, C.c_int64,
                                          vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp]),
 }

@@ -4,7 +4,9 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -13,7 +15,62 @@ namespace fgl {
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 
+static std::atomic<long long> g_dense_fallbacks{0};
+
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec {
+  int id;
+  int64_t a[3];
+  cudaEvent_t e0, e1;
+};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_rec;
+}  // namespace
+
+// Inside a stream capture the events become external event-record nodes of
+// the graph (cudaEventRecordExternal): they record -- with timestamps -- each
+// time the executable graph replays, so the kernels are timed live in the
+// pipeline that is actually measured.
+static cudaError_t prof_record(cudaEvent_t e, cudaStream_t st, bool captured) {
+  return captured ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+}
+
+ProfMark prof_begin(cudaStream_t st) {
+  ProfMark m;
+  if (!g_prof.load(std::memory_order_relaxed)) return m;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs == cudaStreamCaptureStatusInvalidated) return m;
+  if (cudaEventCreate(&m.e0) != cudaSuccess) return ProfMark{};
+  m.captured = cs == cudaStreamCaptureStatusActive;
+  if (prof_record(m.e0, st, m.captured) != cudaSuccess) {
+    cudaGetLastError();
+    cudaEventDestroy(m.e0);
+    return ProfMark{};
+  }
+  m.st = st;
+  return m;
+}
+
+void prof_end(const ProfMark& m, int id, int64_t a0, int64_t a1, int64_t a2) {
+  if (!m.e0) return;
+  cudaEvent_t e1 = nullptr;
+  if (cudaEventCreate(&e1) != cudaSuccess) {
+    cudaEventDestroy(m.e0);
+    return;
+  }
+  if (prof_record(e1, m.st, m.captured) != cudaSuccess) {
+    cudaGetLastError();
+    cudaEventDestroy(e1);
+    cudaEventDestroy(m.e0);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_rec.push_back(ProfRec{id, {a0, a1, a2}, m.e0, e1});
+}
+void count_dense_fallback() { g_dense_fallbacks.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[512];
@@ -68,6 +125,40 @@ const char* fgl_last_error(void) { return fgl::g_last_error.c_str(); }
 int fgl_version(void) { return 100; }
 
 int64_t fgl_launch_count(void) { return fgl::g_launches.load(std::memory_order_relaxed); }
+int64_t fgl_dense_fallback_count(void) { return fgl::g_dense_fallbacks.load(std::memory_order_relaxed); }
+
+int fgl_profile(int32_t enable) {
+  fgl::g_prof.store(enable != 0);
+  return FGL_OK;
+}
+
+int fgl_profile_read(int64_t cap, int32_t* ids, int64_t* args3, double* ms, int64_t* count) {
+  std::lock_guard<std::mutex> lk(fgl::g_prof_mu);
+  int64_t k = 0;
+  for (auto& r : fgl::g_prof_rec) {
+    float t = 0.f;
+    // a record whose capture was aborted (the work then ran eagerly) never
+    // executed: skip it
+    if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&t, r.e0, r.e1) != cudaSuccess) {
+      cudaGetLastError();
+      cudaEventDestroy(r.e0);
+      cudaEventDestroy(r.e1);
+      continue;
+    }
+    if (k < cap) {
+      if (ids) ids[k] = r.id;
+      if (args3)
+        for (int i = 0; i < 3; ++i) args3[3 * k + i] = r.a[i];
+      if (ms) ms[k] = t;
+    }
+    ++k;
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  if (count) *count = k;
+  fgl::g_prof_rec.clear();
+  return FGL_OK;
+}
 
 int fgl_device_check(int device) {
   cudaDeviceProp p;

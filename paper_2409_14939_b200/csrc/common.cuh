@@ -25,6 +25,31 @@ int cuda_status(cudaError_t e, const char* what);
 // it as gpu_launches); every launch site is written FGL_COUNT_LAUNCH(), k<<<...>>>(...).
 void count_launch();
 #define FGL_COUNT_LAUNCH() ::fgl::count_launch()
+// Dense layers that ran on the SIMT kernels because their shape is outside
+// the tensor-core envelope (fgl_dense_fallback_count; bench.py requires 0).
+void count_dense_fallback();
+
+// ------------------------------------------------------- live kernel timing --
+// Measurement hook (fgl_profile, bench.py's per-stage rooflines): while
+// enabled, the dominant launches of each stage are bracketed by CUDA events
+// on their own stream (event-record nodes when the stream is being captured
+// into a graph), tagged with a kernel id and three shape ints.
+enum ProfId : int {
+  kProfSelect = 1,      // select_bal + select_hub of one hop      (a0 = hop)
+  kProfSpmmGather = 2,  // layer-0 block aggregation, spmm_pipe    (a0 = rows, a1 = d)
+  kProfSpmm = 3,        // fgl_spmm                                 (a0 = rows, a1 = d)
+  kProfDenseFwd = 4,    // tc_gemm3 mode 0                          (a0 = M, a1 = N, a2 = K)
+  kProfDgrad = 5,       // tc_gemm3 mode 1                          (a0 = M, a1 = N, a2 = K)
+  kProfWgrad = 6,       // tc_wgrad3 (+ its partial reduction)      (a0 = M, a1 = K, a2 = N)
+  kProfGather = 7,      // x0 row gather (Match / cache / store)    (a0 = rows, a1 = d)
+};
+struct ProfMark {
+  cudaEvent_t e0 = nullptr;
+  cudaStream_t st = nullptr;
+  bool captured = false;
+};
+ProfMark prof_begin(cudaStream_t st);
+void prof_end(const ProfMark& m, int id, int64_t a0, int64_t a1 = 0, int64_t a2 = 0);
 
 #define FGL_CUDA(call)                                              \
   do {                                                              \
@@ -157,22 +182,18 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 // Fixed grid for device-count-driven ("persistent") kernels: 2 CTAs per SM.
 constexpr int kPersistentCTAs = 2 * kNumSMs;
 
-// tcgen05 3xTF32 GEMM (tc_gemm.cu).  mode 0: C = act(A W + bias), W [K, N];
+// tcgen05 3xTF32 GEMM (tc_gemm3.cu).  mode 0: C = act(A W + bias), W [K, N];
 // mode 1: C = (A * (mask > 0)) W^T, W [N, K].  Returns false if the shape is
-// outside the kernel's envelope; *err receives an FGL status otherwise.
+// outside the kernel's envelope (the caller then runs the SIMT kernel and
+// counts it with count_dense_fallback); *err receives an FGL status otherwise.
 bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
              const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
              cudaStream_t st, int* err);
-// Warp-specialised TMA variant of tc_gemm (tc_gemm3.cu); same contract.
 bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
               cudaStream_t st, int* err, int accum = 0);
+// tcgen05 3xTF32 weight gradient partials: part[c][K+1][N] (row K = db).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
                int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
-bool tc_wgrad4(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
-               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
-// tcgen05 3xTF32 weight gradient partials: part[c][K+1][N] (row K = db).
-bool tc_wgrad(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
-              int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
 
 }  // namespace fgl

@@ -676,6 +676,7 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
     return FGL_E_INVALID;
   }
   if (num_rows == 0) return FGL_OK;
+  const ProfMark pm = prof_begin(st);
   const int d4 = (d + 3) / 4;
   if (d4 <= 1) launch_spmm<1, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
@@ -700,6 +701,7 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
     set_error("fgl_spmm: feature dim %d above 1024 is not supported", d);
     return FGL_E_UNSUPPORTED;
   }
+  prof_end(pm, kProfSpmm, num_rows, d);
   FGL_LAUNCH_CHECK("spmm_kernel");
   return FGL_OK;
 }
@@ -728,6 +730,7 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   }
   if (tc_gemm(0, H, ldh, nullptr, 0, W, b, Z, ldz, n, dout, din, relu, (cudaStream_t)stream, &err))
     return err;
+  count_dense_fallback();
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
   FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
                                                       relu, nullptr, 0);
@@ -761,13 +764,13 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   const int64_t outs = (int64_t)(din + 1) * dout;
   if (n > 0) {
     int werr = 0;
-    const int tc_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 128)));
     // at least `tpc` 64-row tiles per CTA: small layers then use a few CTAs
     // (fewer per-CTA prologues, fewer partials to reduce, fewer SMs taken
     // from the concurrent chain); the large layer 0 still spans all SMs
     static const int tpc = getenv("FGL_WG_TPC") ? std::max(1, atoi(getenv("FGL_WG_TPC"))) : 16;
     const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(ceil_div(n, 64), tpc)));
     int used_chunks = chunks, kp1 = 0;
+    const ProfMark pm = prof_begin(st);
     bool split_done = false;
     if (din + 1 > 128 && !(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15)) {
       // wide inputs: feature slices of 124 rows of dW on the tensor cores; each
@@ -791,15 +794,12 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     }
     if (split_done) {
       // dW / db complete
-    } else if (tc_wgrad4(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr) ||
-        tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
+    } else if (tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
       if (werr) return werr;
       used_chunks = tc3_chunks;
       kp1 = din + 1;
-    } else if (tc_wgrad(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc_chunks, st, &werr)) {
-      if (werr) return werr;
-      used_chunks = tc_chunks;
     } else {
+      count_dense_fallback();
       const int vec = (ldh % 4 == 0) && !(reinterpret_cast<uintptr_t>(H) & 15);
       dim3 g(chunks, ky, nz);
       FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
@@ -808,10 +808,12 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     if (!split_done)
       FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
           pw, used_chunks, outs, dW, (int64_t)din * dout, db, kp1);
+    prof_end(pm, kProfWgrad, n, din, dout);
     int err = 0;
     if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
       if (err) return err;
     } else if (dH) {
+      count_dense_fallback();
       dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
       FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0,
                                         Xout, ldxo);
@@ -834,6 +836,7 @@ int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ld
   if (n == 0) return FGL_OK;
   int err = 0;
   if (tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) return err;
+  count_dense_fallback();
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
   FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0, Xout,
                                                         ldxo);

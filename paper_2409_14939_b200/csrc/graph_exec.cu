@@ -7,24 +7,47 @@
 // ~0.6 us (tools/probes/launch_probe.cu).  The chain's shape is the same for
 // every batch -- only sizes and pointers change -- so the trainer captures each
 // batch on its stream (fgl_capture_begin), and fgl_capture_end_launch folds the
-// new capture into one executable graph per slot with cudaGraphExecUpdate
+// new capture into one executable graph per caller-owned handle (fgl_exec) with cudaGraphExecUpdate
 // (parameters and grid sizes change, the topology does not), instantiating only
 // when the update is refused (first use, or a batch that took a different
 // kernel path).  Any failure aborts the capture; the caller then runs the
 // batch eagerly, so the results never depend on whether a graph was used.
+#include <atomic>
+
 #include "common.cuh"
 
 namespace fgl {
 namespace {
-constexpr int kSlots = 4;
-cudaGraphExec_t g_exec[kSlots] = {nullptr, nullptr, nullptr, nullptr};
-int64_t g_stats[3] = {0, 0, 0};  // launches, updates, instantiations
+std::atomic<int64_t> g_stats[3];  // launches, updates, instantiations (process-wide counters)
 }  // namespace
 }  // namespace fgl
+
+// One executable graph, owned by the caller (a Pipeline keeps one per
+// sequence it replays: batch chain, prepare, sampler, window chain), so two
+// pipelines -- or two devices -- never update each other's executables.
+struct fgl_exec {
+  cudaGraphExec_t exec = nullptr;
+  int device = -1;
+};
 
 using namespace fgl;
 
 extern "C" {
+
+int fgl_exec_create(fgl_exec** out) {
+  if (!out) return FGL_E_INVALID;
+  fgl_exec* h = new fgl_exec();
+  FGL_CUDA(cudaGetDevice(&h->device));
+  *out = h;
+  return FGL_OK;
+}
+
+int fgl_exec_destroy(fgl_exec* h) {
+  if (!h) return FGL_OK;
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  delete h;
+  return FGL_OK;
+}
 
 int fgl_capture_begin(void* stream) {
   FGL_CUDA(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
@@ -40,44 +63,52 @@ int fgl_capture_abort(void* stream) {
   return FGL_OK;
 }
 
-int fgl_capture_end_launch(int32_t slot, void* stream) {
-  if (slot < 0 || slot >= kSlots) {
-    set_error("fgl_capture_end_launch: slot %d out of range", slot);
+int fgl_capture_end_launch(fgl_exec* h, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h) {
+    fgl_capture_abort(stream);
+    set_error("fgl_capture_end_launch: null executable handle");
     return FGL_E_INVALID;
   }
-  cudaStream_t st = (cudaStream_t)stream;
+  int dev = -1;
+  FGL_CUDA(cudaGetDevice(&dev));
+  if (dev != h->device) {
+    fgl_capture_abort(stream);
+    set_error("fgl_capture_end_launch: handle of device %d used on device %d", h->device, dev);
+    return FGL_E_INVALID;
+  }
   cudaGraph_t g = nullptr;
   FGL_CUDA(cudaStreamEndCapture(st, &g));
   bool ok = false;
-  if (g_exec[slot]) {
+  if (h->exec) {
     cudaGraphExecUpdateResultInfo info;
-    if (cudaGraphExecUpdate(g_exec[slot], g, &info) == cudaSuccess) {
+    if (cudaGraphExecUpdate(h->exec, g, &info) == cudaSuccess) {
       ok = true;
       ++g_stats[1];
     } else {
       cudaGetLastError();
-      cudaGraphExecDestroy(g_exec[slot]);
-      g_exec[slot] = nullptr;
+      cudaGraphExecDestroy(h->exec);
+      h->exec = nullptr;
     }
   }
   if (!ok) {
-    cudaError_t e = cudaGraphInstantiate(&g_exec[slot], g, 0);
+    cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
     if (e != cudaSuccess) {
       cudaGraphDestroy(g);
-      g_exec[slot] = nullptr;
+      h->exec = nullptr;
       return cuda_status(e, "cudaGraphInstantiate");
     }
     ++g_stats[2];
   }
   cudaGraphDestroy(g);
-  FGL_CUDA(cudaGraphLaunch(g_exec[slot], st));
+  FGL_CUDA(cudaGraphLaunch(h->exec, st));
   ++g_stats[0];
   return FGL_OK;
 }
 
 int fgl_capture_stats(int64_t* out3) {
   if (!out3) return FGL_E_INVALID;
-  for (int i = 0; i < 3; ++i) out3[i] = g_stats[i];
+  for (int i = 0; i < 3; ++i) out3[i] = g_stats[i].load();
   return FGL_OK;
 }
 

@@ -245,6 +245,7 @@ int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8 * 4), 148 * 16));
   auto* ld = reinterpret_cast<unsigned long long*>(loaded);
   auto* ht = reinterpret_cast<unsigned long long*>(hits);
+  const ProfMark pm = prof_begin((cudaStream_t)stream);
   if (vec)
     FGL_COUNT_LAUNCH(), gather_rows_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(
         feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, prev_row_map, cache_slot, cache_x,
@@ -253,6 +254,7 @@ int fgl_gather_rows_cached(const float* feats, int64_t ldf, int32_t d, const int
     FGL_COUNT_LAUNCH(), gather_rows_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(
         feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, prev_row_map, cache_slot, cache_x,
         ldc, out, ldo, ld, ht);
+  prof_end(pm, kProfGather, n, d);
   FGL_LAUNCH_CHECK("gather_rows_kernel");
   return FGL_OK;
 }
@@ -263,6 +265,30 @@ int fgl_gather_rows(const float* feats, int64_t ldf, int32_t d, const int32_t* i
                     void* stream) {
   return fgl_gather_rows_cached(feats, ldf, d, ids, n, prev_bitmap, prev_prefix, prev_base, prev_x, ldp, nullptr,
                                 nullptr, nullptr, 0, out, ldo, loaded, nullptr, stream);
+}
+
+// Page-lock (and map) a host feature table the caller allocated -- e.g. a
+// shared-memory table every rank of a node maps -- so the loader reads it
+// zero-copy; *dev_ptr receives the device address of its first byte.
+int fgl_host_register(void* host, int64_t bytes, void** dev_ptr) {
+  if (!host || bytes <= 0 || !dev_ptr) {
+    set_error("fgl_host_register: bad arguments");
+    return FGL_E_INVALID;
+  }
+  FGL_CUDA(cudaHostRegister(host, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  void* d = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&d, host, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(host);
+    return cuda_status(e, "cudaHostGetDevicePointer");
+  }
+  *dev_ptr = d;
+  return FGL_OK;
+}
+
+int fgl_host_unregister(void* host) {
+  FGL_CUDA(cudaHostUnregister(host));
+  return FGL_OK;
 }
 
 }  // extern "C"

@@ -1164,11 +1164,6 @@ __global__ void __launch_bounds__(kWalkThreads) walk_kernel(const int64_t* __res
   }
 }
 
-// measurement hook (fgl_profile_select): events around select launches
-std::mutex g_sel_mu;
-bool g_sel_prof = false;
-std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_sel_ev;
-
 int select_grid(int K) {
   static int cache[9] = {0};
   if (cache[K]) return cache[K];
@@ -1199,28 +1194,6 @@ extern "C" {
 
 int fgl_debug_select_finish(int64_t* host, int64_t n) {
   return cudaMemcpyFromSymbol(host, g_sel_finish, sizeof(int64_t) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
-}
-
-int fgl_profile_select(int32_t enable) {
-  g_sel_prof = enable != 0;
-  return FGL_OK;
-}
-
-int fgl_profile_select_read(double* ms_out, int64_t cap, int64_t* launches) {
-  std::lock_guard<std::mutex> lk(g_sel_mu);
-  int64_t k = 0;
-  for (auto& pr : g_sel_ev) {
-    float ms = 0.f;
-    FGL_CUDA(cudaEventSynchronize(pr.second));
-    FGL_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
-    if (ms_out && k < cap) ms_out[k] = ms;
-    ++k;
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
-  }
-  if (launches) *launches = k;
-  g_sel_ev.clear();
-  return FGL_OK;
 }
 
 int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t nb,
@@ -1369,21 +1342,12 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
         bal_grid_of[fan] = per_sm * kNumSMs;
       }
       const int bal_grid = bal_grid_of[fan];
-      cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-      if (g_sel_prof) {
-        cudaEventCreate(&pe0);
-        cudaEventCreate(&pe1);
-        cudaEventRecord(pe0, stream);
-      }
+      const ProfMark pm = prof_begin(stream);  // bench.py: the two launches are the hop's selection
       static const int seldbg = getenv("FGL_SELDBG") ? 1 : 0;
       FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
                                                                                   bal_sv_words(fan), seldbg);
       FGL_COUNT_LAUNCH(), select_hub_kernel<<<4 * kNumSMs, kHubThreads, 0, stream>>>(a);
-      if (g_sel_prof) {  // the events bracket both launches: together they are the hop's selection
-        cudaEventRecord(pe1, stream);
-        std::lock_guard<std::mutex> lk(g_sel_mu);
-        g_sel_ev.emplace_back(pe0, pe1);
-      }
+      prof_end(pm, kProfSelect, h);
     } else if (fan <= kTauMaxFan && !force_stream)
       FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, kSelectSmem, stream>>>(a);
     else if (fan <= 32) FGL_COUNT_LAUNCH(), select_kernel<1><<<select_grid(1), 256, 0, stream>>>(a);

@@ -726,211 +726,6 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   }
 }
 
-// ---------------------------------------------------------------- wgrad v4 --
-// Same partials as tc_wgrad3_kernel, with B' = masked dZ fed to the MMA as an
-// MN-major swizzled operand: the producer's TMA tensor copies land dZ (and
-// the mask) in 64-row x 32-column swizzled boxes that ARE the operand layout,
-// so the converters only split them in place (hi) and beside (lo) with
-// 16-byte shared accesses -- no transpose.  A' = H^T still goes through TMEM
-// (K-major, thread = feature = TMEM lane), and the raw slot is released by
-// the MMA's commit once both of its chunks have been multiplied.
-constexpr int WG4_MT = 64;
-
-struct Wg4Args {
-  const float* H;
-  int64_t ldh;
-  float* part;         // [gridDim.x][N][K+1] (feature-major)
-  int64_t M;
-  int K, N, N_mma, nblk, has_mask, tmem_cols, h_bytes, slot_bytes, R, NC, dbg;
-};
-
-// MN-major tf32 operand: the only smem layout the MMA takes for 32-bit MN-major
-// data is SWIZZLE_128B_BASE32B (layout type 1: 32-byte granules of each
-// 128-byte row XOR-ed with the row index mod 4; atoms of 32 MN elements x 4 K
-// rows), which is what a CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B TMA copy writes.
-__device__ __forceinline__ uint64_t umma_desc_mn_sw128_32b(uint32_t saddr, uint32_t lbo) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;   // stride between 32-element MN atoms
-  d |= (uint64_t)(512 >> 4) << 32;               // stride between 4-row K groups
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)1 << 61;
-  return d;
-}
-
-__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad4_kernel(const __grid_constant__ CUtensorMap tmZ,
-                                                                  const __grid_constant__ CUtensorMap tmM, Wg4Args p) {
-  extern __shared__ __align__(1024) char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int zbox = WG4_MT * 128;                    // one 64-row x 32-column SW128 box
-  const int zreg = p.nblk * zbox;                   // dZ (or mask, or lo) region of a slot
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.R * p.slot_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.R + 2 * p.NC + 1);
-  auto bar = [&](int i) { return smem_u32(bars + i); };
-  // slot layout: [H raw rows | dZ (hi after the split) | lo | mask]
-  auto slot_h = [&](int s) { return smem_u32(smem + s * p.slot_bytes); };
-  auto slot_z = [&](int s) { return slot_h(s) + (uint32_t)p.h_bytes; };
-  const int FULL = 0, EMPTY = p.R, CFULL = 2 * p.R, CEMPTY = 2 * p.R + p.NC, TFULL = 2 * p.R + 2 * p.NC;
-  if (tid == 0) {
-    for (int s = 0; s < p.R; ++s) { mbar_init_n(bar(FULL + s), 1); mbar_init_n(bar(EMPTY + s), 1); }
-    for (int c = 0; c < p.NC; ++c) { mbar_init_n(bar(CFULL + c), G3_CONV_THREADS / 2); mbar_init_n(bar(CEMPTY + c), 1); }
-    mbar_init_n(bar(TFULL), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int64_t tiles = ceil_div(p.M, WG4_MT);
-  if (warp == 0) {
-    if (lane == 0) {
-      tma_prefetch_desc(&tmZ);
-      if (p.has_mask) tma_prefetch_desc(&tmM);
-      int j = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
-        const int s = j % p.R;
-        mbar_wait(bar(EMPTY + s), ((uint32_t)(j / p.R) & 1u) ^ 1u);
-        const int64_t r0 = t * WG4_MT;
-        const int rows = (int)(p.M - r0 < WG4_MT ? p.M - r0 : WG4_MT);
-        const uint32_t hb = (uint32_t)(rows * p.ldh * 4);
-        mbar_arrive_expect_tx(bar(FULL + s), hb + (uint32_t)(zreg * (1 + p.has_mask)));
-        bulk_load(slot_h(s), p.H + r0 * p.ldh, hb, bar(FULL + s));
-        for (int nb = 0; nb < p.nblk; ++nb) {
-          tma_load_2d(slot_z(s) + (uint32_t)(nb * zbox), &tmZ, 32 * nb, (int)r0, bar(FULL + s));
-          if (p.has_mask)
-            tma_load_2d(slot_z(s) + (uint32_t)(2 * zreg + nb * zbox), &tmM, 32 * nb, (int)r0, bar(FULL + s));
-        }
-      }
-    }
-    return;
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
-  tc_fence_before();
-  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  auto ch_hi = [&](int c) { return tmem + (uint32_t)(p.N_mma + 64 * c); };
-  const int my_tiles = (int)(tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
-
-  if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(G3_M, p.N_mma, 0, 1);
-    int cc = 0;
-    for (int j = 0; j < my_tiles; ++j) {
-      const int s = j % p.R;
-      for (int c = 0; c < WG4_MT / 32; ++c, ++cc) {
-        const int cs = cc % p.NC;
-        mbar_wait(bar(CFULL + cs), (uint32_t)(cc / p.NC) & 1u);
-        tc_fence_after();
-        const uint32_t ahi = ch_hi(cs), alo = ahi + 32;
-        if (elect_one()) {
-#pragma unroll
-          for (int st = 0; st < ((p.dbg & 2) ? 0 : 4); ++st) {
-            const uint32_t kg = (uint32_t)((4 * c + st) * 1024);
-            const uint64_t dbh = umma_desc_mn_sw128_32b(slot_z(s) + kg, (uint32_t)zbox);
-            const uint64_t dbl = umma_desc_mn_sw128_32b(slot_z(s) + (uint32_t)zreg + kg, (uint32_t)zbox);
-            mma_tf32_ts(tmem, alo + 8 * st, dbh, idesc, (cc | st) != 0);
-            mma_tf32_ts(tmem, ahi + 8 * st, dbl, idesc, 1);
-            mma_tf32_ts(tmem, ahi + 8 * st, dbh, idesc, 1);
-          }
-          mma_commit(bar(CEMPTY + cs));
-          if (c == WG4_MT / 32 - 1) mma_commit(bar(EMPTY + s));
-        }
-        __syncwarp();
-      }
-    }
-    if (my_tiles > 0 && elect_one()) mma_commit(bar(TFULL));
-    __syncwarp();
-  } else if (warp >= 4 && warp < 12) {
-    // two groups of 4 warps take alternate 32-row chunks
-    const int grp = (warp - 4) >> 2;
-    const int ct = tid - 128 - 128 * grp;  // 0..127 within the group
-    const int quarter = warp & 3;
-    const int m = quarter * 32 + lane;     // A' row = TMEM lane
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    int cc = 0;
-    for (int j = 0; j < my_tiles; ++j) {
-      const int s = j % p.R;
-      const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
-      const int rows = (int)(p.M - t * WG4_MT < WG4_MT ? p.M - t * WG4_MT : WG4_MT);
-      mbar_wait(bar(FULL + s), (uint32_t)(j / p.R) & 1u);
-      const uint32_t hs = slot_h(s), zs = slot_z(s);
-      for (int c = 0; c < WG4_MT / 32; ++c, ++cc) {
-        if (c != grp) continue;
-        const int cs = cc % p.NC;
-        uint32_t hv[32], lv[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int r = 32 * c + q;
-          float x = 0.f;
-          if (r < rows && !(p.dbg & 1)) {
-            if (m < p.K) x = lds32(hs + (uint32_t)((r * p.ldh + m) * 4));
-            else if (m == p.K) x = 1.f;
-          }
-          const float hi = tf32_rna_finite(x);
-          hv[q] = __float_as_uint(hi);
-          lv[q] = __float_as_uint(__fsub_rn(x, hi));
-        }
-        // B': split this chunk's 32 rows of every 32-column box in place; the
-        // boxes' rows past M are zero-filled by the TMA, columns past N too
-        if (!(p.dbg & 4)) {
-          const int per = p.nblk * 256;  // 16-byte units: nblk boxes x 32 rows x 8
-          for (int u = ct; u < per; u += G3_CONV_THREADS / 2) {
-            const uint32_t off = (uint32_t)((u >> 8) * zbox + c * 4096 + (u & 255) * 16);
-            float4 z = lds128(zs + off);
-            if (p.has_mask) {
-              const float4 mk = lds128(zs + (uint32_t)(2 * zreg) + off);
-              z.x = mk.x > 0.f ? z.x : 0.f;
-              z.y = mk.y > 0.f ? z.y : 0.f;
-              z.z = mk.z > 0.f ? z.z : 0.f;
-              z.w = mk.w > 0.f ? z.w : 0.f;
-            }
-            float4 h4, l4;
-            h4.x = tf32_rna_finite(z.x); l4.x = __fsub_rn(z.x, h4.x);
-            h4.y = tf32_rna_finite(z.y); l4.y = __fsub_rn(z.y, h4.y);
-            h4.z = tf32_rna_finite(z.z); l4.z = __fsub_rn(z.z, h4.z);
-            h4.w = tf32_rna_finite(z.w); l4.w = __fsub_rn(z.w, h4.w);
-            sts128(zs + off, h4);
-            sts128(zs + (uint32_t)zreg + off, l4);
-          }
-        }
-        mbar_wait(bar(CEMPTY + cs), ((uint32_t)(cc / p.NC) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t hi_t = ch_hi(cs) + lane_off;
-#pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) {
-          tmem_st8(hi_t + 8 * q8, *reinterpret_cast<uint32_t(*)[8]>(hv + 8 * q8));
-          tmem_st8(hi_t + 32 + 8 * q8, *reinterpret_cast<uint32_t(*)[8]>(lv + 8 * q8));
-        }
-        tmem_st_wait();
-        fence_async_smem();
-        tc_fence_before();
-        mbar_arrive(bar(CFULL + cs));
-      }
-    }
-  } else if (warp >= 12) {
-    const int quarter = warp & 3;
-    const int m = quarter * 32 + lane;
-    float* out = p.part + (int64_t)blockIdx.x * (p.K + 1) * p.N;
-    if (my_tiles > 0) {
-      mbar_wait(bar(TFULL), 0);
-      tc_fence_after();
-    }
-    for (int c0 = 0; c0 < p.N_mma; c0 += 16) {
-      if (c0 >= p.N) break;
-      uint32_t v[16];
-      if (my_tiles > 0) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-      if (m <= p.K) {  // feature-major partials: a warp stores 32 consecutive floats per column
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = my_tiles > 0 ? __uint_as_float(v[q]) : 0.f;
-      }
-    }
-  }
-  tc_fence_before();
-  asm volatile("bar.sync 1, %0;" ::"r"(G3_THREADS - 32) : "memory");
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_free(tmem, p.tmem_cols);
-  }
-}
-
 // ------------------------------------------------------------ host side --
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1065,63 +860,19 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
+  const ProfMark pm = prof_begin(st);
   if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
   else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
+  prof_end(pm, mode == 0 ? kProfDenseFwd : kProfDgrad, M, N, K);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_gemm3_kernel");
   return true;
 }
 
-// fp32 [rows, cols] (ld floats) in 64-row x 32-column 128B_ATOM_32B-swizzled boxes,
-// columns past `cols` and rows past `rows` zero-filled
-bool make_map_wg4(CUtensorMap* m, const float* base, int64_t rows, int cols, int64_t ld) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)WG4_MT};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool tc_wgrad4(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
-               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
-  *err = 0;
-  static const int off = getenv("FGL_WGRAD") ? atoi(getenv("FGL_WGRAD")) : 3;  // opt-in (FGL_WGRAD=4): slower than v3
-  if (off != 4 || tc3_disabled() || M < 1 || K < 1 || K + 1 > G3_M || N < 1 || N > 256) return false;
-  if ((ldh % 4) || (reinterpret_cast<uintptr_t>(H) & 15) || (ldz % 4) || (reinterpret_cast<uintptr_t>(dZ) & 15))
-    return false;
-  if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
-  const int N_mma = (N + 31) / 32 * 32, nblk = N_mma / 32;
-  const int h_bytes = WG4_MT * (int)ldh * 4;  // multiple of 1024 (ldh % 4 == 0)
-  const int has_mask = mask ? 1 : 0;
-  const int slot = h_bytes + nblk * WG4_MT * 128 * (2 + has_mask);
-  const int NC = std::min(4, (512 - N_mma) / 64);
-  if (NC < 1) return false;
-  int R = 4;
-  auto smem_of = [&](int r) { return (int64_t)1024 + (int64_t)r * slot + 8 * (2 * r + 2 * NC + 1) + 16; };
-  while (R > 2 && smem_of(R) > G3_MAX_SMEM) --R;
-  if (smem_of(R) > G3_MAX_SMEM) return false;
-  CUtensorMap mZ, mM;
-  std::memset(&mZ, 0, sizeof(mZ));
-  std::memset(&mM, 0, sizeof(mM));
-  if (!make_map_wg4(&mZ, dZ, M, N, ldz)) return false;
-  if (mask && !make_map_wg4(&mM, mask, M, N, ldm)) return false;
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    e = cudaFuncSetAttribute(tc_wgrad4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
-    if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad4)"); return true; }
-    attr = true;
-  }
-  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  Wg4Args p{H, ldh, part, M, K, N, N_mma, nblk, has_mask, 512, h_bytes, slot, R, NC, dbg};
-  FGL_COUNT_LAUNCH(), tc_wgrad4_kernel<<<chunks, G3_THREADS, smem_of(R), st>>>(mZ, mM, p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad4_kernel");
-  return true;
+bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
+             const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, cudaStream_t st,
+             int* err) {
+  return tc_gemm3(mode, A, lda, mask, ldm, W, bias, C, ldc, M, N, K, relu, st, err, 0);
 }
 
 // Weight-gradient partials part[c][K+1][N] (row K = db) over `chunks` CTAs;

@@ -22,6 +22,9 @@ def init(backend: str = "nccl"):
     import torch.distributed as dist
     rank, world, _ = env_rank()
     if world > 1 and not dist.is_initialized():
+        # the gradient all-reduce is captured into CUDA graphs: the NCCL
+        # watchdog must not query events of captured work
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "0")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
@@ -45,16 +48,48 @@ def lockstep_count(n_local: int, world: int, device=None) -> int:
 
 
 class GradAllReduce:
-    """Averages the flat gradient bucket across ranks (one collective per step)."""
+    """Sums the flat gradient bucket across ranks (one collective per step);
+    the trainer folds the 1/W of the mean into the SGD step (lr / W).
+
+    With the NCCL backend the collective is issued on the caller's current
+    stream and can be captured into the trainer's CUDA graphs (NCCL >= 2.9.6
+    supports stream capture; the communicator is created by ``warmup``
+    before any capture, and the watchdog's asynchronous error handling must
+    be off: TORCH_NCCL_ASYNC_ERROR_HANDLING=0, set by ``init``).  gloo
+    (CPU tests, several ranks sharing one GPU) cannot be captured; the
+    trainer then runs eagerly."""
 
     def __init__(self, world: int):
-        self.world = world
+        self.world = int(world)
+        self.backend = None
+        if self.world > 1:
+            import torch.distributed as dist
+            self.backend = str(dist.get_backend())
+        self.capturable = self.backend == "nccl"
+        self._warm = False
 
-    def allreduce_mean(self, flat):
+    def warmup(self, device=None):
+        """One eager collective: creates the communicator outside any capture."""
+        if self.world <= 1 or self._warm:
+            return
+        import torch
+        import torch.distributed as dist
+        t = torch.zeros(1, dtype=torch.float32, device=device)
+        dist.all_reduce(t)
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        self._warm = True
+
+    def allreduce_sum(self, flat):
         if self.world <= 1:
             return
         import torch.distributed as dist
         dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+
+    def allreduce_mean(self, flat):
+        if self.world <= 1:
+            return
+        self.allreduce_sum(flat)
         flat.mul_(1.0 / self.world)
 
 

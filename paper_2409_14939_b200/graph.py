@@ -103,17 +103,22 @@ _cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def device_graph(g, device="cuda") -> DeviceGraph:
-    """Upload (once, cached per host graph object) and return the device CSR."""
+    """Upload (once per host graph object and device) and return the device CSR."""
     if isinstance(g, DeviceGraph):
         return g
+    import torch
+    dev = torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     try:
-        dg = _cache.get(g)
+        per = _cache.get(g)
     except TypeError:
-        dg = None
+        per = None
+    dg = per.get(str(dev)) if per is not None else None
     if dg is None:
-        dg = DeviceGraph.from_host(g, device)
+        dg = DeviceGraph.from_host(g, dev)
         try:
-            _cache[g] = dg
+            _cache.setdefault(g, {})[str(dev)] = dg
         except TypeError:
             pass
     return dg

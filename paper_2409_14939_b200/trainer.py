@@ -31,7 +31,9 @@ import numpy as np
 from . import _lib
 from .errors import ValidationError
 from .graph import device_graph
+from .memsim import BatchTraffic, CostParams, TrafficReport, t_memory_aware, t_naive
 from .sampler import Fanouts, WindowSampler, derive_seed, make_epoch_batches
+from .store import HostFeatureStore
 
 __all__ = ["ModelConfig", "PipelineFlags", "EpochStats", "TrainReport", "train", "derive_seed",
            "init_params", "DeviceModel", "Pipeline", "StaticFeatureCache", "phase_breakdown", "PHASES"]
@@ -96,7 +98,7 @@ class PipelineFlags:
 class EpochStats:
     loss: float
     accuracy: float
-    traffic: dict
+    traffic: TrafficReport
     phase_seconds: dict
     modeled_fetch_seconds: float = 0.0
 
@@ -206,7 +208,7 @@ class StaticFeatureCache:
 
     POLICIES = ("none", "static-degree")
 
-    def __init__(self, dg, host_feats, d, ld, cache_ratio: float, policy: str = "static-degree",
+    def __init__(self, dg, host_feats: int, d, ld, cache_ratio: float, policy: str = "static-degree",
                  device="cuda"):
         import torch
         if not 0.0 <= cache_ratio <= 1.0:
@@ -225,7 +227,7 @@ class StaticFeatureCache:
             top = torch.argsort(-deg, stable=True)[: self.k].to(torch.int32).contiguous()
             self.slot[top.long()] = torch.arange(self.k, dtype=torch.int32, device=device)
             self.nodes = top
-            _lib.call("fgl_gather_rows", host_feats.data_ptr(), ld, d, top.data_ptr(), self.k, None, None, 0,
+            _lib.call("fgl_gather_rows", host_feats, ld, d, top.data_ptr(), self.k, None, None, 0,
                       None, ld, self.table.data_ptr(), ld, None, torch.cuda.current_stream().cuda_stream)
         else:
             self.nodes = torch.zeros(0, dtype=torch.int32, device=device)
@@ -244,6 +246,8 @@ class Pipeline:
     the host link (zero-copy reads, config 4 of BASELINE.json).
     """
 
+    MAX_MATCH_WINDOW = 16
+
     def __init__(self, g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None,
                  device="cuda", feature_store="device", params=None, dist=None, direct_x0=None,
                  cache_ratio: float = 0.0, cache_policy: str = "static-degree"):
@@ -251,27 +255,40 @@ class Pipeline:
         self.torch = torch
         self.cfg = cfg
         self.flags = flags or PipelineFlags()
+        # device-side limits of a window (checked before any allocation): the
+        # match-degree pass keeps all pair counts of a window in registers
+        # (<= 16 batches), the depth-major relayout of GIN / SAGE ranks up to
+        # 64 batches per pass
+        if self.flags.reorder and cfg.window_n > self.MAX_MATCH_WINDOW:
+            raise ValidationError(f"window_n {cfg.window_n} > {self.MAX_MATCH_WINDOW}: the GPU match-degree "
+                                  f"schedule handles at most {self.MAX_MATCH_WINDOW} batches per window")
+        if cfg.arch != "gcn" and cfg.window_n > 64:
+            raise ValidationError(f"window_n {cfg.window_n} > 64 is not supported for arch {cfg.arch!r}")
         self.device = device
         self.dist = dist
         self.dg = device_graph(g, device)
-        data = _feature_array(feats)
-        if isinstance(data, torch.Tensor):
-            ft = data
+        if isinstance(feats, HostFeatureStore):
+            # a pinned (possibly node-shared) host table: the loader reads it zero-copy
+            self.store = feats
+            feature_store = "host"
+            self.d0 = feats.dim
         else:
-            ft = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))
-        self.d0 = int(ft.shape[1])
+            data = _feature_array(feats)
+            ft = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data, np.float32))
+            self.d0 = int(ft.shape[1])
+            self.store = HostFeatureStore.private(ft) if feature_store == "host" else None
         if self.d0 != cfg.layer_dims[0]:
             raise ValidationError(f"feature dim {self.d0} != model input dim {cfg.layer_dims[0]}")
         self.ldf = _ld(self.d0)
         self.feature_store = feature_store
-        if feature_store == "host":
-            host = torch.zeros((ft.shape[0], self.ldf), dtype=torch.float32).pin_memory()
-            host[:, : self.d0].copy_(ft.cpu() if ft.is_cuda else ft)
-            self.feats = host  # UVA: the pinned host pointer is device-addressable
+        if self.store is not None:
+            self.feats = self.store.table
+            self.feats_ptr = self.store.dev_ptr
         else:
             dev = torch.zeros((ft.shape[0], self.ldf), dtype=torch.float32, device=device)
             dev[:, : self.d0].copy_(ft.to(device) if not ft.is_cuda else ft)
             self.feats = dev
+            self.feats_ptr = dev.data_ptr()
         lab = labels if isinstance(labels, torch.Tensor) else torch.from_numpy(np.asarray(labels, dtype=np.int64))
         self.labels = lab.to(device=device, dtype=torch.int64)
         self.sampler = WindowSampler(self.dg, cfg.fanouts, cfg.batch_size, cfg.window_n, device=device,
@@ -294,13 +311,15 @@ class Pipeline:
             direct_x0 = False
         self.direct_x0 = bool(direct_x0) and feature_store == "device" and self.compact
         self.pairs = torch.zeros(120, dtype=torch.int64, device=device)
-        self.loaded = torch.zeros(1, dtype=torch.int64, device=device)
-        self.cache_hits = torch.zeros(1, dtype=torch.int64, device=device)
+        # rows read from the feature store / served by the static cache, per
+        # schedule position of the window (BatchTraffic rows of memsim.py:52-60)
+        self.loaded = torch.zeros(max(cfg.window_n, 1), dtype=torch.int64, device=device)
+        self.cache_hits = torch.zeros(max(cfg.window_n, 1), dtype=torch.int64, device=device)
         self.cache = None
         if cache_ratio > 0.0 or cache_policy not in StaticFeatureCache.POLICIES:
             if feature_store != "host":
                 raise ValidationError("the static feature cache fronts a host-resident feature store")
-            self.cache = StaticFeatureCache(self.dg, self.feats, self.d0, self.ldf, cache_ratio, cache_policy,
+            self.cache = StaticFeatureCache(self.dg, self.feats_ptr, self.d0, self.ldf, cache_ratio, cache_policy,
                                             device)
         self.loss_dev = torch.zeros(max(cfg.window_n, 1), dtype=torch.float64, device=device)
         dims = cfg.layer_dims
@@ -319,10 +338,12 @@ class Pipeline:
         self._bufs = {}
         self._graveyard = []
         self.gpu_launches = 0
-        self.fused_upper = self._fused_upper_ok()
         self._pre_h0 = None
         self._pre_h0_win = None
         self._agg_stream = None
+        self._execs = {}
+        if self._world() > 1 and hasattr(self.dist, "warmup"):
+            self.dist.warmup(device)
 
     # ------------------------------------------------------------ buffers --
     def _buf(self, name, rows, cols, dtype=None):
@@ -444,15 +465,17 @@ class Pipeline:
         return win.front_range(self.H - i, b)[0]
 
     # -------------------------------------------------------------- batch --
-    def _graph_mode(self) -> bool:
-        import os
-        return (os.environ.get("FGL_GRAPH", "1") != "0" and self._cs is not None and not self.fused_upper
-                and (self.dist is None or getattr(self.dist, "world", 1) <= 1))
+    def _world(self) -> int:
+        return int(getattr(self.dist, "world", 1)) if self.dist is not None else 1
 
     def _graphs_on(self) -> bool:
-        import os
+        """CUDA graphs unless disabled, or a collective that cannot be
+        captured (gloo) sits inside the chain."""
         return (os.environ.get("FGL_GRAPH", "1") != "0"
-                and (self.dist is None or getattr(self.dist, "world", 1) <= 1))
+                and (self._world() <= 1 or bool(getattr(self.dist, "capturable", False))))
+
+    def _graph_mode(self) -> bool:
+        return self._cs is not None and self._graphs_on()
 
     def _graphed(self, stream, slot: int, fn):
         """Run fn() -- work issued on `stream` only, no host reads of device
@@ -472,8 +495,33 @@ class Pipeline:
             self.graph_fallbacks += 1
             return fn()
         self._capturing = False
-        _lib.call("fgl_capture_end_launch", slot, st)
+        try:
+            _lib.call("fgl_capture_end_launch", self._exec(slot), st)
+        except Exception:  # noqa: BLE001 - instantiate / launch refused: run eagerly
+            self.graph_fallbacks += 1
+            return fn()
         return r
+
+    def _exec(self, slot: int):
+        """This pipeline's executable graph for sequence `slot` (0 batch chain,
+        1 prepare, 2 sampler, 3 window chain), created on first use."""
+        h = self._execs.get(slot)
+        if h is None:
+            import ctypes
+            p = ctypes.c_void_p()
+            _lib.call("fgl_exec_create", ctypes.byref(p))
+            h = self._execs[slot] = p.value
+        return h
+
+    def __del__(self):
+        execs = getattr(self, "_execs", None) or {}
+        try:
+            lib = _lib.lib()
+            for h in execs.values():
+                lib.fgl_exec_destroy(h)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+        self._execs = {}
 
     def batch_step(self, win, b, prev, slot, layers, x0_slot):
         """Load x0, forward, loss, backward, SGD for batch b of the window.
@@ -501,7 +549,42 @@ class Pipeline:
             self.graph_fallbacks += 1
             return self._batch_step_body(win, b, prev, slot, layers, x0_slot, external_done=True)
         self._capturing = False
-        _lib.call("fgl_capture_end_launch", 0, st)
+        try:
+            _lib.call("fgl_capture_end_launch", self._exec(0), st)
+        except Exception:  # noqa: BLE001 - instantiate / launch refused: run eagerly
+            self.graph_fallbacks += 1
+            self._batch_step_body(win, b, prev, slot, layers, x0_slot, external_done=True)
+
+    def _gather_x0(self, win, b, prev, slot, x0_slot):
+        """x0 = feats[unique_nodes of batch b] (trainer.py:315) in the batch's
+        row order: rows the previous batch (`prev`, Match) already holds are
+        copied from its block, the rest come from the static HBM cache or the
+        feature store (loader.cu); per-position row counts go to
+        loaded / cache_hits.  With direct_x0 the layer-0 aggregation reads the
+        HBM table itself and there is no x0 block."""
+        s = self.sampler
+        st = self.stream
+        if self.direct_x0:
+            return self.feats
+        u0, u1 = win.unique_range(b)
+        U = u1 - u0
+        ws = s.ws.data_ptr()
+        x0 = self._buf(f"x0_{x0_slot}", U, self.ldf)
+        if prev is not None:
+            p0 = win.unique_range(prev)[0]
+            prev_bm = ws + self.bm_off + 4 * prev * self.words
+            prev_pf = ws + self.prefix_off + 4 * prev * self.words
+            prev_x = self._bufs[f"x0_{1 - x0_slot}"].data_ptr()
+        else:
+            p0, prev_bm, prev_pf, prev_x = 0, None, None, None
+        row_map = s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None
+        cached = self.cache is not None and self.cache.k > 0
+        self._call("fgl_gather_rows_cached", self.feats_ptr, self.ldf, self.d0,
+                   s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf, row_map,
+                   self.cache.slot.data_ptr() if cached else None, self.cache.table.data_ptr() if cached else None,
+                   self.ldf, x0.data_ptr(), self.ldf, self.loaded.data_ptr() + 8 * slot,
+                   self.cache_hits.data_ptr() + 8 * slot if cached else None, st)
+        return x0
 
     def _batch_step_body(self, win, b, prev, slot, layers, x0_slot, external_done=False):
         torch = self.torch
@@ -509,41 +592,15 @@ class Pipeline:
         m = self.model
         dims = self.cfg.layer_dims
         st = self.stream
-        u0, u1 = win.unique_range(b)
-        U = u1 - u0
-        ws = s.ws.data_ptr()
-        if self.direct_x0:
-            x0 = self.feats
-        else:
-            x0 = self._buf(f"x0_{x0_slot}", U, self.ldf)
-        if self.direct_x0:
-            pass
-        elif prev is not None:
-            p0 = win.unique_range(prev)[0]
-            prev_bm = ws + self.bm_off + 4 * prev * self.words
-            prev_pf = ws + self.prefix_off + 4 * prev * self.words
-            prev_x = self._bufs[f"x0_{1 - x0_slot}"].data_ptr()
-        else:
-            p0, prev_bm, prev_pf, prev_x = 0, None, None, None
-        if not self.direct_x0 and self.cache is not None and self.cache.k > 0:
-            self._call("fgl_gather_rows_cached", self.feats.data_ptr(), self.ldf, self.d0,
-                       s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
-                       s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None,
-                       self.cache.slot.data_ptr(), self.cache.table.data_ptr(), self.ldf,
-                       x0.data_ptr(), self.ldf, self.loaded.data_ptr(), self.cache_hits.data_ptr(), st)
-        elif not self.direct_x0:
-            self._call("fgl_gather_rows_cached", self.feats.data_ptr(), self.ldf, self.d0,
-                       s.unique.data_ptr() + 4 * u0, U, prev_bm, prev_pf, p0, prev_x, self.ldf,
-                       s.row_map.data_ptr() if (prev_bm is not None and s.depth_layout) else None,
-                       None, None, self.ldf, x0.data_ptr(), self.ldf, self.loaded.data_ptr(), None, st)
+        x0 = self._gather_x0(win, b, prev, slot, x0_slot)
         # forward
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
-        top_fused = (self.compact and not self.fused_upper and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 48
+        top_fused = (self.compact and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 48
                      and self._fuse_top
                      and (self._rows(win, self.L - 1, b)[1] - self._rows(win, self.L - 1, b)[0]) == s1 - s0)
         X, ldx = x0, self.ldf
         H_bufs, Y_bufs, ns = [], [], []
-        for i in range(1 if self.fused_upper else self.L):
+        for i in range(self.L):
             din, dout = dims[i], dims[i + 1]
             r0, r1 = self._rows(win, i, b)
             n = r1 - r0
@@ -579,9 +636,6 @@ class Pipeline:
             ns.append(n)
             X, ldx = Yb, _ld(dout)
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
-        if self.fused_upper:
-            self._fused_upper_step(win, b, layers, H_bufs, Y_bufs, ns, s0, s1, slot)
-            return
         C = dims[-1]
         r0, _ = self._rows(win, self.L - 1, b)
         rows_ptr = (s.seed_front if self.compact else s.seed_rows).data_ptr() + 4 * s0
@@ -668,9 +722,12 @@ class Pipeline:
         cur = self._cur()
         for ev in wg_done:
             cur.wait_event(ev)
-        if self.dist is not None:
-            self.dist.allreduce_mean(self.model.grad)
-        self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+        world = self._world()
+        if world > 1:
+            # synchronous DP: the SUM of the ranks' gradients, the 1/W of the
+            # mean folded into the step size (one collective per batch)
+            self.dist.allreduce_sum(self.model.grad)
+        self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr) / world, st)
 
     def _side_wgrad_stream(self):
         import os
@@ -718,11 +775,11 @@ class Pipeline:
                     # rows hold <= fanout edges: the software-pipelined short-row
                     # kernel (bit-identical to fgl_spmm)
                     self._call("fgl_spmm_gather", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"],
-                               lay["w"].data_ptr(), n, 0, self.feats.data_ptr(), self.ldf, int(self.feats.shape[0]),
+                               lay["w"].data_ptr(), n, 0, self.feats_ptr, self.ldf, int(self.feats.shape[0]),
                                Hb.data_ptr(), _ld(din), din, self._max_fan, st)
                 else:
                     self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
-                               n, 0, self.feats.data_ptr(), self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din,
+                               n, 0, self.feats_ptr, self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din,
                                st)
                 if self._capturing:  # graph-captured: the window's `prepped` event orders it
                     pre[b] = (Hb, None)
@@ -733,68 +790,21 @@ class Pipeline:
         self._pre_h0 = pre
         self._pre_h0_win = win
 
-    # ------------------------------------------------------ fused upper --
-    def _fused_upper_ok(self) -> bool:
-        import os
-        dims = self.cfg.layer_dims
-        # opt-in (FGL_FUSED=1): correct, but this round's persistent kernel is
-        # latency bound (~200 us per batch vs ~140 us for the separate kernels)
-        if os.environ.get("FGL_FUSED", "0") != "1" or not self.compact or self.L < 2 or self.L > 4:
-            return False
-        return all(1 <= dims[i] <= 128 and dims[i + 1] <= 192 and (dims[i] + 1) * dims[i + 1] <= 24 * 256
-                   for i in range(1, self.L))
-
-    def _fused_upper_step(self, win, b, layers, H_bufs, Y_bufs, ns, s0, s1, slot):
-        """Layers 1..L-1 forward, fp64 loss and backward in ONE persistent
-        kernel (fgl_upper_layers), then layer 0's backward (tcgen05 wgrad)
-        and SGD."""
-        s, m, dims, st = self.sampler, self.model, self.cfg.layer_dims, self.stream
-        a = _lib.FglUpperArgs()
-        a.num_upper = self.L - 1
-        for i in range(1, self.L):
-            din, dout = dims[i], dims[i + 1]
-            r0, r1 = self._rows(win, i, b)
-            q0, q1 = self._rows(win, i - 1, b)
-            n = r1 - r0
-            lay = layers[i]
-            l = a.layer[i - 1]
-            l.indptr = lay["indptr"].data_ptr() + 8 * r0
-            l.col, l.col_base, l.w, l.rows = lay["col"], self._in_base(win, i, b), lay["w"].data_ptr(), n
-            l.t_indptr = lay["t_indptr"].data_ptr() + 8 * q0
-            l.t_col, l.t_base, l.t_w, l.prev_rows = lay["t_col"].data_ptr(), r0, lay["t_w"].data_ptr(), q1 - q0
-            l.din, l.dout = din, dout
-            l.W, l.b, l.dW, l.db = m.W(i), m.b(i), m.dW(i), m.db(i)
-            l.H, l.ldh = self._buf(f"h{i}", n, _ld(din)).data_ptr(), _ld(din)
-            l.Y, l.ldy = self._buf(f"y{i}", n, _ld(dout)).data_ptr(), _ld(dout)
-            l.dH = self._buf(f"dh{i}", n, _ld(din)).data_ptr()
-            l.dY = self._buf(f"dyu{i}", n, _ld(dout)).data_ptr()
-        n0 = ns[0]
-        d1 = dims[1]
-        dY0 = self._buf("dy0", n0, _ld(d1))
-        a.X1, a.ldx1, a.dX1 = Y_bufs[0].data_ptr(), _ld(d1), None
-        a.seed_rows = s.seed_front.data_ptr() + 4 * s0
-        a.seed_row_base = self._rows(win, self.L - 1, b)[0]
-        a.seed_ids = s.seeds_dev.data_ptr() + 4 * s0
-        a.labels = self.labels.data_ptr()
-        a.num_seeds, a.num_classes = s1 - s0, dims[-1]
-        a.loss_sum = self.loss_dev.data_ptr() + 8 * slot
-        wsb = _lib.lib().fgl_upper_ws_bytes(a)
-        ws = self._buf("upper_ws", wsb, 1, self.torch.uint8)
-        self._call("fgl_upper_layers", a, ws.data_ptr(), wsb, st)
-        # dY0 = A_1^T dH_1 over layer 0's (wide) row space: the standalone SpMM
-        lay1 = layers[1]
-        q0 = self._rows(win, 0, b)[0]
-        r0 = self._rows(win, 1, b)[0]
-        self._call("fgl_spmm", lay1["t_indptr"].data_ptr() + 8 * q0, lay1["t_col"].data_ptr(),
-                   lay1["t_w"].data_ptr(), n0, r0, a.layer[0].dH, _ld(d1), None, _ld(d1), dY0.data_ptr(), _ld(d1),
-                   d1, st)
-        # layer 0 backward: dW0 / db0 from H0 and dY0 * relu'(Y0)
-        self._call("fgl_dense_bwd", H_bufs[0].data_ptr(), _ld(dims[0]), n0, dims[0], m.W(0), d1,
-                   dY0.data_ptr(), _ld(d1), Y_bufs[0].data_ptr(), _ld(d1), m.dW(0), m.db(0), None, _ld(dims[0]),
-                   self.bwd_ws.data_ptr(), self.bwd_ws.numel(), st)
-        if self.dist is not None:
-            self.dist.allreduce_mean(self.model.grad)
-        self._call("fgl_sgd", m.flat.data_ptr(), m.grad.data_ptr(), m.grad.numel(), float(self.cfg.lr), st)
+    def row_length_histograms(self, win, order, layers) -> np.ndarray:
+        """[position, layer, row length] counts of every executed batch's
+        model-layer CSR rows (the input of trainer.py:230-242's fetch model);
+        rows without edges land in bin 0.  One device->host read."""
+        torch = self.torch
+        nb, nbin = len(order), max(int(f) for f in self.cfg.fanouts) + 1
+        out = torch.zeros((nb, self.L, nbin), dtype=torch.int64, device=self.device)
+        for j, b in enumerate(order):
+            for i in range(self.L):
+                r0, r1 = self._rows(win, i, b)
+                if r1 <= r0:
+                    continue
+                ip = layers[i]["indptr"][r0 : r1 + 1]
+                out[j, i] = torch.bincount((ip[1:] - ip[:-1]).clamp_(max=nbin - 1), minlength=nbin)[:nbin]
+        return out.cpu().numpy()
 
     # ------------------------------------------------------------- window --
     def run_window(self, seed_lists, rng_seeds, phase=None):
@@ -823,10 +833,13 @@ class Pipeline:
             phase["map"] += t3 - t2
             phase["compute"] += t4 - t3
         self.last_window = win
+        self.last_layers = layers
         return order, self.loss_dev[:nb]
 
     # --------------------------------------------------------- pipelined --
-    LOOKAHEAD = int(os.environ.get("FGL_LOOKAHEAD", "2"))  # windows sampled ahead of the one being trained
+    # windows sampled ahead of the one being trained (>= 1: window w is
+    # always sampled before it is popped)
+    LOOKAHEAD = max(1, int(os.environ.get("FGL_LOOKAHEAD", "2")))
 
     def _sample_async(self, seed_lists, rng_seeds, slot):
         """Stage + launch the window sampler of slot `slot` (LOOKAHEAD + 1
@@ -882,6 +895,10 @@ class Pipeline:
         for k in range(min(self.LOOKAHEAD, len(windows))):
             pending.append(self._sample_async(*windows[k], slot=k % nsmp))
         for w in range(len(windows)):
+            # the caller may still be reading the previous window's losses
+            # (e.g. an asynchronous copy of the yielded view): order this
+            # window's writes after everything the caller has queued
+            self._main.wait_stream(caller)
             win = pending.popleft()
             nb = win.num_batches
             slot = w % 2
@@ -984,37 +1001,44 @@ def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None
     windows = [seed_batches[i : i + cfg.window_n] for i in range(0, len(seed_batches), cfg.window_n)]
     report = TrainReport(config=cfg, flags=flags)
     d = pipe.d0
+    params = cost_params or CostParams()
+    params.validate()
+    fetch = t_memory_aware if flags.memory_aware else t_naive
+    node_bytes = 4 * d
     for _ in range(cfg.epochs):
         phase = dict.fromkeys(PHASES, 0.0)
-        pipe.loaded.zero_()
-        pipe.cache_hits.zero_()
-        loss_sum, seen, base, total_rows = 0.0, 0, 0, 0
+        loss_sum, seen, base = 0.0, 0, 0
+        per_batch, modeled = [], 0.0
         for win_seeds in windows:
             rs = [derive_seed(cfg.seed, 13, base + j) for j in range(len(win_seeds))]
             base += len(win_seeds)
+            pipe.loaded.zero_()
+            pipe.cache_hits.zero_()
             order, losses = pipe.run_window([w.astype(np.int64) for w in win_seeds], rs, phase)
             lv = losses.cpu().numpy()
+            loaded = pipe.loaded.cpu().numpy()
+            hits = pipe.cache_hits.cpu().numpy()
+            win = pipe.last_window
+            hist = pipe.row_length_histograms(win, order, pipe.last_layers)
             for j, bi in enumerate(order):
                 loss_sum += float(lv[j])  # sum of per-seed losses = mean * batch size
                 seen += len(win_seeds[bi])
-            win = pipe.last_window
-            total_rows += win.unique_total()
-        loaded = int(pipe.loaded.item())
-        hits = int(pipe.cache_hits.item())
-        if pipe.cache is not None and pipe.cache.k > 0:
-            # real counts: rows over the host link, rows from the HBM cache, rest Match
-            traffic = {"bytes_host_to_device": loaded * 4 * d, "bytes_served_by_cache": hits * 4 * d,
-                       "bytes_served_by_match": (total_rows - loaded - hits) * 4 * d}
-        elif flags.match:
-            traffic = {"bytes_host_to_device": loaded * 4 * d,
-                       "bytes_served_by_match": (total_rows - loaded) * 4 * d,
-                       "bytes_served_by_cache": 0}
-        else:
-            traffic = {"bytes_host_to_device": total_rows * 4 * d, "bytes_served_by_match": 0,
-                       "bytes_served_by_cache": 0}
+                u0, u1 = win.unique_range(bi)
+                ld, hit = int(loaded[j]), int(hits[j])
+                per_batch.append(BatchTraffic(position=len(per_batch), loaded_nodes=ld, bytes_h2d=ld * node_bytes,
+                                              bytes_cache=hit * node_bytes,
+                                              bytes_match=(u1 - u0 - ld - hit) * node_bytes))
+                # trainer.py:230-242 per batch: layers in order, row lengths ascending
+                total = 0.0
+                for i in range(pipe.L):
+                    for f in np.flatnonzero(hist[j, i]):
+                        if f > 0:
+                            total += int(hist[j, i, f]) * fetch(int(f), cfg.layer_dims[i], params)
+                modeled += total
+        traffic = TrafficReport.from_batches(per_batch, params)
         acc = evaluate(pipe, g, val_ids) if val_ids.size else float("nan")
         report.epochs.append(EpochStats(loss=loss_sum / max(seen, 1), accuracy=acc, traffic=traffic,
-                                        phase_seconds=phase))
+                                        phase_seconds=phase, modeled_fetch_seconds=modeled))
     report.pipeline = pipe
     return report
 
@@ -1057,7 +1081,7 @@ def _forward_only(self, win, b, layers):
     st = self.stream
     u0, u1 = win.unique_range(b)
     x0 = self._buf("x0_eval", u1 - u0, self.ldf)
-    self._call("fgl_gather_rows", self.feats.data_ptr(), self.ldf, self.d0, s.unique.data_ptr() + 4 * u0,
+    self._call("fgl_gather_rows", self.feats_ptr, self.ldf, self.d0, s.unique.data_ptr() + 4 * u0,
                u1 - u0, None, None, 0, None, self.ldf, x0.data_ptr(), self.ldf, None, st)
     X, ldx = x0, self.ldf
     for i in range(self.L):

@@ -296,6 +296,7 @@ def train_fixture():
         ("gcn_noreorder", dict(layer_dims=(16, 32, 2), fanouts=[4, 4]),
          trainer.PipelineFlags(match=False, reorder=False)),
         ("gcn3", dict(layer_dims=(16, 12, 8, 2), fanouts=[3, 3, 2], lr=0.1), trainer.PipelineFlags()),
+        ("gcn_naive", dict(layer_dims=(16, 32, 2), fanouts=[4, 4]), trainer.PipelineFlags(memory_aware=False)),
     ]:
         cfg = trainer.ModelConfig(batch_size=40, window_n=3, epochs=3, seed=0, **{"lr": 0.3, **kw})
         rep = trainer.train(g, feats, labels, cfg, flags)
@@ -304,6 +305,10 @@ def train_fixture():
             "accuracy": [e.accuracy for e in rep.epochs],
             "bytes_h2d": [e.traffic.bytes_host_to_device for e in rep.epochs],
             "bytes_match": [e.traffic.bytes_served_by_match for e in rep.epochs],
+            "bytes_cache": [e.traffic.bytes_served_by_cache for e in rep.epochs],
+            "modeled_io_seconds": [e.traffic.modeled_io_seconds for e in rep.epochs],
+            "modeled_fetch_seconds": [e.modeled_fetch_seconds for e in rep.epochs],
+            "per_batch_epoch0": [vars(b) for b in rep.epochs[0].traffic.per_batch],
         }
     out["two_cluster_digest"] = digest(g.row_offsets, g.col_indices, feats.data, labels)
     return out

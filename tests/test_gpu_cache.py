@@ -34,8 +34,8 @@ def test_cache_window_io_matches_simulate_epoch_io(cfg1_graph, ratio, match):
     deg = np.diff(g.row_offsets.astype(np.int64))
     mask = oracle.cache_mask(g.num_nodes, ratio, deg)
     h2d, mt, ch = oracle.epoch_h2d_bytes([ex], [loads], d, match=match, cached=mask)
-    assert int(pipe.loaded.item()) * 4 * d == h2d
-    assert int(pipe.cache_hits.item()) * 4 * d == ch
+    assert int(pipe.loaded.sum().item()) * 4 * d == h2d
+    assert int(pipe.cache_hits.sum().item()) * 4 * d == ch
     if ratio > 0:
         assert np.array_equal(pipe.cache.mask_numpy(g.num_nodes), mask)
     # the cache only changes where a row comes from, never its value

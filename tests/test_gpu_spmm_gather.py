@@ -1,6 +1,6 @@
 """Short-row SpMM (fgl_spmm_gather, the layer-0 aggregation over the sampled
-block graph: the software-pipelined kernel by default, the TMA gather4
-variant for d > 128 or FGL_GATHER_TMA=1) against the oracle's aggregation
+block graph: the software-pipelined kernel for d <= 128, fgl_spmm above)
+against the oracle's aggregation
 (oracle/minigl_oracle.py aggregate, compute.py:164-185) and against fgl_spmm:
 bit-exact, including empty rows, ragged tails, rows longer than the fast path
 and column offsets (col_base)."""
