@@ -91,3 +91,29 @@ def assert_rel_fro(a, b, tol, what=""):
     r = rel_fro(a, b)
     assert r <= tol, f"{what}: relative Frobenius error {r:.3e} > {tol:g}"
     return r
+
+
+def oracle_backward_masked(dout, caches, csr, params, arch, masks):
+    """oracle.backward (trainer.py:212-228) with the ReLU masks of the hidden
+    layers supplied by the caller (masks[i]: bool [n_local, d_out] of layer
+    i, or None = the oracle's own z > 0).  Feeding the GPU forward's masks
+    separates arithmetic parity from activations that sit within fp32
+    rounding of zero: one such mask flip moves a 10^5-row weight gradient by
+    ~1/sqrt(rows) in relative norm, for any pair of fp32 implementations."""
+    import oracle
+    grads = [None] * len(params)
+    dx = dout
+    last = len(params) - 1
+    for i in range(last, -1, -1):
+        _, h, z = caches[i]
+        if i == last:
+            dz = dx
+        else:
+            m = (z > 0) if masks[i] is None else masks[i]
+            dz = dx * m
+        grads[i] = [h.T @ dz, dz.sum(axis=0)]
+        dh = dz @ params[i][0].T
+        dx = oracle.aggregate(*csr[i][3:6], dh)
+        if arch in ("gin", "sage"):
+            dx = dx + dh
+    return grads
