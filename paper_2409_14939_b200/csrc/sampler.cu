@@ -963,6 +963,226 @@ __global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __g
   }
 }
 
+// ------------------------------------------------------------ select v2 --
+// Same contract as select_bal_kernel (tile of 32 frontier entries per warp,
+// survivors below the node's threshold tau, the min(d, f) smallest (key,
+// slot) pairs emitted in order), with the per-draw overhead cut down:
+//  * each lane draws a CONTIGUOUS run of the tile's Philox blocks, so the
+//    block -> node mapping is one search per lane and the node's parameters
+//    stay in registers while the run stays inside the node;
+//  * the threshold test runs on the raw Philox word (key < tau <=> w <=
+//    (tau << 11) - 1) and a block's survivors take ONE shared atomic;
+//  * survivors are 32-bit words ck << 11 | slot with ck = key >> sh, sh
+//    chosen per node so that ck < 2^21: the selection compares 32-bit words
+//    and the buffers are half the size (more resident warps).  Two survivors
+//    of a node with equal ck but different keys could be ordered by slot
+//    instead of key; the selection checks the selected words and the first
+//    unselected one for equal ck (probability ~1e-5 per node) and sends such
+//    a node to the exact warp path.
+constexpr int kSel2Warps = 4;
+
+struct Sel2Tab {
+  int64_t p0[32], e0[32], obase[32];
+  uint64_t twi[32], k0[32], k1[32];
+  int32_t d[32], dt[32], seg[32], cnt[32], bs[33], u[32], b[32], sh[32];
+};
+
+inline int sel2_buf_words(int fan) {  // u32 words: survivors (32 caps) | queue (32 * fan); >= tau-path scratch
+  const int surv = 32 * bal_cap(fan);
+  return std::max(surv, (kTauCap * 12 + 3) / 4) + 32 * fan;
+}
+inline int sel2_smem(int fan) {
+  return kSel2Warps * (((sel2_buf_words(fan) * 4 + 15) / 16) * 16 + (int)sizeof(Sel2Tab));
+}
+
+__global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const __grid_constant__ SelectArgs a,
+                                                                        int capn, int buf_words) {
+  extern __shared__ __align__(16) uint64_t sbuf2[];
+  const int lane = lane_id(), wib = warp_id();
+  const int wbytes = ((buf_words * 4 + 15) / 16) * 16;
+  char* wbase = reinterpret_cast<char*>(sbuf2) + (int64_t)wib * (wbytes + sizeof(Sel2Tab));
+  uint32_t* sv = reinterpret_cast<uint32_t*>(wbase);
+  Sel2Tab& T = *reinterpret_cast<Sel2Tab*>(wbase + wbytes);
+  const int64_t F = a.scal[kF];
+  const int64_t ebase = a.scal[kHopEdgeBase];
+  const int fan = a.fan;
+  const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
+  uint32_t* bm_base = a.bm_front;
+  const int64_t ntiles = ceil_div(F, 32);
+  const int surv_cap = 32 * capn;  // survivor words; the emission queue follows
+  for (;;) {
+    unsigned long long tix = 0;
+    if (lane == 0) tix = atomicAdd(a.tile_ctr, 1ull);
+    tix = __shfl_sync(0xffffffffu, tix, 0);
+    if ((int64_t)tix >= ntiles) break;
+    const int64_t t0 = (int64_t)tix * 32;
+    int TB;
+    {  // tile setup: node parameters -> the warp's table (registers freed for the draw loop)
+      const int64_t i = t0 + lane;
+      int32_t u = 0, b = 0;
+      int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
+      if (i < F) {
+        u = a.front[i];
+        b = a.fb[i];
+        e0 = __ldg(a.off + u);
+        d = __ldg(a.off + u + 1) - e0;
+        p0 = a.hop_pos[b] + a.scan_deg[i];
+        obase = ebase + a.scan_sel[i];
+      }
+      const bool elig = d > 0 && d <= kBalHub;
+      const int cap = elig ? (int)(d < capn ? d : capn) : 0;
+      const int seg = warp_incl_scan(cap) - cap;
+      const int nblk = elig ? (int)(((p0 + d - 1) >> 2) - (p0 >> 2) + 1) : 0;
+      const int bsum = warp_incl_scan(nblk);
+      TB = __shfl_sync(0xffffffffu, bsum, 31);
+      const uint64_t tau = (double)d <= expect ? kKeyOne
+                                               : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
+      const int sh = max(0, (64 - __clzll((long long)(tau - 1))) - 21);
+      T.p0[lane] = p0; T.e0[lane] = e0; T.obase[lane] = obase;
+      T.twi[lane] = (tau << 11) - 1ull;  // tau = 2^53 wraps to all-ones: every draw survives
+      T.k0[lane] = __ldg(a.keys + 2 * b); T.k1[lane] = __ldg(a.keys + 2 * b + 1);
+      T.d[lane] = (int32_t)(elig ? d : 0); T.dt[lane] = (int32_t)d; T.seg[lane] = seg; T.cnt[lane] = 0;
+      T.bs[lane] = bsum - nblk; T.u[lane] = u; T.b[lane] = b; T.sh[lane] = sh;
+      if (lane == 31) T.bs[32] = TB;
+    }
+    __syncwarp();
+    // ---- Philox over a contiguous run of the tile's blocks per lane
+    {
+      const int per = TB >> 5, rem = TB & 31;
+      int g = lane * per + min(lane, rem);
+      const int gend = g + per + (lane < rem ? 1 : 0);
+      if (g < gend) {
+        int n = bal_find(T.bs, g);
+        int nb_end = T.bs[n + 1];
+        int64_t kb = (T.p0[n] >> 2) - T.bs[n];
+        int32_t s_off = (int32_t)(4 * ((T.p0[n] >> 2) - T.bs[n]) - T.p0[n]);  // slot of word 0 of block g: 4g + s_off
+        int nd = T.d[n], nsh = T.sh[n] + 11, nseg = T.seg[n], ncap = nd < capn ? nd : capn;
+        uint64_t twi = T.twi[n], k0 = T.k0[n], k1 = T.k1[n];
+        for (; g < gend; ++g) {
+          if (g >= nb_end) {  // next node with blocks (zero-block nodes share a start)
+            do { ++n; nb_end = T.bs[n + 1]; } while (g >= nb_end);
+            kb = (T.p0[n] >> 2) - T.bs[n];
+            s_off = (int32_t)(4 * kb - T.p0[n]);
+            nd = T.d[n]; nsh = T.sh[n] + 11; nseg = T.seg[n]; ncap = nd < capn ? nd : capn;
+            twi = T.twi[n]; k0 = T.k0[n]; k1 = T.k1[n];
+          }
+          uint64_t w[4];
+          philox4x64_10((uint64_t)(kb + g) + 1, k0, k1, w[0], w[1], w[2], w[3]);
+          const int s0 = 4 * g + s_off;
+          bool tk[4];
+          int nt = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            tk[q] = (unsigned)(s0 + q) < (unsigned)nd && w[q] <= twi;
+            nt += tk[q] ? 1 : 0;
+          }
+          if (nt) {
+            int c = atomicAdd(&T.cnt[n], nt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (tk[q]) {
+                if (c < ncap) sv[nseg + c] = ((uint32_t)(w[q] >> nsh) << 11) | (uint32_t)(s0 + q);
+                ++c;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const int64_t i = t0 + lane;
+    const int64_t d = T.dt[lane];
+    const bool elig = d > 0 && d <= kBalHub;
+    const int cap = elig ? (int)(d < capn ? d : capn) : 0;
+    const int seg = T.seg[lane];
+    const int want = (int)(d < fan ? d : fan);
+    const int cnt = T.cnt[lane];
+    const bool hub = d > kBalHub && a.hub_list;
+    if (hub) a.hub_list[atomicAdd(a.hub_cnt, 1ull)] = (int32_t)i;
+    bool fb = d > 0 && !hub && (!elig || cnt > cap || cnt < want);
+    uint32_t* q = sv + surv_cap;  // emission queue after the survivors
+    const int nsel = (!fb && !hub && d > 0) ? want : 0;
+    const int qbase = warp_incl_scan(nsel) - nsel;
+    const int nq = __shfl_sync(0xffffffffu, qbase + nsel, 31);
+    if (nsel) {
+      // ---- selection, lane = node: want passes of a minimum search over the
+      // node's 32-bit survivor words, then the tie check
+      const uint32_t* sg = sv + seg;
+      uint32_t prev = 0;
+      bool tie = false;
+      for (int r = 0; r < nsel; ++r) {
+        uint32_t best = 0xffffffffu;
+        for (int jj = 0; jj < cnt; ++jj) {
+          const uint32_t x = sg[jj];
+          if ((r == 0 || x > prev) && x < best) best = x;
+        }
+        tie |= r > 0 && (best >> 11) == (prev >> 11);
+        prev = best;
+        q[qbase + r] = ((uint32_t)lane << 24) | ((uint32_t)r << 11) | (best & 0x7FFu);
+      }
+      if (cnt > nsel) {  // first unselected survivor vs the last selected one
+        uint32_t nxt = 0xffffffffu;
+        for (int jj = 0; jj < cnt; ++jj) {
+          const uint32_t x = sg[jj];
+          if (x > prev && x < nxt) nxt = x;
+        }
+        tie |= (nxt >> 11) == (prev >> 11);
+      }
+      if (tie) {  // equal compressed keys: redo this node exactly
+        fb = true;
+        for (int r = 0; r < nsel; ++r) q[qbase + r] = 0xffffffffu;
+      }
+    }
+    __syncwarp();
+    for (int k0 = 0; k0 < nq; k0 += 128) {
+      uint32_t it[4];
+      int32_t sidx[4];
+      float wv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // four independent gathers in flight per lane
+        const int k = k0 + 32 * r + lane;
+        it[r] = k < nq ? q[k] : 0xffffffffu;
+        if (it[r] != 0xffffffffu) {
+          const int n = (int)(it[r] >> 24);
+          const int64_t ee = T.e0[n] + (int64_t)(it[r] & 0x7FFu);
+          sidx[r] = __ldg(a.col + ee);
+          wv[r] = a.ew ? __ldg(a.ew + ee) : 1.0f;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (it[r] == 0xffffffffu) continue;
+        const int n = (int)(it[r] >> 24);
+        const int64_t o = T.obase[n] + (int64_t)((it[r] >> 11) & 0x1FFFu);
+        a.tgt[o] = T.u[n];
+        a.src[o] = sidx[r];
+        a.wgt[o] = wv[r];
+        if (a.tgt_front) a.tgt_front[o] = (int32_t)(t0 + n);
+        atomicOr(bm_base + (int64_t)T.b[n] * a.words + (sidx[r] >> 5), 1u << (sidx[r] & 31));
+      }
+    }
+    __syncwarp();
+    // ---- exact warp path for overflow / too few survivors / compressed-key ties
+    unsigned big = __ballot_sync(0xffffffffu, fb);
+    uint64_t* wk = reinterpret_cast<uint64_t*>(sv);
+    uint32_t* wsl = reinterpret_cast<uint32_t*>(wk + kTauCap);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int64_t ii = t0 + src;
+      const int32_t uu = T.u[src];
+      const int64_t ee = T.e0[src];
+      const int64_t dd = T.dt[src];
+      const int bb = T.b[src];
+      const int64_t pp = T.p0[src];
+      const int64_t oo = T.obase[src];
+      if (dd <= 2048) tau_select_node<true>(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+      else tau_select_node<false>(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
+    }
+    __syncwarp();
+  }
+}
+
 // Hub nodes (d > kBalHub) of a hop, one CTA each (select_bal_kernel queues
 // them): all 512 threads draw the hub's Philox blocks, survivors below the
 // threshold go to shared memory, and the want smallest (key, slot) pairs are
@@ -1344,8 +1564,27 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       const int bal_grid = bal_grid_of[fan];
       const ProfMark pm = prof_begin(stream);  // bench.py: the two launches are the hop's selection
       static const int seldbg = getenv("FGL_SELDBG") ? 1 : 0;
-      FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
-                                                                                  bal_sv_words(fan), seldbg);
+      static const int selv = getenv("FGL_SELV") ? atoi(getenv("FGL_SELV")) : 2;
+      if (selv == 2) {
+        const int s2 = sel2_smem(fan);
+        static int s2_attr = 0;
+        static int s2_grid_of[kTauMaxFan + 1] = {0};
+        if (s2 > s2_attr) {
+          FGL_CUDA(cudaFuncSetAttribute(select_bal2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+          s2_attr = s2;
+        }
+        if (!s2_grid_of[fan]) {
+          int per_sm = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal2_kernel, kSel2Warps * 32, s2) !=
+                  cudaSuccess || per_sm < 1)
+            per_sm = 2;
+          s2_grid_of[fan] = per_sm * kNumSMs;
+        }
+        FGL_COUNT_LAUNCH(), select_bal2_kernel<<<s2_grid_of[fan], kSel2Warps * 32, s2, stream>>>(
+            a, bal_cap(fan), sel2_buf_words(fan));
+      } else
+        FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
+                                                                                    bal_sv_words(fan), seldbg);
       FGL_COUNT_LAUNCH(), select_hub_kernel<<<4 * kNumSMs, kHubThreads, 0, stream>>>(a);
       prof_end(pm, kProfSelect, h);
     } else if (fan <= kTauMaxFan && !force_stream)

@@ -21,7 +21,7 @@ namespace {
 // latency instead of four: while row i's (<= 8) neighbour rows are being
 // gathered, row i+1's column / weight lists and row i+2's offsets are already
 // in flight.  Accumulation is in CSR order with a rounded multiply then a
-// rounded add (bit-identical to fgl_spmm); rows longer than SP_MAXE take a
+// rounded add (bit-identical to fgl_spmm); rows longer than MAXE take a
 // plain in-order loop.
 __device__ __forceinline__ float4 fmadd4(float4 acc, float w, float4 x) {
   acc.x = __fadd_rn(acc.x, __fmul_rn(w, x.x));
@@ -31,9 +31,11 @@ __device__ __forceinline__ float4 fmadd4(float4 acc, float w, float4 x) {
   return acc;
 }
 
-constexpr int SP_MAXE = 8;
-
-__global__ void __launch_bounds__(256) spmm_pipe_kernel(const int64_t* __restrict__ indptr,
+// MAXE = the rows' edge bound (the hop's fanout, rounded up): the gathered
+// rows live in MAXE float4 registers, so a small bound leaves registers for
+// more resident warps -- more random row reads in flight per SM.
+template <int MAXE, int MINB>
+__global__ void __launch_bounds__(256, MINB) spmm_pipe_kernel(const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ col,
                                                         const float* __restrict__ w, int64_t nrows, int64_t col_base,
                                                         const float* __restrict__ X, int64_t ldx,
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(256) spmm_pipe_kernel(const int64_t* __restric
     const int n = (int)(e - b);
     cl = 0;
     wl = 0.f;
-    if (lane < n && lane < SP_MAXE) {
+    if (lane < n && lane < MAXE) {
       cl = (int32_t)(col[b + lane] - col_base);
       wl = w[b + lane];
     }
@@ -66,9 +68,9 @@ __global__ void __launch_bounds__(256) spmm_pipe_kernel(const int64_t* __restric
   while (r < nrows) {
     const int n = (int)(e0 - b0);
     // stage 1: gather row r's neighbour feature rows
-    float4 x[SP_MAXE];
+    float4 x[MAXE];
 #pragma unroll
-    for (int u = 0; u < SP_MAXE; ++u) {
+    for (int u = 0; u < MAXE; ++u) {
       const int32_t c = __shfl_sync(0xffffffffu, cl0, u);
       x[u] = (u < n && lane < d4) ? __ldg(reinterpret_cast<const float4*>(X + (int64_t)c * ldx) + lane)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -80,9 +82,9 @@ __global__ void __launch_bounds__(256) spmm_pipe_kernel(const int64_t* __restric
     int64_t b2, e2;
     ip_pair(r + 2 * nw, b2, e2);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (n <= SP_MAXE) {
+    if (n <= MAXE) {
 #pragma unroll
-      for (int u = 0; u < SP_MAXE; ++u) {
+      for (int u = 0; u < MAXE; ++u) {
         const float wk = __shfl_sync(0xffffffffu, wl0, u);
         if (u < n) acc = fmadd4(acc, wk, x[u]);
       }
@@ -125,18 +127,23 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
   }
   if (num_rows == 0) return FGL_OK;
   if (d <= 128) {
-    static int per_sm = 0;
-    if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_pipe_kernel, 256, 0) != cudaSuccess ||
-                    per_sm < 1))
-      per_sm = 2;
+    static const int minb = getenv("FGL_PIPE_MINB") ? atoi(getenv("FGL_PIPE_MINB")) : 4;
+    auto kern = max_row_len <= 4 ? (minb >= 5 ? spmm_pipe_kernel<4, 5> : spmm_pipe_kernel<4, 4>)
+              : max_row_len <= 6 ? (minb >= 5 ? spmm_pipe_kernel<6, 5> : spmm_pipe_kernel<6, 4>)
+              : max_row_len <= 8 ? spmm_pipe_kernel<8, 4>
+              : max_row_len <= 12 ? spmm_pipe_kernel<12, 2> : spmm_pipe_kernel<16, 2>;
     // rows per warp: 0 = persistent grid (one wave); > 0 = finite CTAs that
     // retire, so a concurrent high-priority stream gets SM slots sooner
     static const int rpw = getenv("FGL_PIPE_RPW") ? atoi(getenv("FGL_PIPE_RPW")) : 8;
+    int per_sm = 0;
+    if (rpw <= 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess ||
+                     per_sm < 1))
+      per_sm = 2;
     const int64_t cap = rpw > 0 ? ceil_div(num_rows, 8LL * rpw) : (int64_t)kNumSMs * per_sm;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_rows, 8), cap));
     const ProfMark pm = prof_begin((cudaStream_t)stream);
-    FGL_COUNT_LAUNCH(), spmm_pipe_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, col, w, num_rows, col_base, X,
-                                                                                ldx, Y, ldy, (d + 3) / 4);
+    FGL_COUNT_LAUNCH(), kern<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, col, w, num_rows, col_base, X, ldx, Y,
+                                                                    ldy, (d + 3) / 4);
     prof_end(pm, kProfSpmmGather, num_rows, d);
     FGL_LAUNCH_CHECK("spmm_pipe_kernel");
     return FGL_OK;

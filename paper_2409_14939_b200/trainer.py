@@ -300,7 +300,8 @@ class Pipeline:
         self.model = DeviceModel(cfg.layer_dims, params if params is not None else init_params(cfg.layer_dims, cfg.seed), device)
         self.L = cfg.num_layers
         self.H = len(cfg.fanouts)
-        self._max_fan = min(16, max(int(f) for f in cfg.fanouts))
+        # row-length bound of model layer 0 (rows of the last hop hold <= its fanout edges)
+        self._max_fan = min(16, int(cfg.fanouts.counts[-1]))
         self.compact = cfg.arch == "gcn"
         # direct_x0: with the feature table resident in HBM, the layer-0
         # aggregation gathers neighbour rows straight from the table (the x0

@@ -93,27 +93,38 @@ def assert_rel_fro(a, b, tol, what=""):
     return r
 
 
-def oracle_backward_masked(dout, caches, csr, params, arch, masks):
+def oracle_backward_masked(dout, caches, csr, params, arch, masks, fp64=False):
     """oracle.backward (trainer.py:212-228) with the ReLU masks of the hidden
     layers supplied by the caller (masks[i]: bool [n_local, d_out] of layer
     i, or None = the oracle's own z > 0).  Feeding the GPU forward's masks
     separates arithmetic parity from activations that sit within fp32
     rounding of zero: one such mask flip moves a 10^5-row weight gradient by
-    ~1/sqrt(rows) in relative norm, for any pair of fp32 implementations."""
+    ~1/sqrt(rows) in relative norm, for any pair of fp32 implementations.
+    fp64=True evaluates the same backward in float64 (the exact answer the
+    fp32 implementations approximate)."""
     import oracle
     grads = [None] * len(params)
-    dx = dout
+    dt = np.float64 if fp64 else np.float32
+    dx = np.asarray(dout, dtype=dt)
     last = len(params) - 1
     for i in range(last, -1, -1):
         _, h, z = caches[i]
+        h = np.asarray(h, dtype=dt)
         if i == last:
             dz = dx
         else:
             m = (z > 0) if masks[i] is None else masks[i]
             dz = dx * m
         grads[i] = [h.T @ dz, dz.sum(axis=0)]
-        dh = dz @ params[i][0].T
-        dx = oracle.aggregate(*csr[i][3:6], dh)
+        dh = dz @ np.asarray(params[i][0], dtype=dt).T
+        tip, tix, tw = csr[i][3:6]
+        if fp64:
+            import scipy.sparse as sp
+            a_t = sp.csr_matrix((np.asarray(tw, np.float64), np.asarray(tix, np.int64), np.asarray(tip, np.int64)),
+                                shape=(len(tip) - 1, dh.shape[0]))
+            dx = a_t @ dh
+        else:
+            dx = oracle.aggregate(tip, tix, tw, dh)
         if arch in ("gin", "sage"):
             dx = dx + dh
     return grads
