@@ -609,7 +609,7 @@ def stage_profile(pipe, wins, cfg, torch):
             bytes_ = 8 * (rows + n) + E * (4 + 4) + 4 * E * d0 + 4 * rows * d0
             stages["aggregate_l0"] = _roof(
                 "hbm", bytes_ / t / 1e9, hbm_peak, "GB/s", "aggregate_l0",
-                kernel="spmm_pipe_kernel (fgl_spmm_gather)" if agg_id == 2 else "spmm_kernel (fgl_spmm)",
+                kernel="spmm_lean_kernel (fgl_spmm_gather)" if agg_id == 2 else "fgl_spmm (layer-0 rows)",
                 launches=n, ms_per_window=t * 1e3 / nwin, bytes_per_launch=bytes_ / n,
                 model="memsim.py:96 / Eq. 3: 8(n+1) + E(4+4) + 4 E d + 4 n d", peak_source=peak_src,
                 flops_per_launch=2 * E * d0 / n)
@@ -648,6 +648,11 @@ def stage_profile(pipe, wins, cfg, torch):
                              peak_source="measured: pinned host->device cudaMemcpy of 1 GiB on this box")
     per_stage_ms = {k: v["ms_per_window"] for k, v in stages.items()}
     per_stage_ms["window"] = window_ms
+    names = {1: "select", 2: "aggregate_l0 (fgl_spmm_gather)", 3: "fgl_spmm (other aggregations incl. transposed)",
+             4: "dense_fwd", 5: "dgrad", 6: "wgrad", 7: "x0 gather", 8: "top layer", 9: "sgd"}
+    per_stage_ms["kernels"] = {names.get(int(i), str(int(i))): {"ms_per_window": float(ms[ids == i].sum()) / nwin,
+                                                                "launches_per_window": int((ids == i).sum()) / nwin}
+                               for i in np.unique(ids)}
     dom = max(stages, key=lambda k: stages[k]["ms_per_window"]) if stages else None
     head = dict(stages[dom]) if dom else {}
     if head:

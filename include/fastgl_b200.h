@@ -238,13 +238,11 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
              int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
              float* Y, int64_t ldy, int32_t d, void* stream);
 
-/* fgl_spmm for short rows (every row <= max_row_len edges, e.g. the sampled
- * block graph whose rows hold at most `fanout` edges; max_row_len <= 16), with
- * the neighbour feature rows staged in shared memory by TMA gather4 copies
- * (X is [x_rows, ldx] fp32, ldx <= 256).  No self term.  Bit-identical to
- * fgl_spmm (compute.py:115-185); a 16-row block whose edges exceed the
- * staging buffer is read from global memory instead, so a wrong max_row_len
- * costs speed, not correctness. */
+/* The layer-0 aggregation of the trainer: fgl_spmm over the sampled block
+ * graph (rows of <= max_row_len <= 16 edges, the last hop's fanout) gathering
+ * straight from the HBM feature table X [x_rows, ldx], ldx <= 256.  No self
+ * term.  Same kernels and results as fgl_spmm (compute.py:115-185); its own
+ * entry point so the stage profile (fgl_profile id 2) can tell it apart. */
 int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
                     int64_t col_base, const float* X, int64_t ldx, int64_t x_rows, float* Y, int64_t ldy,
                     int32_t d, int32_t max_row_len, void* stream);

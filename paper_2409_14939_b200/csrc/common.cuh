@@ -42,6 +42,8 @@ enum ProfId : int {
   kProfDgrad = 5,       // tc_gemm3 mode 1                          (a0 = M, a1 = N, a2 = K)
   kProfWgrad = 6,       // tc_wgrad3 (+ its partial reduction)      (a0 = M, a1 = K, a2 = N)
   kProfGather = 7,      // x0 row gather (Match / cache / store)    (a0 = rows, a1 = d)
+  kProfTopLayer = 8,    // fused top layer (agg, logits, loss, dH)  (a0 = B, a1 = din, a2 = C)
+  kProfSgd = 9,         // SGD step                                 (a0 = params)
 };
 struct ProfMark {
   cudaEvent_t e0 = nullptr;

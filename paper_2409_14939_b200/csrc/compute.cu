@@ -107,58 +107,76 @@ __global__ void __launch_bounds__(256) spmm_kernel(
   }
 }
 
-// d <= 64 (one float4 per lane, half a warp per row): the row's offsets and
-// each edge's (col, w) are lane-uniform loads (broadcast, no shuffles), the
-// next row's offsets are fetched while the current row gathers, and up to 4
-// neighbour rows are in flight per step.  Same CSR-order arithmetic as
-// spmm_kernel (bit-identical); lean enough for the transposed aggregation's
-// ~1-edge rows, which made spmm_kernel instruction/latency bound.
-__global__ void __launch_bounds__(256) spmm_half_kernel(
-    const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
-    const float* __restrict__ w, int64_t nrows, int64_t col_base, const float* __restrict__ X,
-    int64_t ldx, const float* __restrict__ self_x, int64_t ld_self, float* __restrict__ Y,
-    int64_t ldy, int d4) {
-  const int lane = threadIdx.x & 15;
-  const int64_t hw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;  // half-warp id
-  const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
-  int64_t r = hw;
-  int64_t e0 = 0, e1 = 0;
-  if (r < nrows) { e0 = indptr[r]; e1 = indptr[r + 1]; }
-  while (r < nrows) {
-    const int64_t rn = r + nhw;
-    int64_t f0 = 0, f1 = 0;
-    if (rn < nrows) { f0 = indptr[rn]; f1 = indptr[rn + 1]; }  // next row's offsets, in flight
+// Rows of <= 32 float4 chunks (d <= 128): W threads per row (16 for d <= 64,
+// 32 above), lane = 16-byte chunk; the row's (col, w) pairs are loaded once
+// per W edges and broadcast by shuffles; neighbour rows are gathered G at a
+// time (G loads in flight per lane, then G multiply-adds in CSR order:
+// bit-identical to spmm_kernel).  At most 32 registers, so 64 warps per SM
+// keep their random row reads in flight -- what a bare random-row read needs
+// to approach its ceiling (tools/probes/row_gather_probe.cu: 5.6 TB/s for
+// 400-byte rows at 64 warps / SM, 4.6 TB/s at 32).  Serves the layer-0
+// aggregation (fgl_spmm_gather: rows of <= fanout edges from the HBM feature
+// table), the upper layers and the transposed (~1-edge rows) backward
+// aggregations.
+template <int G, int W>
+__global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ col, const float* __restrict__ w,
+    int64_t nrows, int64_t col_base, const float* __restrict__ X, int64_t ldx, const float* __restrict__ self_x,
+    int64_t ld_self, float* __restrict__ Y, int64_t ldy, int d4) {
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned mask = W == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / W;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / W; r < nrows; r += ng) {
+    int64_t v = 0;
+    if (lane < 2) v = indptr[r + lane];
+    const int64_t b = __shfl_sync(mask, v, 0, W);
+    const int n = (int)(__shfl_sync(mask, v, 1, W) - b);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t e = e0; e < e1; e += 4) {
-      const int n = (int)(e1 - e < 4 ? e1 - e : 4);
-      int32_t c[4];
-      float wk[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        c[u] = u < n ? (int32_t)(__ldg(col + e + u) - col_base) : 0;
-        wk[u] = u < n ? __ldg(w + e + u) : 0.f;
+    for (int u0 = 0; u0 < n; u0 += W) {
+      const int m = n - u0 < W ? n - u0 : W;
+      int32_t cl = 0;
+      float wl = 0.f;
+      if (lane < m) {
+        cl = (int32_t)(col[b + u0 + lane] - col_base);
+        wl = w[b + u0 + lane];
       }
-      float4 x[4];
+      for (int u = 0; u < m; u += G) {
+        float4 x[G];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        x[u] = (u < n && lane < d4) ? __ldg(reinterpret_cast<const float4*>(X + (int64_t)c[u] * ldx) + lane)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < G; ++k) {
+          const int32_t c = __shfl_sync(mask, cl, (u + k) & (W - 1), W);
+          x[k] = (u + k < m && lane < d4) ? __ldg(reinterpret_cast<const float4*>(X + (int64_t)c * ldx) + lane)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (u < n) acc = fmadd4(acc, wk[u], x[u]);
+        for (int k = 0; k < G; ++k) {
+          const float wk = __shfl_sync(mask, wl, (u + k) & (W - 1), W);
+          if (u + k < m) acc = fmadd4(acc, wk, x[k]);
+        }
+      }
     }
     if (lane < d4) {
-      if (self_x) {  // GIN: h = aggregate + x, one rounded add (trainer.py:189-190)
+      if (self_x) {  // GIN / SAGE root term: h = aggregate + x, one rounded add (trainer.py:189-190)
         const float4 sx = reinterpret_cast<const float4*>(self_x + r * ld_self)[lane];
         acc.x = __fadd_rn(acc.x, sx.x); acc.y = __fadd_rn(acc.y, sx.y);
         acc.z = __fadd_rn(acc.z, sx.z); acc.w = __fadd_rn(acc.w, sx.w);
       }
       reinterpret_cast<float4*>(Y + r * ldy)[lane] = acc;
     }
-    r = rn;
-    e0 = f0;
-    e1 = f1;
   }
+}
+
+void launch_spmm_lean(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows, int64_t col_base,
+                      const float* X, int64_t ldx, const float* self_x, int64_t ld_self, float* Y, int64_t ldy,
+                      int d4, cudaStream_t st) {
+  const int per_cta = d4 <= 16 ? 16 : 8;  // rows per 256-thread CTA
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, per_cta), (int64_t)kNumSMs * 8));
+  if (d4 <= 16)
+    FGL_COUNT_LAUNCH(), spmm_lean_kernel<2, 16><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
+                                                                     ld_self, Y, ldy, d4);
+  else
+    FGL_COUNT_LAUNCH(), spmm_lean_kernel<2, 32><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
+                                                                     ld_self, Y, ldy, d4);
 }
 
 template <int L, int CPL>
@@ -660,10 +678,32 @@ using namespace fgl;
 
 extern "C" {
 
+static int spmm_dispatch(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
+                         int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
+                         float* Y, int64_t ldy, int32_t d, cudaStream_t st, int prof_id) {
+  if (num_rows == 0) return FGL_OK;
+  const ProfMark pm = prof_begin(st);
+  const int d4 = (d + 3) / 4;
+  if (d4 <= 1) launch_spmm<1, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 4) launch_spmm<4, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 8) launch_spmm<8, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 32) launch_spmm_lean(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 64) launch_spmm<32, 2>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 128) launch_spmm<32, 4>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 256) launch_spmm<32, 8>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else {
+    set_error("fgl_spmm: feature dim %d above 1024 is not supported", d);
+    return FGL_E_UNSUPPORTED;
+  }
+  prof_end(pm, prof_id, num_rows, d);
+  FGL_LAUNCH_CHECK("spmm_kernel");
+  return FGL_OK;
+}
+
 int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
              int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
              float* Y, int64_t ldy, int32_t d, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
   if (num_rows < 0 || d < 1 || !indptr || !Y || ldy < d || ldx < d || (ldx % 4) || (ldy % 4) ||
       (self_x && (ld_self % 4))) {
     set_error("fgl_spmm: bad arguments (d=%d ldx=%lld ldy=%lld; leading dims must be multiples of 4)",
@@ -675,35 +715,32 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
     set_error("fgl_spmm: feature pointers must be 16-byte aligned");
     return FGL_E_INVALID;
   }
-  if (num_rows == 0) return FGL_OK;
-  const ProfMark pm = prof_begin(st);
-  const int d4 = (d + 3) / 4;
-  if (d4 <= 1) launch_spmm<1, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 4) launch_spmm<4, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 8) launch_spmm<8, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 16) {
-    static const int half = getenv("FGL_SPMM_HALF") ? atoi(getenv("FGL_SPMM_HALF")) : 1;
-    if (half) {
-      static const int bps = getenv("FGL_SPMM_GRID") ? atoi(getenv("FGL_SPMM_GRID")) : 8;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_rows, 16), (int64_t)148 * bps));
-      FGL_COUNT_LAUNCH(), spmm_half_kernel<<<grid, 256, 0, st>>>(indptr, col, w, num_rows, col_base, X, ldx, self_x,
-                                                                  ld_self, Y, ldy, d4);
-    } else {
-      launch_spmm<16, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-    }
+  return spmm_dispatch(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d, (cudaStream_t)stream,
+                       kProfSpmm);
+}
+
+// Layer-0 aggregation over the sampled block graph (rows of <= max_row_len
+// edges gathered straight from the HBM feature table): the same kernels as
+// fgl_spmm, kept as its own entry point (and profiling id) for the stage
+// rooflines; the row bound is validated, not needed by the kernel.
+int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows, int64_t col_base,
+                    const float* X, int64_t ldx, int64_t x_rows, float* Y, int64_t ldy, int32_t d,
+                    int32_t max_row_len, void* stream) {
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) {
+    set_error("fgl_spmm_gather: feature pointers must be 16-byte aligned");
+    return FGL_E_INVALID;
   }
-  else if (d4 <= 32) launch_spmm<32, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 64) launch_spmm<32, 2>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 128) launch_spmm<32, 4>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 256) launch_spmm<32, 8>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else {
-    set_error("fgl_spmm: feature dim %d above 1024 is not supported", d);
+  if (num_rows < 0 || d < 1 || d > 256 || ldx > 256 || !indptr || !Y || !X || ldy < d || ldx < d || (ldx % 4) ||
+      (ldy % 4) || max_row_len < 0 || x_rows < 1) {
+    set_error("fgl_spmm_gather: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if (max_row_len > 16) {
+    set_error("fgl_spmm_gather: rows longer than 16 edges use fgl_spmm");
     return FGL_E_UNSUPPORTED;
   }
-  prof_end(pm, kProfSpmm, num_rows, d);
-  FGL_LAUNCH_CHECK("spmm_kernel");
-  return FGL_OK;
+  return spmm_dispatch(indptr, col, w, num_rows, col_base, X, ldx, nullptr, ldx, Y, ldy, d, (cudaStream_t)stream,
+                       kProfSpmmGather);
 }
 
 int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
@@ -884,9 +921,11 @@ int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_
   const int chunks = (int)ceil_div(B, TOP_ROWS);
   float* part = static_cast<float*>(ws);
   double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
+  const ProfMark pm = prof_begin((cudaStream_t)chain_stream);
   FGL_COUNT_LAUNCH(), top_layer_kernel<<<chunks, 256, 0, (cudaStream_t)chain_stream>>>(
       H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp, agg_indptr, agg_col, agg_w,
       agg_col_base);
+  prof_end(pm, kProfTopLayer, B, din, C);
   FGL_LAUNCH_CHECK("top_layer_kernel");
   if (reduce_stream && reduce_stream != chain_stream) {
     // the reduction is off the chain: the caller orders reduce_stream after
@@ -918,7 +957,9 @@ int fgl_sgd(float* params, const float* grads, int64_t n, float lr, void* stream
     return FGL_E_INVALID;
   }
   if (n == 0) return FGL_OK;
+  const ProfMark pm = prof_begin((cudaStream_t)stream);
   FGL_COUNT_LAUNCH(), sgd_kernel<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
+  prof_end(pm, kProfSgd, n);
   FGL_LAUNCH_CHECK("sgd_kernel");
   return FGL_OK;
 }

@@ -1,5 +1,5 @@
 """Short-row SpMM (fgl_spmm_gather, the layer-0 aggregation over the sampled
-block graph: the software-pipelined kernel for d <= 128, fgl_spmm above)
+block graph: the lean high-occupancy kernel shared with fgl_spmm)
 against the oracle's aggregation
 (oracle/minigl_oracle.py aggregate, compute.py:164-185) and against fgl_spmm:
 bit-exact, including empty rows, ragged tails, rows longer than the fast path
