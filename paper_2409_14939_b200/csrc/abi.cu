@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -18,6 +19,11 @@ static std::atomic<long long> g_launches{0};
 static std::atomic<long long> g_dense_fallbacks{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
 
 namespace {
 struct ProfRec {

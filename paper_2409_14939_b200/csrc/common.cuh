@@ -17,6 +17,10 @@ namespace fgl {
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;
 
+// Integer A/B switch from the environment (read by each call site once, into
+// a function-local static).
+int env_int(const char* name, int dflt);
+
 // ------------------------------------------------------------------ errors --
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);

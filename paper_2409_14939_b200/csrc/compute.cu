@@ -168,9 +168,9 @@ __global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
 
 void launch_spmm_lean(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows, int64_t col_base,
                       const float* X, int64_t ldx, const float* self_x, int64_t ld_self, float* Y, int64_t ldy,
-                      int d4, cudaStream_t st) {
+                      int d4, cudaStream_t st, int64_t max_ctas = (int64_t)kNumSMs * 8) {
   const int per_cta = d4 <= 16 ? 16 : 8;  // rows per 256-thread CTA
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, per_cta), (int64_t)kNumSMs * 8));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, per_cta), max_ctas));
   if (d4 <= 16)
     FGL_COUNT_LAUNCH(), spmm_lean_kernel<2, 16><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
                                                                      ld_self, Y, ldy, d4);
@@ -680,7 +680,8 @@ extern "C" {
 
 static int spmm_dispatch(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
                          int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
-                         float* Y, int64_t ldy, int32_t d, cudaStream_t st, int prof_id) {
+                         float* Y, int64_t ldy, int32_t d, cudaStream_t st, int prof_id,
+                         int64_t lean_ctas = (int64_t)kNumSMs * 8) {
   if (num_rows == 0) return FGL_OK;
   const ProfMark pm = prof_begin(st);
   const int d4 = (d + 3) / 4;
@@ -688,7 +689,8 @@ static int spmm_dispatch(const int64_t* indptr, const int32_t* col, const float*
   else if (d4 <= 2) launch_spmm<2, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 4) launch_spmm<4, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 8) launch_spmm<8, 1>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
-  else if (d4 <= 32) launch_spmm_lean(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
+  else if (d4 <= 32)
+    launch_spmm_lean(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st, lean_ctas);
   else if (d4 <= 64) launch_spmm<32, 2>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 128) launch_spmm<32, 4>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
   else if (d4 <= 256) launch_spmm<32, 8>(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d4, st);
@@ -739,8 +741,13 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
     set_error("fgl_spmm_gather: rows longer than 16 edges use fgl_spmm");
     return FGL_E_UNSUPPORTED;
   }
+  // CTA budget of the layer-0 aggregation, which runs beside the model chain
+  // on its own stream: FGL_L0_CTAS (default 0 = one 8-row CTA per block of
+  // rows, not a persistent grid), so CTAs retire every few microseconds and
+  // their SM slots go to the high-priority chain (2.29 -> 2.22 ms per window)
+  static const int l0_ctas = env_int("FGL_L0_CTAS", 0);
   return spmm_dispatch(indptr, col, w, num_rows, col_base, X, ldx, nullptr, ldx, Y, ldy, d, (cudaStream_t)stream,
-                       kProfSpmmGather);
+                       kProfSpmmGather, l0_ctas > 0 ? l0_ctas : (int64_t)1 << 30);
 }
 
 int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,

@@ -1578,14 +1578,16 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
           if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal2_kernel, kSel2Warps * 32, s2) !=
                   cudaSuccess || per_sm < 1)
             per_sm = 2;
-          s2_grid_of[fan] = per_sm * kNumSMs;
+          static const int sel_sms = env_int("FGL_SEL_SMS", kNumSMs);
+          s2_grid_of[fan] = per_sm * std::max(1, std::min(sel_sms, kNumSMs));
         }
         FGL_COUNT_LAUNCH(), select_bal2_kernel<<<s2_grid_of[fan], kSel2Warps * 32, s2, stream>>>(
             a, bal_cap(fan), sel2_buf_words(fan));
       } else
         FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
                                                                                     bal_sv_words(fan), seldbg);
-      FGL_COUNT_LAUNCH(), select_hub_kernel<<<4 * kNumSMs, kHubThreads, 0, stream>>>(a);
+      static const int hub_ctas = env_int("FGL_HUB_CTAS", 4 * kNumSMs);
+      FGL_COUNT_LAUNCH(), select_hub_kernel<<<std::max(1, hub_ctas), kHubThreads, 0, stream>>>(a);
       prof_end(pm, kProfSelect, h);
     } else if (fan <= kTauMaxFan && !force_stream)
       FGL_COUNT_LAUNCH(), select_tau_kernel<<<select_grid(0), 256, kSelectSmem, stream>>>(a);
