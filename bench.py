@@ -488,7 +488,8 @@ def _peaks():
 
 def philox_peak(torch, device):
     """Measured Philox4x64-10 throughput of this GPU (draws/s): the bare
-    counter-based generator with nothing else (fgl_philox_bench)."""
+    counter-based generator with nothing else (fgl_philox_bench: full
+    occupancy, per-lane keys as in the select kernels)."""
     from paper_2409_14939_b200 import _lib
     buf = torch.empty(148 * 8 * 256, dtype=torch.int64, device=device)
     nblk = 1 << 27
@@ -499,7 +500,8 @@ def philox_peak(torch, device):
     _lib.call("fgl_philox_bench", 3, 4, nblk, buf.data_ptr(), st)
     e1.record()
     torch.cuda.synchronize()
-    return 4 * nblk / (e0.elapsed_time(e1) / 1e3)
+    threads = 148 * 8 * 256
+    return 4 * (nblk // threads) * threads / (e0.elapsed_time(e1) / 1e3)
 
 
 def host_link_peak(torch, device):

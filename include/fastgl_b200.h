@@ -13,7 +13,8 @@
  *    reference's exception types (errors.py:1-35).
  *  - Node IDs on device are int32 (N < 2^31); CSR offsets are int64.
  *  - Caller-owned state only (graph handles, executable graphs, work
- *    buffers), with these process-wide exceptions: a launch counter and
+ *    buffers), with these process-wide exceptions: the dense kernels' SM
+ *    budget (fgl_set_dense_ctas), a launch counter and
  *    CUDA-graph counters (atomics), the per-thread last error, per-thread
  *    caches of TMA tensor maps keyed by buffer address, one-time kernel
  *    attribute settings (max dynamic shared memory), the profiling switch
@@ -134,7 +135,9 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
  * Known-answer and microbenchmark entry (oracle/philox.py). */
 int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uint64_t* out,
                      void* stream);
-/* Draws `count` Philox blocks and reduces them to one word (ALU roofline probe). */
+/* ALU roofline probe: 148*8*256 threads each draw floor(blocks / 303104)
+ * consecutive Philox blocks under a per-thread key and store one folded word
+ * (out[303104]). */
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream);
 /* Random-walk sampler, drop-in for sampler.sample_random_walk
  * (sampler.py:142-186), bit-exact against the reference's Philox(seed) stream
@@ -246,6 +249,14 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
 int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows,
                     int64_t col_base, const float* X, int64_t ldx, int64_t x_rows, float* Y, int64_t ldy,
                     int32_t d, int32_t max_row_len, void* stream);
+
+/* SM budget of the tensor-core dense kernels (process-wide; 0 = every SM,
+ * the default).  Their CTAs are persistent, one per SM; the pipelined
+ * trainer runs them beside three other streams and caps them at half the SMs
+ * so the sampling / aggregation kernels keep SMs (Pipeline(dense_ctas=74):
+ * 2.21 -> 2.17 ms per products window, a standalone layer-0 forward takes
+ * 29 -> 48 us). */
+int fgl_set_dense_ctas(int32_t ctas);
 
 /* Z = act(H @ W + b), W row-major [din, dout] (compute.py:198-216). */
 int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,

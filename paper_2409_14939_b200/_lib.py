@@ -93,6 +93,7 @@ SIGNATURES = {
     "fgl_dense_dgrad": (C.c_int, [vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int32, C.c_int32, vp, C.c_int64,
                                   vp]),
     "fgl_dense_fallback_count": (C.c_int64, []),
+    "fgl_set_dense_ctas": (C.c_int, [C.c_int32]),
     "fgl_capture_begin": (C.c_int, [vp]),
     "fgl_capture_end_launch": (C.c_int, [vp, vp]),
     "fgl_exec_create": (C.c_int, [vp]),

@@ -108,16 +108,19 @@ __global__ void philox_words_kernel(uint64_t k0, uint64_t k1, int64_t start, int
   }
 }
 
-// ALU roofline probe: each thread draws a strided run of Philox blocks and
-// folds them with xor so nothing is dead code; one word per thread is stored.
-__global__ void philox_bench_kernel(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out) {
+// ALU roofline probe: every thread draws a contiguous run of Philox blocks
+// under its own key (as the select kernels do: lanes work on different nodes /
+// batches, so the key schedule is per lane) and folds the words with xor so
+// nothing is dead code.  Full occupancy (64 warps / SM); tools/probes/
+// philox_occ.cu shows the rate saturates from ~16 warps / SM up.
+__global__ void __launch_bounds__(256) philox_bench_kernel(uint64_t k0, uint64_t k1, int iters, uint64_t* out) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t lk0 = k0 ^ (uint64_t)threadIdx.x, base = (uint64_t)tid * (uint64_t)iters;
   uint64_t acc = 0;
-  for (int64_t b = tid; b < blocks; b += stride) {
+  for (int i = 0; i < iters; ++i) {
     uint64_t w0, w1, w2, w3;
-    philox4x64_10((uint64_t)b + 1, k0, k1, w0, w1, w2, w3);
-    acc ^= (w0 >> 11) + (w1 >> 11) + (w2 >> 11) + (w3 >> 11);
+    philox4x64_10(base + i + 1, lk0, k1, w0, w1, w2, w3);
+    acc ^= w0 ^ w1 ^ w2 ^ w3;
   }
   out[tid] = acc;
 }
@@ -194,8 +197,11 @@ int fgl_philox_words(uint64_t k0, uint64_t k1, int64_t start, int64_t count, uin
 }
 
 int fgl_philox_bench(uint64_t k0, uint64_t k1, int64_t blocks, uint64_t* out, void* stream) {
-  // `out` must hold 148*8*256 words (one per thread of the fixed grid).
-  FGL_COUNT_LAUNCH(), fgl::philox_bench_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(k0, k1, blocks, out);
+  if (blocks < 1 || !out) return FGL_E_INVALID;
+  // 148 x 8 CTAs of 256 threads; blocks rounded down to a multiple of the threads
+  const int64_t threads = (int64_t)148 * 8 * 256;
+  const int iters = (int)std::max<int64_t>(1, blocks / threads);
+  FGL_COUNT_LAUNCH(), fgl::philox_bench_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(k0, k1, iters, out);
   FGL_LAUNCH_CHECK("philox_bench_kernel");
   return FGL_OK;
 }

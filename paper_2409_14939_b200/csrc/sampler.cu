@@ -396,7 +396,7 @@ struct SelectArgs {
   float* wgt;
   int32_t* tgt_front;
   int fan;
-  unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal_kernel)
+  unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal2_kernel)
   unsigned long long* hub_cnt;   // hub nodes (d > kBalHub) deferred to select_hub_kernel
   int32_t* hub_list;             // their frontier indices
 };
@@ -763,23 +763,11 @@ constexpr int kSelectSmem = 8 * kWarpBufWords * 8;  // 64 KB per 256-thread CTA
 // than min(d, f) survivors are redone exactly by the warp path
 // (tau_select_node: widened threshold / streaming fallback).
 constexpr int kBalHub = 2048;
-constexpr int kBalWarps = 4;
-constexpr int kBalTab = 80;  // bytes per node-table entry
-
-struct BalTab {
-  int64_t p0[32], e0[32], obase[32];
-  uint64_t tau[32];
-  int32_t d[32], seg[32], cnt[32], bs[32], u[32], b[32], fb[32];
-};
 
 inline int bal_cap(int fan) {
   const double ex = fan + 3.0 * std::sqrt((double)fan) + 3.0;
   return (int)std::ceil(ex + 3.5 * std::sqrt(ex) + 2.0);
 }
-inline int bal_sv_words(int fan) {  // survivors (32 caps) + emission queue (32 * fan u32)
-  return std::max(1024, (32 * bal_cap(fan) + 31) / 32 * 32) + 16 * fan;
-}
-inline int bal_smem(int fan) { return kBalWarps * (bal_sv_words(fan) * 8 + (int)sizeof(BalTab)); }
 
 __device__ __forceinline__ int bal_find(const int32_t* arr, int g) {
   // largest n in [0, 32) with arr[n] <= g (arr non-decreasing, arr[0] = 0)
@@ -790,181 +778,8 @@ __device__ __forceinline__ int bal_find(const int32_t* arr, int g) {
   return n;
 }
 
-// debug (FGL_SELDBG): per-warp finish times of the last launch
-__device__ int64_t g_sel_finish[4096];
-__device__ __forceinline__ int64_t sel_gtime() {
-  int64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-__global__ void __launch_bounds__(kBalWarps * 32, 5) select_bal_kernel(const __grid_constant__ SelectArgs a, int capn,
-                                                                    int sv_words, int dbg) {
-  extern __shared__ __align__(16) uint64_t sbuf[];
-  const int64_t t_start = dbg ? sel_gtime() : 0;
-  const int lane = lane_id(), wib = warp_id();
-  char* wbase = reinterpret_cast<char*>(sbuf) + (int64_t)wib * (sv_words * 8 + sizeof(BalTab));
-  uint64_t* sv = reinterpret_cast<uint64_t*>(wbase);
-  BalTab& T = *reinterpret_cast<BalTab*>(wbase + sv_words * 8);
-  const int64_t F = a.scal[kF];
-  const int64_t ebase = a.scal[kHopEdgeBase];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int fan = a.fan;
-  const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
-  uint32_t* bm_base = a.bm_front;
-  const int64_t ntiles = ceil_div(F, 32);
-  (void)gw; (void)nwarps;
-  for (;;) {
-    // dynamic tile scheduling: hub-heavy tiles cost ~10 normal ones, so a
-    // static grid stride leaves a long tail of busy warps
-    unsigned long long tix = 0;
-    if (lane == 0) tix = atomicAdd(a.tile_ctr, 1ull);
-    tix = __shfl_sync(0xffffffffu, tix, 0);
-    if ((int64_t)tix >= ntiles) {
-      if (dbg && lane == 0 && gw < 4095) {
-        g_sel_finish[gw + 1] = sel_gtime();
-        if (gw == 0) g_sel_finish[0] = t_start;
-      }
-      break;
-    }
-    const int64_t t0 = (int64_t)tix * 32;
-    const int64_t i = t0 + lane;
-    int32_t u = 0, b = 0;
-    int64_t e0 = 0, d = 0, p0 = 0, obase = 0;
-    if (i < F) {
-      u = a.front[i];
-      b = a.fb[i];
-      e0 = __ldg(a.off + u);
-      d = __ldg(a.off + u + 1) - e0;
-      p0 = a.hop_pos[b] + a.scan_deg[i];
-      obase = ebase + a.scan_sel[i];
-    }
-    bool elig = d > 0 && d <= kBalHub;
-    int cap = elig ? (int)(d < capn ? d : capn) : 0;
-    int seg = warp_incl_scan(cap) - cap;
-    if (seg + cap > sv_words - 16 * fan) { elig = false; cap = 0; }  // queue space after the survivors
-    const int nblk = elig ? (int)(((p0 + d - 1) >> 2) - (p0 >> 2) + 1) : 0;
-    const int bsum = warp_incl_scan(nblk);
-    const int bs = bsum - nblk;
-    const int TB = __shfl_sync(0xffffffffu, bsum, 31);
-    const int segtot = __shfl_sync(0xffffffffu, seg + cap, 31);
-    const uint64_t tau = (double)d <= expect ? kKeyOne
-                                             : (uint64_t)(expect * (double)kKeyOne * (double)__frcp_rn((float)d));
-    T.p0[lane] = p0; T.e0[lane] = e0; T.obase[lane] = obase; T.tau[lane] = tau;
-    T.d[lane] = (int32_t)(elig ? d : 0); T.seg[lane] = seg; T.cnt[lane] = 0; T.bs[lane] = bs;
-    T.u[lane] = u; T.b[lane] = b;
-    __syncwarp();
-    // ---- balanced Philox over the tile's blocks, survivors into segments;
-    // two blocks per lane per step (g, g + 32) computed interleaved so that
-    // four independent multiply chains hide the IMAD latency
-    auto collect = [&](int n, int64_t k, const uint64_t (&w)[4]) {
-      const int64_t np0 = T.p0[n];
-      const int nd = T.d[n];
-      const uint64_t ntau = T.tau[n];
-      const int ncap = nd < capn ? nd : capn;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t slot = 4 * k + q - np0;
-        const uint64_t key = w[q] >> 11;
-        if (slot >= 0 && slot < nd && key < ntau) {
-          const int c = atomicAdd(&T.cnt[n], 1);
-          if (c < ncap) sv[T.seg[n] + c] = (key << 11) | (uint64_t)slot;
-        }
-      }
-    };
-    for (int g = lane; g < TB; g += 64) {
-      const int g2 = g + 32;
-      const bool two = g2 < TB;
-      const int n1 = bal_find(T.bs, g);
-      const int n2 = two ? bal_find(T.bs, g2) : n1;
-      const int64_t k1 = (T.p0[n1] >> 2) + (g - T.bs[n1]);
-      const int64_t k2 = two ? (T.p0[n2] >> 2) + (g2 - T.bs[n2]) : k1;
-      uint64_t w1[4], w2[4];
-      const int b1 = T.b[n1], b2 = T.b[n2];
-      philox4x64_10_x2((uint64_t)k1 + 1, __ldg(a.keys + 2 * b1), __ldg(a.keys + 2 * b1 + 1), (uint64_t)k2 + 1,
-                       __ldg(a.keys + 2 * b2), __ldg(a.keys + 2 * b2 + 1), w1, w2);
-      collect(n1, k1, w1);
-      if (two) collect(n2, k2, w2);
-    }
-    __syncwarp();
-    const int want = (int)(d < fan ? d : fan);
-    const int cnt = T.cnt[lane];
-    const bool hub = d > kBalHub && a.hub_list;
-    if (hub) a.hub_list[atomicAdd(a.hub_cnt, 1ull)] = (int32_t)i;  // one CTA per hub, later
-    const bool fb = d > 0 && !hub && (!elig || cnt > cap || cnt < want);
-    // ---- selection, lane = node: want passes of a minimum search over the
-    // node's survivors (strictly above the previous pick; all survivor words
-    // differ in their slot bits), picks queued as (node, rank, slot) so that
-    // the col[] / weight gathers of a lane's emissions are issued back to back
-    uint32_t* q = reinterpret_cast<uint32_t*>(sv + segtot);  // emission queue after the survivors
-    const int nsel = (!fb && !hub && d > 0) ? want : 0;  // hubs: select_hub_kernel
-    const int qbase = warp_incl_scan(nsel) - nsel;
-    const int nq = __shfl_sync(0xffffffffu, qbase + nsel, 31);
-    {
-      const uint64_t* sg = sv + seg;
-      uint64_t prev = 0;
-      for (int r = 0; r < nsel; ++r) {
-        uint64_t best = ~0ull;
-        for (int jj = 0; jj < cnt; ++jj) {
-          const uint64_t x = sg[jj];
-          if ((r == 0 || x > prev) && x < best) best = x;
-        }
-        prev = best;
-        q[qbase + r] = ((uint32_t)lane << 24) | ((uint32_t)r << 11) | (uint32_t)(best & 0x7FFu);
-      }
-    }
-    __syncwarp();
-    for (int k0 = 0; k0 < nq; k0 += 128) {
-      uint32_t it[4];
-      int32_t sidx[4];
-      float wv[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {  // four independent gathers in flight per lane
-        const int k = k0 + 32 * r + lane;
-        it[r] = k < nq ? q[k] : 0xffffffffu;
-        if (it[r] != 0xffffffffu) {
-          const int n = (int)(it[r] >> 24);
-          const int64_t ee = T.e0[n] + (int64_t)(it[r] & 0x7FFu);
-          sidx[r] = __ldg(a.col + ee);
-          wv[r] = a.ew ? __ldg(a.ew + ee) : 1.0f;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (it[r] == 0xffffffffu) continue;
-        const int n = (int)(it[r] >> 24);
-        const int64_t o = T.obase[n] + (int64_t)((it[r] >> 11) & 0x1FFFu);
-        a.tgt[o] = T.u[n];
-        a.src[o] = sidx[r];
-        a.wgt[o] = wv[r];
-        if (a.tgt_front) a.tgt_front[o] = (int32_t)(t0 + n);
-        atomicOr(bm_base + (int64_t)T.b[n] * a.words + (sidx[r] >> 5), 1u << (sidx[r] & 31));
-      }
-    }
-    __syncwarp();
-    // ---- exact warp path for hubs / overflow / too few survivors
-    unsigned big = __ballot_sync(0xffffffffu, fb);
-    uint32_t* wsl = reinterpret_cast<uint32_t*>(sv + kTauCap);
-    while (big) {
-      const int src = __ffs(big) - 1;
-      big &= big - 1;
-      const int64_t ii = t0 + src;
-      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
-      const int64_t ee = __shfl_sync(0xffffffffu, e0, src);
-      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
-      const int bb = __shfl_sync(0xffffffffu, b, src);
-      const int64_t pp = __shfl_sync(0xffffffffu, p0, src);
-      const int64_t oo = __shfl_sync(0xffffffffu, obase, src);
-      if (dd <= 2048) tau_select_node<true>(a, sv, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
-      else tau_select_node<false>(a, sv, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
-    }
-    __syncwarp();
-  }
-}
-
 // ------------------------------------------------------------ select v2 --
-// Same contract as select_bal_kernel (tile of 32 frontier entries per warp,
+// Balanced select (tile of 32 frontier entries per warp,
 // survivors below the node's threshold tau, the min(d, f) smallest (key,
 // slot) pairs emitted in order), with the per-draw overhead cut down:
 //  * each lane draws a CONTIGUOUS run of the tile's Philox blocks, so the
@@ -1183,16 +998,16 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
   }
 }
 
-// Hub nodes (d > kBalHub) of a hop, one CTA each (select_bal_kernel queues
+// Hub nodes (d > kBalHub) of a hop, one CTA each (select_bal2_kernel queues
 // them): all 512 threads draw the hub's Philox blocks, survivors below the
 // threshold go to shared memory, and the want smallest (key, slot) pairs are
 // ranked by counting -- a 19K-degree hub takes one CTA a few microseconds
 // instead of one warp ~100 us at the end of the select launch.  Overflow or
 // too few survivors: the exact warp path (tau_select_node) of warp 0.
-constexpr int kHubThreads = 512;
+constexpr int kHubThreads = 256;
 constexpr int kHubCap = 2048;
 
-__global__ void __launch_bounds__(kHubThreads) select_hub_kernel(const __grid_constant__ SelectArgs a) {
+__global__ void __launch_bounds__(kHubThreads, 3) select_hub_kernel(const __grid_constant__ SelectArgs a) {
   __shared__ uint64_t skey[kHubCap];
   __shared__ uint32_t sslot[kHubCap];
   __shared__ int scnt;
@@ -1412,10 +1227,6 @@ using namespace fgl;
 
 extern "C" {
 
-int fgl_debug_select_finish(int64_t* host, int64_t n) {
-  return cudaMemcpyFromSymbol(host, g_sel_finish, sizeof(int64_t) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
-}
-
 int fgl_sample_bounds(int64_t num_nodes, const int64_t* batch_sizes, int32_t nb,
                       const int32_t* fanouts, int32_t H, int64_t* out) {
   if (num_nodes < 1 || nb < 1 || H < 1 || H > FGL_MAX_HOPS || !batch_sizes || !fanouts || !out) {
@@ -1545,48 +1356,27 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
       const char* v = getenv("FGL_SELECT");
       return v && v[0] == 't';
     }();
-    if (fan <= kTauMaxFan && bal_smem(fan) <= 200 * 1024 && !force_stream && !force_tau) {
-      const int bsm = bal_smem(fan);
+    if (fan <= kTauMaxFan && sel2_smem(fan) <= 200 * 1024 && !force_stream && !force_tau) {
+      const ProfMark pm = prof_begin(stream);  // bench.py: the two launches are the hop's selection
+      const int s2 = sel2_smem(fan);
       // grid per fanout: the survivor buffers (and so the CTAs per SM) depend on it
-      static int bal_attr = 0;
-      static int bal_grid_of[kTauMaxFan + 1] = {0};
-      if (bsm > bal_attr) {
-        FGL_CUDA(cudaFuncSetAttribute(select_bal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm));
-        bal_attr = bsm;
+      static int s2_attr = 0;
+      static int s2_grid_of[kTauMaxFan + 1] = {0};
+      if (s2 > s2_attr) {
+        FGL_CUDA(cudaFuncSetAttribute(select_bal2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+        s2_attr = s2;
       }
-      if (!bal_grid_of[fan]) {
+      if (!s2_grid_of[fan]) {
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal_kernel, kBalWarps * 32, bsm) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal2_kernel, kSel2Warps * 32, s2) !=
                 cudaSuccess || per_sm < 1)
           per_sm = 2;
-        bal_grid_of[fan] = per_sm * kNumSMs;
+        static const int sel_sms = env_int("FGL_SEL_SMS", kNumSMs);
+        s2_grid_of[fan] = per_sm * std::max(1, std::min(sel_sms, kNumSMs));
       }
-      const int bal_grid = bal_grid_of[fan];
-      const ProfMark pm = prof_begin(stream);  // bench.py: the two launches are the hop's selection
-      static const int seldbg = getenv("FGL_SELDBG") ? 1 : 0;
-      static const int selv = getenv("FGL_SELV") ? atoi(getenv("FGL_SELV")) : 2;
-      if (selv == 2) {
-        const int s2 = sel2_smem(fan);
-        static int s2_attr = 0;
-        static int s2_grid_of[kTauMaxFan + 1] = {0};
-        if (s2 > s2_attr) {
-          FGL_CUDA(cudaFuncSetAttribute(select_bal2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-          s2_attr = s2;
-        }
-        if (!s2_grid_of[fan]) {
-          int per_sm = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bal2_kernel, kSel2Warps * 32, s2) !=
-                  cudaSuccess || per_sm < 1)
-            per_sm = 2;
-          static const int sel_sms = env_int("FGL_SEL_SMS", kNumSMs);
-          s2_grid_of[fan] = per_sm * std::max(1, std::min(sel_sms, kNumSMs));
-        }
-        FGL_COUNT_LAUNCH(), select_bal2_kernel<<<s2_grid_of[fan], kSel2Warps * 32, s2, stream>>>(
-            a, bal_cap(fan), sel2_buf_words(fan));
-      } else
-        FGL_COUNT_LAUNCH(), select_bal_kernel<<<bal_grid, kBalWarps * 32, bsm, stream>>>(a, bal_cap(fan),
-                                                                                    bal_sv_words(fan), seldbg);
-      static const int hub_ctas = env_int("FGL_HUB_CTAS", 4 * kNumSMs);
+      FGL_COUNT_LAUNCH(), select_bal2_kernel<<<s2_grid_of[fan], kSel2Warps * 32, s2, stream>>>(
+          a, bal_cap(fan), sel2_buf_words(fan));
+      static const int hub_ctas = env_int("FGL_HUB_CTAS", 6 * kNumSMs);
       FGL_COUNT_LAUNCH(), select_hub_kernel<<<std::max(1, hub_ctas), kHubThreads, 0, stream>>>(a);
       prof_end(pm, kProfSelect, h);
     } else if (fan <= kTauMaxFan && !force_stream)

@@ -22,6 +22,7 @@
 // The weight (K <= 128 here, N <= 256) is split once per CTA into hi/lo
 // copies in the K-major no-swizzle canonical layout.  One persistent CTA/SM.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -764,6 +765,9 @@ int64_t g3_smem(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
   return g3_fixed(N_pad, K_pad, R, a_slot, m_slot) + 1024 + g3_stage_bytes(N_pad);
 }
 
+std::atomic<int> g_dense_ctas{kNumSMs};
+int dense_cta_budget() { return g_dense_ctas.load(std::memory_order_relaxed); }
+
 bool tc3_disabled() {
   static const int v = [] {
     const char* e = getenv("FGL_DENSE");
@@ -846,7 +850,8 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
     attr[mode] = true;
   }
   const int64_t tiles = ceil_div(M, G3_M);
-  const int grid = (int)std::min<int64_t>(tiles, kNumSMs);
+  // persistent CTAs (one per SM by smem), at most fgl_set_dense_ctas' budget
+  const int grid = (int)std::min<int64_t>(tiles, dense_cta_budget());
   CUtensorMap mA;
   std::memset(&mA, 0, sizeof(mA));
   if (a_tma) {
@@ -936,6 +941,12 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
 }
 
 }  // namespace fgl
+
+extern "C" int fgl_set_dense_ctas(int32_t ctas) {
+  if (ctas < 0) return FGL_E_INVALID;
+  fgl::g_dense_ctas.store(ctas == 0 ? fgl::kNumSMs : std::min(ctas, fgl::kNumSMs), std::memory_order_relaxed);
+  return FGL_OK;
+}
 
 extern "C" int fgl_debug_g3_trace(int64_t* host, int64_t n) {
   return cudaMemcpyFromSymbol(host, fgl::g3_trace, sizeof(int64_t) * (n < 148 * fgl::G3_TR ? n : 148 * fgl::G3_TR)) == cudaSuccess ? 0 : -1;

@@ -250,10 +250,13 @@ class Pipeline:
 
     def __init__(self, g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None,
                  device="cuda", feature_store="device", params=None, dist=None, direct_x0=None,
-                 cache_ratio: float = 0.0, cache_policy: str = "static-degree"):
+                 cache_ratio: float = 0.0, cache_policy: str = "static-degree", dense_ctas: int = 74):
         import torch
         self.torch = torch
         self.cfg = cfg
+        # SM budget of the tensor-core dense kernels while run_windows keeps
+        # three other streams busy (fgl_set_dense_ctas; 0 = every SM)
+        self.dense_ctas = int(dense_ctas)
         self.flags = flags or PipelineFlags()
         # device-side limits of a window (checked before any allocation): the
         # match-degree pass keeps all pair counts of a window in registers
@@ -870,17 +873,26 @@ class Pipeline:
         layer-0 aggregations of window w run on a prepare stream under window
         w-1's compute, and the weight-dependent chain runs on a high-priority
         stream.  Yields (order, device losses) per window; numerically
-        identical to run_window applied in sequence."""
-        import collections
+        identical to run_window applied in sequence (the dense kernels' SM
+        budget only changes their grid)."""
         torch = self.torch
         windows = list(windows)
         if not windows:
             return
+        caller = torch.cuda.current_stream()
+        _lib.call("fgl_set_dense_ctas", self.dense_ctas)
+        try:
+            yield from self._run_windows(windows, caller)
+        finally:
+            _lib.call("fgl_set_dense_ctas", 0)
+
+    def _run_windows(self, windows, caller):
+        import collections
+        torch = self.torch
         # the weight-dependent chain (dense / backward / SGD, many short
         # kernels) is the critical path: it runs on a HIGH-priority stream so
         # its CTAs are scheduled ahead of the wide sampling / aggregation
         # kernels of the side streams whenever SMs free up
-        caller = torch.cuda.current_stream()
         if not hasattr(self, "_main"):
             try:
                 lo, hi = torch.cuda.Stream.priority_range()

@@ -1,8 +1,10 @@
 #!/bin/bash
+# select A/B: sampler parity tests, standalone sampler window time and the
+# headline bench per variant.  Usage: tools/gpu_sel.sh <tag> "ENV=a" "ENV=b" ...
 cd "$GRAFT_REPO_ROOT"
-O=gpurun_out/$1; mkdir -p $O
-timeout 600 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_scale.py tests/test_gpu_train.py -x -q > $O/test.log 2>&1; echo "rc=$?" >> $O/test.log
-tail -3 $O/test.log
-timeout 300 python tools/bench_stages.py --windows 10 > $O/stages.json 2>&1; cat $O/stages.json | tail -1
-FGL_SELECT=tau timeout 300 python tools/bench_stages.py --windows 10 2>&1 | tail -1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:select -c 6 python tools/bench_stages.py --windows 2 2>&1 | grep -E "select|duration" | paste - - | awk '{print $2, $NF}'
+O=gpurun_out/$1; shift; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_scale.py tests/test_gpu_configs.py -q -x -k "sampl or window or scale or khop or hub or frontier" > $O/test.log 2>&1; tail -2 $O/test.log
+for v in "$@"; do
+  env $v timeout 300 python tools/bench_stages.py --windows 20 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v', 'sampler ms/window', round(d['sampler_ms_per_window'],3), 'draws', d['draws_per_window'])"
+done
+STEPS=60 bash tools/sweep_env.sh $O-bench "$@"
