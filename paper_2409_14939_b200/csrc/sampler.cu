@@ -36,6 +36,9 @@ namespace fgl {
 namespace {
 
 constexpr int kScanThreads = 256;
+// CTAs of the sampler's scan / compaction / degree passes (4 per SM: their
+// phases are latency bound, so more resident warps, not fewer, set the pace)
+constexpr int kSampCTAs = 4 * kNumSMs;
 constexpr int kMaxFanout = 256;
 
 struct SampleWs {
@@ -46,7 +49,7 @@ struct SampleWs {
   int32_t* fb;         // [fcap] batch of each frontier entry
   int64_t* scan_deg;   // [fcap]
   int64_t* scan_sel;   // [fcap]
-  int64_t* part;       // [2*kPersistentCTAs + 2]
+  int64_t* part;       // [2*kSampCTAs + 2]
   int64_t* pos;        // [nb]   running Philox position per batch
   int64_t* hop_pos;    // [nb]   position at the start of the current hop
   int64_t* scal;       // [8]
@@ -77,7 +80,7 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_fb = take(4 * L.fcap);
   L.off_sdeg = take(8 * L.fcap);
   L.off_ssel = take(8 * L.fcap);
-  L.off_part = take(8 * (2 * kPersistentCTAs + 2));
+  L.off_part = take(8 * (2 * kSampCTAs + 2));
   L.off_pos = take(8 * nb);
   L.off_hoppos = take(8 * nb);
   L.off_scal = take(8 * 8);
@@ -825,10 +828,12 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
   uint32_t* bm_base = a.bm_front;
   const int64_t ntiles = ceil_div(F, 32);
   const int surv_cap = 32 * capn;  // survivor words; the emission queue follows
-  for (;;) {
-    unsigned long long tix = 0;
-    if (lane == 0) tix = atomicAdd(a.tile_ctr, 1ull);
-    tix = __shfl_sync(0xffffffffu, tix, 0);
+  // first tile = the warp's global index (no atomic: with small frontiers
+  // thousands of warps would otherwise serialise on the counter just to find
+  // no work), later tiles from the dynamic counter past the static ones
+  const int64_t nwarps = (int64_t)gridDim.x * kSel2Warps;
+  unsigned long long tix = (unsigned long long)(blockIdx.x * (int64_t)kSel2Warps + wib);
+  for (;; ) {
     if ((int64_t)tix >= ntiles) break;
     const int64_t t0 = (int64_t)tix * 32;
     int TB;
@@ -995,6 +1000,10 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
       else tau_select_node<false>(a, wk, wsl, ii, uu, ee, dd, bb, pp, oo, expect);
     }
     __syncwarp();
+    if (nwarps >= ntiles) break;  // every tile was handed out statically
+    unsigned long long nx = 0;
+    if (lane == 0) nx = atomicAdd(a.tile_ctr, 1ull);
+    tix = (unsigned long long)nwarps + __shfl_sync(0xffffffffu, nx, 0);
   }
 }
 
@@ -1084,12 +1093,12 @@ __global__ void posmap_kernel(const int32_t* __restrict__ front, const int64_t* 
                               int32_t nb, const uint32_t* __restrict__ bm_all,
                               const int32_t* __restrict__ wprefix, int64_t words,
                               int32_t* __restrict__ posmap) {
-  const int64_t F = fo[nb];
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < F;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int b = find_segment(fo, nb, j);
+  // batch = blockIdx.y: the segment is known, no per-entry search
+  const int b = blockIdx.y;
+  const int64_t j1 = fo[b + 1];
+  for (int64_t j = fo[b] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < j1;
+       j += (int64_t)gridDim.x * blockDim.x)
     posmap[bm_rank(bm_all, wprefix, (int64_t)b * words, 0, front[j])] = (int32_t)j;
-  }
 }
 
 // window rows of hop h's edges (+ frontier index of the source in hop h+1's
@@ -1100,11 +1109,11 @@ __global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t*
                                  const int32_t* __restrict__ wprefix, int64_t words,
                                  const int32_t* __restrict__ posmap, int32_t* __restrict__ lt,
                                  int32_t* __restrict__ ls, int32_t* __restrict__ sf) {
-  const int64_t e0 = eoff[0], e1 = eoff[nb];
-  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
+  // batch = blockIdx.y (edges are hop-major / batch-minor): no per-edge search
+  const int b = blockIdx.y;
+  const int64_t e1 = eoff[b + 1], bw = (int64_t)b * words;
+  for (int64_t e = eoff[b] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int b = find_segment(eoff, nb, e);
-    const int64_t bw = (int64_t)b * words;
     const int32_t rs = bm_rank(bm_all, wprefix, bw, 0, src[e]);
     if (lt) lt[e] = bm_rank(bm_all, wprefix, bw, 0, tgt[e]);
     if (ls) ls[e] = rs;
@@ -1302,7 +1311,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   const int64_t words = Lw.words;
   const int64_t nwords = words * nb;
   const int64_t fcap = o->frontier_stride;
-  const int G = kPersistentCTAs;
+  const int G = kSampCTAs;
   int64_t* counts = o->counts;
   int64_t* status = counts + FGL_CNT_STATUS(H, nb);
   int64_t* uniq_off = counts + FGL_CNT_UNIQ(H, nb);
@@ -1400,12 +1409,13 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
 
   // translation: window rows, and frontier indices through per-hop position maps
   const bool want_rows = o->tgt_row || o->src_row || o->src_front;
-  const int TG = 4 * G;
+  const int TG = 4 * kPersistentCTAs;
+  const int TGb = std::max(1, TG / nb);  // CTAs per batch of the 2-D (x, batch) translation grids
   for (int h = 0; h <= H; ++h) {
     const bool has_list = h < H && (o->src_front || (h == 0 && o->seed_front));
     if (has_list) {
-      FGL_COUNT_LAUNCH(), posmap_kernel<<<TG, 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb, w.bm_all,
-                                            w.wprefix, words, w.posmap);
+      FGL_COUNT_LAUNCH(), posmap_kernel<<<dim3(TGb, nb), 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb,
+                                                                       w.bm_all, w.wprefix, words, w.posmap);
     }
     if (h == 0 && (o->seed_rows || o->seed_front)) {
       FGL_COUNT_LAUNCH(), translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), TG), 256, 0,
@@ -1413,9 +1423,9 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
                                          words, w.posmap, o->seed_rows, o->seed_front);
     }
     if (h >= 1 && want_rows) {  // hop h-1 sources live in hop h's frontier
-      FGL_COUNT_LAUNCH(), translate_kernel<<<TG, 256, 0, stream>>>(o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all,
-                                               w.wprefix, words, h < H ? w.posmap : nullptr,
-                                               o->tgt_row, o->src_row, o->src_front);
+      FGL_COUNT_LAUNCH(), translate_kernel<<<dim3(TGb, nb), 256, 0, stream>>>(
+          o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all, w.wprefix, words, h < H ? w.posmap : nullptr,
+          o->tgt_row, o->src_row, o->src_front);
     }
     FGL_LAUNCH_CHECK("translate");
   }

@@ -7,4 +7,4 @@ timeout 900 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_scale.py t
 for v in "$@"; do
   env $v timeout 300 python tools/bench_stages.py --windows 20 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v', 'sampler ms/window', round(d['sampler_ms_per_window'],3), 'draws', d['draws_per_window'])"
 done
-STEPS=60 bash tools/sweep_env.sh $O-bench "$@"
+STEPS=60 bash tools/sweep_env.sh $(basename $O)-bench "$@"
