@@ -189,7 +189,9 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 constexpr int kPersistentCTAs = 2 * kNumSMs;
 
 // tcgen05 3xTF32 GEMM (tc_gemm3.cu).  mode 0: C = act(A W + bias), W [K, N];
-// mode 1: C = (A * (mask > 0)) W^T, W [N, K].  Returns false if the shape is
+// mode 1: C = (A * (mask > 0)) W^T, W [N, K].  ldw = W's row stride (default
+// the row length: N in mode 0, K in mode 1), so callers can pass column / K
+// slices of a wider W; accum adds into C (K slices).  Returns false if the shape is
 // outside the kernel's envelope (the caller then runs the SIMT kernel and
 // counts it with count_dense_fallback); *err receives an FGL status otherwise.
 bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
@@ -197,7 +199,7 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
              cudaStream_t st, int* err);
 bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
-              cudaStream_t st, int* err, int accum = 0);
+              cudaStream_t st, int* err, int accum = 0, int64_t ldw = -1);
 // tcgen05 3xTF32 weight gradient partials: part[c][K+1][N] (row K = db).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
                int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);

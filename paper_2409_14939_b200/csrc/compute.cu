@@ -350,8 +350,12 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(
 // kp1 == 0: partial element i is output i (dW row-major, then db); kp1 = K+1:
 // partials are stored feature-major ([N][K+1], coalesced tensor-core
 // epilogue), element j = n*(K+1) + k is output k*N + n (k == K: db[n]).
+// kp1 > 0 (tensor-core partials, feature-major [N][kp1]): element (nn, k) ->
+// out[k * ldo + col0 + nn] for k < kp1 - 1 (dW rows), out2[col0 + nn] for the
+// last (db).  kp1 == 0 (SIMT partials): element i -> out[i] / out2[i - split].
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int chunks, int64_t n,
-                                       float* __restrict__ out, int64_t split, float* __restrict__ out2, int kp1) {
+                                       float* __restrict__ out, int64_t split, float* __restrict__ out2, int kp1,
+                                       int64_t ldo = 0, int64_t col0 = 0) {
   __shared__ float sm[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t i = blockIdx.x * 32 + lane;
@@ -372,12 +376,13 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int chunk
     float t = sm[0][lane];
 #pragma unroll
     for (int g = 1; g < 8; ++g) t = __fadd_rn(t, sm[g][lane]);
-    int64_t o = i;
     if (kp1 > 0) {
       const int64_t nn = i / kp1, k = i - nn * kp1;
-      o = k * (n / kp1) + nn;
+      if (k < kp1 - 1) out[k * ldo + col0 + nn] = t;
+      else out2[col0 + nn] = t;
+    } else {
+      if (i < split) out[i] = t; else out2[i - split] = t;
     }
-    if (o < split) out[o] = t; else out2[o - split] = t;
   }
 }
 
@@ -750,6 +755,33 @@ int fgl_spmm_gather(const int64_t* indptr, const int32_t* col, const float* w, i
                        kProfSpmmGather, l0_ctas > 0 ? l0_ctas : (int64_t)1 << 30);
 }
 
+// dH = (dX * (Xout > 0)) W^T on the tensor cores, the reduction (dout) in K
+// slices of <= 128 accumulated into dH (wide outputs: papers' 172 classes)
+static bool dgrad_tc(const float* dX, int64_t lddx, const float* Xout, int64_t ldxo, int64_t n, const float* W,
+                     int32_t din, int32_t dout, float* dH, int64_t lddh, cudaStream_t st, int* err) {
+  if ((lddx % 4) || (Xout && (ldxo % 4)) || (lddh % 4) || (reinterpret_cast<uintptr_t>(dH) & 15)) return false;
+  // [column slice of dH (rows of W)] x [K slice of dout]: the widest slices
+  // whose first tile fits shared memory; K slices accumulate into dH
+  for (int nsw = 256; nsw >= 64; nsw /= 2) {
+    for (int ksw = 128; ksw >= 32; ksw /= 2) {
+      bool ok = true, first = true;
+      for (int n0 = 0; n0 < din && ok; n0 += nsw) {
+        const int ns = din - n0 < nsw ? din - n0 : nsw;
+        for (int k0 = 0; k0 < dout && ok; k0 += ksw) {
+          const int ks = dout - k0 < ksw ? dout - k0 : ksw;
+          ok = tc_gemm3(1, dX + k0, lddx, Xout ? Xout + k0 : nullptr, ldxo, W + (int64_t)n0 * dout + k0, nullptr,
+                        dH + n0, lddh, n, ns, ks, 0, st, err, k0 > 0, dout);
+          if (*err) return true;
+          if (!ok && !first) return false;  // a later slice fell outside: the caller recomputes dH whole
+          first = false;
+        }
+      }
+      if (ok) return true;
+    }
+  }
+  return false;
+}
+
 int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const float* W,
                   const float* b, int32_t dout, float* Z, int64_t ldz, int32_t relu, void* stream) {
   if (n < 0 || din < 1 || dout < 1 || !W || !Z || ldh < din || ldz < dout) {
@@ -758,22 +790,36 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
   }
   if (n == 0) return FGL_OK;
   int err = 0;
-  if (din > 128 && dout <= 256 && !(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15)) {
-    // wide inputs (Reddit: 602): K slices of 128 on the tensor cores, each
-    // adding into Z (bias / ReLU with the last slice); fp32 sums of slices
-    bool ok = true;
-    for (int k0 = 0; k0 < din && ok; k0 += 128) {
-      const int ks = din - k0 < 128 ? din - k0 : 128;
-      const bool last = k0 + ks >= din;
-      ok = tc_gemm3(0, H + k0, ldh, nullptr, 0, W + (int64_t)k0 * dout, last ? b : nullptr, Z, ldz, n, dout, ks,
-                    last ? relu : 0, (cudaStream_t)stream, &err, k0 > 0);
-      if (err) return err;
+  if (!(ldh % 4) && !(ldz % 4) && !(reinterpret_cast<uintptr_t>(H) & 15) && !(reinterpret_cast<uintptr_t>(Z) & 15)) {
+    // the tensor-core kernel on [column slice of Z] x [K slice of W] tiles
+    // (one tile for the usual <= 128 x 128 layers; wide inputs -- Reddit 602
+    // -- and wide outputs -- papers' 172 classes -- in slices), each K slice
+    // adding into Z (bias / ReLU with the last); fp32 sums.  Slice widths: the
+    // largest whose first (widest) tile fits the kernel's shared memory (the
+    // weight's hi / lo images grow with K x N)
+    bool ok = false;
+    for (int ksw = 128; ksw >= 64 && !ok; ksw /= 2) {
+      for (int nsw = 128; nsw >= 32 && !ok; nsw /= 2) {
+        ok = true;
+        bool first = true;
+        for (int n0 = 0; n0 < dout && ok; n0 += nsw) {
+          const int ns = dout - n0 < nsw ? dout - n0 : nsw;
+          for (int k0 = 0; k0 < din && ok; k0 += ksw) {
+            const int ks = din - k0 < ksw ? din - k0 : ksw;
+            const bool last = k0 + ks >= din;
+            ok = tc_gemm3(0, H + k0, ldh, nullptr, 0, W + (int64_t)k0 * dout + n0, last && b ? b + n0 : nullptr,
+                          Z + n0, ldz, n, ns, ks, last ? relu : 0, (cudaStream_t)stream, &err, k0 > 0, dout);
+            if (err) return err;
+            if (!ok && !first) goto simt;  // a later slice fell outside: recompute Z whole below
+            first = false;
+          }
+        }
+      }
     }
     if (ok) return FGL_OK;
+  simt:;
     // a slice fell outside the envelope: the SIMT kernel below recomputes Z whole
   }
-  if (tc_gemm(0, H, ldh, nullptr, 0, W, b, Z, ldz, n, dout, din, relu, (cudaStream_t)stream, &err))
-    return err;
   count_dense_fallback();
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));
   FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(H, ldh, W, dout, 0, b, Z, ldz, n, dout, din,
@@ -813,48 +859,54 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     // from the concurrent chain); the large layer 0 still spans all SMs
     static const int tpc = getenv("FGL_WG_TPC") ? std::max(1, atoi(getenv("FGL_WG_TPC"))) : 16;
     const int tc3_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(ceil_div(n, 64), tpc)));
-    int used_chunks = chunks, kp1 = 0;
     const ProfMark pm = prof_begin(st);
-    bool split_done = false;
-    if (din + 1 > 128 && !(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15)) {
-      // wide inputs: feature slices of 124 rows of dW on the tensor cores; each
-      // slice's partials are reduced straight into its rows of dW (db from the
-      // first slice, the others' db rows land in scratch)
-      float* scratch_db = pw + (int64_t)tc3_chunks * 125 * dout;
-      float* slice_part = scratch_db + dout;
-      bool ok = true;
-      for (int k0 = 0; k0 < din && ok; k0 += 124) {
-        const int ks = din - k0 < 124 ? din - k0 : 124;
-        ok = tc_wgrad3(H + k0, ldh, dX, lddx, Xout, ldxo, n, ks, dout, slice_part, tc3_chunks, st, &werr);
-        if (werr) return werr;
-        if (ok) {
-          const int64_t o = (int64_t)(ks + 1) * dout;
-          FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(o, 32), 256, 0, st>>>(
-              slice_part, tc3_chunks, o, dW + (int64_t)k0 * dout, (int64_t)ks * dout, k0 == 0 ? db : scratch_db,
-              ks + 1);
+    bool tc_done = false;
+    if (!(ldh % 4) && !(reinterpret_cast<uintptr_t>(H) & 15) && !(lddx % 4) &&
+        !(reinterpret_cast<uintptr_t>(dX) & 15) && (!Xout || (!(ldxo % 4) && !(reinterpret_cast<uintptr_t>(Xout) & 15)))) {
+      // tensor cores over [<= 128 output features] x [<= 124 input features]
+      // slices (wide inputs: Reddit 602; wide outputs: papers 172 classes);
+      // each slice's partials are reduced straight into its block of dW (db
+      // from the first K slice, the others' db rows land in scratch)
+      const int kmax = din + 1 > 128 ? 124 : din;
+      bool ok = false, later_fail = false;
+      for (int nsw = 128; nsw >= 32 && !ok && !later_fail; nsw /= 2) {  // the widest N slice that fits
+        const int nmax = dout < nsw ? dout : nsw;
+        float* slice_part = pw;
+        float* scratch_db = pw + (int64_t)tc3_chunks * (kmax + 1) * nmax;
+        ok = true;
+        bool first = true;
+        for (int n0 = 0; n0 < dout && ok; n0 += nsw) {
+          const int ns = dout - n0 < nsw ? dout - n0 : nsw;
+          for (int k0 = 0; k0 < din && ok; k0 += kmax) {
+            const int ks = din - k0 < kmax ? din - k0 : kmax;
+            ok = tc_wgrad3(H + k0, ldh, dX + n0, lddx, Xout ? Xout + n0 : nullptr, ldxo, n, ks, ns, slice_part,
+                           tc3_chunks, st, &werr);
+            if (werr) return werr;
+            if (ok) {
+              const int64_t o = (int64_t)(ks + 1) * ns;
+              FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(o, 32), 256, 0, st>>>(
+                  slice_part, tc3_chunks, o, dW + (int64_t)k0 * dout, 0, k0 == 0 ? db : scratch_db, ks + 1, dout, n0);
+            } else if (!first) {
+              later_fail = true;
+            }
+            first = false;
+          }
         }
       }
-      split_done = ok;
+      tc_done = ok;
     }
-    if (split_done) {
-      // dW / db complete
-    } else if (tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, tc3_chunks, st, &werr)) {
-      if (werr) return werr;
-      used_chunks = tc3_chunks;
-      kp1 = din + 1;
-    } else {
+    if (!tc_done) {
       count_dense_fallback();
       const int vec = (ldh % 4 == 0) && !(reinterpret_cast<uintptr_t>(H) & 15);
       dim3 g(chunks, ky, nz);
       FGL_COUNT_LAUNCH(), wgrad_partial_kernel<<<g, 256, 0, st>>>(H, ldh, dX, lddx, Xout, ldxo, n, din, dout,
                                                                   rows_per, pw, vec);
-    }
-    if (!split_done)
       FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, st>>>(
-          pw, used_chunks, outs, dW, (int64_t)din * dout, db, kp1);
+          pw, chunks, outs, dW, (int64_t)din * dout, db, 0);
+    }
     prof_end(pm, kProfWgrad, n, din, dout);
     int err = 0;
-    if (dH && tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) {
+    if (dH && dgrad_tc(dX, lddx, Xout, ldxo, n, W, din, dout, dH, lddh, st, &err)) {
       if (err) return err;
     } else if (dH) {
       count_dense_fallback();
@@ -879,7 +931,7 @@ int fgl_dense_dgrad(const float* dX, int64_t lddx, const float* Xout, int64_t ld
   }
   if (n == 0) return FGL_OK;
   int err = 0;
-  if (tc_gemm(1, dX, lddx, Xout, ldxo, W, nullptr, dH, lddh, n, din, dout, 0, st, &err)) return err;
+  if (dgrad_tc(dX, lddx, Xout, ldxo, n, W, din, dout, dH, lddh, st, &err)) return err;
   count_dense_fallback();
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(din, BN));
   FGL_COUNT_LAUNCH(), gemm_kernel<<<grid, 256, 0, st>>>(dX, lddx, W, dout, 1, nullptr, dH, lddh, n, din, dout, 0, Xout,

@@ -51,9 +51,11 @@ struct G3Args {
   int64_t M;
   int N, K, N_pad, K_pad, R, NC, relu, has_mask, tmem_cols, a_slot_bytes, m_slot_bytes, dbg;
   int stage_off, stage_pitch, w_vec;  // coalesced-epilogue staging tile (byte offset in smem, pitch in floats), or -1
-  int accum;  // mode 0: C += A W (earlier K slices already in C)
-  int a_tma;  // A tiles by TMA tensor copies of a column slice (rows of a_lds floats in smem)
+  int accum;  // C += (earlier K slices already in C)
+  int a_tma;  // A (and mask) tiles by TMA tensor copies of a column slice (rows of a_lds floats in smem)
   int a_lds;  // smem row stride of an A tile, floats (= lda for whole-row bulk copies)
+  int m_lds;  // smem row stride of a mask tile, floats (= ldm for whole-row bulk copies)
+  int64_t ldw;  // W row stride, floats
 };
 
 // debug timeline (FGL_G3DBG & 8): per CTA, globaltimer stamps of each role's
@@ -80,7 +82,8 @@ __device__ __forceinline__ float tf32_rna_finite(float x) {
 
 template <int MODE>
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmC,
-                                                                 const __grid_constant__ CUtensorMap tmA, G3Args p) {
+                                                                 const __grid_constant__ CUtensorMap tmA,
+                                                                 const __grid_constant__ CUtensorMap tmM, G3Args p) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -131,12 +134,15 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
         const int64_t r0 = t * G3_M;
         const int rows = (int)(p.M - r0 < G3_M ? p.M - r0 : G3_M);
         const uint32_t abytes = p.a_tma ? (uint32_t)(G3_M * p.a_lds * 4) : (uint32_t)(rows * p.lda * 4);
-        const uint32_t mbytes = p.has_mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        const uint32_t mbytes = !p.has_mask ? 0u : p.a_tma ? (uint32_t)(G3_M * p.m_lds * 4) : (uint32_t)(rows * p.ldm * 4);
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), abytes + mbytes);
         if (p.a_tma) tma_load_2d(smem_u32(slot), &tmA, 0, (int)r0, bar(FULL + s));  // OOB rows / cols: zeros
         else bulk_load(smem_u32(slot), p.A + r0 * p.lda, abytes, bar(FULL + s));
-        if (p.has_mask) bulk_load(smem_u32(slot + p.a_slot_bytes), p.mask + r0 * p.ldm, mbytes, bar(FULL + s));
+        if (p.has_mask) {
+          if (p.a_tma) tma_load_2d(smem_u32(slot + p.a_slot_bytes), &tmM, 0, (int)r0, bar(FULL + s));
+          else bulk_load(smem_u32(slot + p.a_slot_bytes), p.mask + r0 * p.ldm, mbytes, bar(FULL + s));
+        }
       }
     }
     return;
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
     auto wload = [&](int r, int c) {      // W[r][c..c+3], zero outside
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < wr && c < rl) {
-        const float* src = p.W + (int64_t)r * rl + c;
+        const float* src = p.W + (int64_t)r * p.ldw + c;
         if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
         else {
           v.x = __ldg(src);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
       mbar_wait(bar(FULL + s), (uint32_t)(j / R) & 1u);
       if (row == 0 && grp == 0) G3T(3 + 9 * j);
       const uint32_t xr = smem_u32(slots + s * slot_bytes) + (uint32_t)(row * p.a_lds * 4);
-      const uint32_t mr = smem_u32(slots + s * slot_bytes + p.a_slot_bytes) + (uint32_t)(row * p.ldm * 4);
+      const uint32_t mr = smem_u32(slots + s * slot_bytes + p.a_slot_bytes) + (uint32_t)(row * p.m_lds * 4);
       for (int c = 0; c < nch; ++c, ++cc) {
         if ((cc & 1) != grp) continue;
         const int cs = cc % NC;
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
         if (et == 0) bulk_wait_read0();
         asm volatile("bar.sync 2, 128;" ::: "memory");
       }
-      const bool acc_stage = MODE == 0 && p.accum && tma_out;
+      const bool acc_stage = p.accum && tma_out;
       if (acc_stage) {
         // K split: the earlier slices' sum arrives in the staging boxes by TMA
         // (same SW128 layout the stores use: conflict-free, coalesced)
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
               const float4 pv = lds128(box + (uint32_t)(((cc ^ (r_loc & 7)) & 7) << 4));
               prev[q] = pv.x; prev[q + 1] = pv.y; prev[q + 2] = pv.z; prev[q + 3] = pv.w;
             }
-          } else if (MODE == 0 && p.accum) {  // K split without staging: row-contiguous loads
+          } else if (p.accum) {  // K split without staging: row-contiguous loads
 #pragma unroll
             for (int q = 0; q < 16; ++q)
               prev[q] = (row < p.M && c0 + h + q < p.N) ? out[c0 + h + q] : 0.f;
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             float y = __uint_as_float(v[h + q]);
-            if (MODE == 0 && p.accum) y = __fadd_rn(prev[q], y);
+            if (p.accum) y = __fadd_rn(prev[q], y);
             if (MODE == 0 && p.bias) y = __fadd_rn(y, sbias[c0 + h + q]);
             if (p.relu) y = y > 0.f ? y : 0.f;
             x[q] = y;
@@ -477,9 +483,13 @@ struct Wg3Args {
   int nacc;   // TMEM accumulators (tiles round-robin over them)
   int h_tma;  // H tiles by TMA tensor copies of a column slice (rows of h_lds floats in smem)
   int h_lds;  // smem row stride of an H tile, floats (= ldh for whole-row bulk copies)
+  int z_tma;  // dZ (and mask) tiles by TMA tensor copies of a column slice (N slices)
+  int z_lds, m_lds;  // smem row strides of the dZ / mask tiles, floats
 };
 
-__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_constant__ CUtensorMap tmH, Wg3Args p) {
+__global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_constant__ CUtensorMap tmH,
+                                                                  const __grid_constant__ CUtensorMap tmZ,
+                                                                  const __grid_constant__ CUtensorMap tmM, Wg3Args p) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -511,13 +521,19 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
         const int64_t r0 = t * WG3_MT;
         const int rows = (int)(p.M - r0 < WG3_MT ? p.M - r0 : WG3_MT);
         const uint32_t hb = p.h_tma ? (uint32_t)(WG3_MT * p.h_lds * 4) : (uint32_t)(rows * p.ldh * 4);
-        const uint32_t zb = (uint32_t)(rows * p.ldz * 4), mb = p.mask ? (uint32_t)(rows * p.ldm * 4) : 0u;
+        const uint32_t zb = p.z_tma ? (uint32_t)(WG3_MT * p.z_lds * 4) : (uint32_t)(rows * p.ldz * 4);
+        const uint32_t mb = !p.mask ? 0u : p.z_tma ? (uint32_t)(WG3_MT * p.m_lds * 4) : (uint32_t)(rows * p.ldm * 4);
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
         if (p.h_tma) tma_load_2d(smem_u32(slot), &tmH, 0, (int)r0, bar(FULL + s));  // OOB rows / cols: zeros
         else bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
-        bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
-        if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
+        if (p.z_tma) {
+          tma_load_2d(smem_u32(slot + p.h_bytes), &tmZ, 0, (int)r0, bar(FULL + s));
+          if (p.mask) tma_load_2d(smem_u32(slot + p.h_bytes + p.z_bytes), &tmM, 0, (int)r0, bar(FULL + s));
+        } else {
+          bulk_load(smem_u32(slot + p.h_bytes), p.dZ + r0 * p.ldz, zb, bar(FULL + s));
+          if (p.mask) bulk_load(smem_u32(slot + p.h_bytes + p.z_bytes), p.mask + r0 * p.ldm, mb, bar(FULL + s));
+        }
       }
     }
     return;
@@ -630,8 +646,8 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
           if (rb + 4 <= rows && 4 * n4 + 4 <= p.N && p.mask) {
             // interior block (the common case): no row / feature predicates
             float4 mk[4];
-            const uint32_t za = zs + (uint32_t)((rb * p.ldz + 4 * n4) * 4), zr = (uint32_t)(p.ldz * 4);
-            const uint32_t ma = ms + (uint32_t)((rb * p.ldm + 4 * n4) * 4), mr = (uint32_t)(p.ldm * 4);
+            const uint32_t za = zs + (uint32_t)((rb * p.z_lds + 4 * n4) * 4), zr = (uint32_t)(p.z_lds * 4);
+            const uint32_t ma = ms + (uint32_t)((rb * p.m_lds + 4 * n4) * 4), mr = (uint32_t)(p.m_lds * 4);
 #pragma unroll
             for (int i = 0; i < 4; ++i) e[i] = lds128(za + (uint32_t)i * zr);
 #pragma unroll
@@ -647,10 +663,10 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
             const int nn = 4 * n4 < p.N ? 4 * n4 : 0;
             float4 mk[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) e[i] = lds128(zs + (uint32_t)(((rb + i) * p.ldz + nn) * 4));
+            for (int i = 0; i < 4; ++i) e[i] = lds128(zs + (uint32_t)(((rb + i) * p.z_lds + nn) * 4));
             if (p.mask) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) mk[i] = lds128(ms + (uint32_t)(((rb + i) * p.ldm + nn) * 4));
+              for (int i = 0; i < 4; ++i) mk[i] = lds128(ms + (uint32_t)(((rb + i) * p.m_lds + nn) * 4));
             } else {
 #pragma unroll
               for (int i = 0; i < 4; ++i) mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -757,6 +773,21 @@ bool make_map_sw128(CUtensorMap* m, const float* base, int64_t rows, int cols, i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 [rows, cols] row-major (ld floats) in boxes of [box_rows x box_cols]
+// (box_cols = cols rounded up to 4; columns past `cols` and rows past `rows`
+// read as zeros): a column slice of a wider matrix, rows packed in smem
+bool make_map_cols(CUtensorMap* m, const float* base, int64_t rows, int cols, int64_t ld, int box_cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int64_t g3_fixed(int N_pad, int K_pad, int R, int64_t a_slot, int64_t m_slot) {
   return 1024 + 2 * (int64_t)N_pad * ((K_pad + 31) / 32) * 128 + R * (a_slot + m_slot) + 8 * (2 * R + 22) + 16 + 4 * N_pad;
 }
@@ -782,9 +813,10 @@ bool tc3_disabled() {
 // back); *err receives an FGL status otherwise.
 bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, cudaStream_t st,
-              int* err, int accum) {
+              int* err, int accum, int64_t ldw) {
   *err = 0;
-  if (tc3_disabled() || M < 1 || N < 1 || K < 1 || K > 128 || lda < K) return false;
+  if (ldw < 0) ldw = mode == 0 ? N : K;
+  if (tc3_disabled() || M < 1 || N < 1 || K < 1 || K > 128 || lda < K || ldw < (mode == 0 ? N : K)) return false;
   if ((lda % 4) || (reinterpret_cast<uintptr_t>(A) & 15)) return false;
   const int has_mask = (mode == 1 && mask) ? 1 : 0;
   if (has_mask && ((ldm % 4) || ldm < K || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
@@ -794,11 +826,14 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   // TMEM: two accumulators + a ring of NC A chunks (64 columns each)
   const int NC = std::min(8, (512 - 2 * N_pad) / (2 * G3_KCH));
   if (NC < 2) return false;
-  // a column slice of a wide A (lda > 256 floats: whole-row bulk copies would
-  // not fit): 2-D TMA tensor copies of [128 rows x K_box] tiles instead
-  const int a_tma = (mode == 0 && lda > 256) ? 1 : 0;
-  const int a_lds = a_tma ? (K + 3) / 4 * 4 : (int)lda;
-  const int64_t a_slot = (int64_t)G3_M * a_lds * 4, m_slot = has_mask ? (int64_t)G3_M * ldm * 4 : 0;
+  // a column slice of A (a K slice, or rows wider than 256 floats that
+  // whole-row bulk copies could not stage): 2-D TMA tensor copies of [128
+  // rows x K_box] tiles of A (and of the mask) instead
+  const int K4 = (K + 3) / 4 * 4;
+  const int a_tma = (lda > 256 || lda > K4 || (has_mask && (ldm > 256 || ldm > K4))) ? 1 : 0;
+  const int a_lds = a_tma ? K4 : (int)lda;
+  const int m_lds = a_tma ? K4 : (int)ldm;
+  const int64_t a_slot = (int64_t)G3_M * a_lds * 4, m_slot = has_mask ? (int64_t)G3_M * m_lds * 4 : 0;
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
   static const int rmax = getenv("FGL_G3SLOTS") ? atoi(getenv("FGL_G3SLOTS")) : G3_MAX_SLOTS;
   // stage mode: 1 (default) = stage the epilogue for TMA tensor stores; 0 =
@@ -812,6 +847,11 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   if (stage_pref == 0 && R < 3 && rmax >= 3 &&
       g3_fixed(N_pad, K_pad, 3, a_slot, m_slot) <= G3_MAX_SMEM) {
     R = 3;
+    stage = false;
+  }
+  if (R == 0) {  // no room for the staging tile (wide N with a mask): direct row stores
+    for (int r = 3; r >= 2 && R == 0; --r)
+      if (g3_fixed(N_pad, K_pad, r, a_slot, m_slot) <= G3_MAX_SMEM) R = r;
     stage = false;
   }
   if (R == 0) return false;
@@ -839,7 +879,8 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   const int64_t stage_off = (g3_fixed(N_pad, K_pad, R, a_slot, m_slot) - 1024 + 1023) / 1024 * 1024;
   G3Args p{A, mask, W, bias, C, lda, ldm, ldc, M, N, K, N_pad, K_pad, R, NC, relu, has_mask, cols,
            (int)a_slot, (int)m_slot, dbg, coal ? (int)stage_off : -1, 0,
-           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0), accum, a_tma, a_lds};
+           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0) && (ldw % 4 == 0), accum, a_tma,
+           a_lds, m_lds, ldw};
   const int64_t smem = coal ? g3_smem(N_pad, K_pad, R, a_slot, m_slot) : g3_fixed(N_pad, K_pad, R, a_slot, m_slot);
   static bool attr[2] = {false, false};
   cudaError_t e;
@@ -852,22 +893,15 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
   const int64_t tiles = ceil_div(M, G3_M);
   // persistent CTAs (one per SM by smem), at most fgl_set_dense_ctas' budget
   const int grid = (int)std::min<int64_t>(tiles, dense_cta_budget());
-  CUtensorMap mA;
+  CUtensorMap mA, mM;
   std::memset(&mA, 0, sizeof(mA));
-  if (a_tma) {
-    EncodeTiledFn fn = encode_fn();
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
-    cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-    cuuint32_t box[2] = {(cuuint32_t)a_lds, (cuuint32_t)G3_M};
-    cuuint32_t es[2] = {1, 1};
-    if (!fn || fn(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
-  }
+  std::memset(&mM, 0, sizeof(mM));
+  if (a_tma && (!make_map_cols(&mA, A, M, K, lda, a_lds, G3_M) ||
+                (has_mask && !make_map_cols(&mM, mask, M, K, ldm, m_lds, G3_M))))
+    return false;
   const ProfMark pm = prof_begin(st);
-  if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
-  else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, mA, p);
+  if (mode == 0) FGL_COUNT_LAUNCH(), tc_gemm3_kernel<0><<<grid, G3_THREADS, smem, st>>>(mC, mA, mM, p);
+  else FGL_COUNT_LAUNCH(), tc_gemm3_kernel<1><<<grid, G3_THREADS, smem, st>>>(mC, mA, mM, p);
   prof_end(pm, mode == 0 ? kProfDenseFwd : kProfDgrad, M, N, K);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_gemm3_kernel");
@@ -894,7 +928,12 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   // [64 rows x K_box] tiles instead of whole-row bulk copies
   const int h_tma = ldh > 256 ? 1 : 0;
   const int h_lds = h_tma ? (K + 3) / 4 * 4 : (int)ldh;
-  const int hb = WG3_MT * h_lds * 4, zb = WG3_MT * (int)ldz * 4, mb = mask ? WG3_MT * (int)ldm * 4 : 0;
+  // a column slice of dZ / mask (an N slice of a wider layer, or rows wider
+  // than 256 floats): TMA tensor copies of [64 rows x N_box] tiles
+  const int N4 = (N + 3) / 4 * 4;
+  const int z_tma = (ldz > 256 || ldz > N4 || (mask && (ldm > 256 || ldm > N4))) ? 1 : 0;
+  const int z_lds = z_tma ? N4 : (int)ldz, m_lds = z_tma ? N4 : (int)ldm;
+  const int hb = WG3_MT * h_lds * 4, zb = WG3_MT * z_lds * 4, mb = mask ? WG3_MT * m_lds * 4 : 0;
   // deepest raw-tile ring that fits next to the chunk ring: the kernel is a
   // stream over H / dZ / mask, so bytes in flight per SM set its speed
   static const int env_r = getenv("FGL_WG3_R") ? atoi(getenv("FGL_WG3_R")) : 0;
@@ -920,21 +959,17 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc, h_tma, h_lds};
-  CUtensorMap mH;
+  Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc, h_tma, h_lds,
+            z_tma, z_lds, m_lds};
+  CUtensorMap mH, mZ, mM;
   std::memset(&mH, 0, sizeof(mH));
-  if (h_tma) {
-    EncodeTiledFn fn = encode_fn();
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
-    cuuint64_t strides[1] = {(cuuint64_t)ldh * 4};
-    cuuint32_t box[2] = {(cuuint32_t)h_lds, (cuuint32_t)WG3_MT};
-    cuuint32_t es[2] = {1, 1};
-    if (!fn || fn(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(H), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
-  }
-  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(mH, p);
+  std::memset(&mZ, 0, sizeof(mZ));
+  std::memset(&mM, 0, sizeof(mM));
+  if (h_tma && !make_map_cols(&mH, H, M, K, ldh, h_lds, WG3_MT)) return false;
+  if (z_tma && (!make_map_cols(&mZ, dZ, M, N, ldz, z_lds, WG3_MT) ||
+                (mask && !make_map_cols(&mM, mask, M, N, ldm, m_lds, WG3_MT))))
+    return false;
+  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
   return true;

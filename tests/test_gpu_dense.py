@@ -13,7 +13,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(1000, 100, 64), (4097, 64, 64), (300, 64, 47), (129, 47, 64), (777, 128, 172),
-          (50, 12, 2), (5000, 602, 64), (3, 8, 16), (3000, 301, 47), (1500, 129, 64)]
+          (50, 12, 2), (5000, 602, 64), (3, 8, 16), (3000, 301, 47), (1500, 129, 64),
+          (1024, 64, 172), (2000, 300, 200), (700, 64, 300)]
 
 
 def _ld(d):
@@ -34,7 +35,11 @@ def _close(got, ref):
 
 @pytest.mark.parametrize("n,din,dout", SHAPES)
 def test_forward_and_backward(n, din, dout):
+    """Every shape runs on the tensor cores (wide inputs in K slices, wide
+    outputs -- papers' 172 classes -- in N slices, the dgrad reduction in K
+    slices): the SIMT fallback counter must not move."""
     from paper_2409_14939_b200 import _lib
+    fb0 = _lib.lib().fgl_dense_fallback_count()
     rng = np.random.default_rng(n + din + dout)
     H = rng.standard_normal((n, din)).astype(np.float32)
     W = (rng.standard_normal((din, dout)) * 0.3).astype(np.float32)
@@ -64,6 +69,13 @@ def test_forward_and_backward(n, din, dout):
     _close(dW[: din * dout].cpu().numpy().reshape(din, dout), H.astype(np.float64).T @ dz)
     _close(dW[din * dout :].cpu().numpy(), dz.sum(0))
     _close(dH[:, :din].cpu().numpy(), dz @ W.astype(np.float64).T)
+    # the chain's separate dgrad entry point (fgl_dense_dgrad)
+    dH2 = torch.empty((n, _ld(din)), dtype=torch.float32, device="cuda")
+    _lib.call("fgl_dense_dgrad", dXd.data_ptr(), _ld(dout), Z.data_ptr(), _ld(dout), n, Wd.data_ptr(), din, dout,
+              dH2.data_ptr(), _ld(din), st)
+    _close(dH2[:, :din].cpu().numpy(), dz @ W.astype(np.float64).T)
+    if os.environ.get("FGL_DENSE", "") == "":
+        assert _lib.lib().fgl_dense_fallback_count() == fb0, "a dense kernel took the SIMT fallback"
 
 
 def test_simt_fallback_matches():
