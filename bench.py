@@ -472,8 +472,8 @@ def _measured_traffic(kernel):
         return None
 
 
-_TRAFFIC_KEYS = {"select": "select_bal_kernel", "aggregate_l0": "spmm_kernel_l0", "dense_fwd": "tc_gemm3_kernel_l0",
-                 "wgrad": "tc_wgrad3_kernel_l0", "gather": "gather_rows_kernel_host"}
+_TRAFFIC_KEYS = {"select": "select_bal2_kernel", "aggregate_l0": "spmm_lean_kernel_l0",
+                 "dense_fwd": "tc_gemm3_kernel_l0", "wgrad": "tc_wgrad3_kernel_l0", "gather": "gather_rows_kernel_host"}
 
 
 def _peaks():
@@ -518,7 +518,7 @@ def host_link_peak(torch, device):
 
 def _roof(bound, achieved, peak, unit, traffic_key=None, **extra):
     out = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak if peak else None,
-           "traffic": _measured_traffic(traffic_key) if traffic_key else None}
+           "traffic": _measured_traffic(_TRAFFIC_KEYS.get(traffic_key, traffic_key)) if traffic_key else None}
     out.update(extra)
     return out
 
