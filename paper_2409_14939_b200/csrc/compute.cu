@@ -764,7 +764,7 @@ static bool dgrad_tc(const float* dX, int64_t lddx, const float* Xout, int64_t l
   // whose first tile fits shared memory; K slices accumulate into dH
   for (int nsw = 256; nsw >= 64; nsw /= 2) {
     for (int ksw = 128; ksw >= 32; ksw /= 2) {
-      bool ok = true, first = true;
+      bool ok = true;
       for (int n0 = 0; n0 < din && ok; n0 += nsw) {
         const int ns = din - n0 < nsw ? din - n0 : nsw;
         for (int k0 = 0; k0 < dout && ok; k0 += ksw) {
@@ -772,8 +772,8 @@ static bool dgrad_tc(const float* dX, int64_t lddx, const float* Xout, int64_t l
           ok = tc_gemm3(1, dX + k0, lddx, Xout ? Xout + k0 : nullptr, ldxo, W + (int64_t)n0 * dout + k0, nullptr,
                         dH + n0, lddh, n, ns, ks, 0, st, err, k0 > 0, dout);
           if (*err) return true;
-          if (!ok && !first) return false;  // a later slice fell outside: the caller recomputes dH whole
-          first = false;
+          // a later slice may fall outside (the first K slice runs on tc_dense4,
+          // accumulating slices on tc_gemm3): narrower slices rewrite dH whole
         }
       }
       if (ok) return true;
@@ -801,7 +801,6 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     for (int ksw = 128; ksw >= 64 && !ok; ksw /= 2) {
       for (int nsw = 128; nsw >= 32 && !ok; nsw /= 2) {
         ok = true;
-        bool first = true;
         for (int n0 = 0; n0 < dout && ok; n0 += nsw) {
           const int ns = dout - n0 < nsw ? dout - n0 : nsw;
           for (int k0 = 0; k0 < din && ok; k0 += ksw) {
@@ -810,15 +809,15 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
             ok = tc_gemm3(0, H + k0, ldh, nullptr, 0, W + (int64_t)k0 * dout + n0, last && b ? b + n0 : nullptr,
                           Z + n0, ldz, n, ns, ks, last ? relu : 0, (cudaStream_t)stream, &err, k0 > 0, dout);
             if (err) return err;
-            if (!ok && !first) goto simt;  // a later slice fell outside: recompute Z whole below
-            first = false;
+            // a later slice may fall outside (the first K slice runs on
+            // tc_dense4, accumulating slices on tc_gemm3): narrower slices
+            // rewrite Z whole
           }
         }
       }
     }
     if (ok) return FGL_OK;
-  simt:;
-    // a slice fell outside the envelope: the SIMT kernel below recomputes Z whole
+    // no slicing fits the envelope: the SIMT kernel below computes Z
   }
   count_dense_fallback();
   dim3 grid((unsigned)ceil_div(n, BM), (unsigned)ceil_div(dout, BN));

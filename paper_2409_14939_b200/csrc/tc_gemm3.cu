@@ -80,6 +80,74 @@ __device__ __forceinline__ float tf32_rna_finite(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
+// the weight operand B[n][k] split into tf32 hi / lo K-major SWIZZLE_128B
+// boxes of 32 K columns, by `nt` threads (t0 = 0..nt-1); 4x4 blocks over
+// [N_pad x K_pad] (padding included: no zeroing pass), four 16-byte W loads,
+// a register transpose for mode 0 (B = W^T), eight 16-byte shared stores
+template <int MODE>
+__device__ __forceinline__ void split_weight_image(const float* __restrict__ W, int64_t ldw, int K, int N, int K_pad,
+                                                   int N_pad, bool vec, char* sB_hi, char* sB_lo, int t0, int nt) {
+  const int b_box = N_pad * 128;
+  const int K4 = K_pad >> 2, N4 = N_pad >> 2, nblk = K4 * N4;
+  const int rl = MODE == 0 ? N : K;  // W row length
+  const int wr = MODE == 0 ? K : N;  // W rows
+  auto wload = [&](int r, int c) {   // W[r][c..c+3], zero outside
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < wr && c < rl) {
+      const float* src = W + (int64_t)r * ldw + c;
+      if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
+      else {
+        v.x = __ldg(src);
+        if (c + 1 < rl) v.y = __ldg(src + 1);
+        if (c + 2 < rl) v.z = __ldg(src + 2);
+        if (c + 3 < rl) v.w = __ldg(src + 3);
+      }
+    }
+    return v;
+  };
+  constexpr int PER = 2;
+  for (int b0 = t0; b0 < nblk; b0 += PER * nt) {
+    float4 w[PER][4];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int b = b0 + u * nt;
+      const int k4 = b % K4, n4 = b / K4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[u][i] = b < nblk ? (MODE == 0 ? wload(4 * k4 + i, 4 * n4) : wload(4 * n4 + i, 4 * k4))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int b = b0 + u * nt;
+      if (b >= nblk) break;
+      const int k4 = b % K4, n4 = b / K4;
+      float4 r4[4];  // r4[jn] = B[4 n4 + jn][4 k4 .. 4 k4 + 3]
+      if (MODE == 0) {
+        r4[0] = make_float4(w[u][0].x, w[u][1].x, w[u][2].x, w[u][3].x);
+        r4[1] = make_float4(w[u][0].y, w[u][1].y, w[u][2].y, w[u][3].y);
+        r4[2] = make_float4(w[u][0].z, w[u][1].z, w[u][2].z, w[u][3].z);
+        r4[3] = make_float4(w[u][0].w, w[u][1].w, w[u][2].w, w[u][3].w);
+      } else {
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) r4[jn] = w[u][jn];
+      }
+#pragma unroll
+      for (int jn = 0; jn < 4; ++jn) {
+        const int n = 4 * n4 + jn, k = 4 * k4;
+        float4 h4, l4;
+        h4.x = tf32_hi(r4[jn].x); l4.x = __fsub_rn(r4[jn].x, h4.x);
+        h4.y = tf32_hi(r4[jn].y); l4.y = __fsub_rn(r4[jn].y, h4.y);
+        h4.z = tf32_hi(r4[jn].z); l4.z = __fsub_rn(r4[jn].z, h4.z);
+        h4.w = tf32_hi(r4[jn].w); l4.w = __fsub_rn(r4[jn].w, h4.w);
+        const uint32_t off = (uint32_t)((k >> 5) * b_box) + sw128_off(n, k & 31);
+        sts128(smem_u32(sB_hi) + off, h4);
+        sts128(smem_u32(sB_lo) + off, l4);
+      }
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmC,
                                                                  const __grid_constant__ CUtensorMap tmA,
@@ -162,65 +230,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_gemm3_kernel(const __grid_co
     // 16-byte W loads, a register transpose (mode 0: B = W^T), eight 16-byte
     // shared stores; consecutive threads take consecutive k4 (conflict-free).
     const int nt = 192, t0 = warp < 4 ? tid - 64 : tid - 384 + 64;
-    const int K4 = K_pad >> 2, N4 = N_pad >> 2, nblk = K4 * N4;
-    const bool vec = p.w_vec;
-    const int rl = MODE == 0 ? p.N : p.K;  // W row length
-    const int wr = MODE == 0 ? p.K : p.N;  // W rows
-    auto wload = [&](int r, int c) {      // W[r][c..c+3], zero outside
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < wr && c < rl) {
-        const float* src = p.W + (int64_t)r * p.ldw + c;
-        if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
-        else {
-          v.x = __ldg(src);
-          if (c + 1 < rl) v.y = __ldg(src + 1);
-          if (c + 2 < rl) v.z = __ldg(src + 2);
-          if (c + 3 < rl) v.w = __ldg(src + 3);
-        }
-      }
-      return v;
-    };
-    constexpr int PER = 3;  // blocks per thread with all loads in flight
-    for (int b0 = t0; b0 < nblk; b0 += PER * nt) {
-      float4 w[PER][4];
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int b = b0 + u * nt;
-        const int k4 = b % K4, n4 = b / K4;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          w[u][i] = b < nblk ? (MODE == 0 ? wload(4 * k4 + i, 4 * n4) : wload(4 * n4 + i, 4 * k4))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int b = b0 + u * nt;
-        if (b >= nblk) break;
-        const int k4 = b % K4, n4 = b / K4;
-        float4 r4[4];  // r4[jn] = B[4 n4 + jn][4 k4 .. 4 k4 + 3]
-        if (MODE == 0) {
-          r4[0] = make_float4(w[u][0].x, w[u][1].x, w[u][2].x, w[u][3].x);
-          r4[1] = make_float4(w[u][0].y, w[u][1].y, w[u][2].y, w[u][3].y);
-          r4[2] = make_float4(w[u][0].z, w[u][1].z, w[u][2].z, w[u][3].z);
-          r4[3] = make_float4(w[u][0].w, w[u][1].w, w[u][2].w, w[u][3].w);
-        } else {
-#pragma unroll
-          for (int jn = 0; jn < 4; ++jn) r4[jn] = w[u][jn];
-        }
-#pragma unroll
-        for (int jn = 0; jn < 4; ++jn) {
-          const int n = 4 * n4 + jn, k = 4 * k4;
-          float4 h4, l4;
-          h4.x = tf32_hi(r4[jn].x); l4.x = __fsub_rn(r4[jn].x, h4.x);
-          h4.y = tf32_hi(r4[jn].y); l4.y = __fsub_rn(r4[jn].y, h4.y);
-          h4.z = tf32_hi(r4[jn].z); l4.z = __fsub_rn(r4[jn].z, h4.z);
-          h4.w = tf32_hi(r4[jn].w); l4.w = __fsub_rn(r4[jn].w, h4.w);
-          const uint32_t off = (uint32_t)((k >> 5) * b_box) + sw128_off(n, k & 31);
-          sts128(smem_u32(sB_hi) + off, h4);
-          sts128(smem_u32(sB_lo) + off, l4);
-        }
-      }
-    }
+    split_weight_image<MODE>(p.W, p.ldw, p.K, p.N, K_pad, N_pad, p.w_vec, sB_hi, sB_lo, t0, nt);
     fence_async_smem();
     asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
     if (t0 == 0) {
@@ -743,6 +753,253 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   }
 }
 
+// ------------------------------------------------------------ tc_dense4 --
+// Forward / dgrad GEMM for the usual layer shapes (K <= 128, N <= 128, one
+// tile), organised around the TMA engine and shared-memory operands:
+//
+//   warp 0      producer: one 2-D TMA tensor copy per [128 rows x 32 K]
+//               SWIZZLE_128B box of A (and of the ReLU mask for dgrad) into a
+//               ring of S box stages -- the box layout IS the K-major
+//               SWIZZLE_128B operand layout the tensor core reads, so A is
+//               never re-laid-out;
+//   warps 4-7   splitters, thread = row: read the row's 32 floats of a box
+//               (conflict-free: the swizzle spreads 8 rows over the banks),
+//               mask, write hi = tf32(x) back in place and lo = x - hi to the
+//               box's TMEM slot (tcgen05.st, lane = row);
+//   warp 1      MMA issuer: per 8-wide K step lo*W_hi (A from TMEM), hi*W_lo,
+//               hi*W_hi (A from shared memory) into a double-buffered fp32
+//               accumulator; one commit per box frees its stage;
+//   warps 8-11  epilogue: tcgen05.ld, bias, ReLU, SW128 staging boxes, TMA
+//               tensor stores.
+//
+// Against tc_gemm3 (whole-row bulk copies converted into a TMEM A ring by
+// thread-per-row converters): a stage is 16 KB instead of a 51 KB tile, so
+// 8 stages (128 KB of loads in flight per SM) fit beside the weight images,
+// and the tensor core reads the hi part straight from the landed box.  Same
+// rounding and the same MMA order as tc_gemm3 (bit-identical results).
+constexpr int T4_THREADS = 384;  // 12 warps, roles above (warps 2-3 only split the weight)
+constexpr int T4_M = 128;
+constexpr int T4_BOX = T4_M * 128;  // one [128 rows x 32 fp32] SW128 box
+constexpr int T4_MAX_STAGES = 12;
+
+struct T4Args {
+  const float* W;      // mode 0: [K, N] row-major; mode 1: [N, K] row-major (row stride ldw)
+  const float* bias;   // mode 0 only, [N] or null
+  int64_t M, ldw;
+  int N, K, N_pad, K_pad, S, relu, has_mask, tmem_cols, w_vec, stage_off, dbg;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmM,
+                                                                  const __grid_constant__ CUtensorMap tmC, T4Args p) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = p.S, N_pad = p.N_pad;
+  const int KB = (p.K + 31) / 32;  // A boxes per tile (= weight image boxes)
+  const int b_box = N_pad * 128;
+  char* sB_hi = smem;
+  char* sB_lo = sB_hi + KB * b_box;
+  char* stages = sB_lo + KB * b_box;  // S x {A box, mask box}
+  const int stage_bytes = T4_BOX * (1 + p.has_mask);
+  char* stg = smem + p.stage_off;     // epilogue staging: ceil(N_pad / 32) boxes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + ((N_pad + 31) / 32) * T4_BOX);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  const int FULL = 0, SPLIT = S, EMPTY = 2 * S, TFULL = 3 * S, TEMPTY = 3 * S + 2, BREADY = 3 * S + 4;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init_n(bar(FULL + s), 1);
+      mbar_init_n(bar(SPLIT + s), 128);
+      mbar_init_n(bar(EMPTY + s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init_n(bar(TFULL + a), 1);
+      mbar_init_n(bar(TEMPTY + a), 128);
+    }
+    mbar_init_n(bar(BREADY), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tiles = ceil_div(p.M, T4_M);
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer --
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      if (p.has_mask) tma_prefetch_desc(&tmM);
+      int g = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int b = 0; b < KB; ++b, ++g) {
+          const int s = g % S;
+          mbar_wait(bar(EMPTY + s), ((uint32_t)(g / S) & 1u) ^ 1u);
+          const uint32_t dst = smem_u32(stages + s * stage_bytes);
+          mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)stage_bytes);
+          tma_load_2d(dst, &tmA, 32 * b, (int)(t * T4_M), bar(FULL + s));  // OOB rows / columns: zeros
+          if (p.has_mask) tma_load_2d(dst + T4_BOX, &tmM, 32 * b, (int)(t * T4_M), bar(FULL + s));
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  // the weight image, by every non-producer warp but the MMA issuer (the
+  // first boxes are still in flight), then bias -> shared
+  if (warp >= 2) {
+    split_weight_image<MODE>(p.W, p.ldw, p.K, p.N, p.K_pad, N_pad, p.w_vec, sB_hi, sB_lo, tid - 64, T4_THREADS - 64);
+    for (int c = tid - 64; c < N_pad; c += T4_THREADS - 64)
+      sbias[c] = (MODE == 0 && p.bias && c < p.N) ? p.bias[c] : 0.f;
+    fence_async_smem();
+    asm volatile("bar.sync 3, %0;" ::"r"(T4_THREADS - 64) : "memory");
+    if (tid == 64) mbar_arrive(bar(BREADY));
+  }
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(T4_THREADS - 32) : "memory");
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: accumulators [0, 2 N_pad), box s's lo part at 2 N_pad + 32 s
+  auto lo_col = [&](int s) { return tmem + (uint32_t)(2 * N_pad + 32 * s); };
+
+  if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    const uint32_t idesc = idesc_tf32(T4_M, N_pad, 0, 0);
+    const uint32_t bh = smem_u32(sB_hi), bl = smem_u32(sB_lo);
+    mbar_wait(bar(BREADY), 0);
+    tc_fence_after();
+    int j = 0, g = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      const uint32_t acc = tmem + (uint32_t)(a * N_pad);
+      mbar_wait(bar(TEMPTY + a), ((uint32_t)(j >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      for (int b = 0; b < KB; ++b, ++g) {
+        const int s = g % S;
+        mbar_wait(bar(SPLIT + s), (uint32_t)(g / S) & 1u);
+        tc_fence_after();
+        const int kst = min(32, p.K_pad - 32 * b) / 8;
+        const uint32_t ahi = smem_u32(stages + s * stage_bytes), alo = lo_col(s);
+        if (elect_one()) {
+          for (int st = 0; st < ((p.dbg & 2) ? 0 : kst); ++st) {
+            const uint32_t bo = (uint32_t)(b * b_box + st * 32);
+            const uint64_t dbh = umma_desc_sw128(bh + bo), dbl = umma_desc_sw128(bl + bo);
+            const uint64_t dah = umma_desc_sw128(ahi + (uint32_t)(st * 32));
+            mma_tf32_ts(acc, alo + 8 * st, dbh, idesc, (b | st) != 0);
+            mma_tf32(acc, dah, dbl, idesc, 1);
+            mma_tf32(acc, dah, dbh, idesc, 1);
+          }
+          mma_commit(bar(EMPTY + s));  // stage (and its TMEM lo slot) free once these MMAs complete
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(bar(TFULL + a));
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // --------------------------------------------------------- splitters --
+    const int r = (warp & 3) * 32 + lane;  // row = TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    int g = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int b = 0; b < KB; ++b, ++g) {
+        const int s = g % S;
+        mbar_wait(bar(FULL + s), (uint32_t)(g / S) & 1u);
+        const uint32_t xr = smem_u32(stages + s * stage_bytes) + (uint32_t)(r * 128);
+        uint32_t lv[32];
+#pragma unroll
+        for (int h = 0; h < ((p.dbg & 1) ? 0 : 2); ++h) {
+          float4 x[4], m[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = 4 * h + q;  // 16-byte chunk c (k = 4c..4c+3) sits at chunk c ^ (r & 7)
+            x[q] = lds128(xr + (uint32_t)((c ^ (r & 7)) << 4));
+            if (MODE == 1 && p.has_mask) m[q] = lds128(xr + T4_BOX + (uint32_t)((c ^ (r & 7)) << 4));
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = 4 * h + q;
+            float xs[4] = {x[q].x, x[q].y, x[q].z, x[q].w};
+            if (MODE == 1 && p.has_mask) {
+              const float ms[4] = {m[q].x, m[q].y, m[q].z, m[q].w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (!(ms[u] > 0.f)) xs[u] = 0.f;
+            }
+            float hs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              hs[u] = tf32_rna_finite(xs[u]);
+              lv[4 * c + u] = __float_as_uint(__fsub_rn(xs[u], hs[u]));
+            }
+            sts128(xr + (uint32_t)((c ^ (r & 7)) << 4), make_float4(hs[0], hs[1], hs[2], hs[3]));
+          }
+        }
+        if (!(p.dbg & 1)) {
+          tmem_st32(lo_col(s) + lane_off, lv);
+          tmem_st_wait();
+        }
+        fence_async_smem();  // hi stores -> visible to the tensor core (async proxy)
+        tc_fence_before();
+        mbar_arrive(bar(SPLIT + s));
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------------------------------------------------- epilogue --
+    const int quarter = warp & 3, et = tid - 256, r_loc = quarter * 32 + lane;
+    const uint32_t stg_u = smem_u32(stg);
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      mbar_wait(bar(TFULL + a), (uint32_t)(j >> 1) & 1u);
+      tc_fence_after();
+      if (j > 0) {  // the previous tile's TMA stores must have finished reading staging
+        if (et == 0) bulk_wait_read0();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
+      for (int c0 = 0; c0 < N_pad; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N_pad + c0);
+        tmem_ld16_nowait(ta, v);
+        if (c0 + 16 < N_pad) tmem_ld16_nowait(ta + 16, v + 16);
+        tmem_ld_wait();
+        const int ncol = c0 + 16 < N_pad ? 32 : 16;
+        const uint32_t box = stg_u + (uint32_t)((c0 >> 5) * T4_BOX) + (uint32_t)(r_loc * 128);
+#pragma unroll
+        for (int h = 0; h < 32; h += 4) {
+          if (h >= ncol) break;
+          float x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float y = __uint_as_float(v[h + q]);
+            if (MODE == 0 && p.bias) y = __fadd_rn(y, sbias[c0 + h + q]);
+            if (p.relu) y = y > 0.f ? y : 0.f;
+            x[q] = y;
+          }
+          sts128(box + (uint32_t)((((h >> 2) ^ (r_loc & 7)) & 7) << 4), make_float4(x[0], x[1], x[2], x[3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(TEMPTY + a));  // accumulator drained: tile j+2's MMAs may start
+      fence_async_smem();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (et == 0) {
+        for (int c0 = 0; c0 < N_pad; c0 += 32)
+          tma_store_2d(&tmC, stg_u + (uint32_t)((c0 >> 5) * T4_BOX), c0, (int)(t * T4_M));
+        bulk_commit();
+      }
+    }
+    if (et == 0) bulk_wait0();
+  }
+  // warps 1-11 (warp 0 returned after issuing its copies)
+  tc_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(T4_THREADS - 32) : "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, p.tmem_cols);
+  }
+}
+
 // ------------------------------------------------------------ host side --
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -807,6 +1064,79 @@ bool tc3_disabled() {
   return v != 0;
 }
 
+// tensor maps are host microseconds to encode and the trainer reuses the same
+// buffers every batch: keep the last few per thread
+bool cached_map_sw128(CUtensorMap* out, const float* base, int64_t rows, int cols, int64_t ld) {
+  struct Entry { const float* base; int64_t rows, ld; int cols; CUtensorMap m; };
+  static thread_local Entry cache[16];
+  static thread_local int next = 0;
+  for (auto& c : cache)
+    if (c.base == base && c.rows == rows && c.cols == cols && c.ld == ld) { *out = c.m; return true; }
+  if (!make_map_sw128(out, base, rows, cols, ld)) return false;
+  Entry& c = cache[next];
+  next = (next + 1) % 16;
+  c.base = base; c.rows = rows; c.cols = cols; c.ld = ld; c.m = *out;
+  return true;
+}
+
+bool tc4_disabled() {
+  static const int v = getenv("FGL_TC4") ? atoi(getenv("FGL_TC4")) == 0 : 0;
+  return v != 0;
+}
+
+// tc_dense4_kernel for one [M x N] output with K <= 128, N <= 128 and no K-slice
+// accumulation; false outside that envelope (tc_gemm3 then runs the tile)
+bool tc_dense4(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
+               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, int64_t ldw,
+               cudaStream_t st, int* err) {
+  *err = 0;
+  if (tc4_disabled() || M < 1 || K < 1 || K > 128 || N < 1 || N > 128) return false;
+  const int has_mask = (mode == 1 && mask) ? 1 : 0;
+  if ((lda % 4) || (ldc % 4) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(C) & 15))
+    return false;
+  if (has_mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
+  const int N_pad = (N + 15) / 16 * 16, K_pad = (K + 7) / 8 * 8, KB = (K + 31) / 32;
+  const int64_t stage_bytes = (int64_t)T4_BOX * (1 + has_mask);
+  const int nob = (N_pad + 31) / 32;
+  auto fixed = [&](int S) {
+    return 1024 + 2 * (int64_t)KB * N_pad * 128 + (int64_t)S * stage_bytes + (int64_t)nob * T4_BOX + 8 * (3 * S + 5) +
+           16 + 4 * N_pad;
+  };
+  static const int env_s = getenv("FGL_TC4_STAGES") ? atoi(getenv("FGL_TC4_STAGES")) : 0;
+  int S = std::min(env_s > 0 ? env_s : T4_MAX_STAGES, (512 - 2 * N_pad) / 32);
+  while (S >= 2 && fixed(S) > G3_MAX_SMEM) --S;
+  if (S < 2) return false;
+  int cols = 32;
+  while (cols < 2 * N_pad + 32 * S) cols <<= 1;
+  if (cols > 512) return false;
+  CUtensorMap mA, mM, mC;
+  std::memset(&mM, 0, sizeof(mM));
+  if (!cached_map_sw128(&mA, A, M, K, lda) || !cached_map_sw128(&mC, C, M, N, ldc) ||
+      (has_mask && !cached_map_sw128(&mM, mask, M, K, ldm)))
+    return false;
+  static bool attr[2] = {false, false};
+  if (!attr[mode]) {
+    const cudaError_t e =
+        mode == 0 ? cudaFuncSetAttribute(tc_dense4_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM)
+                  : cudaFuncSetAttribute(tc_dense4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_dense4)"); return true; }
+    attr[mode] = true;
+  }
+  static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
+  const int stage_off = (int)(2 * (int64_t)KB * N_pad * 128 + (int64_t)S * stage_bytes);
+  T4Args p{W, bias, M, ldw, N, K, N_pad, K_pad, S, relu, has_mask, cols,
+           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0) && (ldw % 4 == 0), stage_off, dbg};
+  const int grid = (int)std::min<int64_t>(ceil_div(M, T4_M), dense_cta_budget());
+  const int64_t smem = fixed(S);
+  const ProfMark pm = prof_begin(st);
+  if (mode == 0) FGL_COUNT_LAUNCH(), tc_dense4_kernel<0><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, p);
+  else FGL_COUNT_LAUNCH(), tc_dense4_kernel<1><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, p);
+  prof_end(pm, mode == 0 ? kProfDenseFwd : kProfDgrad, M, N, K);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) *err = cuda_status(e, "tc_dense4_kernel");
+  return true;
+}
+
 }  // namespace
 
 // Returns false if the shape is outside this kernel's envelope (caller falls
@@ -816,6 +1146,9 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
               int* err, int accum, int64_t ldw) {
   *err = 0;
   if (ldw < 0) ldw = mode == 0 ? N : K;
+  if (!accum && !tc3_disabled() && ldw >= (mode == 0 ? N : K) &&
+      tc_dense4(mode, A, lda, mask, ldm, W, bias, C, ldc, M, N, K, relu, ldw, st, err))
+    return true;
   if (tc3_disabled() || M < 1 || N < 1 || K < 1 || K > 128 || lda < K || ldw < (mode == 0 ? N : K)) return false;
   if ((lda % 4) || (reinterpret_cast<uintptr_t>(A) & 15)) return false;
   const int has_mask = (mode == 1 && mask) ? 1 : 0;

@@ -104,14 +104,38 @@ class DeviceWindow:
     seed_off_host: np.ndarray
     _host_counts: np.ndarray | None = None
 
+    _pinned = None  # (pinned host copy of the counts, event) queued by prefetch_counts
+
+    def _counts_len(self) -> int:
+        n = counts_layout(self.num_hops, self.num_batches)["len"]
+        if self.s.depth_layout:
+            n += self.num_batches * (self.num_hops + 1)
+        return n
+
+    def prefetch_counts(self, pinned, stream) -> None:
+        """Queue the counts read-back on `stream` right behind the sampler
+        (asynchronous, into the pinned buffer `pinned`): host_counts then only
+        waits for an event that completed long before the window trains."""
+        import torch
+        n = self._counts_len()
+        pinned[:n].copy_(self.s.counts[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._pinned = (pinned, ev)
+
     def host_counts(self) -> np.ndarray:
         """One device->host read of the counts vector (the window's only sync);
         with the depth layout the per-(batch, depth) counts follow it."""
         if self._host_counts is None:
-            n = counts_layout(self.num_hops, self.num_batches)["len"]
-            if self.s.depth_layout:
-                n += self.num_batches * (self.num_hops + 1)
-            c = self.s.counts[:n].cpu().numpy()
+            n = self._counts_len()
+            if self._pinned is not None:
+                pinned, ev = self._pinned
+                from .trainer import _host_trace
+                with _host_trace()("wait counts"):
+                    ev.synchronize()
+                c = pinned[:n].numpy().copy()
+            else:
+                c = self.s.counts[:n].cpu().numpy()
             _lib.status_error(int(c[counts_layout(self.num_hops, self.num_batches)["status"]]),
                               "fgl_sample_window")
             self._host_counts = c
@@ -272,7 +296,9 @@ class WindowSampler:
         keys = np.array([philox_key(s) for s in seeds_for_rng], dtype=np.uint64).reshape(-1)
         n = int(off[-1])
         if self._pin_done is not None:
-            self._pin_done.synchronize()  # the previous window's copy has left the staging buffers
+            from .trainer import _host_trace
+            with _host_trace()("wait staging"):
+                self._pin_done.synchronize()  # the previous window's copy has left the staging buffers
         self._pin_seeds.numpy()[:n] = flat
         meta = self._pin_meta.numpy()
         meta[: nb + 1] = off

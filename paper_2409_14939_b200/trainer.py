@@ -32,7 +32,7 @@ from . import _lib
 from .errors import ValidationError
 from .graph import device_graph
 from .memsim import BatchTraffic, CostParams, TrafficReport, t_memory_aware, t_naive
-from .sampler import Fanouts, WindowSampler, derive_seed, make_epoch_batches
+from .sampler import Fanouts, WindowSampler, counts_layout, derive_seed, make_epoch_batches
 from .store import HostFeatureStore
 
 __all__ = ["ModelConfig", "PipelineFlags", "EpochStats", "TrainReport", "train", "derive_seed",
@@ -256,7 +256,7 @@ class Pipeline:
         self.cfg = cfg
         # SM budget of the tensor-core dense kernels while run_windows keeps
         # three other streams busy (fgl_set_dense_ctas; 0 = every SM)
-        self.dense_ctas = int(dense_ctas)
+        self.dense_ctas = int(os.environ.get("FGL_DENSE_CTAS", dense_ctas))
         self.flags = flags or PipelineFlags()
         # device-side limits of a window (checked before any allocation): the
         # match-degree pass keeps all pair counts of a window in registers
@@ -387,9 +387,15 @@ class Pipeline:
         chain on the host (schedule.py:68-113)."""
         if not self.flags.reorder or nb < 2:
             return list(range(nb))
-        ws = win.s.ws.data_ptr()
-        self._call("fgl_match_counts", ws + self.bm_off, self.words, nb, self.pairs.data_ptr(), self.stream)
-        pairs = self.pairs.cpu().numpy()
+        pre = getattr(win, "pairs_host", None)
+        if pre is not None:  # read back behind the sampler (_sample_async)
+            with _host_trace()("wait pairs"):
+                pre[1].synchronize()
+            pairs = pre[0].numpy().copy()
+        else:
+            ws = win.s.ws.data_ptr()
+            self._call("fgl_match_counts", ws + self.bm_off, self.words, nb, self.pairs.data_ptr(), self.stream)
+            pairs = self.pairs.cpu().numpy()
         sizes = [win.unique_range(b)[1] - win.unique_range(b)[0] for b in range(nb)]
         m = np.zeros((nb, nb), dtype=np.float64)
         for i in range(nb):
@@ -864,8 +870,30 @@ class Pipeline:
             win = self._graphed(self._side, 2, lambda: smp.run(nb, off, stream=self._side))
             win.sampled = torch.cuda.Event()
             win.sampled.record(self._side)
+            # the window's counts and match matrix, read back right behind the
+            # sampler: when the window comes up for training (LOOKAHEAD windows
+            # later) its schedule needs no device round trip, so the prepare
+            # and chain launches are not held behind a busy GPU
+            if not hasattr(self, "_pin_counts"):
+                self._pin_counts = [torch.zeros(self._counts_cap(), dtype=torch.int64).pin_memory()
+                                    for _ in range(self.LOOKAHEAD + 1)]
+                self._pairs_dev = [torch.zeros_like(self.pairs) for _ in range(self.LOOKAHEAD + 1)]
+                self._pin_pairs = [torch.zeros(self.pairs.numel(), dtype=torch.int64).pin_memory()
+                                   for _ in range(self.LOOKAHEAD + 1)]
+            win.prefetch_counts(self._pin_counts[slot], self._side)
+            if self.flags.reorder and nb >= 2:
+                self._call("fgl_match_counts", smp.ws.data_ptr() + self.bm_off, self.words, nb,
+                           self._pairs_dev[slot].data_ptr(), self._side.cuda_stream)
+                self._pin_pairs[slot].copy_(self._pairs_dev[slot], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._side)
+                win.pairs_host = (self._pin_pairs[slot], ev)
         self.gpu_launches += 1
         return win
+
+    def _counts_cap(self) -> int:
+        H, nb = self.H, self.cfg.window_n
+        return counts_layout(H, nb)["len"] + nb * (H + 1)
 
     def run_windows(self, windows):
         """Train a sequence of windows [(seed_lists, rng_seeds), ...] on three
@@ -902,79 +930,121 @@ class Pipeline:
             self._prep = torch.cuda.Stream(device=self.device)
             self._io = torch.cuda.Stream(device=self.device)
             self._prep_done = {}
+        if not hasattr(self, "_slot_done"):
+            self._slot_done = {}
         self._main.wait_stream(caller)
         nsmp = self.LOOKAHEAD + 1
+        trace = _host_trace()
         pending = collections.deque()
         for k in range(min(self.LOOKAHEAD, len(windows))):
             pending.append(self._sample_async(*windows[k], slot=k % nsmp))
+
+        def issue_prepare(w):
+            """Schedule window w (its counts and match matrix were read back
+            behind its sampler) and queue its block CSRs and layer-0
+            aggregations on the prepare stream.  Issued right after window
+            w-1's chain, so the prepare runs under that whole chain."""
+            with trace(f"window {w}: counts + schedule"):
+                win = pending.popleft()
+                nb = win.num_batches
+                self.sampler = win.s
+                self._io.wait_event(win.sampled)
+                with torch.cuda.stream(self._io):
+                    self._cs = self._io
+                    win.host_counts()
+                    order = self.schedule(win, nb)
+                    self._cs = None
+            with trace(f"window {w}: prepare issue"):
+                slot = w % 2
+                self._prep.wait_event(win.sampled)
+                if slot in self._prep_done:  # prepare buffers of this slot: window w-2 has trained
+                    self._prep.wait_event(self._prep_done[slot])
+                with torch.cuda.stream(self._prep):
+                    self._cs = self._prep
+
+                    def _prep_work():
+                        lay = self.prepare(win, slot)
+                        self._launch_l0_aggs(win, order, lay, slot, stream=self._prep)
+                        return lay
+                    layers = self._graphed(self._prep, 1, _prep_work)
+                    prepped = torch.cuda.Event()
+                    prepped.record(self._prep)
+                    self._cs = None
+            return win, order, layers, prepped, self._pre_h0
+
+        nxt = issue_prepare(0)
         for w in range(len(windows)):
+            win, order, layers, prepped, pre_h0 = nxt
+            nb = win.num_batches
+            self.sampler = win.s
+            self._pre_h0, self._pre_h0_win = pre_h0, win
             # the caller may still be reading the previous window's losses
             # (e.g. an asynchronous copy of the yielded view): order this
             # window's writes after everything the caller has queued
             self._main.wait_stream(caller)
-            win = pending.popleft()
-            nb = win.num_batches
-            slot = w % 2
-            self.sampler = win.s
-            # the window's sizes and match counts are read on a small stream
-            # that waits for this window's sampling only (not for the prepare
-            # or sampling work queued behind it)
-            self._io.wait_event(win.sampled)
-            with torch.cuda.stream(self._io):
-                self._cs = self._io
-                win.host_counts()
-                order = self.schedule(win, nb)
-                self._cs = None
-            self._prep.wait_event(win.sampled)
-            if slot in self._prep_done:  # prepare buffers of this slot: window w-2 has trained
-                self._prep.wait_event(self._prep_done[slot])
-            with torch.cuda.stream(self._prep):
-                self._cs = self._prep
-                # the weight-independent work of window w -- block CSRs and the
-                # layer-0 aggregations -- runs under window w-1's compute and
-                # the sampling of later windows; buffers alternate between slots
-                def _prep_work():
-                    lay = self.prepare(win, slot)
-                    self._launch_l0_aggs(win, order, lay, slot, stream=self._prep)
-                    return lay
-                layers = self._graphed(self._prep, 1, _prep_work)
-                prepped = torch.cuda.Event()
-                prepped.record(self._prep)
-                self._cs = None
-            if w + self.LOOKAHEAD < len(windows):
-                k = w + self.LOOKAHEAD
-                pending.append(self._sample_async(*windows[k], slot=k % nsmp))
-            with torch.cuda.stream(self._main):
-                self._cs = self._main
-                self._main.wait_event(prepped)
-                if self._graph_mode() and os.environ.get("FGL_GRAPH_WINDOW", "1") != "0":
-                    # the whole window's chain (8 batch steps) as ONE graph:
-                    # no launch gaps between batches either
-                    for b in order:
-                        pre = self._pre_h0.get(b) if (self._pre_h0 is not None and self._pre_h0_win is win) else None
-                        if pre is not None and pre[1] is not None:
-                            self._main.wait_event(pre[1])
+            with trace(f"window {w}: chain issue"):
+                with torch.cuda.stream(self._main):
+                    self._cs = self._main
+                    self._main.wait_event(prepped)
+                    if self._graph_mode() and os.environ.get("FGL_GRAPH_WINDOW", "1") != "0":
+                        # the whole window's chain (8 batch steps) as ONE graph:
+                        # no launch gaps between batches either
+                        for b in order:
+                            pre = self._pre_h0.get(b) if (self._pre_h0 is not None and self._pre_h0_win is win) else None
+                            if pre is not None and pre[1] is not None:
+                                self._main.wait_event(pre[1])
 
-                    def _window_chain():
+                        def _window_chain():
+                            for j, b in enumerate(order):
+                                prev = order[j - 1] if (j > 0 and self.flags.match) else None
+                                self._batch_step_body(win, b, prev, j, layers, j % 2, external_done=True)
+                        self._graphed(self._main, 3, _window_chain)
+                    else:
                         for j, b in enumerate(order):
                             prev = order[j - 1] if (j > 0 and self.flags.match) else None
-                            self._batch_step_body(win, b, prev, j, layers, j % 2, external_done=True)
-                    self._graphed(self._main, 3, _window_chain)
-                else:
-                    for j, b in enumerate(order):
-                        prev = order[j - 1] if (j > 0 and self.flags.match) else None
-                        self.batch_step(win, b, prev, j, layers, j % 2)
-                ev = torch.cuda.Event()
-                ev.record(self._main)
-            self._cs = None
-            if not hasattr(self, "_slot_done"):
-                self._slot_done = {}
+                            self.batch_step(win, b, prev, j, layers, j % 2)
+                    ev = torch.cuda.Event()
+                    ev.record(self._main)
+                self._cs = None
             self._slot_done[w % nsmp] = ev
-            self._prep_done[slot] = ev
+            self._prep_done[w % 2] = ev
             self.last_window = win
+            # next: the sampler LOOKAHEAD windows ahead (its slot was freed by
+            # window w-1's chain), then window w+1's prepare -- both queued
+            # while this window's chain runs on the device
+            with trace(f"window {w}: sampler issue"):
+                if w + self.LOOKAHEAD < len(windows):
+                    k = w + self.LOOKAHEAD
+                    pending.append(self._sample_async(*windows[k], slot=k % nsmp))
+            if w + 1 < len(windows):
+                nxt = issue_prepare(w + 1)
+                self.sampler = win.s
+                self._pre_h0, self._pre_h0_win = pre_h0, win
             caller.wait_stream(self._main)  # the caller's stream sees this window's losses / weights
             yield order, self.loss_dev[:nb]
         self.sampler = self._samplers[0]
+
+
+def _host_trace():
+    """Host-side ranges for tools/timeline.py (FGL_HOST_TRACE=1: profiler
+    record_function annotations; otherwise no-op context managers)."""
+    mode = os.environ.get("FGL_HOST_TRACE", "0")
+    if mode == "1":
+        import torch
+        return torch.profiler.record_function
+    import contextlib
+    if mode == "2":  # perf_counter sums per phase in HOST_TIMES (tools/host_phases.py)
+        @contextlib.contextmanager
+        def timed(name):
+            t = time.perf_counter()
+            yield
+            key = name.split(": ", 1)[-1]
+            HOST_TIMES[key] = HOST_TIMES.get(key, 0.0) + time.perf_counter() - t
+        return timed
+    return lambda name: contextlib.nullcontext()
+
+
+HOST_TIMES: dict = {}
 
 
 def train(g, feats, labels, cfg: ModelConfig, flags: PipelineFlags | None = None, *,

@@ -38,6 +38,26 @@ def run(mode, K=40):
                 self._dup.run(nb, off, stream=self._side)
             return win
         P._sample_async = twice
+    elif mode == "nosample":  # diagnostic: windows re-used, no sampling after the first ones
+        orig = P._sample_async
+        cache = {}
+
+        def reuse(self, seed_lists, rng_seeds, slot):
+            if slot not in cache:
+                cache[slot] = orig(self, seed_lists, rng_seeds, slot)
+            return cache[slot]
+        P._sample_async = reuse
+    elif mode.startswith("skip:"):  # diagnostic: drop the named library calls (results invalid)
+        names = set(mode[5:].split(","))
+        orig_call = P._call
+        state = {"n": 0}
+
+        def call(self, name, *args):
+            if name in names and state.get("armed"):
+                return 0
+            return orig_call(self, name, *args)
+        P._call = call
+        P._armed_state = state
     elif mode in ("agg2", "chain2"):
         orig_call = P._call
         target = "fgl_spmm_gather" if mode == "agg2" else "fgl_dense_fwd"
@@ -51,6 +71,8 @@ def run(mode, K=40):
     for _ in pipe.run_windows(wins[:5]):
         pass
     torch.cuda.synchronize()
+    if hasattr(P, "_armed_state"):
+        P._armed_state["armed"] = True
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in pipe.run_windows(wins[5:5 + K]):

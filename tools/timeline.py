@@ -3,6 +3,7 @@ streams live) from CUPTI via torch.profiler: every kernel's start / end and
 stream over a few windows, written as JSON for offline analysis
 (tools/timeline_report.py).  Usage: python tools/timeline.py OUT.json [config]"""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -26,7 +27,8 @@ def main():
         pass
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    acts = [ProfilerActivity.CUDA] + ([ProfilerActivity.CPU] if os.environ.get("FGL_HOST_TRACE") == "1" else [])
+    with profile(activities=acts) as prof:
         for _ in pipe.run_windows(wins[6:16]):
             pass
         torch.cuda.synchronize()
@@ -35,6 +37,8 @@ def main():
     ev = [dict(name=e["name"], ts=e["ts"], dur=e["dur"], stream=e.get("args", {}).get("stream"),
                cat=e.get("cat")) for e in tr["traceEvents"] if e.get("ph") == "X" and e.get("cat") in
           ("kernel", "gpu_memcpy", "gpu_memset")]
+    ev += [dict(name=e["name"], ts=e["ts"], dur=e["dur"], stream="host", cat="host") for e in tr["traceEvents"]
+           if e.get("ph") == "X" and e.get("cat") == "user_annotation" and e["name"].startswith("window")]
     json.dump(ev, open(out, "w"))
     Path(out + ".trace.json").unlink()
     print("events", len(ev))
