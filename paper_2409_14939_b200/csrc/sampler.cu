@@ -402,7 +402,6 @@ struct SelectArgs {
   unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal2_kernel)
   unsigned long long* hub_cnt;   // hub nodes (d > kBalHub) deferred to select_hub_kernel
   int32_t* hub_list;             // their frontier indices
-  int tile_quota;                // select_bal2_kernel: finite CTAs (per-warp tile quota) instead of a persistent grid
 };
 
 template <int K>
@@ -834,12 +833,7 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
   // no work), later tiles from the dynamic counter past the static ones
   const int64_t nwarps = (int64_t)gridDim.x * kSel2Warps;
   unsigned long long tix = (unsigned long long)(blockIdx.x * (int64_t)kSel2Warps + wib);
-  // finite CTAs: a warp takes at most `quota` tiles (one more than its even
-  // share), so CTAs retire while the hop is still running and the block
-  // scheduler can hand their SM slots to the higher-priority training chain
-  // (a persistent grid held every SM's register file for the whole hop)
-  const int64_t quota = a.tile_quota ? (ntiles + nwarps - 1) / nwarps + 1 : (int64_t)1 << 40;
-  for (int64_t done = 0; done < quota; ++done) {
+  for (;;) {
     if ((int64_t)tix >= ntiles) break;
     const int64_t t0 = (int64_t)tix * 32;
     int TB;
@@ -1347,8 +1341,6 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   int rc = compact_front(0);
   if (rc) return rc;
 
-  // upper bound of each hop's frontier (all batches): sizes the finite select grid
-  int64_t f_ub = std::min<int64_t>(total_seeds, fcap);
   for (int h = 0; h < H; ++h) {
     const int fan = fanouts[h];
     const int32_t* front = o->frontier + h * fcap;
@@ -1389,19 +1381,9 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
                 cudaSuccess || per_sm < 1)
           per_sm = 2;
         static const int sel_sms = env_int("FGL_SEL_SMS", kNumSMs);
-        static const int sel_per_sm = env_int("FGL_SEL_PER_SM", 0);  // cap CTAs per SM (leave room for other streams)
-        if (sel_per_sm > 0) per_sm = std::min(per_sm, sel_per_sm);
         s2_grid_of[fan] = per_sm * std::max(1, std::min(sel_sms, kNumSMs));
       }
-      // finite grid: one 32-entry tile per warp at the frontier's upper bound
-      // (warps past the real frontier exit at once; the quota bounds the rest)
-      static const int finite = env_int("FGL_SEL_FINITE", 0);  // measured slower (2.26 vs 2.20 ms per window)
-      int grid = s2_grid_of[fan];
-      if (finite) {
-        a.tile_quota = 1;
-        grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ceil_div(f_ub, 32), kSel2Warps), 1 << 20));
-      }
-      FGL_COUNT_LAUNCH(), select_bal2_kernel<<<grid, kSel2Warps * 32, s2, stream>>>(
+      FGL_COUNT_LAUNCH(), select_bal2_kernel<<<s2_grid_of[fan], kSel2Warps * 32, s2, stream>>>(
           a, bal_cap(fan), sel2_buf_words(fan));
       static const int hub_ctas = env_int("FGL_HUB_CTAS", 6 * kNumSMs);
       FGL_COUNT_LAUNCH(), select_hub_kernel<<<std::max(1, hub_ctas), kHubThreads, 0, stream>>>(a);
@@ -1413,7 +1395,6 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
     else FGL_COUNT_LAUNCH(), select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
     FGL_LAUNCH_CHECK("select_kernel");
-    f_ub = std::min<int64_t>(std::min<int64_t>(f_ub * fan, (int64_t)nb * g->num_nodes), fcap);
     rc = compact_front(h + 1);
     if (rc) return rc;
   }

@@ -47,6 +47,16 @@ def run(mode, K=40):
                 cache[slot] = orig(self, seed_lists, rng_seeds, slot)
             return cache[slot]
         P._sample_async = reuse
+    elif mode == "skip_aggT1":  # diagnostic: drop the transposed layer-1 aggregation (n > 50K rows)
+        orig_call = P._call
+        state = {}
+
+        def call(self, name, *args):
+            if name == "fgl_spmm" and state.get("armed") and int(args[3]) > 50000:
+                return 0
+            return orig_call(self, name, *args)
+        P._call = call
+        P._armed_state = state
     elif mode.startswith("skip:"):  # diagnostic: drop the named library calls (results invalid)
         names = set(mode[5:].split(","))
         orig_call = P._call

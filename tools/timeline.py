@@ -34,9 +34,12 @@ def main():
         torch.cuda.synchronize()
     prof.export_chrome_trace(out + ".trace.json")
     tr = json.load(open(out + ".trace.json"))
+    def launch_args(a):
+        return {k: a.get(k) for k in ("grid", "block", "registers per thread", "shared memory",
+                                      "est. achieved occupancy %", "warps per SM", "blocks per SM") if k in a}
     ev = [dict(name=e["name"], ts=e["ts"], dur=e["dur"], stream=e.get("args", {}).get("stream"),
-               cat=e.get("cat")) for e in tr["traceEvents"] if e.get("ph") == "X" and e.get("cat") in
-          ("kernel", "gpu_memcpy", "gpu_memset")]
+               cat=e.get("cat"), **launch_args(e.get("args", {}))) for e in tr["traceEvents"]
+          if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
     ev += [dict(name=e["name"], ts=e["ts"], dur=e["dur"], stream="host", cat="host") for e in tr["traceEvents"]
            if e.get("ph") == "X" and e.get("cat") == "user_annotation" and e["name"].startswith("window")]
     json.dump(ev, open(out, "w"))
