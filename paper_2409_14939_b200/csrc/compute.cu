@@ -179,7 +179,6 @@ void launch_spmm_lean(const int64_t* indptr, const int32_t* col, const float* w,
                                                                      ld_self, Y, ldy, d4);
 }
 
-
 template <int L, int CPL>
 void launch_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows,
                  int64_t col_base, const float* X, int64_t ldx, const float* self_x,

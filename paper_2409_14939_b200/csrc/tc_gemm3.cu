@@ -1000,6 +1000,7 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
   }
 }
 
+
 // ------------------------------------------------------------ host side --
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1083,6 +1084,7 @@ bool tc4_disabled() {
   static const int v = getenv("FGL_TC4") ? atoi(getenv("FGL_TC4")) == 0 : 0;
   return v != 0;
 }
+
 
 // tc_dense4_kernel for one [M x N] output with K <= 128, N <= 128 and no K-slice
 // accumulation; false outside that envelope (tc_gemm3 then runs the tile)
