@@ -473,7 +473,7 @@ def _measured_traffic(kernel):
 
 
 _TRAFFIC_KEYS = {"select": "select_bal2_kernel", "aggregate_l0": "spmm_lean_kernel_l0",
-                 "dense_fwd": "tc_gemm3_kernel_l0", "wgrad": "tc_wgrad3_kernel_l0", "gather": "gather_rows_kernel_host"}
+                 "dense_fwd": "tc_dense4_kernel_l0", "wgrad": "tc_wgrad3_kernel_l0", "gather": "gather_rows_kernel_host"}
 
 
 def _peaks():
@@ -618,9 +618,9 @@ def stage_profile(pipe, wins, cfg, torch):
     # --- dense forward / dgrad / weight gradient: HBM (intensity below the ridge); tensor pipe reported
     for name, pid, byte_fn, flop_fn, kname in [
             ("dense_fwd", 4, lambda M, N, K: 4 * (M * K + K * N + 2 * M * N), lambda M, N, K: 2 * M * N * K,
-             "tc_gemm3_kernel<0> (all layers)"),
+             "tc_dense4_kernel<0> (all layers; tc_gemm3 for K slices)"),
             ("dgrad", 5, lambda M, N, K: 4 * (2 * M * K + K * N + M * N), lambda M, N, K: 2 * M * N * K,
-             "tc_gemm3_kernel<1> (all layers)"),
+             "tc_dense4_kernel<1> (all layers; tc_gemm3 for K slices)"),
             ("wgrad", 6, lambda M, K, N: 4 * (M * K + 2 * M * N), lambda M, K, N: 2 * M * K * N,
              "tc_wgrad3_kernel + reduce_partials (all layers)")]:
         mask = ids == pid
