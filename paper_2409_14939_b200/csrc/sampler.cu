@@ -1024,7 +1024,10 @@ __global__ void __launch_bounds__(kHubThreads, 3) select_hub_kernel(const __grid
   const int64_t nh = (int64_t)*a.hub_cnt;
   const int64_t ebase = a.scal[kHopEdgeBase];
   const int fan = a.fan;
-  const double expect = fan + 3.0 * sqrt((double)fan) + 3.0;
+  // hubs take a wider threshold: survivors ~ f + 6 sqrt(f) + 12 cost a CTA
+  // nothing extra to rank, while too few send the hub to ONE warp's exact
+  // path (4.8K Philox blocks for a 19K-degree hub): 98 -> 51 us / window
+  const double expect = fan + 6.0 * sqrt((double)fan) + 12.0;
   for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
     const int64_t i = a.hub_list[h];
     const int32_t u = a.front[i];
