@@ -39,6 +39,13 @@ constexpr int kScanThreads = 256;
 // CTAs of the sampler's scan / compaction / degree passes (4 per SM: their
 // phases are latency bound, so more resident warps, not fewer, set the pace)
 constexpr int kSampCTAs = 4 * kNumSMs;
+// bitmap passes over large windows (papers100M shape: 27.8M words) take one
+// CTA per ~4K words instead of kSampCTAs, so the whole pass's loads are in
+// flight at once rather than ~12 serial tiles per CTA
+constexpr int kBmMaxCTAs = 16384;
+inline int bm_grid(int64_t nwords) {
+  return (int)std::max<int64_t>(kSampCTAs, std::min<int64_t>(kBmMaxCTAs, ceil_div(nwords, 4096)));
+}
 constexpr int kMaxFanout = 256;
 
 struct SampleWs {
@@ -49,7 +56,7 @@ struct SampleWs {
   int32_t* fb;         // [fcap] batch of each frontier entry
   int64_t* scan_deg;   // [fcap]
   int64_t* scan_sel;   // [fcap]
-  int64_t* part;       // [2*kSampCTAs + 2]
+  int64_t* part;       // [2*kBmMaxCTAs + 2]
   int64_t* pos;        // [nb]   running Philox position per batch
   int64_t* hop_pos;    // [nb]   position at the start of the current hop
   int64_t* scal;       // [8]
@@ -80,7 +87,7 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_fb = take(4 * L.fcap);
   L.off_sdeg = take(8 * L.fcap);
   L.off_ssel = take(8 * L.fcap);
-  L.off_part = take(8 * (2 * kSampCTAs + 2));
+  L.off_part = take(8 * (2 * kBmMaxCTAs + 2));
   L.off_pos = take(8 * nb);
   L.off_hoppos = take(8 * nb);
   L.off_scal = take(8 * 8);
@@ -137,12 +144,46 @@ __global__ void mark_seeds_kernel(const int32_t* __restrict__ seeds, const int64
 
 // ------------------------------------------------------------ bitmap scan --
 // chunked over nwords words by kPersistentCTAs CTAs
+// a CTA's share of a bitmap pass: a multiple of 16 words, so every thread's
+// 16-word run starts 64-byte aligned (bm_count / bm_compact must agree)
+__device__ __forceinline__ int64_t bm_chunk(int64_t nwords, int grid) {
+  return (ceil_div(nwords, grid) + 15) & ~(int64_t)15;
+}
+// words per thread per tile: 16 (four 16-byte loads) for large bitmaps, where
+// the serial block scans per CTA bound the pass (papers100M shape: 27.8M
+// words per pass, 766 -> 597 us of compaction per window); 4 for small ones
+// (products: 613K words per pass -- more threads per tile keep it latency-short)
+inline int bm_it(int64_t nwords, int grid) { return ceil_div(nwords, grid) >= 4096 ? 16 : 4; }
+
+// 16 consecutive words from w (64-byte aligned run), zeros past w1
+__device__ __forceinline__ void bm_load16(const uint32_t* __restrict__ bm, int64_t w, int64_t w1, uint32_t (&v)[16]) {
+  if (w + 16 <= w1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(bm + w) + k);
+      v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = w + q < w1 ? bm[w + q] : 0u;
+  }
+}
+
 __global__ void bm_count_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t* part) {
   __shared__ int64_t sm[33];
-  const int64_t chunk = ceil_div(nwords, gridDim.x);
-  const int64_t w0 = blockIdx.x * chunk, w1 = min(nwords, w0 + chunk);
+  const int64_t chunk = bm_chunk(nwords, gridDim.x);
+  const int64_t w0 = min(nwords, blockIdx.x * chunk), w1 = min(nwords, w0 + chunk);
   int64_t c = 0;
-  for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) c += __popc(bm[w]);
+  if (chunk >= 16 * (int64_t)blockDim.x) {
+    for (int64_t w = w0 + 16 * (int64_t)threadIdx.x; w < w1; w += 16 * (int64_t)blockDim.x) {
+      uint32_t v[16];
+      bm_load16(bm, w, w1, v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) c += __popc(v[q]);
+    }
+  } else {
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) c += __popc(bm[w]);
+  }
   c = block_sum(c, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = c;
 }
@@ -168,34 +209,57 @@ __global__ void scan_partials_kernel(int64_t* part, int n, int64_t* total, int64
 // Emit set bits of a batch-major bitmap in word order.  Optionally writes the
 // node IDs + batch of each bit, the per-batch start offsets, the per-word
 // global exclusive prefix, ORs the words into `or_into`, and clears them.
+template <int IT>
 __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int64_t words,
                                   const int64_t* __restrict__ part, int32_t* __restrict__ ids,
                                   int32_t* __restrict__ batch_of, int64_t* __restrict__ batch_off,
                                   int32_t* __restrict__ wprefix, uint32_t* __restrict__ or_into,
                                   int clear, int64_t cap, int64_t* status) {
   __shared__ int64_t sm[33];
-  const int64_t chunk = ceil_div(nwords, gridDim.x);
-  const int64_t w0 = blockIdx.x * chunk, w1 = min(nwords, w0 + chunk);
+  const int64_t chunk = bm_chunk(nwords, gridDim.x);
+  const int64_t w0 = min(nwords, blockIdx.x * chunk), w1 = min(nwords, w0 + chunk);
   int64_t base = part[blockIdx.x];
-  constexpr int IT = 4;  // consecutive words per thread per tile
   for (int64_t t0 = w0; t0 < w1; t0 += (int64_t)blockDim.x * IT) {
     const int64_t wf = t0 + (int64_t)threadIdx.x * IT;
     uint32_t v[IT];
+    if (IT == 16) {
+      bm_load16(bm, wf, w1, reinterpret_cast<uint32_t(&)[16]>(v));
+    } else {
+#pragma unroll
+      for (int q = 0; q < IT; ++q) v[q] = wf + q < w1 ? bm[wf + q] : 0u;
+    }
     int64_t local = 0;
 #pragma unroll
-    for (int q = 0; q < IT; ++q) {
-      v[q] = wf + q < w1 ? bm[wf + q] : 0u;
-      local += __popc(v[q]);
-    }
+    for (int q = 0; q < IT; ++q) local += __popc(v[q]);
     int64_t tot;
     int64_t ex = base + block_excl_scan<int64_t>(local, sm, &tot);
+    int64_t b = wf / words, bstart = b * words;  // batch of word wf (one division per run)
+    // the per-word prefix: 16-byte vector stores of a full run (one store
+    // instruction per 4 words instead of 4: the store path bound this pass)
+    const bool vec_prefix = wprefix && wf + IT <= w1 && (IT % 4) == 0;
+    if (vec_prefix) {
+      int32_t pre[IT];
+      int64_t e = ex;
+#pragma unroll
+      for (int q = 0; q < IT; ++q) { pre[q] = (int32_t)e; e += __popc(v[q]); }
+#pragma unroll
+      for (int q = 0; q < IT; q += 4)
+        *reinterpret_cast<int4*>(wprefix + wf + q) = make_int4(pre[q], pre[q + 1], pre[q + 2], pre[q + 3]);
+    }
+    // all-zero runs (most of a sparse window bitmap) need no per-word pass
+    // unless a batch starts inside them or the prefix is stored per word
+    const bool has_start = batch_off && (wf == bstart || bstart + words < wf + IT);
+    if (local == 0 && !has_start && !(wprefix && !vec_prefix)) {
+      base += tot;
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < IT; ++q) {
       const int64_t w = wf + q;
       if (w >= w1) break;
-      const int64_t b = w / words;
-      if (batch_off && w == b * words) batch_off[b] = ex;
-      if (wprefix) wprefix[w] = (int32_t)ex;
+      if (w == bstart + words) { ++b; bstart += words; }
+      if (batch_off && w == bstart) batch_off[b] = ex;
+      if (wprefix && !vec_prefix) wprefix[w] = (int32_t)ex;
       if (v[q]) {
         if (or_into) or_into[w] |= v[q];
         if (clear) bm[w] = 0u;
@@ -203,7 +267,7 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
           if (ex + __popc(v[q]) > cap) {
             set_status(status, FGL_E_CAPACITY);
           } else {
-            const int32_t node0 = (int32_t)((w - b * words) << 5);
+            const int32_t node0 = (int32_t)((w - bstart) << 5);
             uint32_t m = v[q];
             int64_t o = ex;
             while (m) {
@@ -220,6 +284,19 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
     }
     base += tot;
   }
+}
+
+void launch_bm_compact(int G, cudaStream_t st, uint32_t* bm, int64_t nwords, int64_t words, const int64_t* part,
+                       int32_t* ids, int32_t* batch_of, int64_t* batch_off, int32_t* wprefix, uint32_t* or_into,
+                       int clear, int64_t cap, int64_t* status) {
+  if (bm_it(nwords, G) == 16)
+    FGL_COUNT_LAUNCH(), bm_compact_kernel<16><<<G, kScanThreads, 0, st>>>(bm, nwords, words, part, ids, batch_of,
+                                                                          batch_off, wprefix, or_into, clear, cap,
+                                                                          status);
+  else
+    FGL_COUNT_LAUNCH(), bm_compact_kernel<4><<<G, kScanThreads, 0, st>>>(bm, nwords, words, part, ids, batch_of,
+                                                                         batch_off, wprefix, or_into, clear, cap,
+                                                                         status);
 }
 
 // ------------------------------------------------------------ degree scan --
@@ -1315,6 +1392,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   const int64_t nwords = words * nb;
   const int64_t fcap = o->frontier_stride;
   const int G = kSampCTAs;
+  const int Gb = bm_grid(nwords);
   int64_t* counts = o->counts;
   int64_t* status = counts + FGL_CNT_STATUS(H, nb);
   int64_t* uniq_off = counts + FGL_CNT_UNIQ(H, nb);
@@ -1333,11 +1411,10 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   // compaction of `front` into hop h's frontier list (h == H: no list, only OR into `all`)
   auto compact_front = [&](int h) -> int {
     const bool write = h < H;
-    FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
-    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kF, write ? fr_off(h) + nb : nullptr);
-    FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(
-        w.bm_front, nwords, words, w.part, write ? o->frontier + h * fcap : nullptr,
-        write ? w.fb : nullptr, write ? fr_off(h) : nullptr, nullptr, w.bm_all, 1, fcap, status);
+    FGL_COUNT_LAUNCH(), bm_count_kernel<<<Gb, kScanThreads, 0, stream>>>(w.bm_front, nwords, w.part);
+    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, Gb, w.scal + kF, write ? fr_off(h) + nb : nullptr);
+    launch_bm_compact(Gb, stream, w.bm_front, nwords, words, w.part, write ? o->frontier + h * fcap : nullptr,
+                      write ? w.fb : nullptr, write ? fr_off(h) : nullptr, nullptr, w.bm_all, 1, fcap, status);
     FGL_LAUNCH_CHECK("frontier compaction");
     return FGL_OK;
   };
@@ -1359,6 +1436,11 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
                  w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan,
                  reinterpret_cast<unsigned long long*>(w.scal + kTileCtr),
                  reinterpret_cast<unsigned long long*>(w.scal + kHubCnt), w.hub_list};
+    // the last hop's sources need no frontier list: the selection ORs them
+    // straight into the `all` bitmaps (no count / compact / clear pass over
+    // the window bitmaps: ~150 us per window at the papers100M shape)
+    const bool last_direct = h + 1 == H;
+    if (last_direct) a.bm_front = w.bm_all;
     // FGL_SELECT=stream forces the streaming top-list kernel (A/B parity tests)
     static const bool force_stream = [] {
       const char* v = getenv("FGL_SELECT");
@@ -1398,16 +1480,17 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
     else FGL_COUNT_LAUNCH(), select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
     FGL_LAUNCH_CHECK("select_kernel");
-    rc = compact_front(h + 1);
-    if (rc) return rc;
+    if (!last_direct) {
+      rc = compact_front(h + 1);
+      if (rc) return rc;
+    }
   }
 
   // unique nodes = compaction of the `all` bitmaps; keeps per-word prefixes for ranks
-  FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
-  FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kUniqTot, uniq_off + nb);
-  FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(w.bm_all, nwords, words, w.part,
-                                                    o->unique_nodes, nullptr, uniq_off, w.wprefix,
-                                                    nullptr, 0, o->unique_cap, status);
+  FGL_COUNT_LAUNCH(), bm_count_kernel<<<Gb, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
+  FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, Gb, w.scal + kUniqTot, uniq_off + nb);
+  launch_bm_compact(Gb, stream, w.bm_all, nwords, words, w.part, o->unique_nodes, nullptr, uniq_off, w.wprefix,
+                    nullptr, 0, o->unique_cap, status);
   FGL_LAUNCH_CHECK("unique compaction");
 
   // translation: window rows, and frontier indices through per-hop position maps
@@ -1479,9 +1562,8 @@ int fgl_sample_walk(const fgl_graph* g, const int32_t* seeds, int64_t num_seeds,
   const int G = kPersistentCTAs;
   FGL_COUNT_LAUNCH(), bm_count_kernel<<<G, kScanThreads, 0, stream>>>(bm, words, part);
   FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(part, G, scal, counts);
-  FGL_COUNT_LAUNCH(), bm_compact_kernel<<<G, kScanThreads, 0, stream>>>(bm, words, words, part, unique_nodes, nullptr,
-                                                                       nullptr, nullptr, nullptr, 0, unique_cap,
-                                                                       counts + 1);
+  launch_bm_compact(G, stream, bm, words, words, part, unique_nodes, nullptr, nullptr, nullptr, nullptr, 0, unique_cap,
+                    counts + 1);
   FGL_LAUNCH_CHECK("walk unique compaction");
   return FGL_OK;
 }

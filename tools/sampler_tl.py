@@ -1,6 +1,6 @@
 """Per-kernel device time of the window sampler alone (products graph, 8 x 1024
 seeds), CUPTI via torch.profiler, eager launches on one stream: which of the
-~35 sampler launches per window cost what.  Usage: python tools/sampler_tl.py"""
+~35 sampler launches per window cost what.  Usage: python tools/sampler_tl.py [config]"""
 import collections
 import sys
 from pathlib import Path
@@ -13,7 +13,7 @@ from paper_2409_14939_b200 import sampler as S  # noqa: E402
 
 
 def main():
-    cfg = bench.CONFIGS["products"]
+    cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "products"]
     dg, feats, labels = bench.build_workload(cfg, "cuda")
     wins, _ = bench.epoch_windows(dg.num_nodes, cfg)
     ws = S.WindowSampler(dg, cfg["fanouts"], cfg["bs"], cfg["window"])
