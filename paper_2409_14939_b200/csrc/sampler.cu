@@ -52,6 +52,7 @@ struct SampleWs {
   uint32_t* bm_front;  // [nb*W]
   uint32_t* bm_all;    // [nb*W]
   int32_t* wprefix;    // [nb*W] exclusive popcount prefix of bm_all (global)
+  uint2* wrank;        // [nb*W] {prefix, bm_all word} interleaved: a rank costs one sector
   int32_t* posmap;     // [ucap] window row -> index in a hop's frontier list
   int32_t* fb;         // [fcap] batch of each frontier entry
   int64_t* scan_deg;   // [fcap]
@@ -70,7 +71,7 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
   int64_t words, fcap, bytes;
-  int64_t off_front_bm, off_all_bm, off_wprefix, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
+  int64_t off_front_bm, off_all_bm, off_wprefix, off_wrank, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
       off_pos, off_hoppos, off_scal, off_hub;
 };
 
@@ -83,6 +84,7 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_front_bm = take(4 * L.words * nb);
   L.off_all_bm = take(4 * L.words * nb);
   L.off_wprefix = take(4 * L.words * nb);
+  L.off_wrank = take(8 * L.words * nb);
   L.off_posmap = take(4 * std::max<int64_t>(ucap, 1));
   L.off_fb = take(4 * L.fcap);
   L.off_sdeg = take(8 * L.fcap);
@@ -102,6 +104,7 @@ SampleWs carve(void* base, const WsLayout& L) {
   w.bm_front = reinterpret_cast<uint32_t*>(p + L.off_front_bm);
   w.bm_all = reinterpret_cast<uint32_t*>(p + L.off_all_bm);
   w.wprefix = reinterpret_cast<int32_t*>(p + L.off_wprefix);
+  w.wrank = reinterpret_cast<uint2*>(p + L.off_wrank);
   w.posmap = reinterpret_cast<int32_t*>(p + L.off_posmap);
   w.fb = reinterpret_cast<int32_t*>(p + L.off_fb);
   w.scan_deg = reinterpret_cast<int64_t*>(p + L.off_sdeg);
@@ -214,7 +217,7 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
                                   const int64_t* __restrict__ part, int32_t* __restrict__ ids,
                                   int32_t* __restrict__ batch_of, int64_t* __restrict__ batch_off,
                                   int32_t* __restrict__ wprefix, uint32_t* __restrict__ or_into,
-                                  int clear, int64_t cap, int64_t* status) {
+                                  int clear, int64_t cap, int64_t* status, uint2* __restrict__ wrank) {
   __shared__ int64_t sm[33];
   const int64_t chunk = bm_chunk(nwords, gridDim.x);
   const int64_t w0 = min(nwords, blockIdx.x * chunk), w1 = min(nwords, w0 + chunk);
@@ -245,6 +248,11 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
 #pragma unroll
       for (int q = 0; q < IT; q += 4)
         *reinterpret_cast<int4*>(wprefix + wf + q) = make_int4(pre[q], pre[q + 1], pre[q + 2], pre[q + 3]);
+      if (wrank) {
+#pragma unroll
+        for (int q = 0; q < IT; q += 2)
+          *reinterpret_cast<uint4*>(wrank + wf + q) = make_uint4((uint32_t)pre[q], v[q], (uint32_t)pre[q + 1], v[q + 1]);
+      }
     }
     // all-zero runs (most of a sparse window bitmap) need no per-word pass
     // unless a batch starts inside them or the prefix is stored per word
@@ -259,7 +267,10 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
       if (w >= w1) break;
       if (w == bstart + words) { ++b; bstart += words; }
       if (batch_off && w == bstart) batch_off[b] = ex;
-      if (wprefix && !vec_prefix) wprefix[w] = (int32_t)ex;
+      if (wprefix && !vec_prefix) {
+        wprefix[w] = (int32_t)ex;
+        if (wrank) wrank[w] = make_uint2((uint32_t)ex, v[q]);
+      }
       if (v[q]) {
         if (or_into) or_into[w] |= v[q];
         if (clear) bm[w] = 0u;
@@ -288,15 +299,15 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
 
 void launch_bm_compact(int G, cudaStream_t st, uint32_t* bm, int64_t nwords, int64_t words, const int64_t* part,
                        int32_t* ids, int32_t* batch_of, int64_t* batch_off, int32_t* wprefix, uint32_t* or_into,
-                       int clear, int64_t cap, int64_t* status) {
+                       int clear, int64_t cap, int64_t* status, uint2* wrank = nullptr) {
   if (bm_it(nwords, G) == 16)
     FGL_COUNT_LAUNCH(), bm_compact_kernel<16><<<G, kScanThreads, 0, st>>>(bm, nwords, words, part, ids, batch_of,
                                                                           batch_off, wprefix, or_into, clear, cap,
-                                                                          status);
+                                                                          status, wrank);
   else
     FGL_COUNT_LAUNCH(), bm_compact_kernel<4><<<G, kScanThreads, 0, st>>>(bm, nwords, words, part, ids, batch_of,
                                                                          batch_off, wprefix, or_into, clear, cap,
-                                                                         status);
+                                                                         status, wrank);
 }
 
 // ------------------------------------------------------------ degree scan --
@@ -1160,33 +1171,28 @@ __global__ void __launch_bounds__(kHubThreads, 3) select_hub_kernel(const __grid
 }
 
 // ------------------------------------------------------------ translate ----
-__device__ __forceinline__ int32_t bm_rank(const uint32_t* __restrict__ bm,
-                                           const int32_t* __restrict__ wprefix, int64_t base_word,
-                                           int64_t uniq_base, int32_t g) {
-  const int64_t w = base_word + (g >> 5);
-  const uint32_t below = (1u << (g & 31)) - 1u;
-  return (int32_t)(wprefix[w] + __popc(bm[w] & below) - uniq_base);
+__device__ __forceinline__ int32_t bm_rank(const uint2* __restrict__ wrank, int64_t base_word, int32_t g) {
+  const uint2 pw = __ldg(wrank + base_word + (g >> 5));  // {prefix, word}: one 8-byte load, one sector
+  return (int32_t)(pw.x + __popc(pw.y & ((1u << (g & 31)) - 1u)));
 }
 
 // posmap[row(frontier[j])] = j for every entry j of one hop's frontier list
 __global__ void posmap_kernel(const int32_t* __restrict__ front, const int64_t* __restrict__ fo,
-                              int32_t nb, const uint32_t* __restrict__ bm_all,
-                              const int32_t* __restrict__ wprefix, int64_t words,
+                              int32_t nb, const uint2* __restrict__ wrank, int64_t words,
                               int32_t* __restrict__ posmap) {
   // batch = blockIdx.y: the segment is known, no per-entry search
   const int b = blockIdx.y;
   const int64_t j1 = fo[b + 1];
   for (int64_t j = fo[b] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < j1;
        j += (int64_t)gridDim.x * blockDim.x)
-    posmap[bm_rank(bm_all, wprefix, (int64_t)b * words, 0, front[j])] = (int32_t)j;
+    posmap[bm_rank(wrank, (int64_t)b * words, front[j])] = (int32_t)j;
 }
 
 // window rows of hop h's edges (+ frontier index of the source in hop h+1's
 // list through posmap, or the source row itself for the last hop)
 __global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
                                  const int64_t* __restrict__ eoff, int32_t nb,
-                                 const uint32_t* __restrict__ bm_all,
-                                 const int32_t* __restrict__ wprefix, int64_t words,
+                                 const uint2* __restrict__ wrank, int64_t words,
                                  const int32_t* __restrict__ posmap, int32_t* __restrict__ lt,
                                  int32_t* __restrict__ ls, int32_t* __restrict__ sf) {
   // batch = blockIdx.y (edges are hop-major / batch-minor): no per-edge search
@@ -1194,8 +1200,8 @@ __global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t*
   const int64_t e1 = eoff[b + 1], bw = (int64_t)b * words;
   for (int64_t e = eoff[b] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t rs = bm_rank(bm_all, wprefix, bw, 0, src[e]);
-    if (lt) lt[e] = bm_rank(bm_all, wprefix, bw, 0, tgt[e]);
+    const int32_t rs = bm_rank(wrank, bw, src[e]);
+    if (lt) lt[e] = bm_rank(wrank, bw, tgt[e]);
     if (ls) ls[e] = rs;
     if (sf) sf[e] = posmap ? posmap[rs] : rs;
   }
@@ -1203,14 +1209,13 @@ __global__ void translate_kernel(const int32_t* __restrict__ tgt, const int32_t*
 
 __global__ void translate_seeds_kernel(const int32_t* __restrict__ seeds,
                                        const int64_t* __restrict__ seed_off, int32_t nb,
-                                       int64_t total, const uint32_t* __restrict__ bm_all,
-                                       const int32_t* __restrict__ wprefix, int64_t words,
+                                       int64_t total, const uint2* __restrict__ wrank, int64_t words,
                                        const int32_t* __restrict__ posmap,
                                        int32_t* __restrict__ rows, int32_t* __restrict__ fidx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int b = find_segment(seed_off, nb, i);
-    const int32_t r = bm_rank(bm_all, wprefix, (int64_t)b * words, 0, seeds[i]);
+    const int32_t r = bm_rank(wrank, (int64_t)b * words, seeds[i]);
     if (rows) rows[i] = r;
     if (fidx) fidx[i] = posmap[r];
   }
@@ -1490,7 +1495,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   FGL_COUNT_LAUNCH(), bm_count_kernel<<<Gb, kScanThreads, 0, stream>>>(w.bm_all, nwords, w.part);
   FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, Gb, w.scal + kUniqTot, uniq_off + nb);
   launch_bm_compact(Gb, stream, w.bm_all, nwords, words, w.part, o->unique_nodes, nullptr, uniq_off, w.wprefix,
-                    nullptr, 0, o->unique_cap, status);
+                    nullptr, 0, o->unique_cap, status, w.wrank);
   FGL_LAUNCH_CHECK("unique compaction");
 
   // translation: window rows, and frontier indices through per-hop position maps
@@ -1501,16 +1506,16 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     const bool has_list = h < H && (o->src_front || (h == 0 && o->seed_front));
     if (has_list) {
       FGL_COUNT_LAUNCH(), posmap_kernel<<<dim3(TGb, nb), 256, 0, stream>>>(o->frontier + h * fcap, fr_off(h), nb,
-                                                                       w.bm_all, w.wprefix, words, w.posmap);
+                                                                       w.wrank, words, w.posmap);
     }
     if (h == 0 && (o->seed_rows || o->seed_front)) {
       FGL_COUNT_LAUNCH(), translate_seeds_kernel<<<(int)std::min<int64_t>(ceil_div(total_seeds, 256), TG), 256, 0,
-                               stream>>>(seeds, seed_off, nb, total_seeds, w.bm_all, w.wprefix,
+                               stream>>>(seeds, seed_off, nb, total_seeds, w.wrank,
                                          words, w.posmap, o->seed_rows, o->seed_front);
     }
     if (h >= 1 && want_rows) {  // hop h-1 sources live in hop h's frontier
       FGL_COUNT_LAUNCH(), translate_kernel<<<dim3(TGb, nb), 256, 0, stream>>>(
-          o->tgt, o->src, counts + (h - 1) * nb, nb, w.bm_all, w.wprefix, words, h < H ? w.posmap : nullptr,
+          o->tgt, o->src, counts + (h - 1) * nb, nb, w.wrank, words, h < H ? w.posmap : nullptr,
           o->tgt_row, o->src_row, o->src_front);
     }
     FGL_LAUNCH_CHECK("translate");
