@@ -964,14 +964,20 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
         int nb_end = T.bs[n + 1];
         int64_t kb = (T.p0[n] >> 2) - T.bs[n];
         int32_t s_off = (int32_t)(4 * ((T.p0[n] >> 2) - T.bs[n]) - T.p0[n]);  // slot of word 0 of block g: 4g + s_off
-        int nd = T.d[n], nsh = T.sh[n] + 11, nseg = T.seg[n], ncap = nd < capn ? nd : capn;
+        // survivor word = (key >> (sh + 11)) << 11 | slot: one funnel shift of
+        // the raw word by sh and a mask (no IMAD on the Philox-bound pipe);
+        // the node's segment as a 32-bit shared address
+        const uint32_t sv_u = (uint32_t)__cvta_generic_to_shared(sv);
+        int nd = T.d[n], nsh = T.sh[n], ncap = nd < capn ? nd : capn;
+        uint32_t sbase = sv_u + 4u * (uint32_t)T.seg[n];
         uint64_t twi = T.twi[n], k0 = T.k0[n], k1 = T.k1[n];
         for (; g < gend; ++g) {
           if (g >= nb_end) {  // next node with blocks (zero-block nodes share a start)
             do { ++n; nb_end = T.bs[n + 1]; } while (g >= nb_end);
             kb = (T.p0[n] >> 2) - T.bs[n];
             s_off = (int32_t)(4 * kb - T.p0[n]);
-            nd = T.d[n]; nsh = T.sh[n] + 11; nseg = T.seg[n]; ncap = nd < capn ? nd : capn;
+            nd = T.d[n]; nsh = T.sh[n]; ncap = nd < capn ? nd : capn;
+            sbase = sv_u + 4u * (uint32_t)T.seg[n];
             twi = T.twi[n]; k0 = T.k0[n]; k1 = T.k1[n];
           }
           uint64_t w[4];
@@ -987,11 +993,11 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const _
           if (nt) {
             int c = atomicAdd(&T.cnt[n], nt);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (tk[q]) {
-                if (c < ncap) sv[nseg + c] = ((uint32_t)(w[q] >> nsh) << 11) | (uint32_t)(s0 + q);
-                ++c;
-              }
+            for (int q = 0; q < 4; ++q) {  // predicated stores, no per-survivor branches
+              const uint32_t word = ((uint32_t)(w[q] >> nsh) & 0xFFFFF800u) | (uint32_t)(s0 + q);
+              if (tk[q] && c < ncap)
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sbase + 4u * (uint32_t)c), "r"(word) : "memory");
+              c += tk[q] ? 1 : 0;
             }
           }
         }
