@@ -39,6 +39,7 @@ constexpr int kScanThreads = 256;
 // CTAs of the sampler's scan / compaction / degree passes (4 per SM: their
 // phases are latency bound, so more resident warps, not fewer, set the pace)
 constexpr int kSampCTAs = 4 * kNumSMs;
+constexpr int kDegTile = 1024;  // frontier entries per tile of the single-pass degree scan
 // bitmap passes over large windows (papers100M shape: 27.8M words) take one
 // CTA per ~4K words instead of kSampCTAs, so the whole pass's loads are in
 // flight at once rather than ~12 serial tiles per CTA
@@ -53,6 +54,8 @@ struct SampleWs {
   uint32_t* bm_all;    // [nb*W]
   int32_t* wprefix;    // [nb*W] exclusive popcount prefix of bm_all (global)
   uint2* wrank;        // [nb*W] {prefix, bm_all word} interleaved: a rank costs one sector
+  uint64_t* lb;        // [2 * (fcap / kDegTile + 2)] degree-scan look-back status words (degrees, selections)
+  int32_t* lbflag;     // [4] degree-scan tile counter
   int32_t* posmap;     // [ucap] window row -> index in a hop's frontier list
   int32_t* fb;         // [fcap] batch of each frontier entry
   int64_t* scan_deg;   // [fcap]
@@ -71,7 +74,7 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
   int64_t words, fcap, bytes;
-  int64_t off_front_bm, off_all_bm, off_wprefix, off_wrank, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
+  int64_t off_front_bm, off_all_bm, off_wprefix, off_wrank, off_lb, off_lbflag, off_posmap, off_fb, off_sdeg, off_ssel, off_part,
       off_pos, off_hoppos, off_scal, off_hub;
 };
 
@@ -85,6 +88,8 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_all_bm = take(4 * L.words * nb);
   L.off_wprefix = take(4 * L.words * nb);
   L.off_wrank = take(8 * L.words * nb);
+  L.off_lbflag = take(16);
+  L.off_lb = take(8 * 2 * (L.fcap / kDegTile + 2));  // right after the counter: one memset clears both
   L.off_posmap = take(4 * std::max<int64_t>(ucap, 1));
   L.off_fb = take(4 * L.fcap);
   L.off_sdeg = take(8 * L.fcap);
@@ -105,6 +110,8 @@ SampleWs carve(void* base, const WsLayout& L) {
   w.bm_all = reinterpret_cast<uint32_t*>(p + L.off_all_bm);
   w.wprefix = reinterpret_cast<int32_t*>(p + L.off_wprefix);
   w.wrank = reinterpret_cast<uint2*>(p + L.off_wrank);
+  w.lb = reinterpret_cast<uint64_t*>(p + L.off_lb);
+  w.lbflag = reinterpret_cast<int32_t*>(p + L.off_lbflag);
   w.posmap = reinterpret_cast<int32_t*>(p + L.off_posmap);
   w.fb = reinterpret_cast<int32_t*>(p + L.off_fb);
   w.scan_deg = reinterpret_cast<int64_t*>(p + L.off_sdeg);
@@ -317,64 +324,109 @@ __device__ __forceinline__ void node_deg_sel(const int64_t* __restrict__ off, in
   s = d < fan ? d : fan;
 }
 
-__global__ void deg_up_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ front,
-                              const int64_t* __restrict__ scal, int fan, int64_t* part) {
-  __shared__ int64_t sm[33];
-  const int64_t F = scal[kF];
-  const int64_t chunk = ceil_div(F, gridDim.x);
-  const int64_t i0 = blockIdx.x * chunk, i1 = min(F, i0 + chunk);
-  int64_t cd = 0, cs = 0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    int64_t d, s;
-    node_deg_sel(off, front[i], fan, d, s);
-    cd += d;
-    cs += s;
-  }
-  cd = block_sum(cd, sm);
-  cs = block_sum(cs, sm);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = cd;
-    part[gridDim.x + 1 + blockIdx.x] = cs;
+// Single-pass degree scan of one hop's frontier (decoupled look-back): per
+// entry the draw offset (exclusive scan of degrees) and the output offset
+// (exclusive scan of min(degree, fanout)), plus both totals -- one launch
+// instead of deg_up + two partial scans + deg_down.  Tiles are claimed in
+// launch order through a counter, so a tile only waits on tiles already
+// running.  Each tile publishes a status word per sum, flag in bits 62-63
+// (1 = its aggregate, 2 = its inclusive prefix) -- one 64-bit store, so no
+// fence orders a flag against its value -- and warp 0 looks back 32 tiles
+// per step.
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// exclusive prefix of tile `tile` from the status words of the tiles before it
+__device__ __forceinline__ int64_t lookback_prefix(const uint64_t* st, int64_t tile, int lane) {
+  constexpr uint64_t kVal = (1ull << 62) - 1;
+  int64_t run = 0;
+  int64_t p0 = tile - 1;
+  for (;;) {
+    const int64_t p = p0 - lane;
+    const uint64_t v = p >= 0 ? ld_status(st + p) : (2ull << 62);  // before tile 0: inclusive 0
+    const unsigned flag = (unsigned)(v >> 62);
+    const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+    const unsigned zero = __ballot_sync(0xffffffffu, flag == 0);
+    const int fi = incl ? __ffs(incl) - 1 : 32;  // nearest tile with its inclusive prefix
+    const unsigned need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1u);
+    if (zero & need) continue;  // a tile up to it has not published yet: re-read
+    int64_t x = lane <= fi ? (int64_t)(v & kVal) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    run += x;
+    if (fi < 32) return run;
+    p0 -= 32;
   }
 }
 
-__global__ void deg_down_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ front,
-                                const int64_t* __restrict__ scal, int fan,
-                                const int64_t* __restrict__ part, int64_t* __restrict__ scan_deg,
-                                int64_t* __restrict__ scan_sel) {
+__global__ void __launch_bounds__(kScanThreads) deg_scan_kernel(const int64_t* __restrict__ off,
+                                                                const int32_t* __restrict__ front, int64_t* scal,
+                                                                int fan, int64_t* __restrict__ scan_deg,
+                                                                int64_t* __restrict__ scan_sel, uint64_t* st_d,
+                                                                uint64_t* st_s, int32_t* ctr) {
   __shared__ int64_t sm[33];
+  __shared__ int64_t pre[2];
+  __shared__ int tile_s;
   const int64_t F = scal[kF];
-  const int64_t chunk = ceil_div(F, gridDim.x);
-  const int64_t i0 = blockIdx.x * chunk, i1 = min(F, i0 + chunk);
-  int64_t bd = part[blockIdx.x], bs = part[gridDim.x + 1 + blockIdx.x];
-  constexpr int IT = 4;  // consecutive frontier entries per thread per tile
-  for (int64_t t0 = i0; t0 < i1; t0 += (int64_t)blockDim.x * IT) {
-    const int64_t first = t0 + (int64_t)threadIdx.x * IT;
-    int64_t d[IT], s[IT], ld = 0, ls = 0;
+  const int64_t ntiles = ceil_div(F, kDegTile);
+  if (threadIdx.x == 0) tile_s = atomicAdd(ctr, 1);
+  __syncthreads();
+  const int64_t tile = tile_s;
+  if (tile >= ntiles) {
+    if (tile == 0 && threadIdx.x == 0) { scal[kCandTot] = 0; scal[kSelTot] = 0; }  // empty frontier
+    return;
+  }
+  constexpr int IT = kDegTile / kScanThreads;
+  const int64_t first = tile * kDegTile + (int64_t)threadIdx.x * IT;
+  int64_t d[IT], s[IT], ld = 0, ls = 0;
 #pragma unroll
-    for (int q = 0; q < IT; ++q) {
-      d[q] = 0;
-      s[q] = 0;
-      if (first + q < i1) node_deg_sel(off, front[first + q], fan, d[q], s[q]);
+  for (int q = 0; q < IT; ++q) {
+    d[q] = 0;
+    s[q] = 0;
+    if (first + q < F) node_deg_sel(off, front[first + q], fan, d[q], s[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {  // exclusive within the thread
+    const int64_t x = d[q], y = s[q];
+    d[q] = ld; s[q] = ls;
+    ld += x; ls += y;
+  }
+  int64_t td, ts;
+  const int64_t ed = block_excl_scan(ld, sm, &td);
+  const int64_t es = block_excl_scan(ls, sm, &ts);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0 && tile > 0) {  // aggregates first: later tiles need not wait for this look-back
+      st_status(st_d + tile, (1ull << 62) | (uint64_t)td);
+      st_status(st_s + tile, (1ull << 62) | (uint64_t)ts);
     }
-#pragma unroll
-    for (int q = 0; q < IT; ++q) {  // exclusive within the thread
-      const int64_t a = d[q], c = s[q];
-      d[q] = ld; s[q] = ls;
-      ld += a; ls += c;
-    }
-    int64_t td, ts;
-    const int64_t ed = bd + block_excl_scan(ld, sm, &td);
-    const int64_t es = bs + block_excl_scan(ls, sm, &ts);
-#pragma unroll
-    for (int q = 0; q < IT; ++q) {
-      if (first + q < i1) {
-        scan_deg[first + q] = ed + d[q];
-        scan_sel[first + q] = es + s[q];
+    const int64_t pd = tile > 0 ? lookback_prefix(st_d, tile, lane) : 0;
+    const int64_t ps = tile > 0 ? lookback_prefix(st_s, tile, lane) : 0;
+    if (lane == 0) {
+      st_status(st_d + tile, (2ull << 62) | (uint64_t)(pd + td));
+      st_status(st_s + tile, (2ull << 62) | (uint64_t)(ps + ts));
+      pre[0] = pd;
+      pre[1] = ps;
+      if (tile == ntiles - 1) {  // the hop's totals
+        scal[kCandTot] = pd + td;
+        scal[kSelTot] = ps + ts;
       }
     }
-    bd += td;
-    bs += ts;
+  }
+  __syncthreads();
+  const int64_t bd = pre[0] + ed, bs = pre[1] + es;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    if (first + q < F) {
+      scan_deg[first + q] = bd + d[q];
+      scan_sel[first + q] = bs + s[q];
+    }
   }
 }
 
@@ -1432,14 +1484,21 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
   int rc = compact_front(0);
   if (rc) return rc;
 
+  // upper bound of each hop's frontier (all batches): sizes the degree-scan grid
+  int64_t f_ub = std::min<int64_t>(total_seeds, fcap);
   for (int h = 0; h < H; ++h) {
     const int fan = fanouts[h];
     const int32_t* front = o->frontier + h * fcap;
-    FGL_COUNT_LAUNCH(), deg_up_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part);
-    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part, G, w.scal + kCandTot, nullptr);
-    FGL_COUNT_LAUNCH(), scan_partials_kernel<<<1, 1024, 0, stream>>>(w.part + G + 1, G, w.scal + kSelTot, nullptr);
-    FGL_COUNT_LAUNCH(), deg_down_kernel<<<G, kScanThreads, 0, stream>>>(g->row_offsets, front, w.scal, fan, w.part,
-                                                    w.scan_deg, w.scan_sel);
+    {  // draw / output offsets of the hop's frontier: one single-pass scan
+      const int64_t tiles_max = fcap / kDegTile + 1;
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles_max, ceil_div(f_ub, kDegTile)));
+      // counter and status words are adjacent in the workspace: one memset
+      const int64_t tiles = std::min<int64_t>(tiles_max + 1, ceil_div(f_ub, kDegTile) + 1);
+      FGL_CUDA(cudaMemsetAsync(w.lbflag, 0, reinterpret_cast<char*>(w.lb + 2 * tiles) -
+                                                reinterpret_cast<char*>(w.lbflag), stream));
+      FGL_COUNT_LAUNCH(), deg_scan_kernel<<<(int)grid, kScanThreads, 0, stream>>>(
+          g->row_offsets, front, w.scal, fan, w.scan_deg, w.scan_sel, w.lb, w.lb + tiles, w.lbflag);
+    }
     FGL_COUNT_LAUNCH(), hop_book_kernel<<<1, 64, 0, stream>>>(w, fr_off(h), nb, h, counts, H, o->edge_cap);
     FGL_LAUNCH_CHECK("degree scan");
     SelectArgs a{g->row_offsets, g->col_indices, g->edge_weights, front, w.fb,
@@ -1491,6 +1550,7 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
     else if (fan <= 128) FGL_COUNT_LAUNCH(), select_kernel<4><<<select_grid(4), 256, 0, stream>>>(a);
     else FGL_COUNT_LAUNCH(), select_kernel<8><<<select_grid(8), 256, 0, stream>>>(a);
     FGL_LAUNCH_CHECK("select_kernel");
+    f_ub = std::min<int64_t>(std::min<int64_t>(f_ub * fan, (int64_t)nb * g->num_nodes), fcap);
     if (!last_direct) {
       rc = compact_front(h + 1);
       if (rc) return rc;
