@@ -295,6 +295,16 @@ int fgl_capture_end_launch(fgl_exec* h, void* stream);
 int fgl_capture_abort(void* stream);
 int fgl_capture_stats(int64_t* out3);
 
+/* Events that order work across captured graphs: recorded / waited on with
+ * cudaEventRecordExternal / cudaEventWaitExternal, so inside a capture they
+ * become event-record / event-wait nodes (the window's chain graph waits for
+ * each batch's layer-0 aggregation inside the prepare graph, not for its
+ * end); outside a capture they are a plain record / wait. */
+int fgl_event_create(void** out);
+int fgl_event_destroy(void* ev);
+int fgl_event_record_ext(void* ev, void* stream);
+int fgl_stream_wait_ext(void* stream, void* ev);
+
 int64_t fgl_softmax_xent_ws_bytes(void);
 int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int64_t row_base,
                      const int32_t* seed_ids, const int64_t* labels, int64_t B, int32_t C,

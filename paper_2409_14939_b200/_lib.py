@@ -100,6 +100,10 @@ SIGNATURES = {
     "fgl_exec_destroy": (C.c_int, [vp]),
     "fgl_capture_abort": (C.c_int, [vp]),
     "fgl_capture_stats": (C.c_int, [vp]),
+    "fgl_event_create": (C.c_int, [vp]),
+    "fgl_event_destroy": (C.c_int, [vp]),
+    "fgl_event_record_ext": (C.c_int, [vp, vp]),
+    "fgl_stream_wait_ext": (C.c_int, [vp, vp]),
     "fgl_softmax_xent_ws_bytes": (C.c_int64, []),
     "fgl_softmax_xent": (C.c_int, [vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, C.c_int32,
                                    vp, C.c_int64, vp, vp, C.c_int64, vp]),

@@ -106,6 +106,44 @@ int fgl_capture_end_launch(fgl_exec* h, void* stream) {
   return FGL_OK;
 }
 
+// Cross-graph ordering: events recorded / waited on with the External flags
+// become event-record / event-wait nodes when the stream is being captured
+// (a plain record/wait outside a capture otherwise), so one graph (the
+// window's batch chain) can wait on a point inside another (the prepare
+// graph's per-batch layer-0 aggregation) instead of on its end.
+int fgl_event_create(void** out) {
+  if (!out) return FGL_E_INVALID;
+  cudaEvent_t e = nullptr;
+  FGL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = e;
+  return FGL_OK;
+}
+
+int fgl_event_destroy(void* ev) {
+  if (ev) cudaEventDestroy((cudaEvent_t)ev);
+  return FGL_OK;
+}
+
+static bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
+
+int fgl_event_record_ext(void* ev, void* stream) {
+  if (!ev) return FGL_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (capturing(st)) FGL_CUDA(cudaEventRecordWithFlags((cudaEvent_t)ev, st, cudaEventRecordExternal));
+  else FGL_CUDA(cudaEventRecord((cudaEvent_t)ev, st));
+  return FGL_OK;
+}
+
+int fgl_stream_wait_ext(void* stream, void* ev) {
+  if (!ev) return FGL_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  FGL_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)ev, capturing(st) ? cudaEventWaitExternal : 0));
+  return FGL_OK;
+}
+
 int fgl_capture_stats(int64_t* out3) {
   if (!out3) return FGL_E_INVALID;
   for (int i = 0; i < 3; ++i) out3[i] = g_stats[i].load();

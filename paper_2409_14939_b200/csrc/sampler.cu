@@ -953,7 +953,7 @@ inline int sel2_smem(int fan) {
   return kSel2Warps * (((sel2_buf_words(fan) * 4 + 15) / 16) * 16 + (int)sizeof(Sel2Tab));
 }
 
-__global__ void __launch_bounds__(kSel2Warps * 32, 6) select_bal2_kernel(const __grid_constant__ SelectArgs a,
+__global__ void __launch_bounds__(kSel2Warps * 32, 8) select_bal2_kernel(const __grid_constant__ SelectArgs a,
                                                                         int capn, int buf_words) {
   extern __shared__ __align__(16) uint64_t sbuf2[];
   const int lane = lane_id(), wib = warp_id();

@@ -529,9 +529,12 @@ class Pipeline:
             lib = _lib.lib()
             for h in execs.values():
                 lib.fgl_exec_destroy(h)
+            for h in (getattr(self, "_xevs", None) or {}).values():
+                lib.fgl_event_destroy(h)
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
         self._execs = {}
+        self._xevs = {}
 
     def batch_step(self, win, b, prev, slot, layers, x0_slot):
         """Load x0, forward, loss, backward, SGD for batch b of the window.
@@ -753,6 +756,25 @@ class Pipeline:
         return self._wg_stream
 
     # --------------------------------------------- layer-0 run-ahead --
+    def _xev_on(self) -> bool:
+        """Per-batch cross-graph events between the prepare graph and the
+        window's chain graph (FGL_XEV=0: the chain waits for the whole prepare)."""
+        return (self._graphs_on() and os.environ.get("FGL_GRAPH_WINDOW", "1") != "0"
+                and os.environ.get("FGL_XEV", "1") != "0")
+
+    def _xev(self, slot: int, key):
+        """External-flag CUDA event (slot, key): key "csr" = the window's block
+        CSRs done, j = the j-th layer-0 aggregation of the window done."""
+        if not hasattr(self, "_xevs"):
+            self._xevs = {}
+        h = self._xevs.get((slot, key))
+        if h is None:
+            import ctypes
+            p = ctypes.c_void_p()
+            _lib.call("fgl_event_create", ctypes.byref(p))
+            h = self._xevs[(slot, key)] = p.value
+        return h
+
     def _launch_l0_aggs(self, win, order, layers, slot: int = 0, stream=None):
         """Layer 0's aggregation H0 = A_0 X (features straight from the HBM
         table) depends on the sampled window only, not on the weights, so
@@ -775,8 +797,11 @@ class Pipeline:
         lay = layers[0]
         din = self.cfg.layer_dims[0]
         pre = {}
+        xev = self._xev_on()
         with torch.cuda.stream(stream):
             st = stream.cuda_stream
+            if xev:  # the window's block CSRs are complete here
+                _lib.call("fgl_event_record_ext", self._xev(slot, "csr"), st)
             for j, b in enumerate(order):
                 r0, r1 = self._rows(win, 0, b)
                 n = r1 - r0
@@ -791,7 +816,9 @@ class Pipeline:
                     self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"], lay["w"].data_ptr(),
                                n, 0, self.feats_ptr, self.ldf, None, self.ldf, Hb.data_ptr(), _ld(din), din,
                                st)
-                if self._capturing:  # graph-captured: the window's `prepped` event orders it
+                if xev:  # batch j's H0 is complete here (an event-record node inside the prepare graph)
+                    _lib.call("fgl_event_record_ext", self._xev(slot, j), st)
+                if self._capturing:  # graph-captured: `prepped` or the per-batch external events order it
                     pre[b] = (Hb, None)
                 else:
                     ev = torch.cuda.Event()
@@ -985,7 +1012,10 @@ class Pipeline:
             with trace(f"window {w}: chain issue"):
                 with torch.cuda.stream(self._main):
                     self._cs = self._main
-                    self._main.wait_event(prepped)
+                    pslot = w % 2
+                    xev = self._xev_on() and self._pre_h0 is not None and self._pre_h0_win is win
+                    if not xev:
+                        self._main.wait_event(prepped)
                     if self._graph_mode() and os.environ.get("FGL_GRAPH_WINDOW", "1") != "0":
                         # the whole window's chain (8 batch steps) as ONE graph:
                         # no launch gaps between batches either
@@ -995,7 +1025,12 @@ class Pipeline:
                                 self._main.wait_event(pre[1])
 
                         def _window_chain():
+                            st = self._main.cuda_stream
+                            if xev:  # event-wait nodes on the prepare graph: batch j starts once its H0 is ready
+                                _lib.call("fgl_stream_wait_ext", st, self._xev(pslot, "csr"))
                             for j, b in enumerate(order):
+                                if xev:
+                                    _lib.call("fgl_stream_wait_ext", st, self._xev(pslot, j))
                                 prev = order[j - 1] if (j > 0 and self.flags.match) else None
                                 self._batch_step_body(win, b, prev, j, layers, j % 2, external_done=True)
                         self._graphed(self._main, 3, _window_chain)
