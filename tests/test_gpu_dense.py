@@ -85,3 +85,24 @@ def test_simt_fallback_matches():
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, FGL_DENSE="simt"), cwd=root,
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+def test_tc_dense4_bitidentical_to_tc_gemm3(tmp_path):
+    """tc_dense4 (TMA boxes in the operand layout, the default for K, N <= 128)
+    keeps tc_gemm3's rounding and MMA order: forward and dgrad outputs are
+    bit-identical to the tc_gemm3 kernel (FGL_TC4=0) at the trainer's layer
+    shapes, ragged row counts and a 47-wide output included."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tag, env in (("tc4", {}), ("tc3", {"FGL_TC4": "0"})):
+        path = tmp_path / f"{tag}.npz"
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "tc4_check.py"), str(path)],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert "fallbacks 0" in r.stdout, r.stdout
+        outs[tag] = np.load(path)
+    for key in ("fwd_134000_100_64", "dgrad_134000_100_64", "fwd_16000_64_64", "dgrad_16000_64_64",
+                "fwd_1000_64_47", "dgrad_1000_64_47", "fwd_77_100_64", "dgrad_77_100_64",
+                "fwd_5000_128_128", "dgrad_5000_128_128", "fwd_3000_36_20"):
+        a, b = outs["tc4"][key], outs["tc3"][key]
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), key
