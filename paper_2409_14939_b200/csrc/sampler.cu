@@ -68,7 +68,11 @@ struct SampleWs {
 };
 
 enum Scal { kF = 0, kCandTot = 1, kSelTot = 2, kEdgeBase = 3, kHopEdgeBase = 4, kUniqTot = 5, kTileCtr = 6,
-            kHubCnt = 7 };
+            kHubCnt = 7, kHubBig = 8 };
+// hubs above this degree are queued at the front of the hub list and taken
+// first by select_hub_kernel (longest first: they no longer start in a late
+// wave and set the kernel's tail)
+constexpr int64_t kGiantHub = 6144;
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -97,7 +101,7 @@ WsLayout ws_layout(int64_t num_nodes, int32_t nb, int64_t fcap, int64_t ucap) {
   L.off_part = take(8 * (2 * kBmMaxCTAs + 2));
   L.off_pos = take(8 * nb);
   L.off_hoppos = take(8 * nb);
-  L.off_scal = take(8 * 8);
+  L.off_scal = take(8 * 16);
   L.off_hub = take(4 * L.fcap);
   L.bytes = o;
   return L;
@@ -438,6 +442,7 @@ __global__ void hop_book_kernel(SampleWs w, const int64_t* __restrict__ fr_off, 
     w.scal[kHopEdgeBase] = w.scal[kEdgeBase];
     w.scal[kTileCtr] = 0;  // dynamic tile counter of this hop's select kernel
     w.scal[kHubCnt] = 0;   // hub nodes deferred to select_hub_kernel
+    w.scal[kHubBig] = 0;   // of them the giant ones (front of the list)
   }
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const int64_t f0 = fr_off[b], f1 = fr_off[b + 1];
@@ -541,7 +546,9 @@ struct SelectArgs {
   int fan;
   unsigned long long* tile_ctr;  // dynamic tile scheduling (select_bal2_kernel)
   unsigned long long* hub_cnt;   // hub nodes (d > kBalHub) deferred to select_hub_kernel
-  int32_t* hub_list;             // their frontier indices
+  int32_t* hub_list;             // their frontier indices: giants from the front, the rest from the back
+  unsigned long long* hub_big_cnt = nullptr;
+  int64_t hub_cap = 0;
 };
 
 template <int K>
@@ -1064,7 +1071,10 @@ __global__ void __launch_bounds__(kSel2Warps * 32, 8) select_bal2_kernel(const _
     const int want = (int)(d < fan ? d : fan);
     const int cnt = T.cnt[lane];
     const bool hub = d > kBalHub && a.hub_list;
-    if (hub) a.hub_list[atomicAdd(a.hub_cnt, 1ull)] = (int32_t)i;
+    if (hub) {
+      if (d > kGiantHub) a.hub_list[atomicAdd(a.hub_big_cnt, 1ull)] = (int32_t)i;
+      else a.hub_list[a.hub_cap - 1 - (int64_t)atomicAdd(a.hub_cnt, 1ull)] = (int32_t)i;
+    }
     bool fb = d > 0 && !hub && (!elig || cnt > cap || cnt < want);
     uint32_t* q = sv + surv_cap;  // emission queue after the survivors
     const int nsel = (!fb && !hub && d > 0) ? want : 0;
@@ -1167,7 +1177,8 @@ __global__ void __launch_bounds__(kHubThreads, 3) select_hub_kernel(const __grid
   __shared__ uint32_t sslot[kHubCap];
   __shared__ int scnt;
   const int tid = threadIdx.x;
-  const int64_t nh = (int64_t)*a.hub_cnt;
+  const int64_t nbig = (int64_t)*a.hub_big_cnt;
+  const int64_t nh = nbig + (int64_t)*a.hub_cnt;
   const int64_t ebase = a.scal[kHopEdgeBase];
   const int fan = a.fan;
   // hubs take a wider threshold: survivors ~ f + 6 sqrt(f) + 12 cost a CTA
@@ -1175,7 +1186,7 @@ __global__ void __launch_bounds__(kHubThreads, 3) select_hub_kernel(const __grid
   // path (4.8K Philox blocks for a 19K-degree hub): 98 -> 51 us / window
   const double expect = fan + 6.0 * sqrt((double)fan) + 12.0;
   for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int64_t i = a.hub_list[h];
+    const int64_t i = h < nbig ? a.hub_list[h] : a.hub_list[a.hub_cap - 1 - (h - nbig)];
     const int32_t u = a.front[i];
     const int b = a.fb[i];
     const int64_t e0 = __ldg(a.off + u);
@@ -1506,6 +1517,8 @@ int fgl_sample_window(const fgl_graph* g, const int32_t* seeds, const int64_t* s
                  w.bm_front, words, o->tgt, o->src, o->wgt, o->tgt_front, fan,
                  reinterpret_cast<unsigned long long*>(w.scal + kTileCtr),
                  reinterpret_cast<unsigned long long*>(w.scal + kHubCnt), w.hub_list};
+    a.hub_big_cnt = reinterpret_cast<unsigned long long*>(w.scal + kHubBig);
+    a.hub_cap = fcap;
     // the last hop's sources need no frontier list: the selection ORs them
     // straight into the `all` bitmaps (no count / compact / clear pass over
     // the window bitmaps: ~150 us per window at the papers100M shape)
