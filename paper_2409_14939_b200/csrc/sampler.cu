@@ -45,7 +45,11 @@ constexpr int kDegTile = 1024;  // frontier entries per tile of the single-pass 
 // flight at once rather than ~12 serial tiles per CTA
 constexpr int kBmMaxCTAs = 16384;
 inline int bm_grid(int64_t nwords) {
-  return (int)std::max<int64_t>(kSampCTAs, std::min<int64_t>(kBmMaxCTAs, ceil_div(nwords, 4096)));
+  // one tile per CTA: 4096 words (16-word runs) for large bitmaps, 1024
+  // words (4-word runs) otherwise -- a 1040-word chunk cost a second block
+  // scan for 16 words (products: 613K words over 592 CTAs)
+  const int64_t per = ceil_div(nwords, kSampCTAs) >= 4096 ? 4096 : 1024;
+  return (int)std::max<int64_t>(kSampCTAs, std::min<int64_t>(kBmMaxCTAs, ceil_div(nwords, per)));
 }
 constexpr int kMaxFanout = 256;
 
@@ -230,6 +234,11 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
                                   int32_t* __restrict__ wprefix, uint32_t* __restrict__ or_into,
                                   int clear, int64_t cap, int64_t* status, uint2* __restrict__ wrank) {
   __shared__ int64_t sm[33];
+  // a tile's node IDs are staged in shared memory and written out coalesced
+  // (dense windows -- products unique sets, ~25 % of bits -- had each thread
+  // write its own run: 32 scattered sectors per store instruction)
+  constexpr int kStageIds = 6144;
+  __shared__ int32_t sids[kStageIds];
   const int64_t chunk = bm_chunk(nwords, gridDim.x);
   const int64_t w0 = min(nwords, blockIdx.x * chunk), w1 = min(nwords, w0 + chunk);
   int64_t base = part[blockIdx.x];
@@ -247,6 +256,8 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
     for (int q = 0; q < IT; ++q) local += __popc(v[q]);
     int64_t tot;
     int64_t ex = base + block_excl_scan<int64_t>(local, sm, &tot);
+    const int64_t tile_base = base;
+    const bool staged = ids && !batch_of && tot <= kStageIds && tile_base + tot <= cap;
     int64_t b = wf / words, bstart = b * words;  // batch of word wf (one division per run)
     // the per-word prefix: 16-byte vector stores of a full run (one store
     // instruction per 4 words instead of 4: the store path bound this pass)
@@ -268,12 +279,9 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
     // all-zero runs (most of a sparse window bitmap) need no per-word pass
     // unless a batch starts inside them or the prefix is stored per word
     const bool has_start = batch_off && (wf == bstart || bstart + words < wf + IT);
-    if (local == 0 && !has_start && !(wprefix && !vec_prefix)) {
-      base += tot;
-      continue;
-    }
+    const bool skip = local == 0 && !has_start && !(wprefix && !vec_prefix);
 #pragma unroll
-    for (int q = 0; q < IT; ++q) {
+    for (int q = 0; q < (skip ? 0 : IT); ++q) {
       const int64_t w = wf + q;
       if (w >= w1) break;
       if (w == bstart + words) { ++b; bstart += words; }
@@ -295,7 +303,8 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
             while (m) {
               const int bit = __ffs(m) - 1;
               m &= m - 1;
-              ids[o] = node0 + bit;
+              if (staged) sids[o - tile_base] = node0 + bit;
+              else ids[o] = node0 + bit;
               if (batch_of) batch_of[o] = (int32_t)b;
               ++o;
             }
@@ -303,6 +312,11 @@ __global__ void bm_compact_kernel(uint32_t* __restrict__ bm, int64_t nwords, int
         }
       }
       ex += __popc(v[q]);
+    }
+    if (ids && !batch_of && tot <= kStageIds && tile_base + tot <= cap) {  // block-uniform
+      __syncthreads();
+      for (int64_t k = threadIdx.x; k < tot; k += blockDim.x) ids[tile_base + k] = sids[k];
+      __syncthreads();
     }
     base += tot;
   }
