@@ -241,6 +241,16 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
              int64_t col_base, const float* X, int64_t ldx, const float* self_x, int64_t ld_self,
              float* Y, int64_t ldy, int32_t d, void* stream);
 
+/* fgl_spmm with the source rows addressed through an id map: row c of X is
+ * X + x_ids[c] * ldx (c = col[e] - col_base) and, with add_self, output row r
+ * adds the root term X[x_ids[self_base + r]] -- the GIN / GraphSAGE layer-0
+ * aggregation straight from the HBM feature table (replaces x0 =
+ * feats[unique_nodes], trainer.py:315, followed by compute.aggregate_forward,
+ * compute.py:115-185, + the root term of trainer.py:189-190).  d in 33..128. */
+int fgl_spmm_ids(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows, int64_t col_base,
+                 const float* X, int64_t ldx, const int32_t* x_ids, int64_t self_base, int32_t add_self, float* Y,
+                 int64_t ldy, int32_t d, void* stream);
+
 /* The layer-0 aggregation of the trainer: fgl_spmm over the sampled block
  * graph (rows of <= max_row_len <= 16 edges, the last hop's fanout) gathering
  * straight from the HBM feature table X [x_rows, ldx], ldx <= 256.  No self

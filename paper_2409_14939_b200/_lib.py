@@ -80,6 +80,8 @@ SIGNATURES = {
                                             vp, vp, vp, C.c_int64, vp]),
     "fgl_prepare_layer": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp, vp,
                                     vp, vp, vp, vp, C.c_int64, vp]),
+    "fgl_spmm_ids": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64, C.c_int32, vp,
+                               C.c_int64, C.c_int32, vp]),
     "fgl_spmm": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_int64,
                            vp, C.c_int64, C.c_int32, vp]),
     "fgl_spmm_gather": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int64, vp, C.c_int64,

@@ -118,11 +118,15 @@ __global__ void __launch_bounds__(256) spmm_kernel(
 // aggregation (fgl_spmm_gather: rows of <= fanout edges from the HBM feature
 // table), the upper layers and the transposed (~1-edge rows) backward
 // aggregations.
+// xids (fgl_spmm_ids): source row c reads X row xids[c] and the root term of
+// output row r is X row xids[self_base + r] (GIN / SAGE layer 0 straight from
+// the HBM feature table, no x0 block); the arithmetic is unchanged.
 template <int G, int W>
 __global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ col, const float* __restrict__ w,
     int64_t nrows, int64_t col_base, const float* __restrict__ X, int64_t ldx, const float* __restrict__ self_x,
-    int64_t ld_self, float* __restrict__ Y, int64_t ldy, int d4) {
+    int64_t ld_self, float* __restrict__ Y, int64_t ldy, int d4, const int32_t* __restrict__ xids = nullptr,
+    int64_t self_base = 0) {
   const int lane = threadIdx.x & (W - 1);
   const unsigned mask = W == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / W;
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
       float wl = 0.f;
       if (lane < m) {
         cl = (int32_t)(col[b + u0 + lane] - col_base);
+        if (xids) cl = __ldg(xids + cl);
         wl = w[b + u0 + lane];
       }
       for (int u = 0; u < m; u += G) {
@@ -157,7 +162,8 @@ __global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
     }
     if (lane < d4) {
       if (self_x) {  // GIN / SAGE root term: h = aggregate + x, one rounded add (trainer.py:189-190)
-        const float4 sx = reinterpret_cast<const float4*>(self_x + r * ld_self)[lane];
+        const int64_t sr = xids ? (int64_t)__ldg(xids + self_base + r) : r;
+        const float4 sx = reinterpret_cast<const float4*>(self_x + sr * ld_self)[lane];
         acc.x = __fadd_rn(acc.x, sx.x); acc.y = __fadd_rn(acc.y, sx.y);
         acc.z = __fadd_rn(acc.z, sx.z); acc.w = __fadd_rn(acc.w, sx.w);
       }
@@ -168,15 +174,16 @@ __global__ void __launch_bounds__(256, 8) spmm_lean_kernel(
 
 void launch_spmm_lean(const int64_t* indptr, const int32_t* col, const float* w, int64_t nrows, int64_t col_base,
                       const float* X, int64_t ldx, const float* self_x, int64_t ld_self, float* Y, int64_t ldy,
-                      int d4, cudaStream_t st, int64_t max_ctas = (int64_t)kNumSMs * 8) {
+                      int d4, cudaStream_t st, int64_t max_ctas = (int64_t)kNumSMs * 8,
+                      const int32_t* xids = nullptr, int64_t self_base = 0) {
   const int per_cta = d4 <= 16 ? 16 : 8;  // rows per 256-thread CTA
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, per_cta), max_ctas));
   if (d4 <= 16)
     FGL_COUNT_LAUNCH(), spmm_lean_kernel<2, 16><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
-                                                                     ld_self, Y, ldy, d4);
+                                                                     ld_self, Y, ldy, d4, xids, self_base);
   else
     FGL_COUNT_LAUNCH(), spmm_lean_kernel<2, 32><<<grid, 256, 0, st>>>(indptr, col, w, nrows, col_base, X, ldx, self_x,
-                                                                     ld_self, Y, ldy, d4);
+                                                                     ld_self, Y, ldy, d4, xids, self_base);
 }
 
 template <int L, int CPL>
@@ -724,6 +731,35 @@ int fgl_spmm(const int64_t* indptr, const int32_t* col, const float* w, int64_t 
   }
   return spmm_dispatch(indptr, col, w, num_rows, col_base, X, ldx, self_x, ld_self, Y, ldy, d, (cudaStream_t)stream,
                        kProfSpmm);
+}
+
+// fgl_spmm with the source rows addressed through an id map (x_ids): the
+// GIN / SAGE layer-0 aggregation (and its root term) read the HBM feature
+// table directly instead of an x0 block gathered first.  Feature widths of
+// 36..128 (the lean kernel); FGL_E_UNSUPPORTED otherwise.
+int fgl_spmm_ids(const int64_t* indptr, const int32_t* col, const float* w, int64_t num_rows, int64_t col_base,
+                 const float* X, int64_t ldx, const int32_t* x_ids, int64_t self_base, int32_t add_self, float* Y,
+                 int64_t ldy, int32_t d, void* stream) {
+  if (num_rows < 0 || d < 1 || !indptr || !Y || !X || !x_ids || ldy < d || ldx < d || (ldx % 4) || (ldy % 4)) {
+    set_error("fgl_spmm_ids: bad arguments");
+    return FGL_E_INVALID;
+  }
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) {
+    set_error("fgl_spmm_ids: feature pointers must be 16-byte aligned");
+    return FGL_E_INVALID;
+  }
+  const int d4 = (d + 3) / 4;
+  if (d4 <= 8 || d4 > 32) {
+    set_error("fgl_spmm_ids: feature width %d outside 33..128", d);
+    return FGL_E_UNSUPPORTED;
+  }
+  if (num_rows == 0) return FGL_OK;
+  const ProfMark pm = prof_begin((cudaStream_t)stream);
+  launch_spmm_lean(indptr, col, w, num_rows, col_base, X, ldx, add_self ? X : nullptr, ldx, Y, ldy, d4,
+                   (cudaStream_t)stream, (int64_t)kNumSMs * 8, x_ids, self_base);
+  prof_end(pm, kProfSpmm, num_rows, d);
+  FGL_LAUNCH_CHECK("spmm_lean_kernel(ids)");
+  return FGL_OK;
 }
 
 // Layer-0 aggregation over the sampled block graph (rows of <= max_row_len

@@ -314,6 +314,12 @@ class Pipeline:
         if direct_x0 is None:
             direct_x0 = False
         self.direct_x0 = bool(direct_x0) and feature_store == "device" and self.compact
+        # GIN / SAGE (depth-major rows): the layer-0 aggregation and its root
+        # term read the table through the batch's row -> node id map
+        # (fgl_spmm_ids) instead of a gathered x0 block (FGL_DIRECT_IDS=0: x0)
+        d4 = (cfg.layer_dims[0] + 3) // 4
+        self.direct_ids = (bool(direct_x0) and feature_store == "device" and not self.compact and 8 < d4 <= 32
+                           and os.environ.get("FGL_DIRECT_IDS", "1") != "0")
         self.pairs = torch.zeros(120, dtype=torch.int64, device=device)
         # rows read from the feature store / served by the static cache, per
         # schedule position of the window (BatchTraffic rows of memsim.py:52-60)
@@ -577,7 +583,7 @@ class Pipeline:
         HBM table itself and there is no x0 block."""
         s = self.sampler
         st = self.stream
-        if self.direct_x0:
+        if self.direct_x0 or self.direct_ids:
             return self.feats
         u0, u1 = win.unique_range(b)
         U = u1 - u0
@@ -636,8 +642,16 @@ class Pipeline:
                 col, base = lay["col"], self._in_base(win, i, b)
                 if i == 0 and self.direct_x0:
                     col, base = lay["col_global"], 0
-                self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
-                           base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
+                if i == 0 and self.direct_ids:
+                    # batch-local row c -> node id unique[u0 + c]: neighbour rows
+                    # and the root term straight from the HBM table
+                    u0 = win.unique_range(b)[0]
+                    self._call("fgl_spmm_ids", lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(),
+                               n, base, self.feats_ptr, self.ldf, s.unique.data_ptr() + 4 * u0, r0 - u0, 1,
+                               Hb.data_ptr(), _ld(din), din, st)
+                else:
+                    self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
+                               base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
             if i == self.L - 1 and top_fused:
                 Yb = None  # the fused top-layer kernel computes the logits itself
             else:
