@@ -798,7 +798,7 @@ class Pipeline:
         kernels of earlier batches.  Results are identical (same kernel, same
         inputs).  Only for the direct-x0 compact layout (features in HBM)."""
         torch = self.torch
-        if not (self.direct_x0 and self.compact):
+        if not ((self.direct_x0 and self.compact) or self.direct_ids):
             self._pre_h0 = None
             return
         if stream is None:
@@ -820,7 +820,12 @@ class Pipeline:
                 r0, r1 = self._rows(win, 0, b)
                 n = r1 - r0
                 Hb = self._buf(f"h0_run{j}s{slot}", n, _ld(din))
-                if self.ldf <= 128:
+                if self.direct_ids:  # GIN / SAGE: table rows through the row -> node id map, root term included
+                    u0 = win.unique_range(b)[0]
+                    self._call("fgl_spmm_ids", lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(), n,
+                               self._in_base(win, 0, b), self.feats_ptr, self.ldf, win.s.unique.data_ptr() + 4 * u0,
+                               r0 - u0, 1, Hb.data_ptr(), _ld(din), din, st)
+                elif self.ldf <= 128:
                     # rows hold <= fanout edges: the software-pipelined short-row
                     # kernel (bit-identical to fgl_spmm)
                     self._call("fgl_spmm_gather", lay["indptr"].data_ptr() + 8 * r0, lay["col_global"],

@@ -350,7 +350,7 @@ def test_papers_sampling_bit_exact():
 def test_direct_table_layer0_bitidentical(products, products_window, arch):
     """GIN / GraphSAGE with the feature table in HBM: the layer-0 aggregation
     and its root term read the table through the batch's row -> node id map
-    (fgl_spmm_ids) instead of a gathered x0 block.  Same rows, same edge order,
+    (fgl_spmm_ids, run ahead of the chain) instead of a gathered x0 block.  Same rows, same edge order,
     same arithmetic: the layer-0 output, the loss and every gradient are
     bit-identical to the x0 path."""
     from paper_2409_14939_b200 import trainer
@@ -367,7 +367,10 @@ def test_direct_table_layer0_bitidentical(products, products_window, arch):
         assert pipe.direct_ids == direct
         _, losses = pipe.run_window([seeds[0]], [rs[0]])
         r0, r1 = pipe._rows(pipe.last_window, 0, 0)
-        h0 = pipe._bufs["h0"][: (r1 - r0) * 100].view(r1 - r0, 100).cpu().numpy()
+        # the x0 path aggregates layer 0 in the batch step; the table path runs it
+        # ahead of the chain (weight-independent) into its own buffer
+        hbuf = pipe._pre_h0[0][0] if pipe._pre_h0 else pipe._bufs["h0"]
+        h0 = hbuf[: (r1 - r0) * 100].view(r1 - r0, 100).cpu().numpy()
         out[direct] = (h0, losses.cpu().numpy().copy(), pipe.model.grads_numpy())
     (h_a, l_a, g_a), (h_b, l_b, g_b) = out[False], out[True]
     assert np.array_equal(h_a.view(np.uint32), h_b.view(np.uint32))
