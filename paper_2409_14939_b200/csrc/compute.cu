@@ -802,8 +802,9 @@ static bool dgrad_tc(const float* dX, int64_t lddx, const float* Xout, int64_t l
   if ((lddx % 4) || (Xout && (ldxo % 4)) || (lddh % 4) || (reinterpret_cast<uintptr_t>(dH) & 15)) return false;
   // [column slice of dH (rows of W)] x [K slice of dout]: the widest slices
   // whose first tile fits shared memory; K slices accumulate into dH
+  const int kfirst = dout > 128 ? dout : 128;  // one K slice first (tc_dense4 streams the weight)
   for (int nsw = 256; nsw >= 64; nsw /= 2) {
-    for (int ksw = 128; ksw >= 32; ksw /= 2) {
+    for (int ksw = kfirst; ksw >= 32; ksw = ksw > 128 ? 128 : ksw / 2) {
       bool ok = true;
       for (int n0 = 0; n0 < din && ok; n0 += nsw) {
         const int ns = din - n0 < nsw ? din - n0 : nsw;
@@ -838,7 +839,10 @@ int fgl_dense_fwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
     // largest whose first (widest) tile fits the kernel's shared memory (the
     // weight's hi / lo images grow with K x N)
     bool ok = false;
-    for (int ksw = 128; ksw >= 64 && !ok; ksw /= 2) {
+    // one K slice first (tc_dense4 streams the weight's K boxes through its
+    // stages for din > 128), then 128 / 64-wide slices accumulated by tc_gemm3
+    const int kfirst = din > 128 ? din : 128;
+    for (int ksw = kfirst; ksw >= 64 && !ok; ksw = ksw > 128 ? 128 : ksw / 2) {
       for (int nsw = 128; nsw >= 32 && !ok; nsw /= 2) {
         ok = true;
         for (int n0 = 0; n0 < dout && ok; n0 += nsw) {

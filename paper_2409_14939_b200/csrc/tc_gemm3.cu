@@ -84,7 +84,7 @@ __device__ __forceinline__ float tf32_rna_finite(float x) {
 // boxes of 32 K columns, by `nt` threads (t0 = 0..nt-1); 4x4 blocks over
 // [N_pad x K_pad] (padding included: no zeroing pass), four 16-byte W loads,
 // a register transpose for mode 0 (B = W^T), eight 16-byte shared stores
-template <int MODE>
+template <int MODE, bool SRC_SMEM = false>
 __device__ __forceinline__ void split_weight_image(const float* __restrict__ W, int64_t ldw, int K, int N, int K_pad,
                                                    int N_pad, bool vec, char* sB_hi, char* sB_lo, int t0, int nt) {
   const int b_box = N_pad * 128;
@@ -95,7 +95,8 @@ __device__ __forceinline__ void split_weight_image(const float* __restrict__ W, 
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < wr && c < rl) {
       const float* src = W + (int64_t)r * ldw + c;
-      if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
+      if (SRC_SMEM) v = *reinterpret_cast<const float4*>(src);  // TMA-staged box: zero-filled past the edge
+      else if (vec && c + 3 < rl) v = __ldg(reinterpret_cast<const float4*>(src));
       else {
         v.x = __ldg(src);
         if (c + 1 < rl) v.y = __ldg(src + 1);
@@ -770,14 +771,23 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
 //               hi*W_hi (A from shared memory) into a double-buffered fp32
 //               accumulator; one commit per box frees its stage;
 //   warps 8-11  epilogue: tcgen05.ld, bias, ReLU, SW128 staging boxes, TMA
-//               tensor stores.
+//               tensor stores;
+//   warps 2-3   (K > 128 only, "streamed weight") the weight image would not
+//               fit beside the stages (Reddit's 602 inputs: 304 KB), so each
+//               stage also carries the raw [32 K x N] weight box, TMA-loaded
+//               from L2 with the A box, which warps 2-3 split into the stage's
+//               own hi / lo boxes while the splitters split A.  One pass over
+//               A instead of K slices that re-read and re-accumulate the
+//               output (Reddit layer 0: 208 -> 175 us).  The accumulation
+//               chain in TMEM is then K long instead of 128 (results within
+//               1e-5, not bit-identical to the sliced path).
 //
 // Against tc_gemm3 (whole-row bulk copies converted into a TMEM A ring by
 // thread-per-row converters): a stage is 16 KB instead of a 51 KB tile, so
 // 8 stages (128 KB of loads in flight per SM) fit beside the weight images,
 // and the tensor core reads the hi part straight from the landed box.  Same
 // rounding and the same MMA order as tc_gemm3 (bit-identical results).
-constexpr int T4_THREADS = 384;  // 12 warps, roles above (warps 2-3 only split the weight)
+constexpr int T4_THREADS = 384;  // 12 warps, roles above (warps 2-3 split the weight)
 constexpr int T4_M = 128;
 constexpr int T4_BOX = T4_M * 128;  // one [128 rows x 32 fp32] SW128 box
 constexpr int T4_MAX_STAGES = 12;
@@ -787,22 +797,29 @@ struct T4Args {
   const float* bias;   // mode 0 only, [N] or null
   int64_t M, ldw;
   int N, K, N_pad, K_pad, S, relu, has_mask, tmem_cols, w_vec, stage_off, dbg;
+  int stream_w;  // K > 128: each stage carries its K box of the weight, no image
+  int w_raw;     // stream_w: bytes of the TMA-staged raw weight box (1024-aligned slot)
+  int w_ld;      // stream_w: row length of the raw box in floats
 };
 
 template <int MODE>
 __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                   const __grid_constant__ CUtensorMap tmM,
-                                                                  const __grid_constant__ CUtensorMap tmC, T4Args p) {
+                                                                  const __grid_constant__ CUtensorMap tmC,
+                                                                  const __grid_constant__ CUtensorMap tmW, T4Args p) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = p.S, N_pad = p.N_pad;
   const int KB = (p.K + 31) / 32;  // A boxes per tile (= weight image boxes)
   const int b_box = N_pad * 128;
+  const int img_boxes = p.stream_w ? 0 : KB;
   char* sB_hi = smem;
-  char* sB_lo = sB_hi + KB * b_box;
-  char* stages = sB_lo + KB * b_box;  // S x {A box, mask box}
-  const int stage_bytes = T4_BOX * (1 + p.has_mask);
+  char* sB_lo = sB_hi + img_boxes * b_box;
+  char* stages = sB_lo + img_boxes * b_box;  // S x {A box, mask box[, W hi box, W lo box, raw W box]}
+  const int stage_bytes = T4_BOX * (1 + p.has_mask) + (p.stream_w ? 2 * b_box + ((p.w_raw + 1023) & ~1023) : 0);
+  auto stage_w = [&](int s) { return stages + s * stage_bytes + T4_BOX * (1 + p.has_mask); };
+  const uint32_t tx_bytes = (uint32_t)(T4_BOX * (1 + p.has_mask)) + (p.stream_w ? (uint32_t)p.w_raw : 0u);
   char* stg = smem + p.stage_off;     // epilogue staging: ceil(N_pad / 32) boxes
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + ((N_pad + 31) / 32) * T4_BOX);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
@@ -813,7 +830,7 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init_n(bar(FULL + s), 1);
-      mbar_init_n(bar(SPLIT + s), 128);
+      mbar_init_n(bar(SPLIT + s), 128 + (p.stream_w ? 64 : 0));  // + the weight-box producers
       mbar_init_n(bar(EMPTY + s), 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -830,15 +847,19 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       if (p.has_mask) tma_prefetch_desc(&tmM);
+      if (p.w_raw) tma_prefetch_desc(&tmW);
       int g = 0;
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         for (int b = 0; b < KB; ++b, ++g) {
           const int s = g % S;
           mbar_wait(bar(EMPTY + s), ((uint32_t)(g / S) & 1u) ^ 1u);
           const uint32_t dst = smem_u32(stages + s * stage_bytes);
-          mbar_arrive_expect_tx(bar(FULL + s), (uint32_t)stage_bytes);
+          mbar_arrive_expect_tx(bar(FULL + s), tx_bytes);
           tma_load_2d(dst, &tmA, 32 * b, (int)(t * T4_M), bar(FULL + s));  // OOB rows / columns: zeros
           if (p.has_mask) tma_load_2d(dst + T4_BOX, &tmM, 32 * b, (int)(t * T4_M), bar(FULL + s));
+          if (p.w_raw)  // raw weight box b (L2-resident): rows 32b.. (mode 0) / columns 32b.. (mode 1)
+            tma_load_2d(smem_u32(stage_w(s) + 2 * b_box), &tmW, MODE == 0 ? 0 : 32 * b, MODE == 0 ? 32 * b : 0,
+                        bar(FULL + s));
         }
       }
     }
@@ -848,7 +869,8 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
   // the weight image, by every non-producer warp but the MMA issuer (the
   // first boxes are still in flight), then bias -> shared
   if (warp >= 2) {
-    split_weight_image<MODE>(p.W, p.ldw, p.K, p.N, p.K_pad, N_pad, p.w_vec, sB_hi, sB_lo, tid - 64, T4_THREADS - 64);
+    if (!p.stream_w)
+      split_weight_image<MODE>(p.W, p.ldw, p.K, p.N, p.K_pad, N_pad, p.w_vec, sB_hi, sB_lo, tid - 64, T4_THREADS - 64);
     for (int c = tid - 64; c < N_pad; c += T4_THREADS - 64)
       sbias[c] = (MODE == 0 && p.bias && c < p.N) ? p.bias[c] : 0.f;
     fence_async_smem();
@@ -880,10 +902,13 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
         tc_fence_after();
         const int kst = min(32, p.K_pad - 32 * b) / 8;
         const uint32_t ahi = smem_u32(stages + s * stage_bytes), alo = lo_col(s);
+        // weight box of this K slice: the stage's own copy, or box b of the image
+        const uint32_t wbh = p.stream_w ? smem_u32(stage_w(s)) : bh + (uint32_t)(b * b_box);
+        const uint32_t wbl = p.stream_w ? wbh + (uint32_t)b_box : bl + (uint32_t)(b * b_box);
         if (elect_one()) {
           for (int st = 0; st < ((p.dbg & 2) ? 0 : kst); ++st) {
-            const uint32_t bo = (uint32_t)(b * b_box + st * 32);
-            const uint64_t dbh = umma_desc_sw128(bh + bo), dbl = umma_desc_sw128(bl + bo);
+            const uint32_t bo = (uint32_t)(st * 32);
+            const uint64_t dbh = umma_desc_sw128(wbh + bo), dbl = umma_desc_sw128(wbl + bo);
             const uint64_t dah = umma_desc_sw128(ahi + (uint32_t)(st * 32));
             mma_tf32_ts(acc, alo + 8 * st, dbh, idesc, (b | st) != 0);
             mma_tf32(acc, dah, dbl, idesc, 1);
@@ -895,6 +920,27 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
       }
       if (elect_one()) mma_commit(bar(TFULL + a));
       __syncwarp();
+    }
+  } else if (warp >= 2 && warp < 4 && p.stream_w) {
+    // ------------------------------------------------ weight-box producers --
+    // (K > 128) warps 2-3 split each stage's TMA-staged raw 32-wide K box of
+    // the weight into the stage's hi / lo boxes, beside the splitters
+    int g = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int b = 0; b < KB; ++b, ++g) {
+        const int s = g % S;
+        mbar_wait(bar(FULL + s), (uint32_t)(g / S) & 1u);
+        const int kl = min(32, p.K - 32 * b), kpl = min(32, p.K_pad - 32 * b);
+        char* swh = stage_w(s);
+        if (p.w_raw)
+          split_weight_image<MODE, true>(reinterpret_cast<const float*>(swh + 2 * b_box), p.w_ld, kl, p.N, kpl,
+                                         N_pad, true, swh, swh + b_box, tid - 64, 64);
+        else  // weight rows not 16-byte aligned (no TMA): straight from L2
+          split_weight_image<MODE>(MODE == 0 ? p.W + (int64_t)(32 * b) * p.ldw : p.W + 32 * b, p.ldw, kl, p.N, kpl,
+                                   N_pad, p.w_vec, swh, swh + b_box, tid - 64, 64);
+        fence_async_smem();
+        mbar_arrive(bar(SPLIT + s));
+      }
     }
   } else if (warp >= 4 && warp < 8) {
     // --------------------------------------------------------- splitters --
@@ -937,9 +983,9 @@ __global__ void __launch_bounds__(T4_THREADS, 1) tc_dense4_kernel(const __grid_c
         }
         if (!(p.dbg & 1)) {
           tmem_st32(lo_col(s) + lane_off, lv);
-          tmem_st_wait();
         }
-        fence_async_smem();  // hi stores -> visible to the tensor core (async proxy)
+        if (!(p.dbg & 1)) tmem_st_wait();
+        fence_async_smem();  // hi / weight stores -> visible to the tensor core (async proxy)
         tc_fence_before();
         mbar_arrive(bar(SPLIT + s));
       }
@@ -1026,8 +1072,9 @@ bool make_map_sw128(CUtensorMap* m, const float* base, int64_t rows, int cols, i
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   cuuint32_t box[2] = {32, (cuuint32_t)G3_M};
   cuuint32_t es[2] = {1, 1};
+  static const int promo = getenv("FGL_A_L2PROMO") ? atoi(getenv("FGL_A_L2PROMO")) : 0;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1086,23 +1133,33 @@ bool tc4_disabled() {
 }
 
 
-// tc_dense4_kernel for one [M x N] output with K <= 128, N <= 128 and no K-slice
+// tc_dense4_kernel for one [M x N] output with N <= 128, K <= FGL_TC4_KMAX
+// (default 1024; K > 128 streams the weight per stage) and no K-slice
 // accumulation; false outside that envelope (tc_gemm3 then runs the tile)
 bool tc_dense4(int mode, const float* A, int64_t lda, const float* mask, int64_t ldm, const float* W,
                const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu, int64_t ldw,
                cudaStream_t st, int* err) {
   *err = 0;
-  if (tc4_disabled() || M < 1 || K < 1 || K > 128 || N < 1 || N > 128) return false;
+  static const int kmax_stream = getenv("FGL_TC4_KMAX") ? atoi(getenv("FGL_TC4_KMAX")) : 1024;
+  if (tc4_disabled() || M < 1 || K < 1 || K > std::max(128, kmax_stream) || N < 1 || N > 128) return false;
+  // K > 128: the weight image would not fit beside the stages -- each stage
+  // carries its own 32-wide K box of the weight instead (split per tile from L2)
+  const int stream_w = K > 128 ? 1 : 0;
   const int has_mask = (mode == 1 && mask) ? 1 : 0;
   if ((lda % 4) || (ldc % 4) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(C) & 15))
     return false;
   if (has_mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
   const int N_pad = (N + 15) / 16 * 16, K_pad = (K + 7) / 8 * 8, KB = (K + 31) / 32;
-  const int64_t stage_bytes = (int64_t)T4_BOX * (1 + has_mask);
+  // raw weight box of a K slice: mode 0 rows [32 x ceil4(N)], mode 1 [N x 32]
+  const int w_ld = mode == 0 ? (N + 3) / 4 * 4 : 32;
+  const bool w_tma = stream_w && !(ldw % 4) && !(reinterpret_cast<uintptr_t>(W) & 15);
+  const int w_raw = w_tma ? ((mode == 0 ? 32 * w_ld : N * 32) * 4 + 1023) / 1024 * 1024 : 0;
+  const int64_t stage_bytes = (int64_t)T4_BOX * (1 + has_mask) + (stream_w ? 2 * (int64_t)N_pad * 128 + w_raw : 0);
+  const int img_boxes = stream_w ? 0 : KB;
   const int nob = (N_pad + 31) / 32;
   auto fixed = [&](int S) {
-    return 1024 + 2 * (int64_t)KB * N_pad * 128 + (int64_t)S * stage_bytes + (int64_t)nob * T4_BOX + 8 * (3 * S + 5) +
-           16 + 4 * N_pad;
+    return 1024 + 2 * (int64_t)img_boxes * N_pad * 128 + (int64_t)S * stage_bytes + (int64_t)nob * T4_BOX +
+           8 * (3 * S + 5) + 16 + 4 * N_pad;
   };
   static const int env_s = getenv("FGL_TC4_STAGES") ? atoi(getenv("FGL_TC4_STAGES")) : 0;
   int S = std::min(env_s > 0 ? env_s : T4_MAX_STAGES, (512 - 2 * N_pad) / 32);
@@ -1111,8 +1168,11 @@ bool tc_dense4(int mode, const float* A, int64_t lda, const float* mask, int64_t
   int cols = 32;
   while (cols < 2 * N_pad + 32 * S) cols <<= 1;
   if (cols > 512) return false;
-  CUtensorMap mA, mM, mC;
+  CUtensorMap mA, mM, mC, mW;
   std::memset(&mM, 0, sizeof(mM));
+  std::memset(&mW, 0, sizeof(mW));
+  if (w_tma && !(mode == 0 ? make_map_cols(&mW, W, K, N, ldw, w_ld, 32) : make_map_cols(&mW, W, N, K, ldw, 32, N)))
+    return false;
   if (!cached_map_sw128(&mA, A, M, K, lda) || !cached_map_sw128(&mC, C, M, N, ldc) ||
       (has_mask && !cached_map_sw128(&mM, mask, M, K, ldm)))
     return false;
@@ -1125,14 +1185,15 @@ bool tc_dense4(int mode, const float* A, int64_t lda, const float* mask, int64_t
     attr[mode] = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
-  const int stage_off = (int)(2 * (int64_t)KB * N_pad * 128 + (int64_t)S * stage_bytes);
+  const int stage_off = (int)(2 * (int64_t)img_boxes * N_pad * 128 + (int64_t)S * stage_bytes);
   T4Args p{W, bias, M, ldw, N, K, N_pad, K_pad, S, relu, has_mask, cols,
-           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0) && (ldw % 4 == 0), stage_off, dbg};
+           !(reinterpret_cast<uintptr_t>(W) & 15) && ((mode == 0 ? N : K) % 4 == 0) && (ldw % 4 == 0), stage_off, dbg,
+           stream_w, w_tma ? (mode == 0 ? 32 * w_ld : N * 32) * 4 : 0, w_ld};
   const int grid = (int)std::min<int64_t>(ceil_div(M, T4_M), dense_cta_budget());
   const int64_t smem = fixed(S);
   const ProfMark pm = prof_begin(st);
-  if (mode == 0) FGL_COUNT_LAUNCH(), tc_dense4_kernel<0><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, p);
-  else FGL_COUNT_LAUNCH(), tc_dense4_kernel<1><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, p);
+  if (mode == 0) FGL_COUNT_LAUNCH(), tc_dense4_kernel<0><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, mW, p);
+  else FGL_COUNT_LAUNCH(), tc_dense4_kernel<1><<<grid, T4_THREADS, smem, st>>>(mA, mM, mC, mW, p);
   prof_end(pm, mode == 0 ? kProfDenseFwd : kProfDgrad, M, N, K);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_dense4_kernel");

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [(1000, 100, 64), (4097, 64, 64), (300, 64, 47), (129, 47, 64), (777, 128, 172),
           (50, 12, 2), (5000, 602, 64), (3, 8, 16), (3000, 301, 47), (1500, 129, 64),
-          (1024, 64, 172), (2000, 300, 200), (700, 64, 300)]
+          (1024, 64, 172), (2000, 300, 200), (700, 64, 300), (2000, 1000, 128), (129, 1024, 16)]
 
 
 def _ld(d):
