@@ -652,30 +652,40 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
   }
 }
 
-// partials -> dW / db (fixed order, 4 independent accumulators per output
-// combined in a fixed tree: deterministic) and the batch loss (fp64)
+// partials -> dW / db and the batch loss (fp64).  A CTA owns 32 outputs; its
+// 8 warps sum interleaved chunks (c = warp mod 8, two independent chains
+// each), combined in a fixed order: deterministic, and 8x fewer dependent L2
+// round trips per thread than one thread per output (12 -> ~3 us)
 __global__ void top_reduce_kernel(const float* __restrict__ part, int chunks, int64_t outs, float* __restrict__ dW,
                                   int64_t split, float* __restrict__ db, const double* __restrict__ loss_part,
                                   double* __restrict__ loss_sum) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32 + lane;
+  float s = 0.f;
   if (i < outs) {
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int c = 0;
-    for (; c + 3 < chunks; c += 4) {
-      s0 = __fadd_rn(s0, part[(int64_t)c * outs + i]);
-      s1 = __fadd_rn(s1, part[(int64_t)(c + 1) * outs + i]);
-      s2 = __fadd_rn(s2, part[(int64_t)(c + 2) * outs + i]);
-      s3 = __fadd_rn(s3, part[(int64_t)(c + 3) * outs + i]);
+    float s1 = 0.f;
+    int c = grp;
+    for (; c + 8 < chunks; c += 16) {
+      s = __fadd_rn(s, part[(int64_t)c * outs + i]);
+      s1 = __fadd_rn(s1, part[(int64_t)(c + 8) * outs + i]);
     }
-    for (; c < chunks; ++c) s0 = __fadd_rn(s0, part[(int64_t)c * outs + i]);
-    const float s = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
-    if (i < split) dW[i] = s; else db[i - split] = s;
+    if (c < chunks) s = __fadd_rn(s, part[(int64_t)c * outs + i]);
+    s = __fadd_rn(s, s1);
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
+  sm[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && i < outs) {
+    float t = sm[0][lane];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t = __fadd_rn(t, sm[g][lane]);
+    if (i < split) dW[i] = t; else db[i - split] = t;
+  }
+  if (blockIdx.x == 0 && grp == 1) {
     double l = 0.0;
-    for (int c = threadIdx.x; c < chunks; c += 32) l += loss_part[c];
+    for (int c = lane; c < chunks; c += 32) l += loss_part[c];
     l = warp_sum(l);
-    if (threadIdx.x == 0) *loss_sum = l;
+    if (lane == 0) *loss_sum = l;
   }
 }
 
@@ -1035,7 +1045,7 @@ int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_
     return FGL_OK;
   }
   const int64_t outs = (int64_t)(din + 1) * C;
-  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 256), 256, 0, (cudaStream_t)chain_stream>>>(
+  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, (cudaStream_t)chain_stream>>>(
       part, chunks, outs, dW, (int64_t)din * C, db, lp, loss_sum);
   FGL_LAUNCH_CHECK("top_reduce_kernel");
   return FGL_OK;
@@ -1047,7 +1057,7 @@ int fgl_top_layer_reduce(int64_t B, int32_t din, int32_t C, float* dW, float* db
   float* part = static_cast<float*>(ws);
   double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
   const int64_t outs = (int64_t)(din + 1) * C;
-  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 256), 256, 0, (cudaStream_t)stream>>>(
+  FGL_COUNT_LAUNCH(), top_reduce_kernel<<<(unsigned)ceil_div(outs, 32), 256, 0, (cudaStream_t)stream>>>(
       part, chunks, outs, dW, (int64_t)din * C, db, lp, loss_sum);
   FGL_LAUNCH_CHECK("top_reduce_kernel");
   return FGL_OK;
