@@ -65,6 +65,13 @@ CONFIGS = {
              "over the host link), GCN (128,64,64,172), fanouts [15,10,5], batch 1024, window 8",
         nodes=111_000_000, edges=1_600_000_000, exponent=3.0, dims=(128, 64, 64, 172),
         fanouts=[15, 10, 5], bs=1024, window=8, arch="gcn", store="host"),
+    "papers_hbm": dict(
+        desc="ogbn-papers100M-shaped synthetic power-law graph (Chung-Lu, exponent 3), 111M nodes / "
+             "1.6B directed edges, 128-d f32 features RESIDENT IN HBM (56.8 GB of the B200's 180 GB: the "
+             "B200-native placement of config 4; layer 0 reads the table directly), GCN (128,64,64,172), "
+             "fanouts [15,10,5], batch 1024, window 8",
+        nodes=111_000_000, edges=1_600_000_000, exponent=3.0, dims=(128, 64, 64, 172),
+        fanouts=[15, 10, 5], bs=1024, window=8, arch="gcn", store="device"),
     "products_host": dict(
         desc="products-shaped graph with the 100-d features in pinned host memory (Match delta "
              "loads over the host link), GCN (100,64,64,47), [15,10,5], batch 1024, window 8",

@@ -323,7 +323,7 @@ int fgl_softmax_xent(const float* logits, int64_t ldl, const int32_t* rows, int6
 
 /* Top model layer of the compact GCN batch in one launch (its rows are the
  * seeds): logits = H W + b, fp64 softmax cross entropy (trainer.py:198-209),
- * dH = dY W^T, and per-CTA partials of dW, db and the loss; din <= 64, C <= 48.
+ * dH = dY W^T, and per-CTA partials of dW, db and the loss; din <= 64, C <= 192.
  * agg_indptr != NULL: H is not read but gathered in-kernel as A X with
  * X = H (ldh), the layer's CSR (agg_indptr over the same rows, agg_col -
  * agg_col_base, agg_w), fgl_spmm arithmetic (bit-identical).

@@ -459,30 +459,35 @@ __global__ void fill_rows_kernel(float* __restrict__ Y, int64_t ldy, int64_t nro
 // (trainer.py:198-209) with dY = (p - onehot)/B, dH = dY W^T, and per-CTA
 // partials of dW = H^T dY, db = sum dY and of the loss (reduced off the
 // critical chain).  Replaces the dense forward, the softmax, the loss sum
-// and the dgrad launches of the top layer.  32 seeds per CTA, din <= 64, C <= 48;
-// fp32 FMA in a fixed order (within 1e-5), fp64 loss.
+// and the dgrad launches of the top layer.  8 seeds per CTA, din <= 64, C <= CW
+// (64: products / Reddit; 192: papers' 172 classes); fp32 FMA in a fixed order
+// (within 1e-5), fp64 loss.  W, W^T and the logits live in dynamic shared
+// memory ((128 CW + 8 CW) floats).
 constexpr int TOP_ROWS = 8;  // one warp per seed row in the softmax; 128 CTAs for a 1024-seed batch
 
+template <int CW>
 __global__ void __launch_bounds__(256) top_layer_kernel(
     const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ rows, int64_t row_base,
     const int32_t* __restrict__ seed_ids, const int64_t* __restrict__ labels, int64_t B, int din, int C,
     const float* __restrict__ W, const float* __restrict__ b, float* __restrict__ dH, int64_t lddh,
     float* __restrict__ part, double* __restrict__ loss_part, const int64_t* __restrict__ agg_indptr,
     const int32_t* __restrict__ agg_col, const float* __restrict__ agg_w, int64_t agg_col_base) {
-  __shared__ __align__(16) float Ws[64][64];   // [k][c]
-  __shared__ __align__(16) float WsT[48][64];  // [c][k]
+  extern __shared__ __align__(16) float top_dyn[];
+  float (*Ws)[CW] = reinterpret_cast<float (*)[CW]>(top_dyn);                 // [64][CW]: [k][c]
+  float (*WsT)[64] = reinterpret_cast<float (*)[64]>(top_dyn + 64 * CW);      // [CW][64]: [c][k]
+  float (*Ys)[CW] = reinterpret_cast<float (*)[CW]>(top_dyn + 128 * CW);      // [TOP_ROWS][CW]
   __shared__ __align__(16) float Hs[TOP_ROWS][68];
-  __shared__ __align__(16) float Ys[TOP_ROWS][48];
   __shared__ double lsum[TOP_ROWS];
+  constexpr int NWV = 64 * CW / 256;  // staged weight elements per thread
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t i0 = (int64_t)blockIdx.x * TOP_ROWS;
   const int nr = (int)(B - i0 < TOP_ROWS ? B - i0 : TOP_ROWS);
   // every global load of the staging is issued before the first shared
   // store (one memory latency, not one per element)
-  float wv[16];
+  float wv[NWV];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int i = t + 256 * u, k = i >> 6, c = i & 63;
+  for (int u = 0; u < NWV; ++u) {
+    const int i = t + 256 * u, k = i / CW, c = i % CW;
     wv[u] = (k < din && c < C) ? __ldg(W + (int64_t)k * C + c) : 0.f;
   }
   if (agg_indptr) {
@@ -515,10 +520,10 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       }
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = t + 256 * u, k = i >> 6, c = i & 63;
+    for (int u = 0; u < NWV; ++u) {
+      const int i = t + 256 * u, k = i / CW, c = i % CW;
       Ws[k][c] = wv[u];
-      if (c < 48) WsT[c][k] = wv[u];
+      WsT[c][k] = wv[u];
     }
     for (int k = lane; k < 68; k += 32) Hs[rw][k] = (rw < nr && k == din) ? 1.f : 0.f;
     __syncwarp();
@@ -541,10 +546,10 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       hv3[u] = v;
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = t + 256 * u, k = i >> 6, c = i & 63;
+    for (int u = 0; u < NWV; ++u) {
+      const int i = t + 256 * u, k = i / CW, c = i % CW;
       Ws[k][c] = wv[u];
-      if (c < 48) WsT[c][k] = wv[u];
+      WsT[c][k] = wv[u];
     }
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
@@ -554,9 +559,10 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
   }
   __syncthreads();
   const int rr = warp;  // every phase: warp = seed row of the CTA
-  // logits: lane -> columns 2 lane, 2 lane + 1
-  {
-    const int c0 = 2 * lane;
+  // logits: lane -> columns 64 j + 2 lane, 64 j + 2 lane + 1
+#pragma unroll
+  for (int j = 0; j < CW / 64; ++j) {
+    const int c0 = 64 * j + 2 * lane;
     float a0 = 0.f, a1 = 0.f;
     for (int k = 0; k < din; ++k) {
       const float h = Hs[rr][k];
@@ -564,8 +570,8 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       a0 = __fmaf_rn(h, w.x, a0);
       a1 = __fmaf_rn(h, w.y, a1);
     }
-    if (c0 < 48) Ys[rr][c0] = c0 < C ? (b ? __fadd_rn(a0, b[c0]) : a0) : 0.f;
-    if (c0 + 1 < 48) Ys[rr][c0 + 1] = c0 + 1 < C ? (b ? __fadd_rn(a1, b[c0 + 1]) : a1) : 0.f;
+    Ys[rr][c0] = c0 < C ? (b ? __fadd_rn(a0, b[c0]) : a0) : 0.f;
+    Ys[rr][c0 + 1] = c0 + 1 < C ? (b ? __fadd_rn(a1, b[c0 + 1]) : a1) : 0.f;
   }
   __syncwarp();
   // softmax cross entropy of the warp's row (fp64); Ys <- dY
@@ -576,10 +582,11 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       for (int c = lane; c < C; c += 32) mx = fmax(mx, (double)Ys[rr][c]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      double ex[2] = {0.0, 0.0};
+      double ex[CW / 32];
       double se = 0.0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < CW / 32; ++u) {
+        ex[u] = 0.0;
         const int c = lane + 32 * u;
         if (c < C) { ex[u] = exp((double)Ys[rr][c] - mx); se += ex[u]; }
       }
@@ -588,7 +595,7 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       const int64_t y = labels[seed_ids ? (int64_t)seed_ids[i0 + rr] : i0 + rr];
       __syncwarp();
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < CW / 32; ++u) {
         const int c = lane + 32 * u;
         if (c < C) {
           const double pc = ex[u] / se;
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(256) top_layer_kernel(
       }
       l = warp_sum(l);
     } else {
-      for (int c = lane; c < 48; c += 32) Ys[rr][c] = 0.f;
+      for (int c = lane; c < CW; c += 32) Ys[rr][c] = 0.f;
     }
     if (lane == 0) lsum[rr] = l;
   }
@@ -1024,19 +1031,33 @@ int fgl_top_layer(const float* H, int64_t ldh, const int32_t* rows, int64_t row_
                   float* dH, int64_t lddh, float* dW, float* db, double* loss_sum, void* ws, int64_t ws_bytes,
                   const int64_t* agg_indptr, const int32_t* agg_col, const float* agg_w, int64_t agg_col_base,
                   void* chain_stream, void* reduce_stream) {
-  if (B < 1 || din < 1 || din > 64 || C < 1 || C > 48 || !H || !rows || !labels || !W || !dH || !dW || !db ||
+  if (B < 1 || din < 1 || din > 64 || C < 1 || C > 192 || !H || !rows || !labels || !W || !dH || !dW || !db ||
       !loss_sum || ldh < din || lddh < din || ws_bytes < fgl_top_layer_ws_bytes(B, din, C) ||
       (agg_indptr && (!agg_col || !agg_w || (ldh % 4) || (reinterpret_cast<uintptr_t>(H) & 15)))) {
-    set_error("fgl_top_layer: bad arguments (din <= 64, C <= 48)");
+    set_error("fgl_top_layer: bad arguments (din <= 64, C <= 192)");
     return FGL_E_INVALID;
   }
   const int chunks = (int)ceil_div(B, TOP_ROWS);
   float* part = static_cast<float*>(ws);
   double* lp = reinterpret_cast<double*>(static_cast<char*>(ws) + ((int64_t)chunks * (din + 1) * C * 4 + 7) / 8 * 8);
   const ProfMark pm = prof_begin((cudaStream_t)chain_stream);
-  FGL_COUNT_LAUNCH(), top_layer_kernel<<<chunks, 256, 0, (cudaStream_t)chain_stream>>>(
-      H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp, agg_indptr, agg_col, agg_w,
-      agg_col_base);
+  if (C <= 64) {
+    FGL_COUNT_LAUNCH(), top_layer_kernel<64><<<chunks, 256, (128 + TOP_ROWS) * 64 * 4, (cudaStream_t)chain_stream>>>(
+        H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp, agg_indptr, agg_col, agg_w,
+        agg_col_base);
+  } else {
+    constexpr int smem = (128 + TOP_ROWS) * 192 * 4;
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(top_layer_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(top_layer_kernel)");
+      attr = true;
+    }
+    FGL_COUNT_LAUNCH(), top_layer_kernel<192><<<chunks, 256, smem, (cudaStream_t)chain_stream>>>(
+        H, ldh, rows, row_base, seed_ids, labels, B, din, C, W, b, dH, lddh, part, lp, agg_indptr, agg_col, agg_w,
+        agg_col_base);
+  }
   prof_end(pm, kProfTopLayer, B, din, C);
   FGL_LAUNCH_CHECK("top_layer_kernel");
   if (reduce_stream && reduce_stream != chain_stream) {

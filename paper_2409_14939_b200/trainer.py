@@ -614,7 +614,7 @@ class Pipeline:
         x0 = self._gather_x0(win, b, prev, slot, x0_slot)
         # forward
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
-        top_fused = (self.compact and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 48
+        top_fused = (self.compact and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 192
                      and self._fuse_top
                      and (self._rows(win, self.L - 1, b)[1] - self._rows(win, self.L - 1, b)[0]) == s1 - s0)
         X, ldx = x0, self.ldf

@@ -91,6 +91,7 @@ def test_trajectory_per_step_1e5(name):
 @pytest.mark.parametrize("arch,dims,fan,direct", [("gcn", (128, 64, 2), [10, 5], False),
                                                   ("gcn", (128, 64, 2), [10, 5], True),
                                                   ("gcn", (128, 48, 32, 7), [6, 4, 3], True),
+                                                  ("gcn", (32, 64, 172), [6, 4], True),  # papers' classes: fused top, CW 192
                                                   ("gin", (128, 16, 3), [5, 3], False)])
 def test_window_steps_match_oracle(cfg1_graph, arch, dims, fan, direct):
     """A window of 4 batches on config 1: per-batch loss and the parameters

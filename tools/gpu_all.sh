@@ -17,6 +17,8 @@ done
 timeout 600 python bench.py --bs 8000 --steps 20 --no-cpu-baseline > $O/bench_products_bs8000.json 2> $O/bench_products_bs8000.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches.csv python bench.py --profile --no-cpu-baseline > $O/prof.log 2>&1
 timeout 1500 python bench.py --config papers --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_papers.json 2> $O/bench_papers.err
+timeout 1500 python bench.py --config papers --cache-ratio 1.0 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_papers_c1.0.json 2> $O/bench_papers_c1.0.err
+timeout 1500 python bench.py --config papers_hbm --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_papers_hbm.json 2> $O/bench_papers_hbm.err
 for f in $O/bench_*.json; do python -c "
 import json
 d = json.loads(open('$f').read().strip().splitlines()[-1])
