@@ -927,7 +927,8 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
       // slices (wide inputs: Reddit 602; wide outputs: papers 172 classes);
       // each slice's partials are reduced straight into its block of dW (db
       // from the first K slice, the others' db rows land in scratch)
-      const int kmax = din + 1 > 128 ? 124 : din;
+      // (din == 128: one slice, db from tc_wgrad3's converters instead of a ones lane)
+      const int kmax = din == 128 ? 128 : din + 1 > 128 ? 124 : din;
       bool ok = false, later_fail = false;
       for (int nsw = 128; nsw >= 32 && !ok && !later_fail; nsw /= 2) {  // the widest N slice that fits
         const int nmax = dout < nsw ? dout : nsw;

@@ -496,8 +496,11 @@ struct Wg3Args {
   int h_lds;  // smem row stride of an H tile, floats (= ldh for whole-row bulk copies)
   int z_tma;  // dZ (and mask) tiles by TMA tensor copies of a column slice (N slices)
   int z_lds, m_lds;  // smem row strides of the dZ / mask tiles, floats
+  int db_conv;  // K == 128 (no TMEM lane left for the ones row): db from the B' converters' column sums
 };
 
+template <bool DBC>  // DBC: db from the converters (p.db_conv, K == 128); a separate
+                    // instantiation keeps the common path's registers / code unchanged
 __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_constant__ CUtensorMap tmH,
                                                                   const __grid_constant__ CUtensorMap tmZ,
                                                                   const __grid_constant__ CUtensorMap tmM, Wg3Args p) {
@@ -511,6 +514,8 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   const int slot_bytes = p.h_bytes + p.z_bytes + p.m_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(slots + p.R * slot_bytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.R + 2 * p.NC + 1);
+  float* dbsm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) &
+                                          ~uintptr_t(15));  // db_conv: [3 groups][8 row quads][N_pad]
   auto bar = [&](int i) { return smem_u32(bars + i); };
   const int FULL = 0, EMPTY = p.R, CFULL = 2 * p.R, CEMPTY = 2 * p.R + p.NC, TFULL = 2 * p.R + 2 * p.NC;
   if (tid == 0) {
@@ -598,6 +603,11 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;     // A' row = TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    // db_conv: this thread's B' items (fixed across chunks) summed over the
+    // rows of its group's chunks, in chunk order (deterministic)
+    float4 dbs[DBC ? 4 : 1];
+#pragma unroll
+    for (int u = 0; u < (DBC ? 4 : 1); ++u) dbs[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     int kk = 0;
     for (int cc = grp; cc < 2 * my_tiles; cc += 3, ++kk) {
       const int j = cc >> 1, c = cc & 1;
@@ -647,11 +657,11 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
         const uint32_t bh = smem_u32(sB) + (uint32_t)(cs * 2 * b_box);
         const int n4s = N_pad >> 2;
         const int items = ((n4s + 7) >> 3) * 64;
-        for (int t = ct; t < ((p.dbg & 4) ? 0 : items); t += G3_CONV_THREADS / 2) {
+        auto b_item = [&](int t, float4& db_acc) {
           const int ph = t & 7, hi_ = t >> 3;
           const int n4 = ph + 8 * (hi_ >> 3);
           const int rq = (((ph >> 1) + (hi_ & 3)) & 3) + 4 * ((hi_ >> 2) & 1);
-          if (n4 >= n4s) continue;
+          if (n4 >= n4s) return;
           const int rb = 32 * c + 4 * rq;
           float4 e[4];
           if (rb + 4 <= rows && 4 * n4 + 4 <= p.N && p.mask) {
@@ -693,6 +703,15 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
               e[i].w = (rv && nv > 3 && mk[i].w > 0.f) ? e[i].w : 0.f;
             }
           }
+          if (DBC) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              db_acc.x = __fadd_rn(db_acc.x, e[i].x);
+              db_acc.y = __fadd_rn(db_acc.y, e[i].y);
+              db_acc.z = __fadd_rn(db_acc.z, e[i].z);
+              db_acc.w = __fadd_rn(db_acc.w, e[i].w);
+            }
+          }
           const float4 col[4] = {make_float4(e[0].x, e[1].x, e[2].x, e[3].x), make_float4(e[0].y, e[1].y, e[2].y, e[3].y),
                                  make_float4(e[0].z, e[1].z, e[2].z, e[3].z), make_float4(e[0].w, e[1].w, e[2].w, e[3].w)};
 #pragma unroll
@@ -706,6 +725,14 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
             sts128(bh + off, h4);
             sts128(bh + (uint32_t)b_box + off, l4);
           }
+        };
+        const int lim = (p.dbg & 4) ? 0 : items;
+        if constexpr (DBC) {  // static item slots: the db accumulators stay in registers
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (ct + u * (G3_CONV_THREADS / 2) < lim) b_item(ct + u * (G3_CONV_THREADS / 2), dbs[u]);
+        } else {
+          for (int t = ct; t < lim; t += G3_CONV_THREADS / 2) b_item(t, dbs[0]);
         }
         if (trc) G3T(5 + 6 * kk);
         tmem_st_wait();
@@ -716,6 +743,19 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
       }
       mbar_arrive(bar(EMPTY + s));
       if (trc) G3T(7 + 6 * kk);
+    }
+    if (DBC) {
+      const int n4s = N_pad >> 2, items = ((n4s + 7) >> 3) * 64;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = ct + u * (G3_CONV_THREADS / 2);
+        if (t >= items) break;
+        const int ph = t & 7, hi_ = t >> 3;
+        const int n4 = ph + 8 * (hi_ >> 3);
+        const int rq = (((ph >> 1) + (hi_ & 3)) & 3) + 4 * ((hi_ >> 2) & 1);
+        if (n4 < n4s) *reinterpret_cast<float4*>(dbsm + (grp * 8 + rq) * N_pad + 4 * n4) = dbs[DBC ? u : 0];
+      }
+      asm volatile("bar.sync 5, %0;" ::"r"(G3_THREADS - 128) : "memory");  // the 12 converter warps
     }
   }
   if (warp >= 12) {
@@ -742,6 +782,13 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = sum[q];
+      }
+    }
+    if (DBC) {  // row K (db): the converters' sums, groups then row quads in a fixed order
+      for (int c = tid - 384; c < p.N; c += 128) {
+        float v = 0.f;
+        for (int g = 0; g < 24; ++g) v = __fadd_rn(v, dbsm[g * N_pad + c]);
+        out[(int64_t)c * (p.K + 1) + p.K] = v;
       }
     }
     if (tid == 384) G3T(71);
@@ -1311,11 +1358,13 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
 }
 
 // Weight-gradient partials part[c][K+1][N] (row K = db) over `chunks` CTAs;
-// returns false outside the envelope (K + 1 <= 128, N <= 256, 16-byte rows).
+// returns false outside the envelope (K <= 128, N <= 256, 16-byte rows; at
+// K = 128 the db row comes from the converters instead of a TMEM ones lane).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
                int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
   *err = 0;
-  if (tc3_disabled() || M < 1 || K < 1 || K + 1 > G3_M || N < 1 || N > 256) return false;
+  if (tc3_disabled() || M < 1 || K < 1 || K > G3_M || N < 1 || N > 256) return false;
+  const int db_conv = K == G3_M ? 1 : 0;
   if ((ldh % 4) || (ldz % 4) || (reinterpret_cast<uintptr_t>(H) & 15) || (reinterpret_cast<uintptr_t>(dZ) & 15))
     return false;
   if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
@@ -1336,7 +1385,8 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   static const int env_nc = getenv("FGL_WG3_NC") ? atoi(getenv("FGL_WG3_NC")) : 0;
   const int NC = env_nc > 0 ? env_nc : WG3_NC;
   auto smem_of = [&](int R) {
-    return 1024 + (int64_t)NC * 2 * N_pad * 128 + (int64_t)R * (hb + zb + mb) + 8 * (2 * R + 2 * NC + 1) + 16;
+    return 1024 + (int64_t)NC * 2 * N_pad * 128 + (int64_t)R * (hb + zb + mb) + 8 * (2 * R + 2 * NC + 1) + 16 +
+           (db_conv ? 16 + 24 * 4 * (int64_t)N_pad : 0);
   };
   int R = env_r > 0 ? env_r : WG3_R_MAX;
   while (R > 2 && smem_of(R) > G3_MAX_SMEM) --R;
@@ -1350,13 +1400,15 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   static bool attr = false;
   cudaError_t e;
   if (!attr) {
-    e = cudaFuncSetAttribute(tc_wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    e = cudaFuncSetAttribute(tc_wgrad3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tc_wgrad3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3_MAX_SMEM);
     if (e != cudaSuccess) { *err = cuda_status(e, "cudaFuncSetAttribute(tc_wgrad3)"); return true; }
     attr = true;
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
   Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc, h_tma, h_lds,
-            z_tma, z_lds, m_lds};
+            z_tma, z_lds, m_lds, db_conv};
   CUtensorMap mH, mZ, mM;
   std::memset(&mH, 0, sizeof(mH));
   std::memset(&mZ, 0, sizeof(mZ));
@@ -1365,7 +1417,8 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   if (z_tma && (!make_map_cols(&mZ, dZ, M, N, ldz, z_lds, WG3_MT) ||
                 (mask && !make_map_cols(&mM, mask, M, N, ldm, m_lds, WG3_MT))))
     return false;
-  FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
+  if (db_conv) FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<true><<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
+  else FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<false><<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
   return true;
