@@ -201,7 +201,11 @@ bool tc_gemm3(int mode, const float* A, int64_t lda, const float* mask, int64_t 
               const float* bias, float* C, int64_t ldc, int64_t M, int N, int K, int relu,
               cudaStream_t st, int* err, int accum = 0, int64_t ldw = -1);
 // tcgen05 3xTF32 weight gradient partials: part[c][K+1][N] (row K = db).
+// nks > 1: the K features in nks slices of kslice in ONE launch (chunks CTAs
+// per slice); slice s's partials at part + s * chunks * (kslice + 1) * N,
+// each [c][K_s + 1][N] with K_s = min(kslice, K - s kslice).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
-               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err);
+               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err, int nks = 1,
+               int kslice = 0);
 
 }  // namespace fgl

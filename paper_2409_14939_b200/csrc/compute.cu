@@ -930,6 +930,26 @@ int fgl_dense_bwd(const float* H, int64_t ldh, int64_t n, int32_t din, const flo
       // (din == 128: one slice, db from tc_wgrad3's converters instead of a ones lane)
       const int kmax = din == 128 ? 128 : din + 1 > 128 ? 124 : din;
       bool ok = false, later_fail = false;
+      // wide inputs (Reddit 602) with one N slice: every K slice in one launch,
+      // the CTAs of a row range on consecutive slices (dZ / mask tiles shared
+      // through L2 instead of re-read from HBM per slice)
+      const int nks = (int)ceil_div(din, kmax);
+      static const int multi = getenv("FGL_WG_MULTI") ? atoi(getenv("FGL_WG_MULTI")) : 1;
+      if (multi && nks > 1 && dout <= 128) {
+        const int cps = std::max(1, std::min(tc3_chunks, kNumSMs / nks));
+        const int64_t stride = (int64_t)cps * (kmax + 1) * dout;
+        float* scratch_db = pw + nks * stride;
+        if ((nks * stride + dout) * 4 <= ws_bytes) {
+          ok = tc_wgrad3(H, ldh, dX, lddx, Xout, ldxo, n, din, dout, pw, cps, st, &werr, nks, kmax);
+          if (werr) return werr;
+          for (int s = 0; ok && s < nks; ++s) {
+            const int k0 = s * kmax, ks = din - k0 < kmax ? din - k0 : kmax;
+            const int64_t o = (int64_t)(ks + 1) * dout;
+            FGL_COUNT_LAUNCH(), reduce_partials_kernel<<<(unsigned)ceil_div(o, 32), 256, 0, st>>>(
+                pw + s * stride, cps, o, dW + (int64_t)k0 * dout, 0, k0 == 0 ? db : scratch_db, ks + 1, dout, 0);
+          }
+        }
+      }
       for (int nsw = 128; nsw >= 32 && !ok && !later_fail; nsw /= 2) {  // the widest N slice that fits
         const int nmax = dout < nsw ? dout : nsw;
         float* slice_part = pw;

@@ -497,6 +497,9 @@ struct Wg3Args {
   int z_tma;  // dZ (and mask) tiles by TMA tensor copies of a column slice (N slices)
   int z_lds, m_lds;  // smem row strides of the dZ / mask tiles, floats
   int db_conv;  // K == 128 (no TMEM lane left for the ones row): db from the B' converters' column sums
+  int nks;      // K slices in this launch (CTA b: slice b % nks, row range b / nks), 1 = a single slice
+  int kslice;   // slice width (nks > 1): slice s covers features [s kslice, min(K, (s+1) kslice))
+  int64_t part_stride;  // floats between the slices' partial regions
 };
 
 template <bool DBC>  // DBC: db from the converters (p.db_conv, K == 128); a separate
@@ -527,10 +530,15 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   __syncthreads();
   if (tid == 0) G3T(0);
   const int64_t tiles = ceil_div(p.M, WG3_MT);
+  // multi-slice launch: CTAs rc * nks .. rc * nks + nks - 1 take the same row
+  // tiles for consecutive K slices, so a dZ / mask tile read from HBM by one
+  // is an L2 hit for the others
+  const int ksl = (int)(blockIdx.x % p.nks), rc = (int)(blockIdx.x / p.nks), G = (int)(gridDim.x / p.nks);
+  const int K = p.nks > 1 ? min(p.kslice, p.K - ksl * p.kslice) : p.K;  // this CTA's features
   if (warp == 0) {
     if (lane == 0) {
       int j = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      for (int64_t t = rc; t < tiles; t += G, ++j) {
         const int s = j % p.R;
         mbar_wait(bar(EMPTY + s), ((uint32_t)(j / p.R) & 1u) ^ 1u);
         if (j < 8) G3T(58 + j);
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
         const uint32_t mb = !p.mask ? 0u : p.z_tma ? (uint32_t)(WG3_MT * p.m_lds * 4) : (uint32_t)(rows * p.ldm * 4);
         char* slot = slots + s * slot_bytes;
         mbar_arrive_expect_tx(bar(FULL + s), hb + zb + mb);
-        if (p.h_tma) tma_load_2d(smem_u32(slot), &tmH, 0, (int)r0, bar(FULL + s));  // OOB rows / cols: zeros
+        if (p.h_tma) tma_load_2d(smem_u32(slot), &tmH, ksl * p.kslice, (int)r0, bar(FULL + s));  // OOB: zeros
         else bulk_load(smem_u32(slot), p.H + r0 * p.ldh, hb, bar(FULL + s));
         if (p.z_tma) {
           tma_load_2d(smem_u32(slot + p.h_bytes), &tmZ, 0, (int)r0, bar(FULL + s));
@@ -563,7 +571,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   // the tensor core's fp32 accumulation loses accuracy over long chains, the
   // epilogue sums the accumulators with IEEE adds), then the A chunk ring
   auto ch_hi = [&](int c) { return tmem + (uint32_t)(p.nacc * N_pad + 64 * c); };
-  const int my_tiles = (int)(tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  const int my_tiles = (int)(tiles > rc ? (tiles - 1 - rc) / G + 1 : 0);
 
   if (warp == 1) {
     const uint32_t idesc = idesc_tf32(G3_M, N_pad, 0, 0);
@@ -612,7 +620,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
     for (int cc = grp; cc < 2 * my_tiles; cc += 3, ++kk) {
       const int j = cc >> 1, c = cc & 1;
       const int s = j % p.R;
-      const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
+      const int64_t t = rc + (int64_t)j * G;
       const int rows = (int)(p.M - t * WG3_MT < WG3_MT ? p.M - t * WG3_MT : WG3_MT);
       mbar_wait(bar(FULL + s), (uint32_t)(j / p.R) & 1u);
       const bool trc = ct == 0 && grp == 0 && kk < 8;
@@ -628,15 +636,15 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
         uint32_t hv[32], lv[32];
         {
           const int nrow = rows - 32 * c;
-          const uint32_t a0 = hs + (uint32_t)((32 * c * p.h_lds + (m < p.K ? m : 0)) * 4);
+          const uint32_t a0 = hs + (uint32_t)((32 * c * p.h_lds + (m < K ? m : 0)) * 4);
           const uint32_t rs = (uint32_t)(p.h_lds * 4);
           float xs[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) xs[q] = lds32(a0 + (uint32_t)q * rs);
-          const float one = m == p.K ? 1.f : 0.f;
+          const float one = m == K ? 1.f : 0.f;
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const float x = q < nrow ? (m < p.K ? xs[q] : one) : 0.f;
+            const float x = q < nrow ? (m < K ? xs[q] : one) : 0.f;
             const float hi = tf32_rna_finite(x);
             hv[q] = __float_as_uint(hi);
             lv[q] = __float_as_uint(__fsub_rn(x, hi));
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
   if (warp >= 12) {
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;
-    float* out = p.part + (int64_t)blockIdx.x * (p.K + 1) * p.N;
+    float* out = p.part + ksl * p.part_stride + (int64_t)rc * (K + 1) * p.N;
     if (my_tiles > 0) {
       mbar_wait(bar(TFULL), 0);
       tc_fence_after();
@@ -778,17 +786,17 @@ __global__ void __launch_bounds__(G3_THREADS, 1) tc_wgrad3_kernel(const __grid_c
 #pragma unroll
         for (int q = 0; q < 16; ++q) sum[q] = a == 0 ? __uint_as_float(v[q]) : __fadd_rn(sum[q], __uint_as_float(v[q]));
       }
-      if (m <= p.K) {  // feature-major partials: a warp stores 32 consecutive floats per column
+      if (m <= K) {  // feature-major partials: a warp stores 32 consecutive floats per column
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (p.K + 1) + m] = sum[q];
+          if (c0 + q < p.N) out[(int64_t)(c0 + q) * (K + 1) + m] = sum[q];
       }
     }
     if (DBC) {  // row K (db): the converters' sums, groups then row quads in a fixed order
       for (int c = tid - 384; c < p.N; c += 128) {
         float v = 0.f;
         for (int g = 0; g < 24; ++g) v = __fadd_rn(v, dbsm[g * N_pad + c]);
-        out[(int64_t)c * (p.K + 1) + p.K] = v;
+        out[(int64_t)c * (K + 1) + K] = v;
       }
     }
     if (tid == 384) G3T(71);
@@ -1361,18 +1369,20 @@ bool tc_gemm(int mode, const float* A, int64_t lda, const float* mask, int64_t l
 // returns false outside the envelope (K <= 128, N <= 256, 16-byte rows; at
 // K = 128 the db row comes from the converters instead of a TMEM ones lane).
 bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const float* mask, int64_t ldm,
-               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err) {
+               int64_t M, int K, int N, float* part, int chunks, cudaStream_t st, int* err, int nks, int kslice) {
   *err = 0;
-  if (tc3_disabled() || M < 1 || K < 1 || K > G3_M || N < 1 || N > 256) return false;
-  const int db_conv = K == G3_M ? 1 : 0;
+  if (nks < 1 || (nks > 1 && (kslice < 1 || kslice + 1 > G3_M || (int64_t)(nks - 1) * kslice >= K))) return false;
+  const int Kw = nks > 1 ? kslice : K;  // widest slice of this launch
+  if (tc3_disabled() || M < 1 || K < 1 || Kw > G3_M || N < 1 || N > 256) return false;
+  const int db_conv = Kw == G3_M ? 1 : 0;
   if ((ldh % 4) || (ldz % 4) || (reinterpret_cast<uintptr_t>(H) & 15) || (reinterpret_cast<uintptr_t>(dZ) & 15))
     return false;
   if (mask && ((ldm % 4) || (reinterpret_cast<uintptr_t>(mask) & 15))) return false;
   const int N_pad = (N + 15) / 16 * 16;
   // a column slice of a wide H (ldh > 256 floats): 2-D TMA tensor copies of
   // [64 rows x K_box] tiles instead of whole-row bulk copies
-  const int h_tma = ldh > 256 ? 1 : 0;
-  const int h_lds = h_tma ? (K + 3) / 4 * 4 : (int)ldh;
+  const int h_tma = (ldh > 256 || nks > 1) ? 1 : 0;
+  const int h_lds = h_tma ? (Kw + 3) / 4 * 4 : (int)ldh;
   // a column slice of dZ / mask (an N slice of a wider layer, or rows wider
   // than 256 floats): TMA tensor copies of [64 rows x N_box] tiles
   const int N4 = (N + 3) / 4 * 4;
@@ -1408,17 +1418,17 @@ bool tc_wgrad3(const float* H, int64_t ldh, const float* dZ, int64_t ldz, const 
   }
   static const int dbg = getenv("FGL_G3DBG") ? atoi(getenv("FGL_G3DBG")) : 0;
   Wg3Args p{H, dZ, mask, ldh, ldz, ldm, part, M, K, N, N_pad, cols, hb, zb, mb, dbg, R, NC, nacc, h_tma, h_lds,
-            z_tma, z_lds, m_lds, db_conv};
+            z_tma, z_lds, m_lds, db_conv, nks, kslice, (int64_t)chunks * (Kw + 1) * N};
   CUtensorMap mH, mZ, mM;
   std::memset(&mH, 0, sizeof(mH));
   std::memset(&mZ, 0, sizeof(mZ));
   std::memset(&mM, 0, sizeof(mM));
-  if (h_tma && !make_map_cols(&mH, H, M, K, ldh, h_lds, WG3_MT)) return false;
+  if (h_tma && !make_map_cols(&mH, H, M, K, ldh, h_lds, WG3_MT)) return false;  // all K columns: slices by offset
   if (z_tma && (!make_map_cols(&mZ, dZ, M, N, ldz, z_lds, WG3_MT) ||
                 (mask && !make_map_cols(&mM, mask, M, N, ldm, m_lds, WG3_MT))))
     return false;
-  if (db_conv) FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<true><<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
-  else FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<false><<<chunks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
+  if (db_conv) FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<true><<<chunks * nks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
+  else FGL_COUNT_LAUNCH(), tc_wgrad3_kernel<false><<<chunks * nks, G3_THREADS, smem, st>>>(mH, mZ, mM, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) *err = cuda_status(e, "tc_wgrad3_kernel");
   return true;
