@@ -614,7 +614,9 @@ class Pipeline:
         x0 = self._gather_x0(win, b, prev, slot, x0_slot)
         # forward
         s0, s1 = int(win.seed_off_host[b]), int(win.seed_off_host[b + 1])
-        top_fused = (self.compact and self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 192
+        # the top layer in one kernel (GCN: with its aggregation; GIN / SAGE: the
+        # aggregation with its root term stays in fgl_spmm, the kernel reads H)
+        top_fused = (self.L >= 2 and dims[-2] <= 64 and dims[-1] <= 192
                      and self._fuse_top
                      and (self._rows(win, self.L - 1, b)[1] - self._rows(win, self.L - 1, b)[0]) == s1 - s0)
         X, ldx = x0, self.ldf
@@ -631,7 +633,7 @@ class Pipeline:
                 Hb, ev = pre
                 if not external_done and ev is not None:
                     self._cur().wait_event(ev)
-            elif i == self.L - 1 and top_fused:
+            elif i == self.L - 1 and top_fused and self.compact:
                 # the fused top-layer kernel gathers H = A X itself
                 Hb = None
                 top_agg = (lay["indptr"].data_ptr() + 8 * r0, lay["col"], lay["w"].data_ptr(),
@@ -652,6 +654,8 @@ class Pipeline:
                 else:
                     self._call("fgl_spmm", lay["indptr"].data_ptr() + 8 * r0, col, lay["w"].data_ptr(), n,
                                base, X.data_ptr(), ldx, self_x, ldx, Hb.data_ptr(), _ld(din), din, st)
+                if i == self.L - 1 and top_fused:
+                    top_agg = (None, None, None, 0, Hb.data_ptr(), _ld(din))
             if i == self.L - 1 and top_fused:
                 Yb = None  # the fused top-layer kernel computes the logits itself
             else:
