@@ -30,11 +30,16 @@ inline int64_t al(int64_t x) { return (x + 255) / 256 * 256; }
 struct GroupWs {
   int32_t* counts;   // [num_keys]
   int32_t* cursor;   // [num_keys]
-  int64_t* part;     // [kPersistentCTAs + 1]
+  int64_t* part;     // [kScanCTAs + 1]
   int32_t* lists;    // [3 * num_keys]: medium, large, huge row lists
   int32_t* nlist;    // [4]
   int64_t bytes;
 };
+
+// the count scans: one 2048-key tile per CTA up to 8 CTAs per SM (GIN / SAGE
+// index every hop over the window's ~5M rows: 296 CTAs walking 8 serial
+// tiles each took 28 us per scan)
+constexpr int kScanCTAs = 8 * kNumSMs;
 
 GroupWs group_ws(void* base, int64_t num_keys) {
   char* p = static_cast<char*>(base);
@@ -42,7 +47,7 @@ GroupWs group_ws(void* base, int64_t num_keys) {
   int64_t o = 0;
   w.counts = reinterpret_cast<int32_t*>(p + o); o = al(o + 4 * num_keys);
   w.cursor = reinterpret_cast<int32_t*>(p + o); o = al(o + 4 * num_keys);
-  w.part = reinterpret_cast<int64_t*>(p + o); o = al(o + 8 * (kPersistentCTAs + 1));
+  w.part = reinterpret_cast<int64_t*>(p + o); o = al(o + 8 * (kScanCTAs + 1));
   w.lists = reinterpret_cast<int32_t*>(p + o); o = al(o + 4 * 3 * num_keys);
   w.nlist = reinterpret_cast<int32_t*>(p + o); o = al(o + 4 * 4);
   w.bytes = o;
@@ -312,7 +317,7 @@ int stable_group_impl(const int32_t* keys, int64_t nnz, int64_t num_keys, int64_
   FGL_CUDA(cudaMemsetAsync(w.cursor, 0, 4 * num_keys, st));
   FGL_CUDA(cudaMemsetAsync(w.nlist, 0, 16, st));
   if (nnz > 0) FGL_COUNT_LAUNCH(), histogram_kernel<<<grid_for(nnz), kThreads, 0, st>>>(keys, nnz, counts);
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kPersistentCTAs, ceil_div(num_keys, 1024)));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kScanCTAs, ceil_div(num_keys, 2048)));
   FGL_COUNT_LAUNCH(), chunk_sum_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part);
   FGL_COUNT_LAUNCH(), part_scan_kernel<<<1, 1024, 0, st>>>(w.part, G);
   FGL_COUNT_LAUNCH(), chunk_scan_kernel<<<G, kThreads, 0, st>>>(counts, num_keys, w.part, base, indptr);
